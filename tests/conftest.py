@@ -1,0 +1,25 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built extension")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+
+    import numpy as np
+    here = os.path.join(ROOT, "tests", "golden")
+    with open(os.path.join(here, "golden.json")) as f:
+        meta = json.load(f)
+    arrays = dict(np.load(os.path.join(here, "golden_arrays.npz")))
+    return meta, arrays
