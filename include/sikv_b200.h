@@ -1,0 +1,144 @@
+/*
+ * sikv_b200.h — C ABI of libsikv_b200.so, the B200 (sm_100a) self-indexing KV-cache path.
+ *
+ * The reference (arXiv 2603.14224's package, /root/reference/pkg/src/sikv) is a Python/numpy
+ * package with no FFI; its boundary is the Python API in sikv/__init__.py.  These entry
+ * points are what that API binds to through ctypes: every reference
+ * function on the decode path maps to one call below, cited next to it.
+ *
+ * Conventions
+ *   - all tensor arguments are DEVICE pointers, contiguous, row-major, owned by the caller
+ *     (the library never allocates or frees); `stream` is a cudaStream_t (NULL = default);
+ *   - calls are asynchronous on `stream`, stateless and re-entrant; argument errors are
+ *     reported synchronously via the return code, device-side data errors via `status_dev`
+ *     (a device int the caller zeroes and reads back: bit0 = fp16 parameter range exceeded,
+ *     bit1 = alpha does not dominate |K'|, bit2 = non-finite input, bit3 = mean certificate
+ *     failed and the sequential fallback ran (informational));
+ *   - return 0 on success, SIKV_EINVAL / SIKV_EUNSUPPORTED / SIKV_ECUDA otherwise; the
+ *     message is available from sikv_last_error() (thread-local).
+ *   - in_dtype: 0 = float32, 1 = float64, 2 = bfloat16.
+ *
+ * Layouts ("reference layout" = the reference's packed numpy arrays, bit for bit):
+ *   codes_ref  [U][L][ceil(G/2)] u8   two 4-bit sign codes per byte, low nibble = lower group
+ *                                     (codebook.py:50-90, bitpack.py:27-48)
+ *   kq_ref/vq_ref [U][L][ceil(D*bits/8)] u8, element e at bits (e % (8/bits))*bits of byte
+ *                                     e/(8/bits) (bitpack.py:27-48)
+ *   *_scales / *_zeros [U][L][D/group] fp16 (quantizer.py:52-94)
+ * Fast layout (D = 128, bits = 2, group = 32, sign_in_quant): see DESIGN.md §3
+ *   signs_fast [U][L][16] u8  sign plane, byte i of token t = reference byte (t+i) mod 16
+ *   recs_fast  [U][L][128] u8 per-token record: K/V 2-bit payloads in mma.sync fragment
+ *                             order, fp16 (scale, zero) x 4 groups for K and V, K sign words
+ */
+#ifndef SIKV_B200_H
+#define SIKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIKV_OK 0
+#define SIKV_EINVAL 1
+#define SIKV_ECUDA 2
+#define SIKV_EUNSUPPORTED 3
+
+const char* sikv_last_error(void);
+int sikv_abi_version(void);
+
+/* ---------------------------------------------------------------- encoder (prefill)
+ * replaces: compute_channel_stats   normalize.py:56-61
+ *           encode_keys             codebook.py:116-125
+ *           build_codebook          codebook.py:128-160
+ *           quantize_key_magnitudes quantizer.py:155-170
+ *           quantize_values         quantizer.py:106-140
+ *           the quantisation half of prefill, cache.py:229-245
+ * what: bit0 = compute mu/alpha (else use the given mu64/alpha64), bit1 = pack + codebook.
+ * bits: 1, 2, 4, 8, or 0 for lossless (codes + codebook only).  codes_in (nullable) replaces
+ * the computed sign codes for the codebook (build_codebook(keys_norm, codes)). */
+size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim);
+int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
+                int64_t dim, int bits, int group_size, int sign_in_quant, int what,
+                const uint8_t* codes_in, double* mu64, double* alpha64, float* mu32, float* alpha32,
+                double* cent64, float* cent32, uint8_t* codes_ref, uint8_t* kq_ref,
+                uint16_t* kq_scales, uint16_t* kq_zeros, uint8_t* vq_ref, uint16_t* vq_scales,
+                uint16_t* vq_zeros, uint8_t* signs_fast, uint8_t* recs_fast, void* workspace,
+                size_t workspace_bytes, int* status_dev, void* stream);
+
+/* full-precision rows: out_k = K[idx] - mu (centred), out_v = V[idx]; float32 or float64 out.
+ * replaces: sink_k / sink_v construction, cache.py:247-270 */
+int sikv_gather_rows(const void* keys, const void* values, int in_dtype, int64_t units,
+                     int64_t tokens, int64_t dim, const int32_t* idx, int64_t n,
+                     const double* mu64, void* out_k, void* out_v, int out_f64, void* stream);
+
+/* decode-time append of one token per unit at ring position pos.
+ * replaces: append_token, cache.py:274-287 */
+int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64_t dim,
+                const double* mu64, void* recent_k, void* recent_v, int64_t rcap, int64_t pos,
+                int out_f64, int* status_dev, void* stream);
+
+/* ---------------------------------------------------------------- fused decode step (hot path)
+ * For every unit: q-bar = sum of its gq query heads, LUT + pair-table scoring of all tokens,
+ * exact top-k (ties -> lower index) of the non-sink tokens, and sparse attention of each of
+ * the gq heads over sinks + recents + selected tokens.
+ * replaces, per unit: select_tokens(cache, sum_h q_h, k=k)   cache.py:290-309
+ *                     sparse_attention(q_h, selection, cache) attention.py:52-62 (for each h)
+ * out [U][gq][128] f32; lse (nullable) [U][gq]; sel (nullable) [U][sel_stride] sorted token
+ * indices (sinks U recents U dynamic); sel_count (nullable) [U]; diag (nullable) [U]
+ * (bits0-1 = selection mode, bit2 = exact rescoring fallback ran).
+ * cap = candidate buffer entries (0 = choose); needs sikv_decode_smem_bytes <= 227 KB. */
+int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap);
+int sikv_decode_default_cap(int64_t tokens, int k, int sinks);
+int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
+                     const float* alpha32, const int32_t* sink_idx, int sinks, const float* sink_k,
+                     const float* sink_v, const float* recent_k, const float* recent_v, int64_t rcap,
+                     int recent, const float* q, int64_t units, int64_t tokens, int gq, int k, int cap,
+                     float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
+                     int32_t* diag, void* stream);
+
+/* fast-path float32 scores only (the decode kernel's scoring, for verification / API).
+ * replaces: build_lut + score_tokens on the group-summed query, retrieval.py:46-77 */
+int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq,
+                    int64_t units, int64_t tokens, float* out, void* stream);
+
+/* ---------------------------------------------------------------- reference-exact float64 API
+ * replaces: build_lut retrieval.py:46-51, build_sign_lut retrieval.py:54-62 */
+int sikv_build_lut_f64(const double* q, const double* cent64, int64_t units, int groups,
+                       int sign_only, double* out, void* stream);
+/* replaces: score_tokens retrieval.py:65-77 (numpy pairwise summation order) */
+int sikv_score_f64(const double* lut, const uint8_t* codes_ref, int64_t units, int groups,
+                   int64_t tokens, double* out, void* stream);
+/* replaces: top_k_select retrieval.py:127-161.  forced [U][nforced] = sink U recent indices
+ * (sorted, unique); out [U][out_stride] sorted; counts [U][2] = (total, dynamic). */
+size_t sikv_topk_workspace_bytes(int64_t units, int64_t tokens);
+int sikv_topk(const void* scores, int scores_f32, int64_t units, int64_t tokens,
+              const int32_t* forced, int nforced, int k, void* workspace, int32_t* out,
+              int out_stride, int32_t* counts, void* stream);
+/* replaces: dequantize_values quantizer.py:143-152 (which = 0) and dequantize_keys
+ * quantizer.py:173-184 / direct-key dequant (which = 1) for the given rows */
+int sikv_dequant_rows(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
+                      const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
+                      const uint16_t* vq_zeros, const double* kfull, const double* vfull,
+                      const double* alpha64, int bits, int group_size, int sign_in_quant,
+                      int64_t units, int64_t tokens, int64_t dim, const int64_t* rows, int64_t n,
+                      int which, double* out, void* stream);
+/* replaces: sparse_attention attention.py:52-62 with cache.gather cache.py:118-158, float64.
+ * ws = [U][heads][sel_stride] doubles; out [U][heads][dim]; chk (nullable) [U][heads]. */
+int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
+                    const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
+                    const uint16_t* vq_zeros, const double* kfull, const double* vfull,
+                    const double* alpha64, int bits, int group_size, int sign_in_quant,
+                    int64_t units, int64_t tokens, int64_t dim, const double* q, int heads,
+                    const int32_t* sel, const int32_t* nsel, int sel_stride,
+                    const int32_t* sink_idx, int sinks, const double* sink_k, const double* sink_v,
+                    const double* recent_k, const double* recent_v, int64_t rcap, double* ws,
+                    double* out, double* chk, void* stream);
+/* replaces: apply_normalization normalize.py:64-69 (out = x - mu, float64) */
+int sikv_center(const void* x, int in_dtype, int64_t units, int64_t tokens, int64_t dim,
+                const double* mu64, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIKV_B200_H */

@@ -21,7 +21,7 @@ kept where it decides bits:
   ``einsum("gd,gcd->gc")`` uses on this host (two-lane SIMD accumulation,
   measured in the build container, ``retrieval.py:50``);
 * token scores = numpy ``sum(axis=1)`` (8-way unrolled pairwise sum,
-  ``retrieval.py:77``) — reproduced by calling numpy itself;
+  ``retrieval.py:77``), restated explicitly in :func:`pairwise_rows`;
 * codebook = sequential ``np.add.at`` scatter (``codebook.py:150-151``);
 * float16 parameters = direct float64 -> float16 rounding (``quantizer.py:98-99``).
 """
@@ -306,15 +306,45 @@ def lut(q: np.ndarray, centroids: np.ndarray) -> np.ndarray:
 
 
 def sign_lut(q: np.ndarray, G: int) -> np.ndarray:
-    """Ablation LUT against raw +-1 patterns (retrieval.py:54-62)."""
+    """Ablation LUT against raw +-1 patterns (retrieval.py:54-62).
+
+    The reference's ``(G,4) @ (4,16)`` matmul sums the four exact products
+    left to right for G > 1 and as (a0 + a2) + (a1 + a3) for G == 1 (the
+    matrix-vector BLAS path); both orders measured in the build container."""
     pats = ((np.arange(NCODE)[:, None] >> _SH) & 1).astype(np.float64) * 2 - 1
-    return np.asarray(q, dtype=np.float64).reshape(G, SUB) @ pats.T
+    p = np.asarray(q, dtype=np.float64).reshape(G, 1, SUB) * pats[None]
+    if G == 1:
+        return (p[..., 0] + p[..., 2]) + (p[..., 1] + p[..., 3])
+    return ((p[..., 0] + p[..., 1]) + p[..., 2]) + p[..., 3]
+
+
+def pairwise_rows(x: np.ndarray) -> np.ndarray:
+    """numpy's pairwise row sum for n <= 128 (8 strided accumulators, then a tree,
+    then the remainder left to right) — the order of ``x.sum(axis=1)``."""
+    n = x.shape[1]
+    if n < 8:
+        r = x[:, 0].copy()
+        for i in range(1, n):
+            r = r + x[:, i]
+        return r
+    assert n <= 128
+    acc = [x[:, j].copy() for j in range(8)]
+    i = 8
+    while i < n - (n % 8):
+        for j in range(8):
+            acc[j] = acc[j] + x[:, i + j]
+        i += 8
+    res = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]))
+    while i < n:
+        res = res + x[:, i]
+        i += 1
+    return res
 
 
 def score(table: np.ndarray, codes: np.ndarray) -> np.ndarray:
     """Sum of looked-up entries per token (retrieval.py:65-77)."""
     G = table.shape[0]
-    return table[np.arange(G)[None, :], codes].sum(axis=1)
+    return pairwise_rows(table[np.arange(G)[None, :], codes])
 
 
 def top_k(scores, k: int, sink=(), recent=()) -> tuple[np.ndarray, int, int, int]:

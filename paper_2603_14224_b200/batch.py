@@ -1,0 +1,209 @@
+"""Batched B200 decode path: many decode units (layer x batch x KV head) in one launch.
+
+This is the hot path the benchmark measures.  A :class:`CacheBatch` holds U units that
+share a prefill length L in the fast HBM layout:
+
+* ``signs``  [U, L, 16]  u8   — sign plane (the retrieval index), rotated by t mod 16;
+* ``recs``   [U, L, 128] u8   — per-token record: 2-bit K magnitudes and V in mma.sync
+  fragment order, fp16 (scale, zero) per 32-channel group, K sign words;
+* ``cent32`` [U, 32, 16, 4] f32, ``alpha32`` [U, 128] f32 — codebook and key scale;
+* sinks (first ``sink_count`` positions, cache.py:253-254) and the recent ring as float32
+  centred K' / V rows.
+
+``decode_step`` = per unit ``select_tokens(cache, sum_h q_h, k)`` + ``sparse_attention``
+for every query head of the GQA group (cache.py:290-309, attention.py:52-62), fused.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib as L_
+
+FD = 128
+
+
+@dataclass
+class CacheBatch:
+    units: int
+    tokens: int
+    mu64: torch.Tensor
+    alpha64: torch.Tensor
+    mu32: torch.Tensor
+    alpha32: torch.Tensor
+    cent64: torch.Tensor
+    cent32: torch.Tensor
+    signs: torch.Tensor
+    recs: torch.Tensor
+    sink_idx: torch.Tensor
+    sink_k: torch.Tensor
+    sink_v: torch.Tensor
+    recent_k: torch.Tensor
+    recent_v: torch.Tensor
+    recent: int = 0
+    ref: dict = field(default_factory=dict)   # optional reference-layout planes
+
+    @property
+    def sinks(self) -> int:
+        return int(self.sink_idx.shape[1])
+
+    @property
+    def recent_capacity(self) -> int:
+        return int(self.recent_k.shape[1])
+
+    @property
+    def length(self) -> int:
+        return self.tokens + self.recent
+
+    def fast_bytes(self) -> int:
+        return self.signs.numel() + self.recs.numel()
+
+
+def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacity: int = 0,
+                keep_reference: bool = False, device=None) -> CacheBatch:
+    dev = device or L_.require_cuda()
+    S = min(sink_count, tokens)
+    f32 = dict(device=dev, dtype=torch.float32)
+    f64 = dict(device=dev, dtype=torch.float64)
+    u8 = dict(device=dev, dtype=torch.uint8)
+    cb = CacheBatch(
+        units=units, tokens=tokens,
+        mu64=torch.empty(units, FD, **f64), alpha64=torch.empty(units, FD, **f64),
+        mu32=torch.empty(units, FD, **f32), alpha32=torch.empty(units, FD, **f32),
+        cent64=torch.empty(units, 32, 16, 4, **f64), cent32=torch.empty(units, 32, 16, 4, **f32),
+        signs=torch.empty(units, tokens, 16, **u8), recs=torch.empty(units, tokens, 128, **u8),
+        sink_idx=torch.arange(S, device=dev, dtype=torch.int32).repeat(units, 1),
+        sink_k=torch.empty(units, S, FD, **f32), sink_v=torch.empty(units, S, FD, **f32),
+        recent_k=torch.empty(units, recent_capacity, FD, **f32),
+        recent_v=torch.empty(units, recent_capacity, FD, **f32),
+    )
+    if keep_reference:
+        cb.ref = dict(
+            codes=torch.empty(units, tokens, 16, **u8),
+            kq=torch.empty(units, tokens, 32, **u8), vq=torch.empty(units, tokens, 32, **u8),
+            ks=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
+            kz=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
+            vs=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
+            vz=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
+        )
+    return cb
+
+
+def _sl(t: torch.Tensor | None, u0: int, n: int):
+    return None if t is None else t[u0:u0 + n]
+
+
+def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tensor,
+                 workspace: torch.Tensor | None = None, check: bool = True) -> None:
+    """Compress raw K/V [n, L, 128] (bf16/f32/f64, on device) into units u0..u0+n-1.
+
+    Replaces prefill (cache.py:212-271) with bits=2, group_size=32, sign_in_quant=True
+    and first-S sinks, batched over units."""
+    n, L, D = keys.shape
+    if values.shape != keys.shape:
+        raise ValueError(f"keys and values must match, got {tuple(keys.shape)} and {tuple(values.shape)}")
+    if D != FD or L != cb.tokens:
+        raise ValueError(f"expected [n, {cb.tokens}, {FD}] keys, got {tuple(keys.shape)}")
+    keys = keys.contiguous()
+    values = values.contiguous()
+    dt = L_.dtype_code(keys)
+    if L_.dtype_code(values) != dt:
+        values = values.to(keys.dtype)
+    need = L_.lib().sikv_encode_workspace_bytes(n, L, D)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=keys.device)
+    status = torch.zeros(1, dtype=torch.int32, device=keys.device)
+    r = cb.ref
+    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, 2, 32, 1, 3, None,
+            L_.ptr(_sl(cb.mu64, u0, n)), L_.ptr(_sl(cb.alpha64, u0, n)), L_.ptr(_sl(cb.mu32, u0, n)),
+            L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.cent64, u0, n)), L_.ptr(_sl(cb.cent32, u0, n)),
+            L_.ptr(_sl(r.get("codes"), u0, n)), L_.ptr(_sl(r.get("kq"), u0, n)),
+            L_.ptr(_sl(r.get("ks"), u0, n)), L_.ptr(_sl(r.get("kz"), u0, n)),
+            L_.ptr(_sl(r.get("vq"), u0, n)), L_.ptr(_sl(r.get("vs"), u0, n)),
+            L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)), L_.ptr(_sl(cb.recs, u0, n)),
+            L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
+    S = cb.sinks
+    if S:
+        L_.call("sikv_gather_rows", L_.ptr(keys), L_.ptr(values), dt, n, L, D,
+                L_.ptr(cb.sink_idx[u0:u0 + n].contiguous()), S, L_.ptr(_sl(cb.mu64, u0, n)),
+                L_.ptr(_sl(cb.sink_k, u0, n)), L_.ptr(_sl(cb.sink_v, u0, n)), 0, L_.stream())
+    if check:
+        L_.raise_status(status, "keys")
+
+
+def prefill_batch(keys: torch.Tensor, values: torch.Tensor, *, sink_count: int = 64,
+                  recent_capacity: int = 0, keep_reference: bool = False) -> CacheBatch:
+    U, L, D = keys.shape
+    cb = empty_batch(U, L, sink_count=sink_count, recent_capacity=recent_capacity,
+                     keep_reference=keep_reference, device=keys.device)
+    prefill_into(cb, 0, keys, values)
+    return cb
+
+
+def append_batch(cb: CacheBatch, k: torch.Tensor, v: torch.Tensor) -> None:
+    """append_token for every unit (cache.py:274-287): row pos = cb.recent of the ring."""
+    if cb.recent >= cb.recent_capacity:
+        raise ValueError("recent buffer full")
+    if k.shape != (cb.units, FD) or v.shape != (cb.units, FD):
+        raise ValueError(f"k and v must have shape ({cb.units}, {FD})")
+    k = k.contiguous()
+    v = v.to(k.dtype).contiguous()
+    status = torch.zeros(1, dtype=torch.int32, device=k.device)
+    L_.call("sikv_append", L_.ptr(k), L_.ptr(v), L_.dtype_code(k), cb.units, FD, L_.ptr(cb.mu64),
+            L_.ptr(cb.recent_k), L_.ptr(cb.recent_v), cb.recent_capacity, cb.recent, 0, L_.ptr(status),
+            L_.stream())
+    cb.recent += 1
+
+
+@dataclass
+class DecodeOutput:
+    out: torch.Tensor                 # [U, Gq, 128] float32
+    lse: torch.Tensor | None          # [U, Gq] natural-log partition function of the logits
+    selection: torch.Tensor | None    # [U, stride] int32 sorted indices (first counts[u] valid)
+    counts: torch.Tensor | None       # [U] int32
+    diag: torch.Tensor | None         # [U] int32
+
+
+def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_selection: bool = False,
+                with_lse: bool = False, with_diag: bool = False, out: torch.Tensor | None = None,
+                sel_buf: torch.Tensor | None = None) -> DecodeOutput:
+    """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16)."""
+    U = cb.units
+    if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
+        raise ValueError(f"q must be [{U}, Gq, {FD}], got {tuple(q.shape)}")
+    Gq = q.shape[1]
+    if k < 0:
+        raise ValueError(f"k must be non-negative, got {k}")
+    qf = q if q.dtype == torch.float32 and q.is_contiguous() else q.float().contiguous()
+    dev = q.device
+    if out is None:
+        out = torch.empty(U, Gq, FD, device=dev, dtype=torch.float32)
+    lse = torch.empty(U, Gq, device=dev, dtype=torch.float32) if with_lse else None
+    sel = cnt = None
+    stride = 0
+    if with_selection:
+        stride = cb.sinks + min(k, cb.tokens - cb.sinks) + cb.recent
+        sel = sel_buf if sel_buf is not None else torch.empty(U, max(stride, 1), device=dev, dtype=torch.int32)
+        cnt = torch.empty(U, device=dev, dtype=torch.int32)
+    diag = torch.empty(U, device=dev, dtype=torch.int32) if with_diag else None
+    L_.call("sikv_decode_step", L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
+            L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.sink_k), L_.ptr(cb.sink_v), L_.ptr(cb.recent_k),
+            L_.ptr(cb.recent_v), cb.recent_capacity, cb.recent, L_.ptr(qf), U, cb.tokens, Gq, k, cap,
+            L_.ptr(out), L_.ptr(lse), L_.ptr(sel), max(stride, 1) if sel is not None else 0, L_.ptr(cnt),
+            L_.ptr(diag), L_.stream())
+    return DecodeOutput(out, lse, sel, cnt, diag)
+
+
+def score_fast(cb: CacheBatch, q: torch.Tensor) -> torch.Tensor:
+    """float32 fast-path scores of every prefill token (group-summed query) [U, L]."""
+    qf = q.float().contiguous()
+    out = torch.empty(cb.units, cb.tokens, device=q.device, dtype=torch.float32)
+    L_.call("sikv_score_fast", L_.ptr(cb.signs), L_.ptr(cb.cent32), L_.ptr(qf), q.shape[1], cb.units,
+            cb.tokens, L_.ptr(out), L_.stream())
+    return out
+
+
+def decode_smem_bytes(tokens: int, k: int, sinks: int, gq: int, cap: int = 0) -> int:
+    return L_.lib().sikv_decode_smem_bytes(tokens, k, sinks, gq, cap)

@@ -1,0 +1,285 @@
+// extern "C" boundary of libsikv_b200.so: argument validation, error reporting, launches.
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdio.h>
+#include <string>
+#include <algorithm>
+
+#include "../../include/sikv_b200.h"
+#include "common.cuh"
+#include "api_types.cuh"
+
+namespace sikv {
+// encode.cu
+size_t encode_workspace_bytes(int64_t U, int64_t L, int D);
+cudaError_t launch_encode(const void*, const void*, int, int64_t, int64_t, int, int, int, int, int,
+                          const uint8_t*, double*, double*, float*, float*, double*, float*, uint8_t*,
+                          uint8_t*, __half*, __half*, uint8_t*, __half*, __half*, uint8_t*, uint8_t*, void*,
+                          int*, cudaStream_t);
+cudaError_t launch_gather_rows(const void*, const void*, int, int64_t, int64_t, int, const int32_t*, int,
+                               const double*, void*, void*, int, cudaStream_t);
+cudaError_t launch_append(const void*, const void*, int, int64_t, int, const double*, void*, void*, int64_t,
+                          int64_t, int, int*, cudaStream_t);
+// decode.cu
+DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap);
+cudaError_t launch_decode(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
+                          const float*, const float*, const float*, const float*, int64_t, int, const float*,
+                          int64_t, int64_t, int, int, int, float*, float*, int32_t*, int, int32_t*, int32_t*,
+                          cudaStream_t, int*);
+cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
+                              cudaStream_t);
+// generic.cu
+cudaError_t launch_lut_f64(const double*, const double*, int64_t, int, int, double*, cudaStream_t);
+cudaError_t launch_score_f64(const double*, const uint8_t*, int64_t, int, int64_t, double*, cudaStream_t);
+size_t topk_workspace_bytes(int64_t U, int64_t L);
+cudaError_t launch_topk(const void*, int, int64_t, int64_t, const int32_t*, int, int, void*, int32_t*, int,
+                        int32_t*, cudaStream_t);
+cudaError_t launch_dequant_rows(const RefPlanes&, int64_t, const int64_t*, int64_t, int, double*, cudaStream_t);
+cudaError_t launch_attend_f64(const AttendArgs&, int64_t, cudaStream_t);
+cudaError_t launch_center(const void*, int, int64_t, int64_t, int, const double*, double*, cudaStream_t);
+}  // namespace sikv
+
+using namespace sikv;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_ret(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) { g_err.clear(); return SIKV_OK; }
+  return fail(SIKV_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define REQUIRE(cond, code, msg) \
+  do { if (!(cond)) return fail((code), (msg)); } while (0)
+
+static bool good_dtype(int d) { return d == IN_F32 || d == IN_F64 || d == IN_BF16; }
+static bool good_bits(int b) { return b == 1 || b == 2 || b == 4 || b == 8; }
+static bool good_group(int g) { return g == 4 || g == 8 || g == 16 || g == 32 || g == 64 || g == 128; }
+static int max_smem() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+
+extern "C" {
+
+const char* sikv_last_error(void) { return g_err.c_str(); }
+int sikv_abi_version(void) { return 1; }
+
+size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
+  return encode_workspace_bytes(units, tokens, (int)dim);
+}
+
+int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
+                int64_t dim, int bits, int group_size, int sign_in_quant, int what,
+                const uint8_t* codes_in, double* mu64, double* alpha64, float* mu32, float* alpha32,
+                double* cent64, float* cent32, uint8_t* codes_ref, uint8_t* kq_ref,
+                uint16_t* kq_scales, uint16_t* kq_zeros, uint8_t* vq_ref, uint16_t* vq_scales,
+                uint16_t* vq_zeros, uint8_t* signs_fast, uint8_t* recs_fast, void* workspace,
+                size_t workspace_bytes, int* status_dev, void* stream) {
+  REQUIRE(keys && values && mu64 && alpha64 && status_dev, SIKV_EINVAL, "null required pointer");
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
+  REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "keys must contain at least one row");
+  REQUIRE(dim >= 4 && dim % 4 == 0, SIKV_EINVAL, "channel count must be a positive multiple of 4");
+  REQUIRE(dim <= 128, SIKV_EUNSUPPORTED, "encoder supports dim <= 128");
+  REQUIRE(bits == 0 || good_bits(bits), SIKV_EINVAL, "bits must be one of (1, 2, 4, 8) or 0 (lossless)");
+  REQUIRE(bits == 0 || (good_group(group_size) && dim % group_size == 0), SIKV_EINVAL,
+          "channel count not divisible by group_size (group_size must be 4..128, power of two)");
+  REQUIRE(what >= 1 && what <= 3, SIKV_EINVAL, "what must be 1, 2 or 3");
+  if (what & 2) {
+    REQUIRE(cent64 || cent32, SIKV_EINVAL, "pack needs a centroid output");
+    REQUIRE(workspace && workspace_bytes >= encode_workspace_bytes(units, tokens, (int)dim), SIKV_EINVAL,
+            "workspace too small (sikv_encode_workspace_bytes)");
+  } else {
+    REQUIRE(workspace && workspace_bytes >= encode_workspace_bytes(units, tokens, (int)dim), SIKV_EINVAL,
+            "workspace too small (sikv_encode_workspace_bytes)");
+  }
+  if (signs_fast || recs_fast) {
+    REQUIRE(signs_fast && recs_fast, SIKV_EINVAL, "fast layout needs both signs_fast and recs_fast");
+    REQUIRE(dim == 128 && bits == 2 && group_size == 32 && sign_in_quant, SIKV_EUNSUPPORTED,
+            "fast layout requires dim=128, bits=2, group_size=32, sign_in_quant");
+  }
+  if (kq_ref) REQUIRE(kq_scales && kq_zeros, SIKV_EINVAL, "kq_ref needs scales and zeros");
+  if (vq_ref) REQUIRE(vq_scales && vq_zeros, SIKV_EINVAL, "vq_ref needs scales and zeros");
+  cudaError_t e = launch_encode(keys, values, in_dtype, units, tokens, (int)dim, bits, group_size,
+                                sign_in_quant, what, codes_in, mu64, alpha64, mu32, alpha32, cent64, cent32,
+                                codes_ref, kq_ref, (__half*)kq_scales, (__half*)kq_zeros, vq_ref,
+                                (__half*)vq_scales, (__half*)vq_zeros, signs_fast, recs_fast, workspace,
+                                status_dev, (cudaStream_t)stream);
+  return cuda_ret(e, "sikv_encode");
+}
+
+int sikv_gather_rows(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
+                     int64_t dim, const int32_t* idx, int64_t n, const double* mu64, void* out_k, void* out_v,
+                     int out_f64, void* stream) {
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "bad in_dtype");
+  REQUIRE(n >= 0 && units >= 1 && tokens >= 1 && dim >= 1, SIKV_EINVAL, "bad shape");
+  if (n == 0) return SIKV_OK;
+  REQUIRE(keys && values && idx && mu64 && out_k && out_v, SIKV_EINVAL, "null pointer");
+  return cuda_ret(launch_gather_rows(keys, values, in_dtype, units, tokens, (int)dim, idx, (int)n, mu64, out_k,
+                                     out_v, out_f64, (cudaStream_t)stream),
+                  "sikv_gather_rows");
+}
+
+int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64_t dim, const double* mu64,
+                void* recent_k, void* recent_v, int64_t rcap, int64_t pos, int out_f64, int* status_dev,
+                void* stream) {
+  REQUIRE(k && v && mu64 && recent_k && recent_v && status_dev, SIKV_EINVAL, "null pointer");
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "bad in_dtype");
+  REQUIRE(pos >= 0 && pos < rcap, SIKV_EINVAL, "recent buffer full (pos >= rcap)");
+  return cuda_ret(launch_append(k, v, in_dtype, units, (int)dim, mu64, recent_k, recent_v, rcap, pos, out_f64,
+                                status_dev, (cudaStream_t)stream),
+                  "sikv_append");
+}
+
+int sikv_decode_default_cap(int64_t tokens, int k, int sinks) {
+  const int64_t ncand = std::max<int64_t>(tokens - sinks, 0);
+  const int64_t keff = std::min<int64_t>(k, ncand);
+  int64_t cap = 2 * keff + 1024;
+  cap = std::max<int64_t>(cap, 1024);
+  return (int)std::min<int64_t>(cap, std::max<int64_t>(ncand, 1024));
+}
+
+int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap) {
+  if (cap <= 0) cap = sikv_decode_default_cap(tokens, k, sinks);
+  return decode_layout(tokens, k, sinks, gq, cap).total;
+}
+
+int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
+                     const float* alpha32, const int32_t* sink_idx, int sinks, const float* sink_k,
+                     const float* sink_v, const float* recent_k, const float* recent_v, int64_t rcap,
+                     int recent, const float* q, int64_t units, int64_t tokens, int gq, int k, int cap,
+                     float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag,
+                     void* stream) {
+  REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
+  REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
+  REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
+  REQUIRE(gq >= 1 && gq <= 8, SIKV_EUNSUPPORTED, "fast decode supports 1..8 query heads per KV head");
+  REQUIRE(k >= 0, SIKV_EINVAL, "k must be non-negative");
+  REQUIRE(sinks >= 0 && sinks <= tokens, SIKV_EINVAL, "sink count out of range");
+  REQUIRE(sinks == 0 || (sink_idx && sink_k && sink_v), SIKV_EINVAL, "sinks need sink_idx/sink_k/sink_v");
+  REQUIRE(recent >= 0 && recent <= rcap, SIKV_EINVAL, "recent count out of range");
+  REQUIRE(recent == 0 || (recent_k && recent_v), SIKV_EINVAL, "recents need recent_k/recent_v");
+  const int64_t keff = std::min<int64_t>(k, tokens - sinks);
+  REQUIRE(sinks + keff + recent >= 1, SIKV_EINVAL, "selection is empty");
+  REQUIRE(!sel || sel_stride >= sinks + keff + recent, SIKV_EINVAL, "sel_stride too small");
+  if (cap <= 0) cap = sikv_decode_default_cap(tokens, k, sinks);
+  int need = decode_layout(tokens, k, sinks, gq, cap).total;
+  REQUIRE(need <= max_smem(), SIKV_EUNSUPPORTED,
+          "decode shared-memory footprint " + std::to_string(need) + " B exceeds the device limit");
+  int smem = 0;
+  cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, sink_k, sink_v, recent_k,
+                                recent_v, rcap, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride,
+                                sel_count, diag, (cudaStream_t)stream, &smem);
+  return cuda_ret(e, "sikv_decode_step");
+}
+
+int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq, int64_t units,
+                    int64_t tokens, float* out, void* stream) {
+  REQUIRE(signs_fast && cent32 && q && out, SIKV_EINVAL, "null pointer");
+  REQUIRE(gq >= 1 && units >= 1 && tokens >= 1, SIKV_EINVAL, "bad shape");
+  return cuda_ret(launch_score_fast(signs_fast, cent32, q, gq, units, tokens, out, (cudaStream_t)stream),
+                  "sikv_score_fast");
+}
+
+int sikv_build_lut_f64(const double* q, const double* cent64, int64_t units, int groups, int sign_only,
+                       double* out, void* stream) {
+  REQUIRE(q && out && (sign_only || cent64), SIKV_EINVAL, "null pointer");
+  REQUIRE(groups >= 1 && units >= 1, SIKV_EINVAL, "bad shape");
+  return cuda_ret(launch_lut_f64(q, cent64, units, groups, sign_only, out, (cudaStream_t)stream),
+                  "sikv_build_lut_f64");
+}
+
+int sikv_score_f64(const double* lut, const uint8_t* codes_ref, int64_t units, int groups, int64_t tokens,
+                   double* out, void* stream) {
+  REQUIRE(lut && codes_ref && out, SIKV_EINVAL, "null pointer");
+  REQUIRE(groups >= 1 && groups <= 128, SIKV_EUNSUPPORTED, "groups must be 1..128");
+  return cuda_ret(launch_score_f64(lut, codes_ref, units, groups, tokens, out, (cudaStream_t)stream),
+                  "sikv_score_f64");
+}
+
+size_t sikv_topk_workspace_bytes(int64_t units, int64_t tokens) { return topk_workspace_bytes(units, tokens); }
+
+int sikv_topk(const void* scores, int scores_f32, int64_t units, int64_t tokens, const int32_t* forced,
+              int nforced, int k, void* workspace, int32_t* out, int out_stride, int32_t* counts, void* stream) {
+  REQUIRE(scores && workspace && out && counts, SIKV_EINVAL, "null pointer");
+  REQUIRE(k >= 0, SIKV_EINVAL, "k must be non-negative");
+  REQUIRE(nforced >= 0 && (nforced == 0 || forced), SIKV_EINVAL, "bad forced list");
+  REQUIRE(tokens >= 0 && tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
+  const int64_t need = std::min<int64_t>(k, tokens - nforced) + nforced;
+  REQUIRE(out_stride >= need, SIKV_EINVAL, "out_stride too small");
+  if (tokens == 0) return SIKV_OK;
+  return cuda_ret(launch_topk(scores, scores_f32, units, tokens, forced, nforced, k, workspace, out, out_stride,
+                              counts, (cudaStream_t)stream),
+                  "sikv_topk");
+}
+
+static RefPlanes make_planes(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
+                             const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
+                             const uint16_t* vq_zeros, const double* kfull, const double* vfull,
+                             const double* alpha64, int bits, int gs, int siq, int64_t L, int64_t D) {
+  RefPlanes p{codes_ref, kq_ref, (const __half*)kq_scales, (const __half*)kq_zeros, vq_ref,
+              (const __half*)vq_scales, (const __half*)vq_zeros, kfull, vfull, alpha64, bits, gs, siq,
+              (int)D, L};
+  return p;
+}
+
+static int check_planes(const RefPlanes& p) {
+  if (p.bits == 16) {
+    REQUIRE(p.kfull && p.vfull, SIKV_EINVAL, "lossless planes missing");
+  } else {
+    REQUIRE(good_bits(p.bits) && good_group(p.gs) && p.D % p.gs == 0, SIKV_EINVAL, "bad bits/group_size");
+    REQUIRE(p.kq && p.ks && p.kz && p.vq && p.vs && p.vz, SIKV_EINVAL, "quantized planes missing");
+    REQUIRE(!p.siq || (p.codes && p.alpha), SIKV_EINVAL, "sign codes / alpha missing");
+  }
+  return SIKV_OK;
+}
+
+int sikv_dequant_rows(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
+                      const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
+                      const uint16_t* vq_zeros, const double* kfull, const double* vfull, const double* alpha64,
+                      int bits, int group_size, int sign_in_quant, int64_t units, int64_t tokens, int64_t dim,
+                      const int64_t* rows, int64_t n, int which, double* out, void* stream) {
+  RefPlanes p = make_planes(codes_ref, kq_ref, kq_scales, kq_zeros, vq_ref, vq_scales, vq_zeros, kfull, vfull,
+                            alpha64, bits, group_size, sign_in_quant, tokens, dim);
+  if (which == 0 && bits != 16) {
+    REQUIRE(vq_ref && vq_scales && vq_zeros, SIKV_EINVAL, "value planes missing");
+  } else {
+    int rc = check_planes(p);
+    if (rc) return rc;
+  }
+  REQUIRE(n >= 0 && (n == 0 || (rows && out)), SIKV_EINVAL, "bad rows");
+  return cuda_ret(launch_dequant_rows(p, units, rows, n, which, out, (cudaStream_t)stream), "sikv_dequant_rows");
+}
+
+int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
+                    const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
+                    const uint16_t* vq_zeros, const double* kfull, const double* vfull, const double* alpha64,
+                    int bits, int group_size, int sign_in_quant, int64_t units, int64_t tokens, int64_t dim,
+                    const double* q, int heads, const int32_t* sel, const int32_t* nsel, int sel_stride,
+                    const int32_t* sink_idx, int sinks, const double* sink_k, const double* sink_v,
+                    const double* recent_k, const double* recent_v, int64_t rcap, double* ws, double* out,
+                    double* chk, void* stream) {
+  RefPlanes p = make_planes(codes_ref, kq_ref, kq_scales, kq_zeros, vq_ref, vq_scales, vq_zeros, kfull, vfull,
+                            alpha64, bits, group_size, sign_in_quant, tokens, dim);
+  int rc = check_planes(p);
+  if (rc) return rc;
+  REQUIRE(q && sel && nsel && ws && out && heads >= 1, SIKV_EINVAL, "null pointer");
+  REQUIRE(sinks == 0 || (sink_idx && sink_k && sink_v), SIKV_EINVAL, "sink rows missing");
+  AttendArgs a{p, q, heads, sel, nsel, sel_stride, sink_idx, sinks, sink_k, sink_v, recent_k, recent_v,
+               rcap, ws, out, chk};
+  return cuda_ret(launch_attend_f64(a, units, (cudaStream_t)stream), "sikv_attend_f64");
+}
+
+int sikv_center(const void* x, int in_dtype, int64_t units, int64_t tokens, int64_t dim, const double* mu64,
+                double* out, void* stream) {
+  REQUIRE(x && mu64 && out, SIKV_EINVAL, "null pointer");
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "bad in_dtype");
+  return cuda_ret(launch_center(x, in_dtype, units, tokens, (int)dim, mu64, out, (cudaStream_t)stream),
+                  "sikv_center");
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Shared device helpers for the self-indexing KV-cache kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace sikv {
+
+// ------------------------------------------------------------------ input dtypes
+enum InDType : int { IN_F32 = 0, IN_F64 = 1, IN_BF16 = 2 };
+
+__device__ __forceinline__ double load_in(const void* p, int dt, int64_t i) {
+  if (dt == IN_F64) return reinterpret_cast<const double*>(p)[i];
+  if (dt == IN_F32) return (double)reinterpret_cast<const float*>(p)[i];
+  return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+}
+
+// ------------------------------------------------------------------ order-preserving keys
+// float -> uint32 with the same ordering; -0.0 is canonicalised to +0.0 first so
+// that ties between -0 and +0 break by index exactly like numpy's stable argsort.
+__device__ __forceinline__ uint32_t f32_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (u == 0x80000000u) u = 0u;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ uint64_t f64_key(double f) {
+  uint64_t u = (uint64_t)__double_as_longlong(f);
+  if (u == 0x8000000000000000ull) u = 0ull;
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// ------------------------------------------------------------------ fast-layout constants
+// D = 128 channels, 32 sign groups (16 packed bytes), 4 quant groups of 32 channels.
+constexpr int FD = 128;
+constexpr int FSIGN = 16;      // bytes per token in the sign plane
+constexpr int FREC = 128;      // bytes per token record
+// record byte offsets
+constexpr int R_KPAY = 0;      // 32 B K magnitude payload, MMA-permuted
+constexpr int R_VPAY = 32;     // 32 B V payload, MMA-permuted
+constexpr int R_KPAR = 64;     // 4 x (qs, zp) fp16
+constexpr int R_VPAR = 80;     // 4 x (qs, zp) fp16
+constexpr int R_KSGN = 96;     // 4 x u32 negative-sign words, MMA-permuted
+
+// ---- K payload permutation (B operand of q~ K^T, m16n8k16, one token per n column)
+// thread t4 of a quad owns words 2*t4 + u (u = 0,1).  Slot i (0..7) of word u holds
+// pair (s = 4u + (i>>1), e = i&1): lo half bits [2i,2i+2) = channel 16s+2t4+8e,
+// hi half bits [16+2i, 16+2i+2) = channel 16s+2t4+8e+1.
+__host__ __device__ __forceinline__ void kpay_pos(int ch, int& word, int& bit) {
+  int s = ch >> 4, r = ch & 15;
+  int e = (r >> 3) & 1, rr = r & 7;        // rr = 2*t4 + hi
+  int t4 = rr >> 1, hi = rr & 1;
+  int u = s >> 2, i = ((s & 3) << 1) | e;
+  word = 2 * t4 + u;
+  bit = 2 * i + 16 * hi;
+}
+// ---- K sign permutation: word t4, pair P = 8u + i  -> lo sign at bit P, hi at 16+P
+__host__ __device__ __forceinline__ void ksgn_pos(int ch, int& word, int& bit) {
+  int s = ch >> 4, r = ch & 15;
+  int e = (r >> 3) & 1, rr = r & 7;
+  int t4 = rr >> 1, hi = rr & 1;
+  int u = s >> 2, i = ((s & 3) << 1) | e;
+  word = t4;
+  bit = 8 * u + i + 16 * hi;
+}
+// ---- V payload permutation (A operand of V^T P^T, m16n8k16, one channel per m row)
+// word g (0..7) holds channels 16m + g + 8e (m = 0..7, e = 0,1):
+// byte j = m>>1, bits [2i', 2i'+2) with i' = 2*(m&1) + e.
+__host__ __device__ __forceinline__ void vpay_pos(int ch, int& word, int& bit) {
+  int m = ch >> 4, r = ch & 15;
+  int g = r & 7, e = r >> 3;
+  word = g;
+  bit = 8 * (m >> 1) + 2 * (2 * (m & 1) + e);
+}
+
+// ------------------------------------------------------------------ warp helpers
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ mma.sync m16n8k16 f16 -> f32
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic) {
+  // (a & mask) | magic
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(mask), "r"(magic));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3_xor_and(uint32_t v, uint32_t s, uint32_t mask) {
+  // v ^ (s & mask)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(r) : "r"(v), "r"(s), "r"(mask));
+  return r;
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+}  // namespace sikv
