@@ -34,6 +34,6 @@ struct AttendArgs {
   double* chk;              // [U][H]
 };
 
-struct DecodeLayout { int off_cand, off_samp, off_forced, off_misc, off_lists, total, nsamp; };
+struct DecodeLayout { int off_cand, off_forced, off_misc, off_bits, off_dyn, off_stage, total, capw; };
 
 }  // namespace sikv

@@ -136,11 +136,14 @@ int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64
 }
 
 int sikv_decode_default_cap(int64_t tokens, int k, int sinks) {
+  // Candidate buffer: ~2k + 1024 entries, shrunk (not below ~1.4k + 512) so that two CTAs
+  // fit on one SM (2 x 113 KB) when possible.
   const int64_t ncand = std::max<int64_t>(tokens - sinks, 0);
   const int64_t keff = std::min<int64_t>(k, ncand);
-  int64_t cap = 2 * keff + 1024;
-  cap = std::max<int64_t>(cap, 1024);
-  return (int)std::min<int64_t>(cap, std::max<int64_t>(ncand, 1024));
+  int64_t cap = std::max<int64_t>(2 * keff + 1024, 1024);
+  const int64_t floor_cap = std::max<int64_t>(keff + keff * 2 / 5 + 512, 1024);
+  while (cap > floor_cap && decode_layout(tokens, k, sinks, 8, (int)cap).total > 113 * 1024) cap -= 64;
+  return (int)cap;
 }
 
 int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap) {

@@ -9,9 +9,10 @@ constexpr int DW = DT / 32;
 
 // ---------------------------------------------------------------- small block utilities
 struct Misc {                      // scalars in shared memory
-  int ncand, nsv, digit, rem_sel, cnt_above, total, fb;
-  uint32_t tau;
+  int ncand, nsv, digit, rem_sel, cnt_above, total, fb, bad;
+  uint32_t tau, maxx;
   int wsum[DW * 2];
+  int wcnt[DW];                    // per-warp candidate counts
 };
 
 __device__ __forceinline__ void block_exscan2(int a, int b, int& ea, int& eb, int& ta, int& tb,
@@ -63,6 +64,66 @@ __device__ __forceinline__ void pick_digit(const int* hist, Misc* ms) {
       c += loc[i];
     }
   }
+}
+
+// ---------------------------------------------------------------- 12-bit radix k-th selection
+constexpr int RB = 12;              // digit bits per pass
+constexpr int NBIN = 1 << RB;       // 4096 bins; thread t owns bins [NBIN-16(t+1), NBIN-16t)
+
+// Block-wide: choose the digit whose descending cumulative count reaches ms->rem_sel.
+__device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
+  const int tid = threadIdx.x;
+  int loc[NBIN / DT], s = 0;
+#pragma unroll
+  for (int i = 0; i < NBIN / DT; ++i) { loc[i] = hist[NBIN - 1 - (NBIN / DT) * tid - i]; s += loc[i]; }
+  int exc, d0, tot, d1;
+  block_exscan2(s, 0, exc, d0, tot, d1, ms->wsum);
+  const int rem = ms->rem_sel;
+  if (exc < rem && rem <= exc + s) {
+    int c = exc;
+#pragma unroll
+    for (int i = 0; i < NBIN / DT; ++i) {
+      if (c < rem && rem <= c + loc[i]) { ms->digit = NBIN - 1 - (NBIN / DT) * tid - i; ms->cnt_above = c; }
+      c += loc[i];
+    }
+  }
+  __syncthreads();
+}
+
+// Exact k-th largest of a multiset of 32-bit values x (all <= maxx).  `each(f)` must call
+// f(x) once per item on the calling thread (every thread calls each()).  Returns the k-th
+// value and how many items equal to it belong to the top `rank` (ties are then resolved by
+// index by the caller).  hist must hold NBIN ints.  Contains __syncthreads.
+template <typename Each>
+__device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, int* hist, Misc* ms,
+                                          uint32_t& kth, int& need_eq) {
+  const int tid = threadIdx.x;
+  const int nbits = maxx ? 32 - __clz(maxx) : 0;
+  if (tid == 0) ms->rem_sel = rank;
+  uint32_t prefix = 0;
+  int shift = nbits;
+  __syncthreads();
+  while (shift > 0) {
+    const int dbits = shift >= RB ? RB : shift;
+    const int hi = shift;            // bits >= hi are already fixed in prefix
+    shift -= dbits;
+    for (int i = tid; i < NBIN; i += DT) hist[i] = 0;
+    __syncthreads();
+    const uint32_t want = hi >= 32 ? 0u : (prefix >> hi);
+    const int sh = shift;
+    each([&](uint32_t x) {
+      if ((hi >= 32 ? 0u : (x >> hi)) == want) atomicAdd(&hist[(x >> sh) & (NBIN - 1)], 1);
+    });
+    __syncthreads();
+    pick_digit_big(hist, ms);
+    prefix |= (uint32_t)ms->digit << shift;
+    __syncthreads();
+    if (tid == 0) ms->rem_sel -= ms->cnt_above;
+    __syncthreads();
+  }
+  kth = prefix;
+  need_eq = ms->rem_sel;
+  __syncthreads();
 }
 
 }  // namespace sikv
