@@ -97,6 +97,10 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
                      int32_t* diag, void* stream);
 
+/* debug: per-unit phase clocks [U][12] int64 (clock64 at phase boundaries) for every
+ * subsequent sikv_decode_step; NULL disables. */
+int sikv_debug_set_decode_profile(void* clocks);
+
 /* fast-path float32 scores only (the decode kernel's scoring, for verification / API).
  * replaces: build_lut + score_tokens on the group-summed query, retrieval.py:46-77 */
 int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq,

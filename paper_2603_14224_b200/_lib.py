@@ -35,6 +35,7 @@ _SIGS = {
     "sikv_decode_step": (I, [P, P, P, P, P, I, P, P, P, P, I64, I, P, I64, I64, I, I, I, P, P, P, I, P,
                              P, P]),
     "sikv_score_fast": (I, [P, P, P, I, I64, I64, P, P]),
+    "sikv_debug_set_decode_profile": (I, [P]),
     "sikv_build_lut_f64": (I, [P, P, I64, I, I, P, P]),
     "sikv_score_f64": (I, [P, P, I64, I, I64, P, P]),
     "sikv_topk_workspace_bytes": (SZ, [I64, I64]),

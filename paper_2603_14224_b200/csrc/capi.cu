@@ -28,6 +28,7 @@ cudaError_t launch_decode(const uint8_t*, const uint8_t*, const float*, const fl
                           cudaStream_t, int*);
 cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
                               cudaStream_t);
+cudaError_t set_decode_profile(long long*);
 // generic.cu
 cudaError_t launch_lut_f64(const double*, const double*, int64_t, int, int, double*, cudaStream_t);
 cudaError_t launch_score_f64(const double*, const uint8_t*, int64_t, int, int64_t, double*, cudaStream_t);
@@ -178,6 +179,10 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                                 recent_v, rcap, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride,
                                 sel_count, diag, (cudaStream_t)stream, &smem);
   return cuda_ret(e, "sikv_decode_step");
+}
+
+int sikv_debug_set_decode_profile(void* clocks) {
+  return cuda_ret(set_decode_profile((long long*)clocks), "sikv_debug_set_decode_profile");
 }
 
 int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq, int64_t units,

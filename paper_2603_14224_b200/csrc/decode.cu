@@ -24,6 +24,8 @@ namespace sikv {
 
 constexpr int TBL_BYTES = 256 * 64 * 4;   // pair table: 256 byte values x 64 columns
 
+__device__ long long* g_prof = nullptr;   // optional per-unit phase clocks (debug / profiling)
+
 constexpr int NB = 8;                     // chunks (of 256 tokens) scored per thread per batch
 constexpr int STAGE_BYTES = 16 * FREC;    // one 16-token block of records
 constexpr int MAX_SAMPLE_CHUNKS = 8;
@@ -64,6 +66,21 @@ __device__ __forceinline__ float score_token(const uint4 w, uint32_t lb, const c
     s = (i == 0) ? v : __fadd_rn(s, v);
   }
   return s;
+}
+
+// NB tokens at once: the 16-step chains of different tokens interleave, hiding FADD latency
+template <int N>
+__device__ __forceinline__ void score_batch(const uint4 (&w)[N], uint32_t lb, const char* T, float (&s)[N]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+#pragma unroll
+    for (int x = 0; x < N; ++x) {
+      const uint32_t wd = (i >> 2) == 0 ? w[x].x : (i >> 2) == 1 ? w[x].y : (i >> 2) == 2 ? w[x].z : w[x].w;
+      const uint32_t off = prmt(wd, lb, 0x5504u | ((uint32_t)(i & 3) << 4));
+      const float v = *reinterpret_cast<const float*>(T + off + 4 * i);
+      s[x] = (i == 0) ? v : __fadd_rn(s[x], v);
+    }
+  }
 }
 
 __device__ __forceinline__ bool forced_bit(const uint32_t* fb, int64_t t) {
@@ -116,6 +133,9 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   // ---------------- A: queries, LUT, pair table, forced bitmap
   for (int i = tid; i < Gq * FD; i += DT) qs[i] = a.q[u * Gq * FD + i];
   for (int i = tid; i < W; i += DT) forced[i] = 0u;
+  long long* prof = g_prof ? g_prof + u * 12 : nullptr;
+#define PROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
+  PROF(0);
   if (tid == 0) { ms->fb = 0; ms->maxx = 0; ms->bad = 0; }
   __syncthreads();
   for (int j = tid; j < S; j += DT) {
@@ -151,6 +171,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   __syncthreads();
 
   const int64_t ncand_all = L - S;
+  const int64_t flim = S > 0 ? (int64_t)a.sink_idx[u * S + S - 1] + 1 : 0;   // sinks are sorted
   const int keff = (int)((int64_t)a.k < ncand_all ? (int64_t)a.k : ncand_all);
   const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
   const int nchunks = (int)((L + 255) >> 8);
@@ -173,14 +194,29 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   uint32_t* seg = cand + 2 * warp * capw;
   int wc = 0;                  // warp-uniform fill count
   uint32_t mx = 0;             // per-thread max x
-  auto push = [&](bool pred, uint32_t x, uint32_t t) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    if (pred) {
-      const int pos = wc + __popc(m & ((1u << lane) - 1));
-      if (pos < capw) { seg[2 * pos] = x; seg[2 * pos + 1] = t; }
-      mx = max(mx, x);
+  // warp-compacted append of this thread's flagged tokens (bit x of `bits` <-> sv[x], token
+  // t0 + 256 x); one warp scan per batch instead of one ballot per token
+  auto push_batch = [&](uint32_t bits, const float* sv, int nb, int t0, uint32_t tau) {
+    const int cnt = __popc(bits);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
     }
-    wc += __popc(m);
+    int pos = wc + inc - cnt;
+    wc += __shfl_sync(0xffffffffu, inc, 31);
+    while (bits) {
+      const int x = __ffs(bits) - 1;
+      bits &= bits - 1;
+      float v = sv[0];
+#pragma unroll
+      for (int y = 1; y < NB; ++y) v = (x == y) ? sv[y] : v;
+      const uint32_t xk = f32_key(v) - tau;
+      if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(t0 + 256 * x); }
+      mx = max(mx, xk);
+      ++pos;
+    }
   };
 
   bool fallback = false;
@@ -188,6 +224,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     uint32_t tau = 1;
     int sstride = 1, nsc = 0;
     if (mode == 3) {
+      PROF(1);
       // ---------------- B1: score the sample chunks (<= 8 per thread, kept in registers)
       sstride = max(16, (nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS);
       nsc = (nchunks + sstride - 1) / sstride;
@@ -198,13 +235,15 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
         const int64_t t = (int64_t)x * sstride * 256 + tid;
         w[x] = (x < nsc && t < L) ? __ldg(signs + t) : make_uint4(0, 0, 0, 0);
       }
+      float sv[MAX_SAMPLE_CHUNKS];
+      score_batch(w, lb, T, sv);
       int nv = 0;
       uint32_t smax = 0;
 #pragma unroll
       for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
         const int64_t t = (int64_t)x * sstride * 256 + tid;
         uint32_t key = 0;
-        if (x < nsc && t < L && !forced_bit(forced, t)) key = f32_key(score_token(w[x], lb, T));
+        if (x < nsc && t < L && !(t < flim && forced_bit(forced, t))) key = f32_key(sv[x]);
         sk[x] = key;
         nv += key != 0;
         smax = max(smax, key);
@@ -231,31 +270,70 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
       }
       if (tid == 0) ms->maxx = 0;
       __syncthreads();
+      {
+        const int cnt_s = 0;
+        (void)cnt_s;
+        uint32_t bits = 0;
 #pragma unroll
-      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-        const int64_t t = (int64_t)x * sstride * 256 + tid;
-        push(x < nsc && sk[x] != 0 && sk[x] >= tau, sk[x] - tau, (uint32_t)t);
+        for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x)
+          if (x < nsc && sk[x] != 0 && sk[x] >= tau) bits |= 1u << x;
+        int cnt = __popc(bits), inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += v;
+        }
+        int pos = wc + inc - cnt;
+        wc += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+        for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+          if ((bits >> x) & 1u) {
+            const uint32_t xk = sk[x] - tau;
+            if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(x * sstride * 256 + tid); }
+            mx = max(mx, xk);
+            ++pos;
+          }
+        }
       }
     }
-    // ---------------- B2: score everything else, keep key >= tau
+    PROF(2);
+    // ---------------- B2: score everything else, keep score >= tau (compared as floats)
+    float tauf;
+    {
+      const uint32_t k2 = tau;
+      tauf = mode == 2 ? -INFINITY : __uint_as_float((k2 & 0x80000000u) ? (k2 & 0x7FFFFFFFu) : ~k2);
+    }
+    const int Li = (int)L;
     for (int c0 = 0; c0 < nchunks; c0 += NB) {
+      int xs = -1;                  // the (at most one, sstride >= 16 > NB) sample chunk here
+      if (mode == 3) {
+        const int cs = ((c0 + sstride - 1) / sstride) * sstride;
+        if (cs < c0 + NB && cs / sstride < nsc) xs = cs - c0;
+      }
+      const int t0 = c0 * 256 + tid;
+      const bool full = (c0 + NB) * 256 <= Li;
       uint4 w[NB];
+      if (full) {
 #pragma unroll
-      for (int x = 0; x < NB; ++x) {
-        const int c = c0 + x;
-        const int64_t t = (int64_t)c * 256 + tid;
-        const bool skip = c >= nchunks || (mode == 3 && c % sstride == 0 && c / sstride < nsc);
-        w[x] = (!skip && t < L) ? __ldg(signs + t) : make_uint4(0, 0, 0, 0);
-      }
+        for (int x = 0; x < NB; ++x) w[x] = __ldg(signs + t0 + 256 * x);
+      } else {
 #pragma unroll
-      for (int x = 0; x < NB; ++x) {
-        const int c = c0 + x;
-        const bool skip = c >= nchunks || (mode == 3 && c % sstride == 0 && c / sstride < nsc);
-        const int64_t t = (int64_t)c * 256 + tid;
-        uint32_t key = 0;
-        if (!skip && t < L && !forced_bit(forced, t)) key = f32_key(score_token(w[x], lb, T));
-        push(key != 0 && key >= tau, key - tau, (uint32_t)t);
+        for (int x = 0; x < NB; ++x) w[x] = t0 + 256 * x < Li ? __ldg(signs + t0 + 256 * x) : make_uint4(0, 0, 0, 0);
       }
+      float sv[NB];
+      score_batch(w, lb, T, sv);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int x = 0; x < NB; ++x)
+        if (sv[x] >= tauf) bits |= 1u << x;
+      if (xs >= 0) bits &= ~(1u << xs);
+      if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NB ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
+      if (c0 * 256 < flim) {
+#pragma unroll
+        for (int x = 0; x < NB; ++x)
+          if (t0 + 256 * x < Li && forced_bit(forced, t0 + 256 * x)) bits &= ~(1u << x);
+      }
+      push_batch(bits, sv, NB, t0, tau);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -265,6 +343,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     for (int w2 = 0; w2 < DW; ++w2) total += ms->wcnt[w2];
     fallback = ms->bad || total < keff;
     if (!fallback) {
+      PROF(3);
       // ---------------- C: exact k-th key among the candidates (pair table is dead now)
       const int n = wc;   // this warp's segment
       uint32_t xk;
@@ -310,6 +389,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     __syncthreads();
   }
 
+  PROF(4);
   // ---------------- ordered scan: dynamic list (smem) + sorted selection (global)
   int32_t* dyn = reinterpret_cast<int32_t*>(sm + a.off_dyn);
   {
@@ -358,6 +438,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   __syncthreads();
   const int ndyn = ms->total;
 
+  PROF(5);
   // ---------------- D: sparse attention over forced rows + dynamic rows
   const int g = lane >> 2, t4 = lane & 3;
   uint32_t qa[8][2];       // q~ = q * alpha-hat, fp16 A fragments (row g = head g)
@@ -457,6 +538,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     });
   }
 
+  PROF(6);
   // -- dynamic rows: cp.async double-buffered staging, dequantised into mma fragments
   const int first = (warp - nbf % DW + DW) % DW;   // this warp's first dynamic block
   if (first < nbd) stage_block(stage, recs, dyn, first * 16, ndyn, lane);
@@ -533,8 +615,10 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   }
   cp_wait<0>();
 
+  PROF(7);
   // ---------------- merge the 8 warp partials (fixed order)
   __syncthreads();
+  PROF(8);
   float* part = reinterpret_cast<float*>(cand);           // [DW][Gq][128]
   float* pm = part + DW * Gq * FD;                         // [DW][Gq]
   float* pl = pm + DW * Gq;                                // [DW][Gq]
@@ -565,6 +649,8 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     a.out[(u * Gq + h) * FD + d] = num / den;
     if (a.lse && d == 0) a.lse[u * Gq + h] = (M + log2f(den)) * 0.6931471805599453f;
   }
+  PROF(9);
+#undef PROF
 }
 
 // ---------------------------------------------------------------- scores only (tests / API)
@@ -645,6 +731,10 @@ cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float
   if (e != cudaSuccess) return e;
   decode_step_kernel<<<(unsigned)U, DT, d.total, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t set_decode_profile(long long* p) {
+  return cudaMemcpyToSymbol(g_prof, &p, sizeof(p));
 }
 
 cudaError_t launch_score_fast(const uint8_t* signs, const float* cent32, const float* q, int Gq,

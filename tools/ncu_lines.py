@@ -1,4 +1,5 @@
-"""Per-CUDA-line stall samples from `ncu --page source --csv --print-source cuda,sass`."""
+"""Per-CUDA-line stall samples and executed instructions from
+`ncu --page source --csv --print-source cuda,sass`."""
 import csv
 import sys
 
@@ -17,11 +18,14 @@ for r in rows:
         continue
     try:
         s = float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0)
+        n = float(r[hdr["Instructions Executed"]] or 0)
     except (ValueError, IndexError):
         continue
-    out.append((s, fname, r[0], r[1]))
+    out.append((s, n, fname, r[0], r[1]))
 tot = sum(x[0] for x in out)
-print("total", tot)
+ntot = sum(x[1] for x in out)
+print(f"total samples {tot:.0f}, warp-instructions {ntot:.0f}")
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-for s, f, ln, src in sorted(out, key=lambda x: -x[0])[:n]:
-    print(f"{100*s/tot:5.1f}% {f}:{ln:5s} {src.strip()[:100]}")
+key = 1 if len(sys.argv) > 3 and sys.argv[3] == "inst" else 0
+for s, ni, f, ln, src in sorted(out, key=lambda x: -x[key])[:n]:
+    print(f"{100*s/tot:5.1f}% {100*ni/ntot:5.1f}%i {f}:{ln:5s} {src.strip()[:95]}")
