@@ -91,11 +91,20 @@ int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64
 int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap);
 int sikv_decode_default_cap(int64_t tokens, int k, int sinks);
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
-                     const float* alpha32, const int32_t* sink_idx, int sinks, const float* sink_k,
-                     const float* sink_v, const float* recent_k, const float* recent_v, int64_t rcap,
-                     int recent, const float* q, int64_t units, int64_t tokens, int gq, int k, int cap,
-                     float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                     int32_t* diag, void* stream);
+                     const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
+                     int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq,
+                     int k, int cap, float* out, float* lse, int32_t* sel, int sel_stride,
+                     int32_t* sel_count, int32_t* diag, void* stream);
+
+/* forced rows (sinks then recents; float32 centred K' and V) -> the decode kernel's fp16
+ * mma-fragment blocks of 16 rows: forced_frag [U][frag_blocks][2][32][32] u32.  Re-packs the
+ * blocks covering rows [row_begin, row_end); rows >= sinks + recent are zero.
+ * replaces: the full-precision sink / recent rows of cache.gather, cache.py:137-144 */
+int sikv_forced_blocks(int sinks, int64_t rcap);
+int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const float* recent_k,
+                     const float* recent_v, int64_t rcap, int recent, const float* alpha32,
+                     int64_t units, uint32_t* forced_frag, int frag_blocks, int row_begin,
+                     int row_end, void* stream);
 
 /* debug: per-unit phase clocks [U][12] int64 (clock64 at phase boundaries) for every
  * subsequent sikv_decode_step; NULL disables. */

@@ -32,8 +32,9 @@ _SIGS = {
     "sikv_append": (I, [P, P, I, I64, I64, P, P, P, I64, I64, I, P, P]),
     "sikv_decode_smem_bytes": (I, [I64, I, I, I, I]),
     "sikv_decode_default_cap": (I, [I64, I, I]),
-    "sikv_decode_step": (I, [P, P, P, P, P, I, P, P, P, P, I64, I, P, I64, I64, I, I, I, P, P, P, I, P,
-                             P, P]),
+    "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P]),
+    "sikv_forced_blocks": (I, [I, I64]),
+    "sikv_pack_forced": (I, [P, P, I, P, P, I64, I, P, I64, P, I, I, I, P]),
     "sikv_score_fast": (I, [P, P, P, I, I64, I64, P, P]),
     "sikv_debug_set_decode_profile": (I, [P]),
     "sikv_build_lut_f64": (I, [P, P, I64, I, I, P, P]),

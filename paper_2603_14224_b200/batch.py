@@ -42,6 +42,7 @@ class CacheBatch:
     sink_v: torch.Tensor
     recent_k: torch.Tensor
     recent_v: torch.Tensor
+    ffrag: torch.Tensor                       # [U, blocks, 2, 32, 32] int32 forced-row fragments
     recent: int = 0
     ref: dict = field(default_factory=dict)   # optional reference-layout planes
 
@@ -78,6 +79,8 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
         sink_k=torch.empty(units, S, FD, **f32), sink_v=torch.empty(units, S, FD, **f32),
         recent_k=torch.empty(units, recent_capacity, FD, **f32),
         recent_v=torch.empty(units, recent_capacity, FD, **f32),
+        ffrag=torch.zeros(units, L_.lib().sikv_forced_blocks(S, recent_capacity), 2, 32, 32,
+                          device=dev, dtype=torch.int32),
     )
     if keep_reference:
         cb.ref = dict(
@@ -129,8 +132,16 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
         L_.call("sikv_gather_rows", L_.ptr(keys), L_.ptr(values), dt, n, L, D,
                 L_.ptr(cb.sink_idx[u0:u0 + n].contiguous()), S, L_.ptr(_sl(cb.mu64, u0, n)),
                 L_.ptr(_sl(cb.sink_k, u0, n)), L_.ptr(_sl(cb.sink_v, u0, n)), 0, L_.stream())
+    _pack_forced(cb, u0, n, 0, cb.ffrag.shape[1] * 16)
     if check:
         L_.raise_status(status, "keys")
+
+
+def _pack_forced(cb: CacheBatch, u0: int, n: int, row_begin: int, row_end: int) -> None:
+    L_.call("sikv_pack_forced", L_.ptr(_sl(cb.sink_k, u0, n)), L_.ptr(_sl(cb.sink_v, u0, n)), cb.sinks,
+            L_.ptr(_sl(cb.recent_k, u0, n)), L_.ptr(_sl(cb.recent_v, u0, n)), cb.recent_capacity, cb.recent,
+            L_.ptr(_sl(cb.alpha32, u0, n)), n, L_.ptr(_sl(cb.ffrag, u0, n)), cb.ffrag.shape[1], row_begin,
+            row_end, L_.stream())
 
 
 def prefill_batch(keys: torch.Tensor, values: torch.Tensor, *, sink_count: int = 64,
@@ -155,6 +166,8 @@ def append_batch(cb: CacheBatch, k: torch.Tensor, v: torch.Tensor) -> None:
             L_.ptr(cb.recent_k), L_.ptr(cb.recent_v), cb.recent_capacity, cb.recent, 0, L_.ptr(status),
             L_.stream())
     cb.recent += 1
+    row = cb.sinks + cb.recent - 1
+    _pack_forced(cb, 0, cb.units, row, row + 1)
 
 
 @dataclass
@@ -189,8 +202,8 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
         cnt = torch.empty(U, device=dev, dtype=torch.int32)
     diag = torch.empty(U, device=dev, dtype=torch.int32) if with_diag else None
     L_.call("sikv_decode_step", L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
-            L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.sink_k), L_.ptr(cb.sink_v), L_.ptr(cb.recent_k),
-            L_.ptr(cb.recent_v), cb.recent_capacity, cb.recent, L_.ptr(qf), U, cb.tokens, Gq, k, cap,
+            L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], cb.recent, L_.ptr(qf), U,
+            cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), max(stride, 1) if sel is not None else 0, L_.ptr(cnt),
             L_.ptr(diag), L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)

@@ -23,9 +23,10 @@ cudaError_t launch_append(const void*, const void*, int, int64_t, int, const dou
 // decode.cu
 DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap);
 cudaError_t launch_decode(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
-                          const float*, const float*, const float*, const float*, int64_t, int, const float*,
-                          int64_t, int64_t, int, int, int, float*, float*, int32_t*, int, int32_t*, int32_t*,
-                          cudaStream_t, int*);
+                          const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*,
+                          float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t, int*);
+cudaError_t launch_pack_forced(const float*, const float*, int, const float*, const float*, int64_t, int,
+                               const float*, int64_t, int, int, int, uint32_t*, cudaStream_t);
 cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
                               cudaStream_t);
 cudaError_t set_decode_profile(long long*);
@@ -152,21 +153,38 @@ int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap) {
   return decode_layout(tokens, k, sinks, gq, cap).total;
 }
 
+int sikv_forced_blocks(int sinks, int64_t rcap) { return (int)std::max<int64_t>(1, (sinks + rcap + 15) / 16); }
+
+int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const float* recent_k,
+                     const float* recent_v, int64_t rcap, int recent, const float* alpha32, int64_t units,
+                     uint32_t* forced_frag, int frag_blocks, int row_begin, int row_end, void* stream) {
+  REQUIRE(alpha32 && forced_frag, SIKV_EINVAL, "null pointer");
+  REQUIRE(sinks == 0 || (sink_k && sink_v), SIKV_EINVAL, "sink rows missing");
+  REQUIRE(recent == 0 || (recent_k && recent_v), SIKV_EINVAL, "recent rows missing");
+  REQUIRE(recent >= 0 && recent <= rcap, SIKV_EINVAL, "recent count out of range");
+  REQUIRE(frag_blocks >= sikv_forced_blocks(sinks, rcap), SIKV_EINVAL, "frag_blocks too small");
+  REQUIRE(row_begin >= 0 && row_end >= row_begin, SIKV_EINVAL, "bad row range");
+  const int b0 = row_begin / 16, b1 = std::min(frag_blocks, (row_end + 15) / 16);
+  return cuda_ret(launch_pack_forced(sink_k, sink_v, sinks, recent_k, recent_v, rcap, recent, alpha32, units,
+                                     frag_blocks, b0, b1, forced_frag, (cudaStream_t)stream),
+                  "sikv_pack_forced");
+}
+
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
-                     const float* alpha32, const int32_t* sink_idx, int sinks, const float* sink_k,
-                     const float* sink_v, const float* recent_k, const float* recent_v, int64_t rcap,
-                     int recent, const float* q, int64_t units, int64_t tokens, int gq, int k, int cap,
-                     float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag,
-                     void* stream) {
+                     const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
+                     int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq, int k,
+                     int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
+                     int32_t* diag, void* stream) {
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
   REQUIRE(gq >= 1 && gq <= 8, SIKV_EUNSUPPORTED, "fast decode supports 1..8 query heads per KV head");
   REQUIRE(k >= 0, SIKV_EINVAL, "k must be non-negative");
   REQUIRE(sinks >= 0 && sinks <= tokens, SIKV_EINVAL, "sink count out of range");
-  REQUIRE(sinks == 0 || (sink_idx && sink_k && sink_v), SIKV_EINVAL, "sinks need sink_idx/sink_k/sink_v");
-  REQUIRE(recent >= 0 && recent <= rcap, SIKV_EINVAL, "recent count out of range");
-  REQUIRE(recent == 0 || (recent_k && recent_v), SIKV_EINVAL, "recents need recent_k/recent_v");
+  REQUIRE(sinks == 0 || sink_idx, SIKV_EINVAL, "sinks need sink_idx");
+  REQUIRE(recent >= 0, SIKV_EINVAL, "recent count out of range");
+  REQUIRE(sinks + recent == 0 || forced_frag, SIKV_EINVAL, "forced rows need forced_frag");
+  REQUIRE(sinks + recent <= 16 * frag_blocks, SIKV_EINVAL, "forced rows exceed frag_blocks");
   const int64_t keff = std::min<int64_t>(k, tokens - sinks);
   REQUIRE(sinks + keff + recent >= 1, SIKV_EINVAL, "selection is empty");
   REQUIRE(!sel || sel_stride >= sinks + keff + recent, SIKV_EINVAL, "sel_stride too small");
@@ -175,9 +193,9 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   REQUIRE(need <= max_smem(), SIKV_EUNSUPPORTED,
           "decode shared-memory footprint " + std::to_string(need) + " B exceeds the device limit");
   int smem = 0;
-  cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, sink_k, sink_v, recent_k,
-                                recent_v, rcap, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride,
-                                sel_count, diag, (cudaStream_t)stream, &smem);
+  cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
+                                recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag,
+                                (cudaStream_t)stream, &smem);
   return cuda_ret(e, "sikv_decode_step");
 }
 

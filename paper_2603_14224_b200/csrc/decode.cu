@@ -36,17 +36,15 @@ struct DecodeArgs {
   const float* cent32;      // [U][32][16][4]
   const float* alpha32;     // [U][128]
   const int32_t* sink_idx;  // [U][S] sorted, unique, < L
-  const float* sink_k;      // [U][S][128] centred K'
-  const float* sink_v;      // [U][S][128]
-  const float* rec_k;       // [U][rcap][128] centred K'
-  const float* rec_v;
+  const uint32_t* ffrag;    // [U][fblocks][2][32 lanes][32 words] forced rows as fp16 fragments
   const float* q;           // [U][Gq][128]
   float* out;               // [U][Gq][128]
   float* lse;               // [U][Gq] natural-log sum of exp(logits), nullable
   int32_t* sel;             // [U][sel_stride], nullable
   int32_t* sel_count;       // [U], nullable
   int32_t* diag;            // [U], nullable
-  int64_t L, rcap;
+  int64_t L;
+  int fblocks;
   int S, R, Gq, k, capw, sel_stride;
   // shared-memory layout (byte offsets)
   int off_cand, off_forced, off_misc, off_bits, off_dyn, off_stage;
@@ -136,6 +134,25 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   long long* prof = g_prof ? g_prof + u * 12 : nullptr;
 #define PROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
   PROF(0);
+  // selection mode and sample geometry first, so the sample's HBM loads overlap the setup
+  const int64_t ncand_all = L - S;
+  const int keff = (int)((int64_t)a.k < ncand_all ? (int64_t)a.k : ncand_all);
+  const int nchunks = (int)((L + 255) >> 8);
+  // selection modes: 0 nothing dynamic, 1 every candidate, 2 all candidates fit (tau = -inf),
+  // 3 sampled threshold
+  int mode;
+  if (keff == 0) mode = 0;
+  else if (keff == ncand_all) mode = 1;
+  else if ((int64_t)nchunks * 32 <= (int64_t)capw) mode = 2;   // every warp's tokens fit its segment
+  else mode = 3;
+  const int sstride = mode == 3 ? max(16, (nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
+  const int nsc = mode == 3 ? (nchunks + sstride - 1) / sstride : 0;
+  uint4 wsamp[MAX_SAMPLE_CHUNKS];
+#pragma unroll
+  for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+    const int64_t t = (int64_t)x * sstride * 256 + tid;
+    wsamp[x] = (x < nsc && t < L) ? __ldg(signs + t) : make_uint4(0, 0, 0, 0);
+  }
   if (tid == 0) { ms->fb = 0; ms->maxx = 0; ms->bad = 0; }
   __syncthreads();
   for (int j = tid; j < S; j += DT) {
@@ -170,19 +187,8 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   }
   __syncthreads();
 
-  const int64_t ncand_all = L - S;
   const int64_t flim = S > 0 ? (int64_t)a.sink_idx[u * S + S - 1] + 1 : 0;   // sinks are sorted
-  const int keff = (int)((int64_t)a.k < ncand_all ? (int64_t)a.k : ncand_all);
   const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
-  const int nchunks = (int)((L + 255) >> 8);
-
-  // selection modes: 0 nothing dynamic, 1 every candidate, 2 all candidates fit (tau = 1),
-  // 3 sampled threshold
-  int mode;
-  if (keff == 0) mode = 0;
-  else if (keff == ncand_all) mode = 1;
-  else if ((int64_t)nchunks * 32 <= (int64_t)capw) mode = 2;   // every warp's tokens fit its segment
-  else mode = 3;
 
   uint32_t* gt = reinterpret_cast<uint32_t*>(sm + a.off_bits);
   uint32_t* eq = gt + W;
@@ -222,23 +228,14 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   bool fallback = false;
   if (mode >= 2) {
     uint32_t tau = 1;
-    int sstride = 1, nsc = 0;
     if (mode == 3) {
       PROF(1);
       // ---------------- B1: score the sample chunks (<= 8 per thread, kept in registers)
-      sstride = max(16, (nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS);
-      nsc = (nchunks + sstride - 1) / sstride;
       uint32_t sk[MAX_SAMPLE_CHUNKS];
-      uint4 w[MAX_SAMPLE_CHUNKS];
-#pragma unroll
-      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-        const int64_t t = (int64_t)x * sstride * 256 + tid;
-        w[x] = (x < nsc && t < L) ? __ldg(signs + t) : make_uint4(0, 0, 0, 0);
-      }
       float sv[MAX_SAMPLE_CHUNKS];
-      score_batch(w, lb, T, sv);
+      score_batch(wsamp, lb, T, sv);
       int nv = 0;
-      uint32_t smax = 0;
+      uint32_t smax = 0, smin = 0xFFFFFFFFu;
 #pragma unroll
       for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
         const int64_t t = (int64_t)x * sstride * 256 + tid;
@@ -247,32 +244,68 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
         sk[x] = key;
         nv += key != 0;
         smax = max(smax, key);
+        if (key) smin = min(smin, key);
       }
       nv = warp_sum(nv);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
-      if (tid == 0) ms->nsv = 0;
+      for (int o = 16; o > 0; o >>= 1) {
+        smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+      }
+      // threshold histogram: 256 value-linear bins over [smin, smax] of the sample
+      int* th = reinterpret_cast<int*>(cand);                  // [256] counts
+      uint32_t* tmin = reinterpret_cast<uint32_t*>(cand) + 256; // [256] min key per bin
+      for (int i = tid; i < 256; i += DT) { th[i] = 0; tmin[i] = 0xFFFFFFFFu; }
+      if (tid == 0) { ms->nsv = 0; ms->tau = 0xFFFFFFFFu; }
       __syncthreads();
-      if (lane == 0) { atomicAdd(&ms->nsv, nv); atomicMax(&ms->maxx, smax); }
+      if (lane == 0) { atomicAdd(&ms->nsv, nv); atomicMax(&ms->maxx, smax); atomicMin(&ms->tau, smin); }
       __syncthreads();
       const int nsv = ms->nsv;
-      const uint32_t smx = ms->maxx;
       const double e = (double)keff * (double)nsv / (double)ncand_all;
       int r = (int)ceil(e + 4.0 * sqrt(e) + 16.0);
       r = min(r, nsv);
       if (r >= 1) {
-        int dummy;
-        radix_kth([&](auto f) {
+        const uint32_t kmx = ms->maxx, kmn = ms->tau;
+        auto unkey = [](uint32_t k2) {
+          return __uint_as_float((k2 & 0x80000000u) ? (k2 & 0x7FFFFFFFu) : ~k2);
+        };
+        const float fmn = unkey(kmn), fmx = unkey(kmx);
+        const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
 #pragma unroll
-          for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) f(sk[x]);
-        }, smx, r, reinterpret_cast<int*>(cand), ms, tau, dummy);
-        // items with key 0 are padding; r <= nsv keeps tau >= 1
+        for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+          if (sk[x]) {
+            const int b = min(255, (int)((unkey(sk[x]) - fmn) * scale));
+            atomicAdd(&th[b], 1);
+            atomicMin(&tmin[b], sk[x]);
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int loc[8], s8 = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) { loc[i] = th[255 - 8 * lane - i]; s8 += loc[i]; }
+          int inc = s8;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+          }
+          int c = inc - s8;
+          if (c < r && r <= inc) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (c < r && r <= c + loc[i]) ms->digit = 255 - 8 * lane - i;
+              c += loc[i];
+            }
+          }
+        }
+        __syncthreads();
+        tau = tmin[ms->digit];          // smallest sample key in the boundary bin
       }
+      __syncthreads();
       if (tid == 0) ms->maxx = 0;
       __syncthreads();
       {
-        const int cnt_s = 0;
-        (void)cnt_s;
         uint32_t bits = 0;
 #pragma unroll
         for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x)
@@ -304,12 +337,11 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
       tauf = mode == 2 ? -INFINITY : __uint_as_float((k2 & 0x80000000u) ? (k2 & 0x7FFFFFFFu) : ~k2);
     }
     const int Li = (int)L;
+    int next_s = mode == 3 ? 0 : 0x7fffffff;      // next sample chunk (already scored in B1)
+    const int end_s = nsc * sstride;
     for (int c0 = 0; c0 < nchunks; c0 += NB) {
       int xs = -1;                  // the (at most one, sstride >= 16 > NB) sample chunk here
-      if (mode == 3) {
-        const int cs = ((c0 + sstride - 1) / sstride) * sstride;
-        if (cs < c0 + NB && cs / sstride < nsc) xs = cs - c0;
-      }
+      if (next_s < c0 + NB && next_s < end_s) { xs = next_s - c0; next_s += sstride; }
       const int t0 = c0 * 256 + tid;
       const bool full = (c0 + NB) * 256 <= Li;
       uint4 w[NB];
@@ -352,11 +384,12 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
       }, ms->maxx, keff, hist, ms, xk, need_eq);
       kstar = xk + tau;
       for (int i = tid; i < 2 * W; i += DT) gt[i] = 0u;
+      if (tid == 0) ms->nsv = 0;
       __syncthreads();
       for (int i = lane; i < n; i += 32) {
         const uint32_t x = seg[2 * i], t = seg[2 * i + 1];
         if (x > xk) atomicOr(&gt[t >> 5], 1u << (t & 31));
-        else if (x == xk) atomicOr(&eq[t >> 5], 1u << (t & 31));
+        else if (x == xk) { atomicOr(&eq[t >> 5], 1u << (t & 31)); atomicAdd(&ms->nsv, 1); }
       }
       __syncthreads();
     }
@@ -374,13 +407,14 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
       }
     }, 0xFFFFFFFFu, keff, fh, ms, kstar, need_eq);
     for (int i = tid; i < 2 * W; i += DT) fgt[i] = 0u;
+    if (tid == 0) ms->nsv = 0;
     __syncthreads();
     for (int c = 0; c < nchunks; ++c) {
       const int64_t t = (int64_t)c * 256 + tid;
       if (t < L && !forced_bit(forced, t)) {
         const uint32_t key = f32_key(score_token(__ldg(signs + t), lb, T));
         if (key > kstar) atomicOr(&fgt[t >> 5], 1u << (t & 31));
-        else if (key == kstar) atomicOr(&feq[t >> 5], 1u << (t & 31));
+        else if (key == kstar) { atomicOr(&feq[t >> 5], 1u << (t & 31)); atomicAdd(&ms->nsv, 1); }
       }
     }
     __syncthreads();
@@ -395,10 +429,16 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   {
     const int per = (W + DT - 1) / DT;
     const int w0 = tid * per, w1 = min(W, w0 + per);
-    int my_eq = 0;
-    if (mode >= 2) for (int x = w0; x < w1; ++x) my_eq += __popc(eq[x]);
-    int eq_before, dummy, t1, t2;
-    block_exscan2(my_eq, 0, eq_before, dummy, t1, t2, ms->wsum);
+    // ties at the k-th key: keep the lowest-index need_eq of them (prefix over the eq
+    // bitmap); when every tie is taken (the usual case) no prefix is needed
+    const bool all_eq = mode < 2 || ms->nsv == need_eq;
+    int eq_before = 0;
+    if (!all_eq) {
+      int my_eq = 0;
+      for (int x = w0; x < w1; ++x) my_eq += __popc(eq[x]);
+      int dummy, t1, t2;
+      block_exscan2(my_eq, 0, eq_before, dummy, t1, t2, ms->wsum);
+    }
     auto dbits = [&](int x, int& eb) -> uint32_t {
       if (mode == 0) return 0u;
       if (mode == 1) {
@@ -407,9 +447,11 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
         return d;
       }
       uint32_t e = eq[x];
-      const int take = min(max(need_eq - eb, 0), __popc(e));
-      eb += __popc(e);
-      while (__popc(e) > take) e &= ~(1u << (31 - __clz(e)));
+      if (!all_eq) {
+        const int take = min(max(need_eq - eb, 0), __popc(e));
+        eb += __popc(e);
+        while (__popc(e) > take) e &= ~(1u << (31 - __clz(e)));
+      }
       return gt[x] | e;
     };
     int nd = 0, nsl = 0, eb = eq_before;
@@ -493,48 +535,39 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     }
   };
 
-  // -- forced rows (fp32 K', V from the sink / recent buffers)
+  // -- forced rows (sinks then recents), pre-packed by pack_forced_kernel as fp16 fragments
   for (int blk = warp; blk < nbf; blk += DW) {
     const int base = blk * 16;
-    auto rowk = [&](int f) -> const float* {
-      return f < S ? a.sink_k + (u * S + f) * FD : a.rec_k + (u * a.rcap + (f - S)) * FD;
-    };
-    auto rowv = [&](int f) -> const float* {
-      return f < S ? a.sink_v + (u * S + f) * FD : a.rec_v + (u * a.rcap + (f - S)) * FD;
-    };
+    const uint4* fk = reinterpret_cast<const uint4*>(a.ffrag + ((u * a.fblocks + blk) * 2 * 32 + lane) * 32);
+    const uint4* fv = fk + 32 * 8;
+    uint32_t kwd[32];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 t = __ldg(fk + i);
+      kwd[4 * i] = t.x; kwd[4 * i + 1] = t.y; kwd[4 * i + 2] = t.z; kwd[4 * i + 3] = t.w;
+    }
+    uint32_t vwd[32];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 t = __ldg(fv + i);
+      vwd[4 * i] = t.x; vwd[4 * i + 1] = t.y; vwd[4 * i + 2] = t.z; vwd[4 * i + 3] = t.w;
+    }
     float sacc[2][4];
     bool valid[2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const float* kr = rowk(min(base + g + 8 * nt, nf - 1));
       sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        uint32_t b[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int d = 16 * s + 2 * t4 + 8 * e;
-          const float2 kk = *reinterpret_cast<const float2*>(kr + d);
-          b[e] = h2u(__floats2half2_rn(kk.x * inva[d], kk.y * inva[d + 1]));
-        }
-        mma16816(sacc[nt], qa[s][0], 0u, qa[s][1], 0u, b[0], b[1]);
-      }
+      for (int s = 0; s < 8; ++s)
+        mma16816(sacc[nt], qa[s][0], 0u, qa[s][1], 0u, kwd[nt * 16 + 2 * s], kwd[nt * 16 + 2 * s + 1]);
       valid[nt][0] = base + 2 * t4 + 8 * nt < nf;
       valid[nt][1] = base + 2 * t4 + 1 + 8 * nt < nf;
     }
-    const float* vr[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) vr[x] = rowv(min(base + 2 * t4 + (x & 1) + 8 * (x >> 1), nf - 1));
     softmax_pv(sacc, valid, [&](int mp, uint32_t (&v)[2][4]) {
 #pragma unroll
-      for (int mm = 0; mm < 2; ++mm) {
-        const int m = 2 * mp + mm;
+      for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int d = 16 * m + g + 8 * (r & 1), pr = r >> 1;
-          v[mm][r] = h2u(__floats2half2_rn(vr[2 * pr][d], vr[2 * pr + 1][d]));
-        }
-      }
+        for (int r = 0; r < 4; ++r) v[mm][r] = vwd[(2 * mp + mm) * 4 + r];
     });
   }
 
@@ -717,19 +750,72 @@ DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap) {
 }
 
 cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float* cent32,
-                          const float* alpha32, const int32_t* sink_idx, int S, const float* sink_k,
-                          const float* sink_v, const float* rec_k, const float* rec_v, int64_t rcap, int R,
-                          const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out,
-                          float* lse, int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag,
-                          cudaStream_t st, int* smem_out) {
+                          const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
+                          int fblocks, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
+                          float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
+                          int32_t* diag, cudaStream_t st, int* smem_out) {
   DecodeLayout d = decode_layout(L, k, S, Gq, cap);
   if (smem_out) *smem_out = d.total;
-  DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, sink_k, sink_v, rec_k, rec_v, q, out, lse, sel,
-               sel_count, diag, L, rcap, S, R, Gq, k, d.capw, sel_stride,
+  DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, ffrag, q, out, lse, sel,
+               sel_count, diag, L, fblocks, S, R, Gq, k, d.capw, sel_stride,
                d.off_cand, d.off_forced, d.off_misc, d.off_bits, d.off_dyn, d.off_stage};
   cudaError_t e = cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, d.total);
   if (e != cudaSuccess) return e;
   decode_step_kernel<<<(unsigned)U, DT, d.total, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Forced rows (sinks then recents) -> fp16 mma fragments, one warp per (unit, 16-row block).
+// K^ = K' / alpha-hat (alpha folded into the query), V as is; rows >= S + R are zero.
+__global__ void pack_forced_kernel(const float* __restrict__ sink_k, const float* __restrict__ sink_v, int S,
+                                   const float* __restrict__ rec_k, const float* __restrict__ rec_v, int64_t rcap,
+                                   int R, const float* __restrict__ alpha32, int fblocks, int b0,
+                                   uint32_t* __restrict__ frag) {
+  const int64_t u = blockIdx.y;
+  const int blk = b0 + blockIdx.x, lane = threadIdx.x;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nf = S + R;
+  auto row = [&](int f, bool key) -> const float* {
+    if (f >= nf) return nullptr;
+    if (f < S) return (key ? sink_k : sink_v) + (u * S + f) * FD;
+    return (key ? rec_k : rec_v) + (u * rcap + (f - S)) * FD;
+  };
+  auto inva = [&](int d) {
+    const float al = alpha32[u * FD + d];
+    return 1.0f / (al > 0.f ? al : 1.0f);
+  };
+  uint32_t* out = frag + ((u * fblocks + blk) * 2 * 32 + lane) * 32;
+  const int base = blk * 16;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const float* kr = row(base + g + 8 * nt, true);
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int d = 16 * s + 2 * t4 + 8 * e;
+        const float x0 = kr ? kr[d] * inva(d) : 0.f, x1 = kr ? kr[d + 1] * inva(d + 1) : 0.f;
+        out[nt * 16 + 2 * s + e] = h2u(__floats2half2_rn(x0, x1));
+      }
+  }
+  uint32_t* ov = out + 32 * 32;
+#pragma unroll
+  for (int m = 0; m < 8; ++m)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int d = 16 * m + g + 8 * (r & 1), pr = r >> 1;
+      const float* va = row(base + 2 * t4 + 8 * pr, false);
+      const float* vb = row(base + 2 * t4 + 8 * pr + 1, false);
+      ov[m * 4 + r] = h2u(__floats2half2_rn(va ? va[d] : 0.f, vb ? vb[d] : 0.f));
+    }
+}
+
+cudaError_t launch_pack_forced(const float* sink_k, const float* sink_v, int S, const float* rec_k,
+                               const float* rec_v, int64_t rcap, int R, const float* alpha32, int64_t U,
+                               int fblocks, int b0, int b1, uint32_t* frag, cudaStream_t st) {
+  if (b1 <= b0 || U == 0) return cudaSuccess;
+  pack_forced_kernel<<<dim3(b1 - b0, (unsigned)U), 32, 0, st>>>(sink_k, sink_v, S, rec_k, rec_v, rcap, R,
+                                                               alpha32, fblocks, b0, frag);
   return cudaGetLastError();
 }
 

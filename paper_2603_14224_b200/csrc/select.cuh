@@ -73,18 +73,20 @@ constexpr int NBIN = 1 << RB;       // 4096 bins; thread t owns bins [NBIN-16(t+
 // Block-wide: choose the digit whose descending cumulative count reaches ms->rem_sel.
 __device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
   const int tid = threadIdx.x;
-  int loc[NBIN / DT], s = 0;
+  constexpr int PER = NBIN / DT;
+  const int top = NBIN - 1 - PER * tid;          // this thread owns bins top, top-1, ..., top-PER+1
+  int s = 0;
 #pragma unroll
-  for (int i = 0; i < NBIN / DT; ++i) { loc[i] = hist[NBIN - 1 - (NBIN / DT) * tid - i]; s += loc[i]; }
+  for (int i = 0; i < PER; ++i) s += hist[top - ((i + tid) & (PER - 1))];   // rotated: no bank conflicts
   int exc, d0, tot, d1;
   block_exscan2(s, 0, exc, d0, tot, d1, ms->wsum);
   const int rem = ms->rem_sel;
   if (exc < rem && rem <= exc + s) {
     int c = exc;
-#pragma unroll
-    for (int i = 0; i < NBIN / DT; ++i) {
-      if (c < rem && rem <= c + loc[i]) { ms->digit = NBIN - 1 - (NBIN / DT) * tid - i; ms->cnt_above = c; }
-      c += loc[i];
+    for (int i = 0; i < PER; ++i) {
+      const int h = hist[top - i];
+      if (c < rem && rem <= c + h) { ms->digit = top - i; ms->cnt_above = c; break; }
+      c += h;
     }
   }
   __syncthreads();
@@ -99,6 +101,7 @@ __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, in
                                           uint32_t& kth, int& need_eq) {
   const int tid = threadIdx.x;
   const int nbits = maxx ? 32 - __clz(maxx) : 0;
+  int* list = hist + NBIN;           // up to 32 items of a small boundary bin (+ counter)
   if (tid == 0) ms->rem_sel = rank;
   uint32_t prefix = 0;
   int shift = nbits;
@@ -108,6 +111,7 @@ __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, in
     const int hi = shift;            // bits >= hi are already fixed in prefix
     shift -= dbits;
     for (int i = tid; i < NBIN; i += DT) hist[i] = 0;
+    if (tid == 0) list[32] = 0;
     __syncthreads();
     const uint32_t want = hi >= 32 ? 0u : (prefix >> hi);
     const int sh = shift;
@@ -116,10 +120,37 @@ __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, in
     });
     __syncthreads();
     pick_digit_big(hist, ms);
-    prefix |= (uint32_t)ms->digit << shift;
+    const uint32_t d = (uint32_t)ms->digit;
+    prefix |= d << shift;
+    const int nb = hist[d];
     __syncthreads();
     if (tid == 0) ms->rem_sel -= ms->cnt_above;
     __syncthreads();
+    if (shift > 0 && nb <= 32) {
+      // finish inside one warp: exact rank among the few items of the boundary bin
+      const uint32_t w2 = prefix >> shift;
+      each([&](uint32_t x) {
+        if ((x >> shift) == w2) list[atomicAdd(&list[32], 1)] = (int)x;
+      });
+      __syncthreads();
+      if (tid < 32) {
+        const uint32_t v = tid < nb ? (uint32_t)list[tid] : 0u;
+        int gt = 0, eqc = 0;
+        for (int j = 0; j < nb; ++j) {
+          const uint32_t o = (uint32_t)list[j];
+          gt += o > v;
+          eqc += o == v;
+        }
+        const int rem = ms->rem_sel;
+        __syncwarp();
+        if (tid < nb && gt < rem && rem <= gt + eqc) { ms->tau = v; ms->digit = rem - gt; }
+      }
+      __syncthreads();
+      kth = ms->tau;
+      need_eq = ms->digit;
+      __syncthreads();
+      return;
+    }
   }
   kth = prefix;
   need_eq = ms->rem_sel;

@@ -154,3 +154,25 @@ def test_decode_with_appends_and_gq7():
 def test_decode_no_sinks_fp32_inputs():
     units, cb, oc, q = make(1000, [5, 6, 7], gq=2, sinks=0, dtype=torch.float32)
     _check_decode(units, cb, oc, q, 100)
+
+
+def test_decode_ties_lowest_index_first():
+    """Repeated key rows give exactly tied scores; the k boundary must keep the lowest
+    indices (stable argsort, retrieval.py:149), in both the sampled and the exact path."""
+    rng = np.random.default_rng(3)
+    L = 9000
+    base = gen_unit(97, 128, 4, 31)
+    reps = np.concatenate([base.keys] * (L // 97 + 1))[:L]
+    V = rng.standard_normal((L, 128))
+    from paper_2603_14224_b200.synth import bf16_round
+    V = bf16_round(V)
+    K_t = torch.tensor(reps[None], dtype=torch.bfloat16, device="cuda")
+    V_t = torch.tensor(V[None], dtype=torch.bfloat16, device="cuda")
+    cb = B.prefill_batch(K_t, V_t, sink_count=64)
+    c = O.prefill(reps, V, sink_count=64)
+    q = torch.tensor(base.queries[None, :4], dtype=torch.float32, device="cuda")
+    for k, cap in ((500, 0), (500, 200), (333, 0)):
+        res = B.decode_step(cb, q, k, cap=cap, with_selection=True)
+        idx = R.select32(c, base.queries[:4].astype(np.float32), k)[0]
+        got = res.selection[0, : res.counts[0]].cpu().numpy()
+        np.testing.assert_array_equal(got, idx)
