@@ -141,13 +141,15 @@ def run_ours(args, rank, world, cfg):
     torch.cuda.set_device(dev)
     cb, q = build_cache(ul, rank * ul, L, gq, 1234, dev)
 
+    from paper_2603_14224_b200.shard import gather_outputs
+
     out = torch.empty(ul, gq, 128, device=dev, dtype=torch.float32)
-    gathered = torch.empty(world * ul, gq, 128, device=dev, dtype=torch.bfloat16) if world > 1 else None
+    model_out = torch.empty(layers, batch, kvh * gq, 128, device=dev, dtype=torch.bfloat16) if world > 1 else None
 
     def step(qq):
         B.decode_step(cb, qq, k, out=out)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, out.to(torch.bfloat16))
+        if world > 1:   # head-sharded outputs -> [layers, batch, H_q, D] on every rank (NCCL)
+            gather_outputs(out.to(torch.bfloat16), layers, batch, kvh, world, out=model_out)
 
     # correctness spot check on this rank (selection of unit 0 vs float32 restatement is in tests)
     for _ in range(args.warmup):

@@ -85,8 +85,11 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
   REQUIRE(keys && values && mu64 && alpha64 && status_dev, SIKV_EINVAL, "null required pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "keys must contain at least one row");
-  REQUIRE(dim >= 4 && dim % 4 == 0, SIKV_EINVAL, "channel count must be a positive multiple of 4");
-  REQUIRE(dim <= 128, SIKV_EUNSUPPORTED, "encoder supports dim <= 128");
+  REQUIRE(dim >= 1, SIKV_EINVAL, "channel count must be positive");
+  if (what & 2) {
+    REQUIRE(dim >= 4 && dim % 4 == 0, SIKV_EINVAL, "channel count must be a positive multiple of 4");
+    REQUIRE(dim <= 128, SIKV_EUNSUPPORTED, "encoder supports dim <= 128");
+  }
   REQUIRE(bits == 0 || good_bits(bits), SIKV_EINVAL, "bits must be one of (1, 2, 4, 8) or 0 (lossless)");
   REQUIRE(bits == 0 || (good_group(group_size) && dim % group_size == 0), SIKV_EINVAL,
           "channel count not divisible by group_size (group_size must be 4..128, power of two)");

@@ -8,6 +8,12 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_sessionstart(session):
+    # the C-ABI library is git-ignored build output: build it in-tree if it is missing/stale
+    from paper_2603_14224_b200 import build
+    build.build()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built extension")
     config.addinivalue_line("markers", "slow: long-running CPU test")

@@ -1,0 +1,413 @@
+"""The per-head drop-in API on the GPU: the reference's own unit tests (ported from
+/root/reference/pkg/tests, same assertions) plus bit-exact parity with the reference's
+golden outputs (tests/golden, produced by running the reference itself)."""
+
+import hashlib
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_14224_b200 as sk
+from oracle import sikv_oracle as O
+from paper_2603_14224_b200.synth import gen_unit
+
+pytestmark = pytest.mark.gpu
+
+
+def N(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(N(a)).tobytes()).hexdigest()
+
+
+# ----------------------------------------------------------------- golden parity (reference outputs)
+GOLD = ["c1_u0", "c1_u1", "win_1k", "append_2k", "gq7_2k", "b4_d64", "direct_d32", "b8_d32",
+        "b1_d128", "lossless_d64", "c2_1unit"]
+
+
+@pytest.mark.parametrize("name", GOLD)
+def test_api_matches_reference_golden(golden, name):
+    meta, arr = golden
+    rec = meta[name]
+    u = gen_unit(rec["L"], rec["D"], rec["gq"] + rec["appends"], rec["seed"])
+    cfg = sk.CacheConfig(bits=rec["bits"], group_size=rec["group"], sink_count=rec["sinks"],
+                         sign_in_quant=rec["sign_in_quant"])
+    K = torch.tensor(u.keys, dtype=torch.bfloat16 if rec["D"] == 128 else torch.float64, device="cuda")
+    V = torch.tensor(u.values, dtype=K.dtype, device="cuda")
+    cache = sk.prefill(K, V, u.window if rec["window"] else None, cfg)
+    np.testing.assert_array_equal(N(cache.norm.mu), arr[f"{name}/mu"])
+    np.testing.assert_array_equal(N(cache.norm.alpha), arr[f"{name}/alpha"])
+    assert sha(cache.codes.packed) == rec["codes_sha"]
+    for tag, q in (("kmag", cache.key_mag), ("kdirect", cache.key_direct), ("values", cache.values)):
+        if tag in rec["planes"]:
+            p = rec["planes"][tag]
+            assert (sha(q.packed), sha(q.scales), sha(q.zeros)) == (p["packed"], p["scales"], p["zeros"]), tag
+    np.testing.assert_allclose(N(cache.codebook.centroids), arr[f"{name}/centroids"], rtol=1e-13, atol=1e-300)
+    np.testing.assert_array_equal(N(cache.codebook.centroids).astype(np.float32),
+                                  arr[f"{name}/centroids"].astype(np.float32))
+    assert N(cache.sink_indices).tolist() == rec["sink_indices"]
+    for a in range(rec["appends"]):
+        q = u.queries[rec["gq"] + a]
+        sk.append_token(cache, q * 0.5, q[::-1].copy())
+    qh = u.queries[: rec["gq"]]
+    qbar = qh.sum(axis=0)
+    # LUT and scores are computed with the reference's float64 order: bit-exact.  The
+    # reference's LUT is built from its own centroids, so feed those to isolate build_lut.
+    lut_ref_cb = sk.build_lut(qbar, sk.Codebook(torch.tensor(arr[f"{name}/centroids"], device="cuda")))
+    np.testing.assert_array_equal(N(lut_ref_cb.table), arr[f"{name}/lut"])
+    assert sha(sk.score_tokens(lut_ref_cb, cache.codes)) == rec["scores_sha"]
+    sel = sk.select_tokens(cache, qbar, k=rec["k"])
+    ref_sel = arr[f"{name}/sel"]
+    got = N(sel.indices)
+    assert len(np.intersect1d(got, ref_sel)) >= len(ref_sel) - 1     # own centroids: ulp-level
+    assert [sel.sink_count, sel.recent_count, sel.dynamic_count] == rec["sel_counts"]
+    ref_sel_t = sk.TokenSelection(torch.tensor(ref_sel, device="cuda"), *rec["sel_counts"])
+    for h, q in enumerate(qh):
+        out = sk.sparse_attention(q, ref_sel_t, cache)
+        np.testing.assert_allclose(N(out.out), arr[f"{name}/attn"][h], rtol=1e-10, atol=1e-13)
+        assert abs(out.weights_checksum - 1.0) < 1e-9
+    assert sk.memory_report(cache).total_bits == rec["memory"]
+
+
+def test_api_selection_exact_vs_oracle():
+    """select_tokens from the same float64 scores is the exact reference set."""
+    u = gen_unit(4096, 128, 4, 100)
+    cache = sk.prefill(u.keys, u.values)
+    oc = O.prefill(u.keys, u.values)
+    for q in u.queries:
+        for kw in (dict(k=256), dict(budget=300), dict(sparsity=0.075)):
+            assert N(sk.select_tokens(cache, q, **kw).indices).tolist() == O.select(oc, q, **kw)[0].tolist()
+        assert N(sk.select_tokens(cache, q, sparsity=0.05, sign_only=True).indices).tolist() == \
+            O.select(oc, q, sparsity=0.05, sign_only=True)[0].tolist()
+
+
+# ----------------------------------------------------------------- ported reference unit tests
+class TestEncodeSignCode:   # test_codebook.py:18-45
+    def test_known(self):
+        assert sk.encode_sign_code([1, 1, 1, 1]) == 15
+        assert sk.encode_sign_code([-1, -1, -1, -1]) == 0
+        assert sk.encode_sign_code([0.5, -0.3, 1.2, -0.1]) == 10
+        assert sk.encode_sign_code([0.0, -1.0, 0.0, -1.0]) == 10
+        assert sk.encode_sign_code([0.0, 0.0, 0.0, 0.0]) == 15
+
+    def test_bijective(self):
+        seen = {sk.encode_sign_code(p) for p in itertools.product((-1.0, 1.0), repeat=4)}
+        assert seen == set(range(16))
+        pats = N(sk.sign_pattern_vectors())
+        for code in range(16):
+            assert sk.encode_sign_code(pats[code]) == code
+
+    def test_wrong_shape(self):
+        with pytest.raises(ValueError, match="shape"):
+            sk.encode_sign_code([1.0, 2.0, 3.0])
+
+
+class TestEncodeKeys:   # test_codebook.py:48-97
+    def test_two_groups(self):
+        assert N(sk.encode_keys([[0.5, -0.3, 1.2, -0.1, 1, 1, 1, 1]]).unpack()).tolist() == [[10, 15]]
+
+    def test_negation_complements(self):
+        K = np.random.default_rng(0).standard_normal((32, 12))
+        np.testing.assert_array_equal(N(sk.encode_keys(-K).unpack()), 15 - N(sk.encode_keys(K).unpack()))
+
+    def test_zero_matrix(self):
+        np.testing.assert_array_equal(N(sk.encode_keys(np.zeros((3, 8))).unpack()), np.full((3, 2), 15))
+
+    def test_indivisible(self):
+        with pytest.raises(ValueError, match="multiple of 4"):
+            sk.encode_keys(np.ones((2, 6)))
+
+    @pytest.mark.parametrize("groups", [1, 2, 3, 7, 32])
+    def test_pack_roundtrip(self, groups):
+        raw = np.random.default_rng(groups).integers(0, 16, size=(40, groups)).astype(np.uint8)
+        mat = sk.SignCodeMatrix.from_codes(raw)
+        np.testing.assert_array_equal(N(mat.unpack()), raw)
+        np.testing.assert_array_equal(N(sk.SignCodeMatrix.from_codes(mat.unpack()).packed), N(mat.packed))
+        np.testing.assert_array_equal(N(mat.packed), O.pack(raw, 4))
+
+    def test_sign_plane(self):
+        K = np.random.default_rng(2).standard_normal((21, 16))
+        codes = sk.encode_keys(K)
+        np.testing.assert_array_equal(N(codes.sign_plane()), np.where(K >= 0, 1.0, -1.0))
+        np.testing.assert_array_equal(N(codes.sign_plane(rows=[3, 17])), np.where(K[[3, 17]] >= 0, 1.0, -1.0))
+
+
+class TestBuildCodebook:   # test_codebook.py:114-170
+    def test_singleton_and_mean(self):
+        K = np.array([[0.5, -0.3, 1.2, -0.1]])
+        cb = N(sk.build_codebook(K, sk.encode_keys(K)).centroids)
+        np.testing.assert_array_equal(cb[0, 10], K[0])
+        np.testing.assert_array_equal(np.delete(cb[0], 10, axis=0), np.zeros((15, 4)))
+        K = np.array([[1, -1, 1, -1], [3, -3, 3, -3]], dtype=float)
+        np.testing.assert_array_equal(N(sk.build_codebook(K, sk.encode_keys(K)).centroids)[0, 10], [2, -2, 2, -2])
+
+    def test_matches_oracle_and_counter(self):
+        K = np.random.default_rng(4).standard_normal((300, 32))
+        codes = sk.encode_keys(K)
+        with sk.collect() as ops:
+            cb = sk.build_codebook(K, codes)
+        assert ops.codebook_subvector_reads == 300 * 8
+        np.testing.assert_allclose(N(cb.centroids), O.codebook(K, O.sign_codes(K)), rtol=1e-12, atol=1e-15)
+
+    def test_external_codes(self):
+        K = np.random.default_rng(7).standard_normal((50, 8))
+        raw = np.random.default_rng(8).integers(0, 16, size=(50, 2))
+        cb = sk.build_codebook(K, sk.SignCodeMatrix.from_codes(raw))
+        np.testing.assert_allclose(N(cb.centroids), O.codebook(K, raw), rtol=1e-12, atol=1e-15)
+
+    def test_shape_mismatch(self):
+        with pytest.raises(ValueError, match="codes describe"):
+            sk.build_codebook(np.ones((4, 8)), sk.encode_keys(np.ones((5, 8))))
+
+
+class TestQuantize:   # test_quantizer.py:217-308
+    def test_grid(self):
+        q = sk.quantize_values([[0.0, 1.0, 2.0, 3.0]], sk.QuantConfig(bits=2, group_size=4))
+        assert N(q.scales).tolist() == [[1.0]] and N(q.zeros).tolist() == [[0.0]]
+        assert N(q.codes()).tolist() == [[0, 1, 2, 3]]
+
+    def test_degenerate(self):
+        q = sk.quantize_values([[5.0] * 4], sk.QuantConfig(2, 4))
+        assert N(q.scales).tolist() == [[0.0]] and N(q.zeros).tolist() == [[5.0]]
+        np.testing.assert_array_equal(N(sk.dequantize_values(q)), [[5.0] * 4])
+
+    def test_rounding_half_away(self):
+        assert N(sk.quantize_values([[0.0, 0.4, 2.6, 3.0]], sk.QuantConfig(2, 4)).codes()).tolist() == [[0, 0, 3, 3]]
+        assert N(sk.quantize_values([[0.0, 0.5, 1.5, 3.0]], sk.QuantConfig(2, 4)).codes()).tolist() == [[0, 1, 2, 3]]
+
+    @pytest.mark.parametrize("bits", [1, 2, 4, 8])
+    def test_matches_oracle_bit_exact(self, bits):
+        V = np.random.default_rng(bits + 10).standard_normal((200, 64)) * 3.0
+        q = sk.quantize_values(V, sk.QuantConfig(bits=bits, group_size=32))
+        o = O.quantize(V, bits, 32)
+        np.testing.assert_array_equal(N(q.packed), o.packed)
+        np.testing.assert_array_equal(N(q.scales), o.scales)
+        np.testing.assert_array_equal(N(q.zeros), o.zeros)
+        np.testing.assert_array_equal(N(sk.dequantize_values(q)), O.dequantize(o))
+        np.testing.assert_array_equal(N(sk.dequantize_values(q, rows=[5, 20])), O.dequantize(o, [5, 20]))
+
+    def test_rejections(self):
+        bad = np.zeros((2, 4))
+        bad[0, 0] = np.inf
+        with pytest.raises(ValueError, match="non-finite"):
+            sk.quantize_values(bad, sk.QuantConfig(2, 4))
+        with pytest.raises(ValueError, match="group_size"):
+            sk.quantize_values(np.zeros((2, 8)), sk.QuantConfig(2, 16))
+        with pytest.raises(ValueError, match="16-bit parameter range"):
+            sk.quantize_values(np.array([[0.0, 1e6, 0.0, 0.0]]), sk.QuantConfig(2, 4))
+
+    def test_dequant_counter(self):
+        q = sk.quantize_values(np.zeros((30, 8)), sk.QuantConfig(2, 4))
+        with sk.collect() as ops:
+            sk.dequantize_values(q, rows=[1, 2, 3])
+        assert ops.dequant_rows == 3
+
+
+class TestKeyMagnitudes:   # test_quantizer.py:311-402
+    def test_exact_recompose(self):
+        K = np.array([[0.5, -0.25, 1.0, -1.0]])
+        a = np.array([0.5, 0.25, 1.0, 1.0])
+        q = sk.quantize_key_magnitudes(K, a, sk.QuantConfig(2, 4))
+        assert N(q.scales).tolist() == [[0.0]] and N(q.zeros).tolist() == [[1.0]]
+        np.testing.assert_array_equal(N(sk.dequantize_keys(q, a, sk.encode_keys(K))), K)
+
+    def test_zero_channel(self):
+        q = sk.quantize_key_magnitudes(np.zeros((3, 4)), np.zeros(4), sk.QuantConfig(2, 4))
+        np.testing.assert_array_equal(N(sk.dequantize_values(q)), np.zeros((3, 4)))
+
+    def test_dominate(self):
+        with pytest.raises(ValueError, match="dominate"):
+            sk.quantize_key_magnitudes(np.full((2, 4), 3.0), np.ones(4), sk.QuantConfig(2, 4))
+
+    def test_sign_flip_isolation(self):
+        rng = np.random.default_rng(13)
+        K = rng.standard_normal((6, 8))
+        K -= K.mean(axis=0)
+        a = np.abs(K).max(axis=0)
+        q = sk.quantize_key_magnitudes(K, a, sk.QuantConfig(8, 4))
+        codes = sk.encode_keys(K)
+        base = N(sk.dequantize_keys(q, a, codes))
+        raw = N(codes.unpack()).copy()
+        raw[2, 1] ^= 0b1000
+        flipped = N(sk.dequantize_keys(q, a, sk.SignCodeMatrix.from_codes(raw)))
+        diff = flipped - base
+        assert diff[2, 4] == pytest.approx(-2 * base[2, 4])
+        diff[2, 4] = 0.0
+        np.testing.assert_array_equal(diff, np.zeros_like(diff))
+
+    def test_matches_oracle(self):
+        rng = np.random.default_rng(15)
+        K = rng.standard_normal((256, 32)) * 2.0
+        K -= K.mean(axis=0)
+        a = np.abs(K).max(axis=0)
+        q = sk.quantize_key_magnitudes(K, a, sk.QuantConfig(4, 32))
+        o = O.quantize_key_mags(K, a, 4, 32)
+        np.testing.assert_array_equal(N(q.packed), o.packed)
+        np.testing.assert_array_equal(N(sk.dequantize_keys(q, a, sk.encode_keys(K))),
+                                      O.dequantize_keys(o, a, O.sign_codes(K)))
+
+    def test_shape_mismatch(self):
+        q = sk.quantize_values(np.zeros((4, 8)), sk.QuantConfig(2, 4))
+        with pytest.raises(ValueError, match="sign codes"):
+            sk.dequantize_keys(q, np.ones(8), sk.encode_keys(np.zeros((5, 8))))
+
+
+class TestRetrieval:   # test_retrieval.py
+    def _single(self):
+        K = np.array([[0.5, -0.3, 1.2, -0.1]])
+        return sk.build_codebook(K, sk.encode_keys(K))
+
+    def test_lut(self):
+        lut = sk.build_lut([1.0, 0.0, 0.0, 0.0], self._single())
+        assert N(lut.table).shape == (1, 16) and N(lut.table)[0, 10] == pytest.approx(0.5)
+        assert N(sk.build_lut(np.ones(4) * 7.0, self._single()).table)[0, 3] == 0.0
+        with pytest.raises(ValueError, match="channels"):
+            sk.build_lut(np.ones(8), self._single())
+
+    def test_singleton_scores_exact(self):
+        rng = np.random.default_rng(1)
+        pats = np.array([[(1.0 if (j >> (3 - p)) & 1 else -1.0) for p in range(4)] for j in range(16)])
+        K = np.hstack([np.abs(rng.standard_normal((16, 4))) * pats for _ in range(3)])
+        codes = sk.encode_keys(K)
+        q = rng.standard_normal(12)
+        np.testing.assert_allclose(N(sk.score_tokens(sk.build_lut(q, sk.build_codebook(K, codes)), codes)), K @ q,
+                                   rtol=1e-6)
+
+    def test_op_counts(self):
+        rng = np.random.default_rng(2)
+        K = rng.standard_normal((40, 16))
+        codes = sk.encode_keys(K)
+        lut = sk.build_lut(rng.standard_normal(16), sk.build_codebook(K, codes))
+        with sk.collect() as ops:
+            sk.score_tokens(lut, codes)
+        assert (ops.lut_lookups, ops.lut_adds, ops.score_muls) == (160, 120, 0)
+
+    def test_group_mismatch(self):
+        with pytest.raises(ValueError, match="groups"):
+            sk.score_tokens(sk.build_lut(np.ones(4), self._single()), sk.encode_keys(np.ones((2, 8))))
+
+    def test_sign_lut(self):
+        rng = np.random.default_rng(3)
+        K = rng.standard_normal((20, 8))
+        q = rng.standard_normal(8)
+        np.testing.assert_allclose(N(sk.score_tokens(sk.build_sign_lut(q, 2), sk.encode_keys(K))),
+                                   np.where(K >= 0, 1.0, -1.0) @ q)
+
+    def test_top_k(self):
+        assert N(sk.top_k_select([0.1, 5.0, 3.0, 2.0], k=2).indices).tolist() == [1, 2]
+        assert N(sk.top_k_select([0.1, 5.0, 3.0, 2.0], k=2, sink={0}).indices).tolist() == [0, 1, 2]
+        assert N(sk.top_k_select([1.0, 1.0, 0.0], k=1).indices).tolist() == [0]
+        sel = sk.top_k_select([1.0, 2.0, 3.0, 4.0], k=1, sink={0, 1}, recent={1, 2})
+        assert N(sel.indices).tolist() == [0, 1, 2, 3]
+        assert (sel.sink_count, sel.recent_count, sel.dynamic_count) == (2, 1, 1)
+        assert sk.top_k_select([3.0, 1.0, 2.0], k=10, sink={0}).dynamic_count == 2
+        assert N(sk.top_k_select([3.0, 1.0, 2.0], k=0, recent={2}).indices).tolist() == [2]
+        assert N(sk.top_k_select([-0.0, 0.0, -1.0], k=1).indices).tolist() == [0]
+        with pytest.raises(ValueError, match="out of range"):
+            sk.top_k_select([1.0, 2.0], k=1, sink={5})
+        with pytest.raises(ValueError, match="non-negative"):
+            sk.top_k_select([1.0], k=-1)
+
+    def test_top_k_random_vs_oracle(self):
+        rng = np.random.default_rng(5)
+        for L in (1, 7, 33, 1000, 5000):
+            s = np.round(rng.standard_normal(L) * 4) / 4      # many exact ties
+            for k in (0, 1, 5, L // 3, L):
+                sink = set(rng.integers(0, L, size=min(3, L)).tolist())
+                got = sk.top_k_select(s, k, sink=sink)
+                assert N(got.indices).tolist() == O.top_k(s, k, sink=sink)[0].tolist()
+
+    def test_resolve(self):
+        assert sk.resolve_dynamic_k(4096, 64, budget=160) == 96
+        assert sk.resolve_dynamic_k(4096, 0, sparsity=0.075) == 307
+        assert sk.resolve_dynamic_k(1000, 0, sparsity=0.0755) == 76
+        with pytest.raises(ValueError, match="exactly one"):
+            sk.resolve_dynamic_k(100, 0)
+
+
+class TestCacheAttention:   # test_cache.py, test_attention.py
+    def test_single_token(self):
+        cache = sk.prefill(np.array([[1.0, -2.0, 3.0, -4.0]]), np.array([[5.0, 6.0, 7.0, 8.0]]),
+                           config=sk.CacheConfig(bits=2, group_size=4, sink_count=64))
+        assert N(cache.codes.unpack()).tolist() == [[15]]
+        Kr, Vr = cache.gather(np.array([0]))
+        np.testing.assert_array_equal(N(Kr), np.zeros((1, 4)))
+        np.testing.assert_array_equal(N(Vr), [[5.0, 6.0, 7.0, 8.0]])
+
+    def test_append_forced_and_centered(self):
+        u = gen_unit(48, 16, 2, 7, bf16=False)
+        cache = sk.prefill(u.keys, u.values, config=sk.CacheConfig(sink_count=4, group_size=16))
+        sk.append_token(cache, u.keys[5], u.values[5])
+        sk.append_token(cache, u.keys[1], u.values[1])
+        assert cache.length == 50
+        sel = sk.select_tokens(cache, np.zeros(16), k=0)
+        assert N(sel.indices).tolist() == [0, 1, 2, 3, 48, 49]
+        Kr, Vr = cache.gather(np.array([48]))
+        np.testing.assert_array_equal(N(Kr)[0], u.keys[5] - N(cache.norm.mu))
+        np.testing.assert_array_equal(N(Vr)[0], u.values[5])
+
+    def test_lossless_full_selection_exact(self):
+        u = gen_unit(96, 16, 4, 2, bf16=False)
+        cache = sk.prefill(u.keys, u.values, config=sk.CacheConfig(bits=16, sink_count=8, group_size=16))
+        Kp = N(sk.apply_normalization(u.keys, cache.norm))
+        for q in u.queries:
+            sel = sk.select_tokens(cache, q, k=cache.prefill_length)
+            err = sk.output_error(sk.sparse_attention(q, sel, cache), sk.exact_attention(q, Kp, u.values))
+            assert err.rel_l2 <= 1e-5
+
+    def test_dequant_row_contract(self):
+        u = gen_unit(256, 32, 4, 2, bf16=False)
+        cache = sk.prefill(u.keys, u.values, config=sk.CacheConfig(sink_count=8))
+        for k in (4, 32):
+            sel = sk.select_tokens(cache, u.queries[0], k=k)
+            with sk.collect() as ops:
+                sk.sparse_attention(u.queries[0], sel, cache)
+            assert ops.dequant_rows == 2 * sel.dynamic_count
+
+    def test_empty_selection(self):
+        u = gen_unit(96, 16, 4, 2, bf16=False)
+        cache = sk.prefill(u.keys, u.values, config=sk.CacheConfig(sink_count=0, group_size=16))
+        with pytest.raises(ValueError, match="empty"):
+            sk.sparse_attention(u.queries[0], sk.top_k_select(np.zeros(96), k=0), cache)
+
+    def test_validation(self):
+        with pytest.raises(ValueError, match="must match"):
+            sk.prefill(np.ones((4, 8)), np.ones((5, 8)))
+        with pytest.raises(ValueError, match="divisible by 4"):
+            sk.prefill(np.ones((4, 6)), np.ones((4, 6)))
+        with pytest.raises(ValueError, match="group_size"):
+            sk.prefill(np.ones((4, 8)), np.ones((4, 8)), config=sk.CacheConfig(group_size=32))
+        with pytest.raises(ValueError, match="at least one row"):
+            sk.compute_channel_stats(np.empty((0, 4)))
+        bad = np.ones((2, 4))
+        bad[1, 2] = np.nan
+        with pytest.raises(ValueError, match="non-finite"):
+            sk.compute_channel_stats(bad)
+
+    def test_read_only_checksum(self):
+        u = gen_unit(256, 32, 8, 10, bf16=False)
+        cache = sk.prefill(u.keys, u.values, u.window, sk.CacheConfig(sink_count=16))
+        before = cache.checksum()
+        for q in u.queries:
+            sel = sk.select_tokens(cache, q, budget=40)
+            sk.sparse_attention(q, sel, cache)
+            sk.select_tokens(cache, q, sparsity=0.1, sign_only=True)
+        assert cache.checksum() == before
+
+    def test_stats_hand_example(self):
+        st = sk.compute_channel_stats([[1, 3], [3, 5]])
+        assert N(st.mu).tolist() == [2.0, 4.0] and N(st.alpha).tolist() == [1.0, 1.0]
+        np.testing.assert_array_equal(N(sk.apply_normalization([[1, 3], [3, 5]], st)), [[-1, -1], [1, 1]])
+
+    def test_stats_fp64_inputs_exact(self):
+        """Non-bf16 float64 keys: the exactness certificate fails and the sequential
+        fallback must still reproduce numpy's bits."""
+        K = np.random.default_rng(9).standard_normal((3000, 32)) * np.exp(np.random.default_rng(1).standard_normal(32))
+        st = sk.compute_channel_stats(K)
+        mu, al = O.channel_stats(K)
+        np.testing.assert_array_equal(N(st.mu), mu)
+        np.testing.assert_array_equal(N(st.alpha), al)
