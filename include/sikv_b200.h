@@ -90,11 +90,16 @@ int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64
  * cap = candidate buffer entries (0 = choose); needs sikv_decode_smem_bytes <= 227 KB. */
 int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap);
 int sikv_decode_default_cap(int64_t tokens, int k, int sinks);
+size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens);
+/* kernel: 0 = auto (persistent warp-specialised kernel when a workspace of
+ * sikv_decode_workspace_bytes is given, it fits shared memory and units >= 2 x SMs),
+ * 1 = one CTA per unit, 2 = force the persistent kernel. */
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
                      int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq,
                      int k, int cap, float* out, float* lse, int32_t* sel, int sel_stride,
-                     int32_t* sel_count, int32_t* diag, void* stream);
+                     int32_t* sel_count, int32_t* diag, void* workspace, size_t workspace_bytes,
+                     int kernel, void* stream);
 
 /* forced rows (sinks then recents; float32 centred K' and V) -> the decode kernel's fp16
  * mma-fragment blocks of 16 rows: forced_frag [U][frag_blocks][2][32][32] u32.  Re-packs the

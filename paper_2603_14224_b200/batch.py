@@ -179,10 +179,25 @@ class DecodeOutput:
     diag: torch.Tensor | None         # [U] int32
 
 
+_WS: dict = {}
+
+
+def _workspace(units: int, tokens: int, device) -> torch.Tensor:
+    need = L_.lib().sikv_decode_workspace_bytes(units, tokens)
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
 def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_selection: bool = False,
                 with_lse: bool = False, with_diag: bool = False, out: torch.Tensor | None = None,
-                sel_buf: torch.Tensor | None = None) -> DecodeOutput:
-    """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16)."""
+                sel_buf: torch.Tensor | None = None, kernel: int = 0) -> DecodeOutput:
+    """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
+
+    kernel: 0 auto, 1 one CTA per unit, 2 warp-specialised persistent kernel."""
     U = cb.units
     if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
         raise ValueError(f"q must be [{U}, Gq, {FD}], got {tuple(q.shape)}")
@@ -201,11 +216,12 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
         sel = sel_buf if sel_buf is not None else torch.empty(U, max(stride, 1), device=dev, dtype=torch.int32)
         cnt = torch.empty(U, device=dev, dtype=torch.int32)
     diag = torch.empty(U, device=dev, dtype=torch.int32) if with_diag else None
+    ws = _workspace(U, cb.tokens, dev)
     L_.call("sikv_decode_step", L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], cb.recent, L_.ptr(qf), U,
             cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), max(stride, 1) if sel is not None else 0, L_.ptr(cnt),
-            L_.ptr(diag), L_.stream())
+            L_.ptr(diag), L_.ptr(ws), ws.numel(), kernel, L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)
 
 

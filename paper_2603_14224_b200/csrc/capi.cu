@@ -30,6 +30,11 @@ cudaError_t launch_pack_forced(const float*, const float*, int, const float*, co
 cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
                               cudaStream_t);
 cudaError_t set_decode_profile(long long*);
+int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap);
+size_t ws_workspace_bytes(int64_t U, int64_t L);
+cudaError_t launch_decode_ws(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
+                             const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*,
+                             float*, int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
 // generic.cu
 cudaError_t launch_lut_f64(const double*, const double*, int64_t, int, int, double*, cudaStream_t);
 cudaError_t launch_score_f64(const double*, const uint8_t*, int64_t, int, int64_t, double*, cudaStream_t);
@@ -59,6 +64,12 @@ static int cuda_ret(cudaError_t e, const char* where) {
 static bool good_dtype(int d) { return d == IN_F32 || d == IN_F64 || d == IN_BF16; }
 static bool good_bits(int b) { return b == 1 || b == 2 || b == 4 || b == 8; }
 static bool good_group(int g) { return g == 4 || g == 8 || g == 16 || g == 32 || g == 64 || g == 128; }
+static int num_sms() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
 static int max_smem() {
   int dev = 0, v = 0;
   cudaGetDevice(&dev);
@@ -91,7 +102,7 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
     REQUIRE(dim <= 128, SIKV_EUNSUPPORTED, "encoder supports dim <= 128");
   }
   REQUIRE(bits == 0 || good_bits(bits), SIKV_EINVAL, "bits must be one of (1, 2, 4, 8) or 0 (lossless)");
-  REQUIRE(bits == 0 || (good_group(group_size) && dim % group_size == 0), SIKV_EINVAL,
+  REQUIRE(!(what & 2) || bits == 0 || (good_group(group_size) && dim % group_size == 0), SIKV_EINVAL,
           "channel count not divisible by group_size (group_size must be 4..128, power of two)");
   REQUIRE(what >= 1 && what <= 3, SIKV_EINVAL, "what must be 1, 2 or 3");
   if (what & 2) {
@@ -145,6 +156,7 @@ int sikv_decode_default_cap(int64_t tokens, int k, int sinks) {
   // fit on one SM (2 x 113 KB) when possible.
   const int64_t ncand = std::max<int64_t>(tokens - sinks, 0);
   const int64_t keff = std::min<int64_t>(k, ncand);
+  if (keff == 0 || keff == ncand) return 1024;        // no candidate selection needed
   int64_t cap = std::max<int64_t>(2 * keff + 1024, 1024);
   const int64_t floor_cap = std::max<int64_t>(keff + keff * 2 / 5 + 512, 1024);
   while (cap > floor_cap && decode_layout(tokens, k, sinks, 8, (int)cap).total > 113 * 1024) cap -= 64;
@@ -173,11 +185,13 @@ int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const 
                   "sikv_pack_forced");
 }
 
+size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens) { return ws_workspace_bytes(units, tokens); }
+
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
                      int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq, int k,
                      int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                     int32_t* diag, void* stream) {
+                     int32_t* diag, void* workspace, size_t workspace_bytes, int kernel, void* stream) {
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
@@ -191,6 +205,23 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   const int64_t keff = std::min<int64_t>(k, tokens - sinks);
   REQUIRE(sinks + keff + recent >= 1, SIKV_EINVAL, "selection is empty");
   REQUIRE(!sel || sel_stride >= sinks + keff + recent, SIKV_EINVAL, "sel_stride too small");
+  // kernel: 0 = auto, 1 = one CTA per unit, 2 = warp-specialised persistent
+  REQUIRE(kernel >= 0 && kernel <= 2, SIKV_EINVAL, "kernel must be 0, 1 or 2");
+  if (kernel != 1 && workspace && workspace_bytes >= ws_workspace_bytes(units, tokens)) {
+    int wcap = cap > 0 ? cap : sikv_decode_default_cap(tokens, k, sinks);
+    // the persistent kernel keeps two hand-off slots; shrink the candidate buffer to fit
+    const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
+    const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
+    while (cap <= 0 && wcap > floor_cap && ws_smem_bytes(tokens, k, sinks, gq, wcap) > max_smem()) wcap -= 64;
+    const bool fits = ws_smem_bytes(tokens, k, sinks, gq, wcap) <= max_smem();
+    if (fits && (kernel == 2 || units >= 2 * num_sms())) {
+      return cuda_ret(launch_decode_ws(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
+                                       frag_blocks, recent, q, units, tokens, gq, k, wcap, out, lse, sel,
+                                       sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
+                      "sikv_decode_step");
+    }
+    REQUIRE(kernel != 2, SIKV_EUNSUPPORTED, "the persistent kernel does not fit this configuration");
+  }
   if (cap <= 0) cap = sikv_decode_default_cap(tokens, k, sinks);
   int need = decode_layout(tokens, k, sinks, gq, cap).total;
   REQUIRE(need <= max_smem(), SIKV_EUNSUPPORTED,

@@ -1,0 +1,672 @@
+// Device building blocks of the fused decode step, shared by the one-unit-per-CTA kernel
+// (decode.cu) and the warp-specialised persistent kernel (decode_ws.cu).
+#pragma once
+#include "common.cuh"
+#include "select.cuh"
+
+namespace sikv {
+
+constexpr int TBL_BYTES = 256 * 64 * 4;   // pair table: 256 byte values x 64 columns
+constexpr int NB = 8;                     // chunks (of 256 tokens) scored per thread per batch
+constexpr int STAGE_BYTES = 16 * FREC;    // one 16-token block of records
+constexpr int MAX_SAMPLE_CHUNKS = 8;
+
+// ---------------------------------------------------------------- pair table
+// LUT[g][c] = q-bar_g . centroid[g][c] (float32, no FMA, the reference pairing) and the
+// byte-pair table T[b][col] = LUT[2p][b & 15] + LUT[2p+1][b >> 4], p = col mod 16.
+template <class Grp>
+__device__ __forceinline__ void build_pair_table(const float* __restrict__ cent, const float* qbar, float* lut,
+                                                 char* T) {
+  const int tid = Grp::tid();
+  for (int e = tid; e < 512; e += DT) {
+    const int g = e >> 4;
+    const float4 c = reinterpret_cast<const float4*>(cent)[e];
+    const float q0 = qbar[4 * g], q1 = qbar[4 * g + 1], q2 = qbar[4 * g + 2], q3 = qbar[4 * g + 3];
+    lut[e] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                       __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+  }
+  Grp::sync();
+  for (int e = tid; e < 256 * 16; e += DT) {
+    const int b = e >> 4, p = e & 15;
+    const float v = __fadd_rn(lut[(2 * p) * 16 + (b & 15)], lut[(2 * p + 1) * 16 + (b >> 4)]);
+    float* row = reinterpret_cast<float*>(T) + b * 64;
+    row[p] = v; row[p + 16] = v; row[p + 32] = v;
+  }
+  Grp::sync();
+}
+
+// ---------------------------------------------------------------- scoring
+// score of the token whose 16-byte rotated sign record is w; lb = byte offset of this
+// lane's first column (64*half + 4*j); T = pair table (row stride 256 B).  Pairs are
+// summed left to right starting at pair (t mod 16) — the order oracle/restate32.py states.
+__device__ __forceinline__ float score_token(const uint4 w, uint32_t lb, const char* T) {
+  const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t off = prmt(ww[i >> 2], lb, 0x5504u | ((uint32_t)(i & 3) << 4));
+    const float v = *reinterpret_cast<const float*>(T + off + 4 * i);
+    s = (i == 0) ? v : __fadd_rn(s, v);
+  }
+  return s;
+}
+
+// N tokens at once: the 16-step chains of different tokens interleave, hiding FADD latency
+template <int N>
+__device__ __forceinline__ void score_batch(const uint4 (&w)[N], uint32_t lb, const char* T, float (&s)[N]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+#pragma unroll
+    for (int x = 0; x < N; ++x) {
+      const uint32_t wd = (i >> 2) == 0 ? w[x].x : (i >> 2) == 1 ? w[x].y : (i >> 2) == 2 ? w[x].z : w[x].w;
+      const uint32_t off = prmt(wd, lb, 0x5504u | ((uint32_t)(i & 3) << 4));
+      const float v = *reinterpret_cast<const float*>(T + off + 4 * i);
+      s[x] = (i == 0) ? v : __fadd_rn(s[x], v);
+    }
+  }
+}
+
+__device__ __forceinline__ bool forced_bit(const uint32_t* fb, int64_t t) {
+  return (fb[t >> 5] >> (t & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t unkey_bits(uint32_t k2) {
+  return (k2 & 0x80000000u) ? (k2 & 0x7FFFFFFFu) : ~k2;
+}
+
+// ---------------------------------------------------------------- async staging
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// stage the 16 records of one dynamic block into shared memory, 16-byte chunk k of token j
+// stored at chunk k ^ (j & 7) so the fragment reads below are bank-conflict free
+__device__ __forceinline__ void stage_block(char* buf, const uint8_t* recs, const int32_t* dyn, int base,
+                                            int ndyn, int lane) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int c = lane + 32 * r, j = c >> 3, kk = c & 7;
+    const int t = dyn[min(base + j, ndyn - 1)];
+    cp_async16(buf + j * FREC + 16 * (kk ^ (j & 7)), recs + (int64_t)t * FREC + 16 * kk);
+  }
+}
+__device__ __forceinline__ const char* chunk(const char* buf, int j, int kk) {
+  return buf + j * FREC + 16 * (kk ^ (j & 7));
+}
+
+// ---------------------------------------------------------------- sparse attention
+// One warp's flash-decode state for the unit's GQA group: q~ fragments (rows = heads),
+// O^T accumulators (M = 128 channels as 8 m-tiles, N = 8 heads), running max / sum of head g.
+struct Attn {
+  uint32_t qa[8][2];
+  float o[8][4];
+  float mrun, lrun;
+};
+
+__device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float* ahat, int Gq, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int d = 16 * s + 2 * t4 + 8 * e;
+      float x0 = 0.f, x1 = 0.f;
+      if (g < Gq) { x0 = qs[g * FD + d] * ahat[d]; x1 = qs[g * FD + d + 1] * ahat[d + 1]; }
+      A.qa[s][e] = h2u(__floats2half2_rn(x0, x1));
+    }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) A.o[m][0] = A.o[m][1] = A.o[m][2] = A.o[m][3] = 0.f;
+  A.mrun = -INFINITY;
+  A.lrun = 0.f;
+}
+
+constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;   // log2(e) / sqrt(128)
+// fp16 magic for a 2-bit code at bits [2i, 2i+2) of each half: 2^(10-2i), so that
+// (w & mask_i) | magic_i is the half 2^(10-2i) + code exactly
+__host__ __device__ constexpr uint32_t kMagic(int i) { return ((25u - 2u * (uint32_t)i) << 10) * 0x00010001u; }
+
+// online softmax update + P V for one 16-token block (scores for head g in sacc)
+template <typename VFrag>
+__device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][4], const bool (&valid)[2][2],
+                                                int lane, VFrag&& vfrag) {
+  const int t4 = lane & 3;
+  float x[4];
+  x[0] = valid[0][0] ? sacc[0][0] * kSoftmaxScale : -INFINITY;
+  x[1] = valid[0][1] ? sacc[0][1] * kSoftmaxScale : -INFINITY;
+  x[2] = valid[1][0] ? sacc[1][0] * kSoftmaxScale : -INFINITY;
+  x[3] = valid[1][1] ? sacc[1][1] * kSoftmaxScale : -INFINITY;
+  float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+  const float mnew = fmaxf(A.mrun, bm);
+  const float fac = exp2f(A.mrun - mnew);
+  A.mrun = mnew;
+  const __half2 p01 = __floats2half2_rn(exp2f(x[0] - mnew), exp2f(x[1] - mnew));
+  const __half2 p23 = __floats2half2_rn(exp2f(x[2] - mnew), exp2f(x[3] - mnew));
+  const float2 f01 = __half22float2(p01), f23 = __half22float2(p23);
+  A.lrun = A.lrun * fac + ((f01.x + f01.y) + (f23.x + f23.y));
+  if (!__all_sync(0xffffffffu, fac == 1.0f)) {   // the running max moved for some head
+    const float fa = __shfl_sync(0xffffffffu, fac, 8 * t4);
+    const float fb = __shfl_sync(0xffffffffu, fac, 8 * t4 + 4);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) { A.o[m][0] *= fa; A.o[m][1] *= fb; A.o[m][2] *= fa; A.o[m][3] *= fb; }
+  }
+#pragma unroll
+  for (int mp = 0; mp < 4; ++mp) {
+    uint32_t v[2][4];      // [m - 2mp][a0..a3]
+    vfrag(mp, v);
+    mma16816(A.o[2 * mp], v[0][0], v[0][1], v[0][2], v[0][3], h2u(p01), h2u(p23));
+    mma16816(A.o[2 * mp + 1], v[1][0], v[1][1], v[1][2], v[1][3], h2u(p01), h2u(p23));
+  }
+}
+
+// forced rows (sinks then recents), pre-packed as fp16 fragments; this warp takes blocks
+// wi, wi + nw, ... of [0, nbf)
+__device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, int nf, int wi, int nw, int lane) {
+  const int t4 = lane & 3;
+  const int nbf = (nf + 15) >> 4;
+  for (int blk = wi; blk < nbf; blk += nw) {
+    const int base = blk * 16;
+    const uint4* fk = reinterpret_cast<const uint4*>(ffrag_u + ((int64_t)blk * 2 * 32 + lane) * 32);
+    const uint4* fv = fk + 32 * 8;
+    uint32_t kwd[32], vwd[32];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 t = __ldg(fk + i);
+      kwd[4 * i] = t.x; kwd[4 * i + 1] = t.y; kwd[4 * i + 2] = t.z; kwd[4 * i + 3] = t.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 t = __ldg(fv + i);
+      vwd[4 * i] = t.x; vwd[4 * i + 1] = t.y; vwd[4 * i + 2] = t.z; vwd[4 * i + 3] = t.w;
+    }
+    float sacc[2][4];
+    bool valid[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, kwd[nt * 16 + 2 * s], kwd[nt * 16 + 2 * s + 1]);
+      valid[nt][0] = base + 2 * t4 + 8 * nt < nf;
+      valid[nt][1] = base + 2 * t4 + 1 + 8 * nt < nf;
+    }
+    attn_softmax_pv(A, sacc, valid, lane, [&](int mp, uint32_t (&v)[2][4]) {
+#pragma unroll
+      for (int mm = 0; mm < 2; ++mm)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[mm][r] = vwd[(2 * mp + mm) * 4 + r];
+    });
+  }
+}
+
+// dynamic rows: blocks first, first + nw, ... of [0, nbd), staged by cp.async (double
+// buffered) and dequantised into mma fragments
+__device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, const int32_t* dyn, int ndyn,
+                                             int first, int nw, char* stage, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nbd = (ndyn + 15) >> 4;
+  if (first < nbd) stage_block(stage, recs_u, dyn, first * 16, ndyn, lane);
+  cp_commit();
+  int buf = 0;
+  for (int db = first; db < nbd; db += nw) {
+    if (db + nw < nbd) stage_block(stage + (buf ^ 1) * STAGE_BYTES, recs_u, dyn, (db + nw) * 16, ndyn, lane);
+    cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+    const char* sb = stage + buf * STAGE_BYTES;
+    const int base = db * 16;
+    float sacc[2][4];
+    bool valid[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int j = g + 8 * nt;
+      const uint2 kw = *reinterpret_cast<const uint2*>(chunk(sb, j, t4 >> 1) + 8 * (t4 & 1));
+      const uint4 kp = *reinterpret_cast<const uint4*>(chunk(sb, j, 4));
+      const uint32_t ks = *reinterpret_cast<const uint32_t*>(chunk(sb, j, 6) + 4 * t4);
+      const uint32_t par[4] = {kp.x, kp.y, kp.z, kp.w};
+      const uint32_t wsrc[4] = {kw.x, kw.x >> 8, kw.y, kw.y >> 8};   // slots 0-3 / 4-7 of each word
+      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+      for (int grp = 0; grp < 4; ++grp) {
+        const __half2 qs2 = u2h(prmt(par[grp], par[grp], 0x1010u));
+        const __half2 zp2 = u2h(prmt(par[grp], par[grp], 0x3232u));
+#pragma unroll
+        for (int ss = 0; ss < 2; ++ss) {
+          const int s = 2 * grp + ss, uu = s >> 2;
+          uint32_t b[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = ((s & 3) << 1) | e;
+            const uint32_t src = wsrc[2 * uu + (i >> 2)];
+            const int ii = i & 3;
+            const uint32_t xx = lop3_and_or(src, 0x00030003u << (2 * ii), kMagic(ii));
+            const __half2 c = __hsub2(u2h(xx), u2h(kMagic(ii)));
+            const uint32_t v = h2u(__hfma2(c, qs2, zp2));
+            b[e] = lop3_xor_and(v, ks << (15 - (8 * uu + i)), 0x80008000u);
+          }
+          mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, b[0], b[1]);
+        }
+      }
+      valid[nt][0] = base + 2 * t4 + 8 * nt < ndyn;
+      valid[nt][1] = base + 2 * t4 + 1 + 8 * nt < ndyn;
+    }
+    // V words and params of tokens 2t4, 2t4+1, 2t4+8, 2t4+9
+    uint32_t vw[4];
+    uint4 vp[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int j = 2 * t4 + (x & 1) + 8 * (x >> 1);
+      vw[x] = *reinterpret_cast<const uint32_t*>(chunk(sb, j, 2 + (g >> 2)) + 4 * (g & 3));
+      vp[x] = *reinterpret_cast<const uint4*>(chunk(sb, j, 5));
+    }
+    attn_softmax_pv(A, sacc, valid, lane, [&](int jg, uint32_t (&v)[2][4]) {
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        const uint32_t pa[4] = {vp[2 * pr].x, vp[2 * pr].y, vp[2 * pr].z, vp[2 * pr].w};
+        const uint32_t pb[4] = {vp[2 * pr + 1].x, vp[2 * pr + 1].y, vp[2 * pr + 1].z, vp[2 * pr + 1].w};
+        const uint32_t xj = prmt(vw[2 * pr], vw[2 * pr + 1],
+                                 (uint32_t)(jg | (jg << 4) | ((4 + jg) << 8) | ((4 + jg) << 12)));
+        const __half2 qs2 = u2h(prmt(pa[jg], pb[jg], 0x5410u));
+        const __half2 zp2 = u2h(prmt(pa[jg], pb[jg], 0x7632u));
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const uint32_t xx = lop3_and_or(xj, 0x00030003u << (2 * ii), kMagic(ii));
+          const __half2 c = __hsub2(u2h(xx), u2h(kMagic(ii)));
+          // m = 2jg + (ii >> 1), e = ii & 1 -> a-register 2*pr + e of fragment m
+          v[ii >> 1][2 * pr + (ii & 1)] = h2u(__hfma2(c, qs2, zp2));
+        }
+      }
+    });
+    __syncwarp();
+    buf ^= 1;
+  }
+  cp_wait<0>();
+}
+
+// this warp's partial (O, m, l) -> shared memory [nw][Gq][128], [nw][Gq], [nw][Gq]
+__device__ __forceinline__ void attn_write_partial(const Attn& A, float* part, float* pm, float* pl, int wi,
+                                                   int Gq, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  float l = A.lrun;
+  l += __shfl_xor_sync(0xffffffffu, l, 1);
+  l += __shfl_xor_sync(0xffffffffu, l, 2);
+  if (t4 == 0 && g < Gq) { pm[wi * Gq + g] = A.mrun; pl[wi * Gq + g] = l; }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int h0 = 2 * t4, h1 = 2 * t4 + 1, d0 = 16 * m + g, d1 = d0 + 8;
+    if (h0 < Gq) { part[(wi * Gq + h0) * FD + d0] = A.o[m][0]; part[(wi * Gq + h0) * FD + d1] = A.o[m][2]; }
+    if (h1 < Gq) { part[(wi * Gq + h1) * FD + d0] = A.o[m][1]; part[(wi * Gq + h1) * FD + d1] = A.o[m][3]; }
+  }
+}
+
+// fixed-order merge of the nw partials (caller synchronises before)
+__device__ __forceinline__ void attn_merge(const float* part, const float* pm, const float* pl, int nw, int Gq,
+                                           int gtid, int gsize, float* out_u, float* lse_u) {
+  for (int e = gtid; e < Gq * FD; e += gsize) {
+    const int h = e / FD, d = e % FD;
+    float M = -INFINITY;
+    for (int w = 0; w < nw; ++w) M = fmaxf(M, pm[w * Gq + h]);
+    float num = 0.f, den = 0.f;
+    for (int w = 0; w < nw; ++w) {
+      const float mw = pm[w * Gq + h];
+      const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      num += part[(w * Gq + h) * FD + d] * f;
+      den += pl[w * Gq + h] * f;
+    }
+    out_u[h * FD + d] = num / den;
+    if (lse_u && d == 0) lse_u[h] = (M + log2f(den)) * 0.6931471805599453f;
+  }
+}
+
+}  // namespace sikv
+
+namespace sikv {
+
+// ---------------------------------------------------------------- unit producer
+// Score every prefill token of one unit and collect the top-k candidates, run by a
+// 256-thread group Grp (the whole CTA, or the producer half of the persistent kernel).
+//
+// Selection modes: 0 nothing dynamic; 1 every candidate selected; 2 every candidate fits
+// the per-warp segments (threshold -inf); 3 sampled threshold tau.  Outputs: per-warp
+// candidate segments (x = key - tau, token) in cand, ms->wcnt / maxx / tau, and on return
+// `fallback` = the segments are unusable (overflow or too few).  In that case the caller
+// runs produce_exact().
+struct UnitGeom {
+  int64_t L;
+  int S, keff, mode, nchunks, capw, sstride, nsc;
+  int64_t flim;        // tokens below flim may be sinks
+};
+
+__device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw, const int32_t* sink_idx_u) {
+  UnitGeom g;
+  g.L = L;
+  g.S = S;
+  const int64_t ncand = L - S;
+  g.keff = (int)((int64_t)k < ncand ? (int64_t)k : ncand);
+  g.nchunks = (int)((L + 255) >> 8);
+  g.capw = capw;
+  if (g.keff == 0) g.mode = 0;
+  else if (g.keff == ncand) g.mode = 1;
+  else if ((int64_t)g.nchunks * 32 <= (int64_t)capw) g.mode = 2;
+  else g.mode = 3;
+  g.sstride = g.mode == 3 ? max(16, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
+  g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
+  g.flim = S > 0 ? (int64_t)sink_idx_u[S - 1] + 1 : 0;
+  return g;
+}
+
+__device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* signs, int tid,
+                                            uint4 (&w)[MAX_SAMPLE_CHUNKS]) {
+#pragma unroll
+  for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+    const int64_t t = (int64_t)x * g.sstride * 256 + tid;
+    w[x] = (x < g.nsc && t < g.L) ? __ldg(signs + t) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+// th / tmin: 256 + 256 words of scratch for the threshold histogram
+template <class Grp>
+__device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
+                                                   const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
+                                                   uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
+                                                   uint32_t& tau_out) {
+  const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
+  const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
+  const int capw = g.capw;
+  uint32_t* seg = cand + 2 * warp * capw;
+  int wc = 0;
+  uint32_t mx = 0;
+  uint32_t tau = 1;
+  if (tid == 0) { ms->maxx = 0; ms->bad = 0; }
+  if (g.mode == 3) {
+    // ---------------- B1: score the sample chunks (kept in registers)
+    uint32_t sk[MAX_SAMPLE_CHUNKS];
+    float sv[MAX_SAMPLE_CHUNKS];
+    score_batch(wsamp, lb, T, sv);
+    int nv = 0;
+    uint32_t smax = 0, smin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+      const int64_t t = (int64_t)x * g.sstride * 256 + tid;
+      uint32_t key = 0;
+      if (x < g.nsc && t < g.L && !(t < g.flim && forced_bit(forced, t))) key = f32_key(sv[x]);
+      sk[x] = key;
+      nv += key != 0;
+      smax = max(smax, key);
+      if (key) smin = min(smin, key);
+    }
+    nv = warp_sum(nv);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+      smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+    }
+    for (int i = tid; i < 256; i += DT) { th[i] = 0; tmin[i] = 0xFFFFFFFFu; }
+    if (tid == 0) { ms->nsv = 0; ms->tau = 0xFFFFFFFFu; }
+    Grp::sync();
+    if (lane == 0) { atomicAdd(&ms->nsv, nv); atomicMax(&ms->maxx, smax); atomicMin(&ms->tau, smin); }
+    Grp::sync();
+    const int nsv = ms->nsv;
+    const double e = (double)g.keff * (double)nsv / (double)(g.L - g.S);
+    int r = (int)ceil(e + 4.0 * sqrt(e) + 16.0);
+    r = min(r, nsv);
+    if (r >= 1) {
+      const uint32_t kmx = ms->maxx, kmn = ms->tau;
+      const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
+      const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
+#pragma unroll
+      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+        if (sk[x]) {
+          const int b = min(255, (int)((__uint_as_float(unkey_bits(sk[x])) - fmn) * scale));
+          atomicAdd(&th[b], 1);
+          atomicMin(&tmin[b], sk[x]);
+        }
+      }
+      Grp::sync();
+      if (warp == 0) {
+        int loc[8], s8 = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { loc[i] = th[255 - 8 * lane - i]; s8 += loc[i]; }
+        int inc = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += v;
+        }
+        int c = inc - s8;
+        if (c < r && r <= inc) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (c < r && r <= c + loc[i]) ms->digit = 255 - 8 * lane - i;
+            c += loc[i];
+          }
+        }
+      }
+      Grp::sync();
+      tau = tmin[ms->digit];          // smallest sample key in the boundary bin
+    }
+    Grp::sync();
+    if (tid == 0) ms->maxx = 0;
+    Grp::sync();
+    uint32_t bits = 0;
+#pragma unroll
+    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x)
+      if (x < g.nsc && sk[x] != 0 && sk[x] >= tau) bits |= 1u << x;
+    const int cnt = __popc(bits);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    int pos = wc + inc - cnt;
+    wc += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+      if ((bits >> x) & 1u) {
+        const uint32_t xk = sk[x] - tau;
+        if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(x * g.sstride * 256 + tid); }
+        mx = max(mx, xk);
+        ++pos;
+      }
+    }
+  }
+  // ---------------- B2: score everything else, keep score >= tau (compared as floats)
+  const float tauf = g.mode == 2 ? -INFINITY : __uint_as_float(unkey_bits(tau));
+  const int Li = (int)g.L;
+  int next_s = g.mode == 3 ? 0 : 0x7fffffff;      // next sample chunk (already scored in B1)
+  const int end_s = g.nsc * g.sstride;
+  // register double buffer: the loads of batch c0 + NB are in flight while batch c0 scores
+  auto load_batch = [&](int c0, uint4 (&w)[NB]) {
+    const int t0 = c0 * 256 + tid;
+    if ((c0 + NB) * 256 <= Li) {
+#pragma unroll
+      for (int x = 0; x < NB; ++x) w[x] = __ldg(signs + t0 + 256 * x);
+    } else {
+#pragma unroll
+      for (int x = 0; x < NB; ++x) w[x] = t0 + 256 * x < Li ? __ldg(signs + t0 + 256 * x) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 wn[NB];
+  load_batch(0, wn);
+  for (int c0 = 0; c0 < g.nchunks; c0 += NB) {
+    int xs = -1;
+    if (next_s < c0 + NB && next_s < end_s) { xs = next_s - c0; next_s += g.sstride; }
+    const int t0 = c0 * 256 + tid;
+    const bool full = (c0 + NB) * 256 <= Li;
+    uint4 w[NB];
+#pragma unroll
+    for (int x = 0; x < NB; ++x) w[x] = wn[x];
+    if (c0 + NB < g.nchunks) load_batch(c0 + NB, wn);
+    float sv[NB];
+    score_batch(w, lb, T, sv);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int x = 0; x < NB; ++x)
+      if (sv[x] >= tauf) bits |= 1u << x;
+    if (xs >= 0) bits &= ~(1u << xs);
+    if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NB ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
+    if (c0 * 256 < g.flim) {
+#pragma unroll
+      for (int x = 0; x < NB; ++x)
+        if (t0 + 256 * x < Li && forced_bit(forced, t0 + 256 * x)) bits &= ~(1u << x);
+    }
+    // warp-compacted append: one scan per batch
+    const int cnt = __popc(bits);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    int pos = wc + inc - cnt;
+    wc += __shfl_sync(0xffffffffu, inc, 31);
+    while (bits) {
+      const int x = __ffs(bits) - 1;
+      bits &= bits - 1;
+      float v = sv[0];
+#pragma unroll
+      for (int y = 1; y < NB; ++y) v = (x == y) ? sv[y] : v;
+      const uint32_t xk = f32_key(v) - tau;
+      if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(t0 + 256 * x); }
+      mx = max(mx, xk);
+      ++pos;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) { ms->wcnt[warp] = wc; atomicMax(&ms->maxx, mx); if (wc > capw) ms->bad = 1; }
+  Grp::sync();
+  int total = 0;
+  for (int w2 = 0; w2 < DW; ++w2) total += ms->wcnt[w2];
+  tau_out = tau;
+  return ms->bad || total < g.keff;
+}
+
+// Exact fallback: multi-pass radix select over rescored keys, then gt / eq bitmaps (zeroed
+// here; smem or global) of key > K* and key == K*.  hist needs NBIN + 33 ints.
+template <class Grp>
+__device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* signs, const char* T,
+                                              const uint32_t* forced, int* hist, Misc* ms, uint32_t* gt,
+                                              uint32_t* eq, uint32_t& kstar, int& need_eq, int& eq_count) {
+  const int tid = Grp::tid(), lane = tid & 31;
+  const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
+  const int64_t L = g.L;
+  const int nchunks = g.nchunks;
+  radix_kth<Grp>([&](auto f) {
+    for (int c = 0; c < nchunks; ++c) {
+      const int64_t t = (int64_t)c * 256 + tid;
+      if (t < L && !forced_bit(forced, t)) f(f32_key(score_token(__ldg(signs + t), lb, T)));
+    }
+  }, 0xFFFFFFFFu, g.keff, hist, ms, kstar, need_eq);
+  const int W = (int)((L + 31) >> 5);
+  for (int i = tid; i < 2 * W; i += DT) (i < W ? gt[i] : eq[i - W]) = 0u;
+  if (tid == 0) ms->nsv = 0;
+  __threadfence();
+  Grp::sync();
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t t = (int64_t)c * 256 + tid;
+    if (t < L && !forced_bit(forced, t)) {
+      const uint32_t key = f32_key(score_token(__ldg(signs + t), lb, T));
+      if (key > kstar) atomicOr(&gt[t >> 5], 1u << (t & 31));
+      else if (key == kstar) { atomicOr(&eq[t >> 5], 1u << (t & 31)); atomicAdd(&ms->nsv, 1); }
+    }
+  }
+  __threadfence();
+  Grp::sync();
+  eq_count = ms->nsv;
+}
+
+// Exact k-th key among the candidate segments, then the gt / eq bitmaps (zeroed here).
+template <class Grp>
+__device__ __forceinline__ void select_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
+                                                       uint32_t maxx, uint32_t tau, int* hist, Misc* ms,
+                                                       uint32_t* gt, uint32_t* eq, uint32_t& kstar,
+                                                       int& need_eq, int& eq_count) {
+  const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
+  const uint32_t* seg = cand + 2 * warp * g.capw;
+  const int n = wcnt[warp];
+  uint32_t xk;
+  radix_kth<Grp>([&](auto f) {
+    for (int i = lane; i < n; i += 32) f(seg[2 * i]);
+  }, maxx, g.keff, hist, ms, xk, need_eq);
+  kstar = xk + tau;
+  const int W = (int)((g.L + 31) >> 5);
+  for (int i = tid; i < W; i += DT) { gt[i] = 0u; eq[i] = 0u; }
+  if (tid == 0) ms->nsv = 0;
+  Grp::sync();
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t x = seg[2 * i], t = seg[2 * i + 1];
+    if (x > xk) atomicOr(&gt[t >> 5], 1u << (t & 31));
+    else if (x == xk) { atomicOr(&eq[t >> 5], 1u << (t & 31)); atomicAdd(&ms->nsv, 1); }
+  }
+  Grp::sync();
+  eq_count = ms->nsv;
+}
+
+// Ordered emission: dynamic list (smem) and the sorted selection (global, nullable).
+// Returns the dynamic count.
+template <class Grp>
+__device__ __forceinline__ int emit_selection(const UnitGeom& g, int mode, const uint32_t* forced,
+                                              const uint32_t* gt, const uint32_t* eq, int need_eq, int eq_count,
+                                              int32_t* dyn, int32_t* sel_u, int R, int32_t* sel_count_u,
+                                              Misc* ms) {
+  const int tid = Grp::tid();
+  const int64_t L = g.L;
+  const int W = (int)((L + 31) >> 5);
+  const int per = (W + DT - 1) / DT;
+  const int w0 = tid * per, w1 = min(W, w0 + per);
+  // ties at the k-th key: keep the lowest-index need_eq of them (prefix over the eq bitmap);
+  // when every tie is taken (the usual case) no prefix is needed
+  const bool all_eq = mode < 2 || eq_count == need_eq;
+  int eq_before = 0;
+  if (!all_eq) {
+    int my_eq = 0;
+    for (int x = w0; x < w1; ++x) my_eq += __popc(eq[x]);
+    int dummy, t1, t2;
+    block_exscan2<Grp>(my_eq, 0, eq_before, dummy, t1, t2, ms->wsum);
+  }
+  auto dbits = [&](int x, int& eb) -> uint32_t {
+    if (mode == 0) return 0u;
+    if (mode == 1) {
+      uint32_t d = ~forced[x];
+      if (x == W - 1 && (L & 31)) d &= (1u << (L & 31)) - 1u;
+      return d;
+    }
+    uint32_t e = eq[x];
+    if (!all_eq) {
+      const int take = min(max(need_eq - eb, 0), __popc(e));
+      eb += __popc(e);
+      while (__popc(e) > take) e &= ~(1u << (31 - __clz(e)));
+    }
+    return gt[x] | e;
+  };
+  int nd = 0, nsl = 0, eb = eq_before;
+  for (int x = w0; x < w1; ++x) {
+    const uint32_t d = dbits(x, eb);
+    nd += __popc(d);
+    nsl += __popc(d | forced[x]);
+  }
+  int dpos, spos, dtot, stot;
+  block_exscan2<Grp>(nd, nsl, dpos, spos, dtot, stot, ms->wsum);
+  eb = eq_before;
+  for (int x = w0; x < w1; ++x) {
+    uint32_t d = dbits(x, eb);
+    uint32_t sb = d | forced[x];
+    while (d) { const int b = __ffs(d) - 1; d &= d - 1; dyn[dpos++] = x * 32 + b; }
+    if (sel_u)
+      while (sb) { const int b = __ffs(sb) - 1; sb &= sb - 1; sel_u[spos++] = x * 32 + b; }
+  }
+  if (sel_u)
+    for (int r = tid; r < R; r += DT) sel_u[stot + r] = (int32_t)(L + r);
+  if (tid == 0 && sel_count_u) *sel_count_u = stot + R;
+  Grp::sync();
+  return dtot;
+}
+
+}  // namespace sikv

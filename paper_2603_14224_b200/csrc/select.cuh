@@ -1,13 +1,25 @@
-// Block-wide selection helpers shared by the fused decode kernel and the generic top-k.
+// Block-/group-wide selection helpers shared by the decode kernels and the generic top-k.
+// Helpers are templated on a thread group: the whole 256-thread CTA (Cta256) or a
+// 256-thread slice of a larger CTA synchronised by a named barrier (NamedGroup).
 #pragma once
 #include "common.cuh"
 
 namespace sikv {
 
-constexpr int DT = 256;            // threads per selection / decode CTA
+constexpr int DT = 256;            // threads per selection / decode group
 constexpr int DW = DT / 32;
 
-// ---------------------------------------------------------------- small block utilities
+struct Cta256 {
+  static __device__ __forceinline__ int tid() { return threadIdx.x; }
+  static __device__ __forceinline__ void sync() { __syncthreads(); }
+};
+template <int ID, int BASE>
+struct NamedGroup {                // threads [BASE, BASE + 256) of the CTA, barrier ID
+  static __device__ __forceinline__ int tid() { return (int)threadIdx.x - BASE; }
+  static __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, 256;\n" ::"n"(ID) : "memory"); }
+};
+
+// ---------------------------------------------------------------- small group utilities
 struct Misc {                      // scalars in shared memory
   int ncand, nsv, digit, rem_sel, cnt_above, total, fb, bad;
   uint32_t tau, maxx;
@@ -15,9 +27,9 @@ struct Misc {                      // scalars in shared memory
   int wcnt[DW];                    // per-warp candidate counts
 };
 
-__device__ __forceinline__ void block_exscan2(int a, int b, int& ea, int& eb, int& ta, int& tb,
-                                              int* wsum) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <class Grp = Cta256>
+__device__ __forceinline__ void block_exscan2(int a, int b, int& ea, int& eb, int& ta, int& tb, int* wsum) {
+  const int t = Grp::tid(), lane = t & 31, warp = t >> 5;
   int ia = a, ib = b;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -25,14 +37,14 @@ __device__ __forceinline__ void block_exscan2(int a, int b, int& ea, int& eb, in
     if (lane >= o) { ia += xa; ib += xb; }
   }
   if (lane == 31) { wsum[warp] = ia; wsum[DW + warp] = ib; }
-  __syncthreads();
+  Grp::sync();
   int pa = 0, pb = 0, sa = 0, sb = 0;
   for (int w = 0; w < DW; ++w) {
     if (w < warp) { pa += wsum[w]; pb += wsum[DW + w]; }
     sa += wsum[w]; sb += wsum[DW + w];
   }
   ea = pa + ia - a; eb = pb + ib - b; ta = sa; tb = sb;
-  __syncthreads();
+  Grp::sync();
 }
 
 // warp-aggregated shared-memory histogram increment (bin < 0 = no-op)
@@ -42,7 +54,7 @@ __device__ __forceinline__ void hist_add(int* hist, int bin) {
   if (bin >= 0 && (int)(threadIdx.x & 31) == leader) atomicAdd(&hist[bin], __popc(peers));
 }
 
-// warp 0 picks the digit whose cumulative count (from the top bin) reaches `rem`
+// warp 0 picks the digit whose cumulative count (from the top bin) reaches `rem` (256 bins)
 __device__ __forceinline__ void pick_digit(const int* hist, Misc* ms) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
@@ -70,16 +82,17 @@ __device__ __forceinline__ void pick_digit(const int* hist, Misc* ms) {
 constexpr int RB = 12;              // digit bits per pass
 constexpr int NBIN = 1 << RB;       // 4096 bins; thread t owns bins [NBIN-16(t+1), NBIN-16t)
 
-// Block-wide: choose the digit whose descending cumulative count reaches ms->rem_sel.
+// Group-wide: choose the digit whose descending cumulative count reaches ms->rem_sel.
+template <class Grp = Cta256>
 __device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
-  const int tid = threadIdx.x;
+  const int tid = Grp::tid();
   constexpr int PER = NBIN / DT;
   const int top = NBIN - 1 - PER * tid;          // this thread owns bins top, top-1, ..., top-PER+1
   int s = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) s += hist[top - ((i + tid) & (PER - 1))];   // rotated: no bank conflicts
   int exc, d0, tot, d1;
-  block_exscan2(s, 0, exc, d0, tot, d1, ms->wsum);
+  block_exscan2<Grp>(s, 0, exc, d0, tot, d1, ms->wsum);
   const int rem = ms->rem_sel;
   if (exc < rem && rem <= exc + s) {
     int c = exc;
@@ -89,50 +102,50 @@ __device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
       c += h;
     }
   }
-  __syncthreads();
+  Grp::sync();
 }
 
 // Exact k-th largest of a multiset of 32-bit values x (all <= maxx).  `each(f)` must call
-// f(x) once per item on the calling thread (every thread calls each()).  Returns the k-th
-// value and how many items equal to it belong to the top `rank` (ties are then resolved by
-// index by the caller).  hist must hold NBIN ints.  Contains __syncthreads.
-template <typename Each>
+// f(x) once per item on the calling thread (every thread of the group calls each()).
+// Returns the k-th value and how many items equal to it belong to the top `rank` (ties
+// are then resolved by index by the caller).  hist must hold NBIN + 33 ints.
+template <class Grp = Cta256, typename Each>
 __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, int* hist, Misc* ms,
                                           uint32_t& kth, int& need_eq) {
-  const int tid = threadIdx.x;
+  const int tid = Grp::tid();
   const int nbits = maxx ? 32 - __clz(maxx) : 0;
   int* list = hist + NBIN;           // up to 32 items of a small boundary bin (+ counter)
   if (tid == 0) ms->rem_sel = rank;
   uint32_t prefix = 0;
   int shift = nbits;
-  __syncthreads();
+  Grp::sync();
   while (shift > 0) {
     const int dbits = shift >= RB ? RB : shift;
     const int hi = shift;            // bits >= hi are already fixed in prefix
     shift -= dbits;
     for (int i = tid; i < NBIN; i += DT) hist[i] = 0;
     if (tid == 0) list[32] = 0;
-    __syncthreads();
+    Grp::sync();
     const uint32_t want = hi >= 32 ? 0u : (prefix >> hi);
     const int sh = shift;
     each([&](uint32_t x) {
       if ((hi >= 32 ? 0u : (x >> hi)) == want) atomicAdd(&hist[(x >> sh) & (NBIN - 1)], 1);
     });
-    __syncthreads();
-    pick_digit_big(hist, ms);
+    Grp::sync();
+    pick_digit_big<Grp>(hist, ms);
     const uint32_t d = (uint32_t)ms->digit;
     prefix |= d << shift;
     const int nb = hist[d];
-    __syncthreads();
+    Grp::sync();
     if (tid == 0) ms->rem_sel -= ms->cnt_above;
-    __syncthreads();
+    Grp::sync();
     if (shift > 0 && nb <= 32) {
       // finish inside one warp: exact rank among the few items of the boundary bin
       const uint32_t w2 = prefix >> shift;
       each([&](uint32_t x) {
         if ((x >> shift) == w2) list[atomicAdd(&list[32], 1)] = (int)x;
       });
-      __syncthreads();
+      Grp::sync();
       if (tid < 32) {
         const uint32_t v = tid < nb ? (uint32_t)list[tid] : 0u;
         int gt = 0, eqc = 0;
@@ -145,16 +158,16 @@ __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, in
         __syncwarp();
         if (tid < nb && gt < rem && rem <= gt + eqc) { ms->tau = v; ms->digit = rem - gt; }
       }
-      __syncthreads();
+      Grp::sync();
       kth = ms->tau;
       need_eq = ms->digit;
-      __syncthreads();
+      Grp::sync();
       return;
     }
   }
   kth = prefix;
   need_eq = ms->rem_sel;
-  __syncthreads();
+  Grp::sync();
 }
 
 }  // namespace sikv

@@ -116,10 +116,14 @@ def _check_decode(units, cb, oc, q, k, **kw):
     return res
 
 
+KERNELS = [1, 2]    # one CTA per unit / warp-specialised persistent
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("k", [256, 0, 1, 4032, 5000])
-def test_decode_selection_and_attention(c1, k):
+def test_decode_selection_and_attention(c1, k, kernel):
     units, cb, oc, q = c1
-    _check_decode(units, cb, oc, q, k)
+    _check_decode(units, cb, oc, q, k, kernel=kernel)
 
 
 def test_decode_matches_reference_selection(c1, golden):
@@ -132,28 +136,60 @@ def test_decode_matches_reference_selection(c1, golden):
     assert len(np.intersect1d(sel, ref)) >= len(ref) - 1
 
 
-def test_decode_fallback_path(c1):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_decode_fallback_path(c1, kernel):
     """A tiny candidate buffer forces the exact multi-pass rescoring path."""
     units, cb, oc, q = c1
-    res = _check_decode(units, cb, oc, q, 256, cap=300)
+    res = _check_decode(units, cb, oc, q, 256, cap=300, kernel=kernel)
     assert (res.diag.cpu().numpy() & 4).all()
 
 
-def test_decode_sampled_threshold_32k():
-    units, cb, oc, q = make(32768, [200, 201])
-    res = _check_decode(units, cb, oc, q, 2048)
+@pytest.fixture(scope="module")
+def c32k():
+    return make(32768, [200, 201, 202])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_decode_sampled_threshold_32k(c32k, kernel):
+    units, cb, oc, q = c32k
+    res = _check_decode(units, cb, oc, q, 2048, kernel=kernel)
     d = res.diag.cpu().numpy()
     assert ((d & 3) == 3).all() and not (d & 4).any()
 
 
-def test_decode_with_appends_and_gq7():
+def test_kernels_agree_bitwise(c32k):
+    """Both kernels run the same arithmetic: outputs and selections are bit-identical."""
+    units, cb, oc, q = c32k
+    r1 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=1)
+    r2 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=2)
+    assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.counts, r2.counts)
+    assert torch.equal(r1.out, r2.out) and torch.equal(r1.lse, r2.lse)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_decode_with_appends_and_gq7(kernel):
     units, cb, oc, q = make(2048, [11, 12], gq=7, appends=3)
-    _check_decode(units, cb, oc, q, 128)
+    _check_decode(units, cb, oc, q, 128, kernel=kernel)
 
 
-def test_decode_no_sinks_fp32_inputs():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_decode_no_sinks_fp32_inputs(kernel):
     units, cb, oc, q = make(1000, [5, 6, 7], gq=2, sinks=0, dtype=torch.float32)
-    _check_decode(units, cb, oc, q, 100)
+    _check_decode(units, cb, oc, q, 100, kernel=kernel)
+
+
+def test_persistent_kernel_many_units():
+    """More units than CTAs: every persistent CTA loops over several units."""
+    units = [gen_unit(1024, 128, 4, 500 + i) for i in range(2)]
+    K = torch.tensor(np.stack([u.keys for u in units]), dtype=torch.bfloat16, device="cuda")
+    V = torch.tensor(np.stack([u.values for u in units]), dtype=torch.bfloat16, device="cuda")
+    reps = 400
+    cb = B.prefill_batch(K.repeat(reps, 1, 1), V.repeat(reps, 1, 1), sink_count=64)
+    q = torch.tensor(np.stack([u.queries[:4] for u in units]), dtype=torch.float32, device="cuda").repeat(reps, 1, 1)
+    r1 = B.decode_step(cb, q, 100, with_selection=True, kernel=1)
+    r2 = B.decode_step(cb, q, 100, with_selection=True, kernel=2)
+    assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.out, r2.out)
+    assert torch.equal(r2.out[0::2], r2.out[0:1].expand(reps, -1, -1))
 
 
 def test_decode_ties_lowest_index_first():
@@ -171,8 +207,8 @@ def test_decode_ties_lowest_index_first():
     cb = B.prefill_batch(K_t, V_t, sink_count=64)
     c = O.prefill(reps, V, sink_count=64)
     q = torch.tensor(base.queries[None, :4], dtype=torch.float32, device="cuda")
-    for k, cap in ((500, 0), (500, 200), (333, 0)):
-        res = B.decode_step(cb, q, k, cap=cap, with_selection=True)
+    for k, cap, kern in ((500, 0, 1), (500, 200, 1), (333, 0, 1), (500, 0, 2), (500, 200, 2)):
+        res = B.decode_step(cb, q, k, cap=cap, with_selection=True, kernel=kern)
         idx = R.select32(c, base.queries[:4].astype(np.float32), k)[0]
         got = res.selection[0, : res.counts[0]].cpu().numpy()
         np.testing.assert_array_equal(got, idx)

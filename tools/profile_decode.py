@@ -15,17 +15,18 @@ ap.add_argument("--L", type=int, default=32768)
 ap.add_argument("--k", type=int, default=2048)
 ap.add_argument("--gq", type=int, default=4)
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--kernel", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 cb, q = bench.build_cache(a.units, 0, a.L, a.gq, 1234, dev)
 out = torch.empty(a.units, a.gq, 128, device=dev)
 for _ in range(a.iters):
-    B.decode_step(cb, q, a.k, out=out)
+    B.decode_step(cb, q, a.k, out=out, kernel=a.kernel)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(5):
-    B.decode_step(cb, q, a.k, out=out)
+    B.decode_step(cb, q, a.k, out=out, kernel=a.kernel)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
@@ -36,7 +37,7 @@ if True:
     from paper_2603_14224_b200 import _lib
     clk = torch.zeros(a.units, 12, dtype=torch.int64, device=dev)
     _lib.call("sikv_debug_set_decode_profile", _lib.ptr(clk))
-    B.decode_step(cb, q, a.k, out=out)
+    B.decode_step(cb, q, a.k, out=out, kernel=a.kernel)
     torch.cuda.synchronize()
     _lib.call("sikv_debug_set_decode_profile", None)
     c = clk.cpu().numpy().astype("float64")
