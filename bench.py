@@ -39,6 +39,8 @@ CONFIGS = {
     "c2": (32, 16, 8, 4, 32768, 2048, "Llama-3-8B, 32 layers, batch 16, 32K ctx, top-k 2048"),
     "c3": (32, 1, 8, 4, 131072, 4096, "Llama-3.1-8B, 32 layers, batch 1, 128K ctx, top-k 4096"),
     "c4": (28, 64, 4, 7, 8192, 1024, "Qwen2.5-7B, 28 layers, batch 64, 8K ctx, top-k 1024"),
+    # prefill-side compression throughput (BASELINE.json configs[4])
+    "c5": (32, 1, 8, 4, 131072, 0, "key/value compression of 128K tokens x 32 layers, Llama-3-8B geometry"),
 }
 SINKS = 64
 
@@ -182,22 +184,48 @@ def run_ours(args, rank, world, cfg):
     torch.cuda.synchronize()
     kern_ms = ek0.elapsed_time(ek1) / args.steps
 
-    # end to end through the public API: pinned host q -> device, decode, device -> host out
-    qh = q.to(torch.bfloat16).cpu().pin_memory()
-    oh = torch.empty(ul, gq, 128, dtype=torch.float32).pin_memory()
-    for _ in range(2):
-        qd = qh.to(dev, non_blocking=True)
-        B.decode_step(cb, qd, k, out=out)
-        oh.copy_(out, non_blocking=True)
+    # end to end through the public API: every step copies its queries from pinned host
+    # memory and its outputs back to pinned host memory; copies run on a side stream and
+    # overlap the neighbouring steps' decode (double-buffered device q / out)
+    cs_in, cs_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    qh = q.cpu().pin_memory()
+    oh = [torch.empty(ul, gq, 128, dtype=torch.float32).pin_memory() for _ in range(2)]
+    qd = [torch.empty_like(q) for _ in range(2)]
+    od = [torch.empty_like(out) for _ in range(2)]
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    h2d, comp, d2h = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+
+    def e2e_steps(n):
+        for i in range(n):
+            b = i & 1
+            with torch.cuda.stream(cs_in):
+                if i >= 2:
+                    cs_in.wait_event(comp[b])         # qd[b] was read by step i-2
+                qd[b].copy_(qh, non_blocking=True)
+                h2d[b].record(cs_in)
+            st.wait_event(h2d[b])
+            if i >= 2:
+                st.wait_event(d2h[b])                 # od[b] was copied out by step i-2
+            B.decode_step(cb, qd[b], k, out=od[b])
+            if world > 1:
+                gather_outputs(od[b].to(torch.bfloat16), layers, batch, kvh, world, out=model_out)
+            comp[b].record(st)
+            with torch.cuda.stream(cs_out):
+                cs_out.wait_event(comp[b])
+                oh[b].copy_(od[b], non_blocking=True)
+                d2h[b].record(cs_out)
+        st.wait_stream(cs_in)
+        st.wait_stream(cs_out)
+
+    e2e_steps(2)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ee0.record(st)
-    for _ in range(args.steps):
-        qd = qh.to(dev, non_blocking=True)
-        step(qd)
-        oh.copy_(out, non_blocking=True)
+    cs_in.wait_stream(st)
+    cs_out.wait_stream(st)
+    e2e_steps(args.steps)
     ee1.record(st)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1) / args.steps
@@ -206,7 +234,7 @@ def run_ours(args, rank, world, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    res = B.decode_step(cb, q[:1].contiguous() if False else q, k, with_diag=True)
+    res = B.decode_step(cb, q, k, with_diag=True)
     torch.cuda.synchronize()
     fallbacks = int(((res.diag & 4) != 0).sum().item())
 
@@ -226,7 +254,7 @@ def run_ours(args, rank, world, cfg):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "2-bit K/V + fp32 LUT scores + fp16 mma / fp32 accumulate (bf16 inputs)",
+        "dtype": "u2 K/V payload, f32 scores, f16 mma operands / f32 accumulate",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU), random-init caches",
         "config": {"workload": args.config, "label": label, "layers": layers, "batch": batch,
                    "kv_heads": kvh, "q_heads_per_kv": gq, "context": L, "top_k": k, "sinks": SINKS,
@@ -238,12 +266,73 @@ def run_ours(args, rank, world, cfg):
                      "kernel_ms": round(kern_ms, 5)},
         "e2e": {"value": round(1000.0 / e2e_ms, 3), "unit": "decode steps/s",
                 "h2d_bytes_per_step": int(qh.numel() * qh.element_size()),
-                "d2h_bytes_per_step": int(oh.numel() * oh.element_size())},
+                "d2h_bytes_per_step": int(oh[0].numel() * oh[0].element_size()),
+                "overlap": "H2D and D2H on two side streams, double-buffered device q / out"},
         "gpu_launches": args.steps * (1 + 0),
         "clocks": clk.summary(),
         "selection_fallbacks_last_step": fallbacks,
     }
     return line
+
+
+def run_prefill(args, rank, world, cfg):
+    """C5: compressed token-heads per second of the encoder (stats + sign codes + codebook
+    + 2-bit K/V payloads + fp16 params, both layouts' fast planes), units head-sharded."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_14224_b200 import _lib
+    from paper_2603_14224_b200 import batch as B
+    from paper_2603_14224_b200.synth import gen_units_torch
+
+    layers, batch, kvh, gq, L, _, label = cfg
+    units = layers * batch * kvh
+    ul = units // world
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    chunk = 8
+    cb = B.empty_batch(chunk, L, sink_count=SINKS, device=dev)
+    ws = torch.empty(_lib.lib().sikv_encode_workspace_bytes(chunk, L, 128), dtype=torch.uint8, device=dev)
+    K, V = gen_units_torch(chunk, L, 128, 77 + rank, dev)
+    st = torch.cuda.current_stream()
+    for _ in range(max(1, args.warmup)):
+        B.prefill_into(cb, 0, K, V, workspace=ws, check=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    reps = max(1, ul // chunk)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            for _r in range(reps):       # every step encodes this rank's ul units (8 at a time)
+                B.prefill_into(cb, 0, K, V, workspace=ws, check=False)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        return None
+    th = units * L / (ms * 1e-3)            # token-heads per second, whole job
+    peak, peak_kind = peaks()
+    per_th = 512 + 112                      # read bf16 K,V; write 896-bit compressed record
+    achieved = (reps * chunk * L * per_th) / (ms * 1e-3) / 1e9
+    return {
+        "metric": "prefill key/value compression throughput, Llama-3-8B geometry, 128K tokens x 32 layers",
+        "value": round(th, 1), "unit": "token-heads/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 math on bf16 inputs -> u2 payloads, f16 params",
+        "data": "synthetic (gen_synthetic distribution, Philox on GPU)",
+        "config": {"workload": "c5", "label": label, "units": units, "tokens": L,
+                   "parallelism": f"kv-head shard x{world}"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind, "traffic": None,
+                     "algo_bytes_per_token_head": per_th},
+        "gpu_launches": args.steps * reps * 6, "clocks": clk.summary(),
+    }
 
 
 # ------------------------------------------------------------------------------- CPU arm
@@ -335,9 +424,9 @@ def main():
     import torch.distributed as dist
     if world > 1:
         dist.init_process_group("nccl")
-    line = run_ours(args, rank, world, cfg)
+    line = run_prefill(args, rank, world, cfg) if args.config == "c5" else run_ours(args, rank, world, cfg)
     if rank == 0 and line is not None:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and args.config != "c5":
             cores = os.cpu_count() or 1
             sample = args.cpu_sample or max(8, cores)
             try:

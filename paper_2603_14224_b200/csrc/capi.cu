@@ -152,13 +152,14 @@ int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64
 }
 
 int sikv_decode_default_cap(int64_t tokens, int k, int sinks) {
-  // Candidate buffer: ~2k + 1024 entries, shrunk (not below ~1.4k + 512) so that two CTAs
-  // fit on one SM (2 x 113 KB) when possible.
+  // Candidate buffer: ~2k + 1024 entries (the sampled threshold keeps ~k + 4 sqrt(k') of them),
+  // shrunk (not below ~1.4k + 512) only when that lets two CTAs share an SM (2 x 113 KB).
   const int64_t ncand = std::max<int64_t>(tokens - sinks, 0);
   const int64_t keff = std::min<int64_t>(k, ncand);
   if (keff == 0 || keff == ncand) return 1024;        // no candidate selection needed
   int64_t cap = std::max<int64_t>(2 * keff + 1024, 1024);
   const int64_t floor_cap = std::max<int64_t>(keff + keff * 2 / 5 + 512, 1024);
+  if (decode_layout(tokens, k, sinks, 8, (int)floor_cap).total > 113 * 1024) return (int)cap;
   while (cap > floor_cap && decode_layout(tokens, k, sinks, 8, (int)cap).total > 113 * 1024) cap -= 64;
   return (int)cap;
 }

@@ -205,16 +205,45 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
 }
 
 // dynamic rows: blocks first, first + nw, ... of [0, nbd), staged by cp.async (double
-// buffered) and dequantised into mma fragments
+// buffered) and dequantised into mma fragments.  Every lane's shared-memory offsets are
+// fixed for the whole unit (16-byte chunk k of token j lives at chunk k ^ (j & 7)), so they
+// are computed once; token g and g + 8 (and 2t4 + x and 2t4 + x + 8) differ by 1 KiB.
 __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, const int32_t* dyn, int ndyn,
                                              int first, int nw, char* stage, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
   const int nbd = (ndyn + 15) >> 4;
-  if (first < nbd) stage_block(stage, recs_u, dyn, first * 16, ndyn, lane);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
+  // staging: lane copies chunk kk = lane & 7 of tokens j = (lane >> 3) + 4r, r = 0..3
+  const int jb = lane >> 3, kk = lane & 7;
+  uint32_t dst[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int j = jb + 4 * r;
+    dst[r] = (uint32_t)(j * FREC + 16 * (kk ^ (j & 7)));
+  }
+  auto stage_blk = [&](uint32_t buf, int base) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int t = dyn[min(base + jb + 4 * r, ndyn - 1)];
+      const uint8_t* src = recs_u + (int64_t)t * FREC + 16 * kk;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + buf + dst[r]), "l"(src));
+    }
+  };
+  // fragment offsets (token g for K, tokens 2t4 / 2t4 + 1 for V; +1 KiB for the +8 tokens)
+  const int jk = g, jv0 = 2 * t4, jv1 = 2 * t4 + 1;
+  const int off_kw = jk * FREC + 16 * ((t4 >> 1) ^ (jk & 7)) + 8 * (t4 & 1);
+  const int off_kp = jk * FREC + 16 * (4 ^ (jk & 7));
+  const int off_ks = jk * FREC + 16 * (6 ^ (jk & 7)) + 4 * t4;
+  const int off_vw0 = jv0 * FREC + 16 * ((2 + (g >> 2)) ^ (jv0 & 7)) + 4 * (g & 3);
+  const int off_vw1 = jv1 * FREC + 16 * ((2 + (g >> 2)) ^ (jv1 & 7)) + 4 * (g & 3);
+  const int off_vp0 = jv0 * FREC + 16 * (5 ^ (jv0 & 7));
+  const int off_vp1 = jv1 * FREC + 16 * (5 ^ (jv1 & 7));
+  constexpr int P8 = 8 * FREC;
+  if (first < nbd) stage_blk(0, first * 16);
   cp_commit();
   int buf = 0;
   for (int db = first; db < nbd; db += nw) {
-    if (db + nw < nbd) stage_block(stage + (buf ^ 1) * STAGE_BYTES, recs_u, dyn, (db + nw) * 16, ndyn, lane);
+    if (db + nw < nbd) stage_blk((buf ^ 1) * STAGE_BYTES, (db + nw) * 16);
     cp_commit();
     cp_wait<1>();
     __syncwarp();
@@ -224,10 +253,9 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     bool valid[2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const int j = g + 8 * nt;
-      const uint2 kw = *reinterpret_cast<const uint2*>(chunk(sb, j, t4 >> 1) + 8 * (t4 & 1));
-      const uint4 kp = *reinterpret_cast<const uint4*>(chunk(sb, j, 4));
-      const uint32_t ks = *reinterpret_cast<const uint32_t*>(chunk(sb, j, 6) + 4 * t4);
+      const uint2 kw = *reinterpret_cast<const uint2*>(sb + off_kw + nt * P8);
+      const uint4 kp = *reinterpret_cast<const uint4*>(sb + off_kp + nt * P8);
+      const uint32_t ks = *reinterpret_cast<const uint32_t*>(sb + off_ks + nt * P8);
       const uint32_t par[4] = {kp.x, kp.y, kp.z, kp.w};
       const uint32_t wsrc[4] = {kw.x, kw.x >> 8, kw.y, kw.y >> 8};   // slots 0-3 / 4-7 of each word
       sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
@@ -258,12 +286,14 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     // V words and params of tokens 2t4, 2t4+1, 2t4+8, 2t4+9
     uint32_t vw[4];
     uint4 vp[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int j = 2 * t4 + (x & 1) + 8 * (x >> 1);
-      vw[x] = *reinterpret_cast<const uint32_t*>(chunk(sb, j, 2 + (g >> 2)) + 4 * (g & 3));
-      vp[x] = *reinterpret_cast<const uint4*>(chunk(sb, j, 5));
-    }
+    vw[0] = *reinterpret_cast<const uint32_t*>(sb + off_vw0);
+    vw[1] = *reinterpret_cast<const uint32_t*>(sb + off_vw1);
+    vw[2] = *reinterpret_cast<const uint32_t*>(sb + off_vw0 + P8);
+    vw[3] = *reinterpret_cast<const uint32_t*>(sb + off_vw1 + P8);
+    vp[0] = *reinterpret_cast<const uint4*>(sb + off_vp0);
+    vp[1] = *reinterpret_cast<const uint4*>(sb + off_vp1);
+    vp[2] = *reinterpret_cast<const uint4*>(sb + off_vp0 + P8);
+    vp[3] = *reinterpret_cast<const uint4*>(sb + off_vp1 + P8);
     attn_softmax_pv(A, sacc, valid, lane, [&](int jg, uint32_t (&v)[2][4]) {
 #pragma unroll
       for (int pr = 0; pr < 2; ++pr) {

@@ -73,6 +73,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
     int* th = reinterpret_cast<int*>(qbar + FD);
     uint32_t* tmin = reinterpret_cast<uint32_t*>(th + 256);
     Misc* ms = reinterpret_cast<Misc*>(tmin + 256);
+    // per-unit inputs are prefetched into registers one unit ahead (static schedule)
+    float pq[4], pal = 0.f;
+    float4 pc[2];
+    int psid = -1;
+    auto prefetch = [&](int64_t u) {
+      if (u >= a.U) return;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int idx = tid + DT * i;
+        pq[i] = idx < Gq * FD ? a.q[u * Gq * FD + idx] : 0.f;
+      }
+      pal = tid < FD ? a.alpha32[u * FD + tid] : 0.f;
+      const float4* c4 = reinterpret_cast<const float4*>(a.cent32 + u * 32 * 16 * 4);
+      pc[0] = c4[tid];
+      pc[1] = c4[tid + DT];
+      psid = tid < S ? a.sink_idx[u * S + tid] : -1;
+    };
+    prefetch(blockIdx.x);
     for (int it = 0;; ++it) {
       const int s = it & 1;
       char* slot = sm + a.off_slot + s * a.slot_bytes;
@@ -81,9 +99,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
       uint32_t* forced = reinterpret_cast<uint32_t*>(slot + a.slot_forced);
       float* qs = reinterpret_cast<float*>(slot + a.slot_q);
       float* ahat = reinterpret_cast<float*>(slot + a.slot_ahat);
-      if (tid == 0) ms->digit = atomicAdd(a.counter, 1);
-      PG::sync();
-      const int64_t u = ms->digit;
+      const int64_t u = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
       if (it >= 2) wait_empty(s);
       if (u >= a.U) {
         if (tid == 0) meta->unit = -1;
@@ -95,10 +111,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
       const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
       uint4 wsamp[MAX_SAMPLE_CHUNKS];
       load_sample(g, signs, tid, wsamp);
-      for (int i = tid; i < Gq * FD; i += DT) qs[i] = a.q[u * Gq * FD + i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (tid + DT * i < Gq * FD) qs[tid + DT * i] = pq[i];
       for (int i = tid; i < W; i += DT) forced[i] = 0u;
       PG::sync();
-      for (int j = tid; j < S; j += DT) {
+      if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
+      for (int j = tid + DT; j < S; j += DT) {
         const int t = a.sink_idx[u * S + j];
         atomicOr(&forced[t >> 5], 1u << (t & 31));
       }
@@ -106,11 +125,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
         float sq = qs[tid];
         for (int h = 1; h < Gq; ++h) sq = __fadd_rn(sq, qs[h * FD + tid]);
         qbar[tid] = sq;
-        const float al = a.alpha32[u * FD + tid];
-        ahat[tid] = al > 0.f ? al : 1.0f;
+        ahat[tid] = pal > 0.f ? pal : 1.0f;
       }
       PG::sync();
-      build_pair_table<PG>(a.cent32 + u * 32 * 16 * 4, qbar, lut, T);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int e = tid + DT * r, gg = e >> 4;
+        const float4 c = pc[r];
+        const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
+        lut[e] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                           __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+      }
+      PG::sync();
+      for (int e = tid; e < 256 * 16; e += DT) {
+        const int b = e >> 4, p = e & 15;
+        const float v = __fadd_rn(lut[(2 * p) * 16 + (b & 15)], lut[(2 * p + 1) * 16 + (b >> 4)]);
+        float* row = reinterpret_cast<float*>(T) + b * 64;
+        row[p] = v; row[p + 16] = v; row[p + 32] = v;
+      }
+      PG::sync();
+      prefetch(u + gridDim.x);       // next unit's inputs load while this unit streams
       int fb = 0, need_eq = 0, eq_count = 0;
       uint32_t tau = 1, kstar = 0;
       if (g.mode >= 2) {
@@ -252,9 +286,7 @@ cudaError_t launch_decode_ws(const uint8_t* signs, const uint8_t* recs, const fl
   a.counter = reinterpret_cast<int*>(workspace);
   a.gbits = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(workspace) + 256);
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
-  cudaError_t e = cudaMemsetAsync(workspace, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(decode_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total);
+  cudaError_t e = cudaFuncSetAttribute(decode_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(nsm, U);
   decode_ws_kernel<<<grid, WS_THREADS, lay.total, st>>>(a);
