@@ -14,6 +14,20 @@ constexpr int MAX_SAMPLE_CHUNKS = 8;
 // ---------------------------------------------------------------- pair table
 // LUT[g][c] = q-bar_g . centroid[g][c] (float32, no FMA, the reference pairing) and the
 // byte-pair table T[b][col] = LUT[2p][b & 15] + LUT[2p+1][b >> 4], p = col mod 16.
+// T rows from the transposed LUT lutT[code * 32 + group]: lanes 0-15 / 16-31 build pairs
+// p = lane & 15 of two byte values, so LUT reads hit banks 2p, 2p+1 and T writes banks p.
+template <class Grp>
+__device__ __forceinline__ void build_pair_rows(const float* lutT, char* T) {
+  const int tid = Grp::tid();
+  const int p = tid & 15;
+  for (int b = tid >> 4; b < 256; b += DT / 16) {
+    const float v = __fadd_rn(lutT[(b & 15) * 32 + 2 * p], lutT[(b >> 4) * 32 + 2 * p + 1]);
+    float* row = reinterpret_cast<float*>(T) + b * 64;
+    row[p] = v; row[p + 16] = v; row[p + 32] = v;
+  }
+  Grp::sync();
+}
+
 template <class Grp>
 __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent, const float* qbar, float* lut,
                                                  char* T) {
@@ -22,17 +36,11 @@ __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent,
     const int g = e >> 4;
     const float4 c = reinterpret_cast<const float4*>(cent)[e];
     const float q0 = qbar[4 * g], q1 = qbar[4 * g + 1], q2 = qbar[4 * g + 2], q3 = qbar[4 * g + 3];
-    lut[e] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
-                       __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+    lut[(e & 15) * 32 + g] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                                       __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
   }
   Grp::sync();
-  for (int e = tid; e < 256 * 16; e += DT) {
-    const int b = e >> 4, p = e & 15;
-    const float v = __fadd_rn(lut[(2 * p) * 16 + (b & 15)], lut[(2 * p + 1) * 16 + (b >> 4)]);
-    float* row = reinterpret_cast<float*>(T) + b * 64;
-    row[p] = v; row[p + 16] = v; row[p + 32] = v;
-  }
-  Grp::sync();
+  build_pair_rows<Grp>(lut, T);
 }
 
 // ---------------------------------------------------------------- scoring
@@ -51,19 +59,43 @@ __device__ __forceinline__ float score_token(const uint4 w, uint32_t lb, const c
   return s;
 }
 
-// N tokens at once: the 16-step chains of different tokens interleave, hiding FADD latency
+// N tokens at once: the 16-step chains of different tokens interleave, hiding FADD latency.
+// Pairs of tokens accumulate with one packed FADD2 (add.rn.f32x2, sm_100a): per lane it is
+// the same correctly rounded float32 add, so the stated order and the bits are unchanged.
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
 template <int N>
 __device__ __forceinline__ void score_batch(const uint4 (&w)[N], uint32_t lb, const char* T, float (&s)[N]) {
+  static_assert(N % 2 == 0, "tokens are scored in pairs");
+  unsigned long long acc[N / 2];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
 #pragma unroll
-    for (int x = 0; x < N; ++x) {
-      const uint32_t wd = (i >> 2) == 0 ? w[x].x : (i >> 2) == 1 ? w[x].y : (i >> 2) == 2 ? w[x].z : w[x].w;
-      const uint32_t off = prmt(wd, lb, 0x5504u | ((uint32_t)(i & 3) << 4));
-      const float v = *reinterpret_cast<const float*>(T + off + 4 * i);
-      s[x] = (i == 0) ? v : __fadd_rn(s[x], v);
+    for (int x = 0; x < N; x += 2) {
+      const uint32_t w0 = (i >> 2) == 0 ? w[x].x : (i >> 2) == 1 ? w[x].y : (i >> 2) == 2 ? w[x].z : w[x].w;
+      const uint32_t w1 = (i >> 2) == 0 ? w[x + 1].x : (i >> 2) == 1 ? w[x + 1].y : (i >> 2) == 2 ? w[x + 1].z
+                                                                                               : w[x + 1].w;
+      const uint32_t sel = 0x5504u | ((uint32_t)(i & 3) << 4);
+      const float v0 = *reinterpret_cast<const float*>(T + prmt(w0, lb, sel) + 4 * i);
+      const float v1 = *reinterpret_cast<const float*>(T + prmt(w1, lb, sel) + 4 * i);
+      const unsigned long long v = pack2(v0, v1);
+      acc[x / 2] = (i == 0) ? v : fadd2(acc[x / 2], v);
     }
   }
+#pragma unroll
+  for (int x = 0; x < N; x += 2) unpack2(acc[x / 2], s[x], s[x + 1]);
 }
 
 __device__ __forceinline__ bool forced_bit(const uint32_t* fb, int64_t t) {

@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
   const int W = (int)((L + 31) >> 5);
   const int S = a.S, R = a.R, Gq = a.Gq;
 
-  if (threadIdx.x < 256) {
+  // role from a value the compiler can prove warp-uniform (keeps uniform-datapath addressing)
+  const int role = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 8), 0);
+  if (role == 0) {
     // ============================================================ producer
     const int tid = PG::tid();
     char* T = sm;
@@ -133,17 +135,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
         const int e = tid + DT * r, gg = e >> 4;
         const float4 c = pc[r];
         const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
-        lut[e] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
-                           __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+        // LUT stored transposed, lutT[code * 32 + group]: the table build below reads it
+        // without bank conflicts
+        lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                                            __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
       }
       PG::sync();
-      for (int e = tid; e < 256 * 16; e += DT) {
-        const int b = e >> 4, p = e & 15;
-        const float v = __fadd_rn(lut[(2 * p) * 16 + (b & 15)], lut[(2 * p + 1) * 16 + (b >> 4)]);
-        float* row = reinterpret_cast<float*>(T) + b * 64;
-        row[p] = v; row[p + 16] = v; row[p + 32] = v;
-      }
-      PG::sync();
+      build_pair_rows<PG>(lut, T);
       prefetch(u + gridDim.x);       // next unit's inputs load while this unit streams
       int fb = 0, need_eq = 0, eq_count = 0;
       uint32_t tau = 1, kstar = 0;
