@@ -85,6 +85,77 @@ __global__ void stats_final_kernel(const void* __restrict__ keys, int dt, int64_
   }
 }
 
+
+// Vectorised statistics for bf16 / f32 inputs: lane l owns channels 4l..4l+3, the 8 warps
+// take interleaved rows; warp partials combine in fixed order (the sums are exact under the
+// certificate, so the order does not matter; otherwise stats_final replays the row order).
+__device__ __forceinline__ int lowbit_f32(float x) {
+  const uint32_t b = __float_as_uint(x);
+  const int e = (int)((b >> 23) & 0xFF);
+  const uint32_t m = b & 0x7FFFFFu;
+  if (e == 0) return m ? -149 + __ffs((int)m) - 1 : 0x7fffffff;
+  return e - 150 + __ffs((int)(m | 0x800000u)) - 1;
+}
+
+template <int DTY>
+__device__ __forceinline__ void load4(const void* p, int64_t idx, float (&x)[4]) {
+  if (DTY == IN_BF16) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p) + idx));
+    x[0] = __uint_as_float(w.x << 16); x[1] = __uint_as_float(w.x & 0xFFFF0000u);
+    x[2] = __uint_as_float(w.y << 16); x[3] = __uint_as_float(w.y & 0xFFFF0000u);
+  } else {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p) + idx));
+    x[0] = w.x; x[1] = w.y; x[2] = w.z; x[3] = w.w;
+  }
+}
+
+template <int DTY>
+__global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __restrict__ keys, int64_t L, int D,
+                                                                 int nsplit, double* __restrict__ part,
+                                                                 int* __restrict__ status) {
+  __shared__ double red[8][128][5];
+  const int u = blockIdx.x, s = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per = (L + nsplit - 1) / nsplit;
+  const int64_t t0 = s * per, t1 = min(L, t0 + per);
+  const bool active = 4 * lane < D;
+  double sum[4] = {-0.0, -0.0, -0.0, -0.0}, sab[4] = {0.0, 0.0, 0.0, 0.0};
+  float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  int low[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+  bool bad = false;
+  if (active) {
+    for (int64_t t = t0 + warp; t < t1; t += 8) {
+      float x[4];
+      load4<DTY>(keys, ((int64_t)u * L + t) * D + 4 * lane, x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bad |= !isfinite(x[i]);
+        sum[i] += (double)x[i];
+        sab[i] += (double)fabsf(x[i]);
+        mn[i] = fminf(mn[i], x[i]);
+        mx[i] = fmaxf(mx[i], x[i]);
+        if (x[i] != 0.f) low[i] = min(low[i], lowbit_f32(x[i]));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double* r = red[warp][4 * lane + i];
+      r[0] = sum[i]; r[1] = sab[i]; r[2] = mn[i]; r[3] = mx[i]; r[4] = __longlong_as_double((long long)low[i]);
+    }
+  }
+  if (bad) atomicOr(status, 4);
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += 256) {
+    double a0 = -0.0, a1 = 0.0, a2 = INFINITY, a3 = -INFINITY;
+    int lo = 0x7fffffff;
+    for (int w = 0; w < 8; ++w) {
+      a0 += red[w][c][0]; a1 += red[w][c][1]; a2 = fmin(a2, red[w][c][2]); a3 = fmax(a3, red[w][c][3]);
+      lo = min(lo, (int)__double_as_longlong(red[w][c][4]));
+    }
+    double* p = part + (((int64_t)u * nsplit + s) * D + c) * 5;
+    p[0] = a0; p[1] = a1; p[2] = a2; p[3] = a3; p[4] = __longlong_as_double((long long)lo);
+  }
+}
+
 // ---------------------------------------------------------------- K2: pack
 struct PackArgs {
   const void* keys; const void* values; int dt;
@@ -137,6 +208,67 @@ __device__ __forceinline__ void quant4(const double (&x)[4], bool active, int lp
   }
 }
 
+
+// Fast quantisation of one lane's 4 elements against the reference's float64 grid.
+// m32 / err: float32 estimates of the exact float64 values and rigorous bounds on their
+// error (|m32 - m| <= err); exact(i) returns the exact float64 value.  The group min / max
+// are found exactly from the few candidates whose interval can hold the extreme, and each
+// code is decided in float32 unless its rounding interval straddles a grid boundary, in
+// which case it is recomputed exactly.  Results are bit-identical to quant4().
+template <typename Exact>
+__device__ __forceinline__ void quant4_fast(const float (&m32)[4], const float (&err)[4], Exact&& exact,
+                                            bool active, int lpg, int levels, uint32_t (&code)[4],
+                                            __half& qs16, __half& zp16, int* status) {
+  float umin = INFINITY, lmax = -INFINITY;
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { umin = fminf(umin, m32[i] + err[i]); lmax = fmaxf(lmax, m32[i] - err[i]); }
+  }
+  for (int o = 1; o < lpg; o <<= 1) {
+    umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+    lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  }
+  double mn = INFINITY, mx = -INFINITY;
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool cmin = m32[i] - err[i] <= umin, cmax = m32[i] + err[i] >= lmax;
+      if (cmin || cmax) {
+        const double e = exact(i);
+        if (cmin) mn = fmin(mn, e);
+        if (cmax) mx = fmax(mx, e);
+      }
+    }
+  }
+  group_minmax(mn, mx, lpg);
+  const double qs = (mx - mn) / (double)levels;
+  qs16 = __double2half(qs);
+  zp16 = __double2half(mn);
+  double qsd = (double)__half2float(qs16);
+  const double zpd = (double)__half2float(zp16);
+  if (active && (!isfinite(qsd) || !isfinite(zpd))) atomicOr(status, 1);
+  if (qs > 0.0 && qsd == 0.0) { qs16 = __float2half(5.9604644775390625e-08f); qsd = 5.9604644775390625e-08; }
+  const float zpf = (float)zpd, iqs = qsd > 0.0 ? 1.0f / (float)qsd : 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t c = 0;
+    if (qsd > 0.0) {
+      const float t = (m32[i] - zpf) * iqs;
+      const float b = (err[i] + fabsf(m32[i] - zpf) * 1.2e-7f) * iqs * 1.0001f + fabsf(t) * 5e-7f + 1e-6f;
+      const float lo = fminf(fmaxf(floorf(t + 0.5f - b), 0.f), (float)levels);
+      const float hi = fminf(fmaxf(floorf(t + 0.5f + b), 0.f), (float)levels);
+      if (lo == hi) {
+        c = (uint32_t)lo;
+      } else {
+        double ce = floor((exact(i) - zpd) / qsd + 0.5);
+        c = (uint32_t)fmin(fmax(ce, 0.0), (double)levels);
+      }
+    }
+    code[i] = c;
+  }
+}
+
+template <int DTY>
 __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int G = a.D / 4;
@@ -153,11 +285,18 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
   const int levels = (1 << a.bits) - 1;
   const bool active = lane < G;
   const int c0 = lane * 4;
+  constexpr bool FAST = DTY != IN_F64;
   double mu[4], al[4];
+  float mu32[4], dmu[4], inva[4];
+  bool mule[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     mu[i] = active ? a.mu64[(int64_t)u * a.D + c0 + i] : 0.0;
     al[i] = active ? a.alpha64[(int64_t)u * a.D + c0 + i] : 0.0;
+    mu32[i] = (float)mu[i];
+    mule[i] = mu[i] <= (double)mu32[i];
+    dmu[i] = (float)fabs(mu[i] - (double)mu32[i]) * 1.0001f;
+    inva[i] = al[i] > 0.0 ? 1.0f / (float)al[i] : 0.f;
   }
   const bool fast = a.signs_fast != nullptr;
   const int64_t tbeg = (int64_t)tile * a.tile, tend = min(a.L, tbeg + a.tile);
@@ -167,24 +306,75 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
 
   for (int64_t t = tbeg + warp; t < tend; t += PACK_WARPS) {
     const int64_t row = ((int64_t)u * a.L + t) * a.D;
-    double kp[4], v[4], m[4];
+    double kp[4];
     uint32_t code = 0;
+    uint32_t kc[4] = {0, 0, 0, 0}, vc[4] = {0, 0, 0, 0};
+    __half kqs = __float2half(0.f), kzp = kqs, vqs = kqs, vzp = kqs;
+    if (FAST) {
+      float kf[4] = {0.f, 0.f, 0.f, 0.f}, vf[4] = {0.f, 0.f, 0.f, 0.f};
+      if (active) {
+        load4<DTY>(a.keys, row + c0, kf);
+        load4<DTY>(a.values, row + c0, vf);
+      }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      double k = active ? load_in(a.keys, a.dt, row + c0 + i) : 0.0;
-      v[i] = active ? load_in(a.values, a.dt, row + c0 + i) : 0.0;
-      kp[i] = k - mu[i];
-      code |= (kp[i] >= 0.0 ? 1u : 0u) << (3 - i);
-    }
-    if (a.codes_in && active)
-      code = (a.codes_in[((int64_t)u * a.L + t) * rowb + (lane >> 1)] >> (4 * (lane & 1))) & 15u;
+      for (int i = 0; i < 4; ++i) {
+        kp[i] = (double)kf[i] - mu[i];
+        // K >= mu exactly, decided in float32 (no float32 lies strictly between mu and fl32(mu))
+        const bool ge = kf[i] > mu32[i] || (kf[i] == mu32[i] && mule[i]);
+        code |= (ge ? 1u : 0u) << (3 - i);
+      }
+      if (a.codes_in && active)
+        code = (a.codes_in[((int64_t)u * a.L + t) * rowb + (lane >> 1)] >> (4 * (lane & 1))) & 15u;
+      if (a.bits > 0) {
+        float m32[4], e32[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (a.siq) {
-        m[i] = al[i] == 0.0 ? 0.0 : fabs(kp[i]) / al[i];
-        if (active && m[i] > 1.0 + 1e-9) atomicOr(a.status, 2);
-      } else {
-        m[i] = kp[i];
+        for (int i = 0; i < 4; ++i) {
+          const float d = kf[i] - mu32[i];
+          if (a.siq) {
+            m32[i] = fabsf(d) * inva[i];
+            e32[i] = (dmu[i] + fabsf(d) * 2.4e-7f) * inva[i] * 1.0001f + m32[i] * 5e-7f + 1e-37f;
+            if (inva[i] == 0.f) { m32[i] = 0.f; e32[i] = 0.f; }
+          } else {
+            m32[i] = d;
+            e32[i] = dmu[i] + fabsf(d) * 1.2e-7f + 1e-37f;
+          }
+        }
+        auto kexact = [&](int i) -> double {
+          return a.siq ? (al[i] == 0.0 ? 0.0 : fabs(kp[i]) / al[i]) : kp[i];
+        };
+        if (a.siq && active) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (m32[i] + e32[i] > 1.0f + 1e-9f && kexact(i) > 1.0 + 1e-9) atomicOr(a.status, 2);
+        }
+        quant4_fast(m32, e32, kexact, active, lpg, levels, kc, kqs, kzp, a.status);
+        const float z4[4] = {0.f, 0.f, 0.f, 0.f};
+        quant4_fast(vf, z4, [&](int i) -> double { return (double)vf[i]; }, active, lpg, levels, vc, vqs, vzp,
+                    a.status);
+      }
+    } else {
+      double v[4], m[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double k = active ? load_in(a.keys, a.dt, row + c0 + i) : 0.0;
+        v[i] = active ? load_in(a.values, a.dt, row + c0 + i) : 0.0;
+        kp[i] = k - mu[i];
+        code |= (kp[i] >= 0.0 ? 1u : 0u) << (3 - i);
+      }
+      if (a.codes_in && active)
+        code = (a.codes_in[((int64_t)u * a.L + t) * rowb + (lane >> 1)] >> (4 * (lane & 1))) & 15u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (a.siq) {
+          m[i] = al[i] == 0.0 ? 0.0 : fabs(kp[i]) / al[i];
+          if (active && m[i] > 1.0 + 1e-9) atomicOr(a.status, 2);
+        } else {
+          m[i] = kp[i];
+        }
+      }
+      if (a.bits > 0) {   // bits == 0: lossless mode, codes + codebook only
+        quant4(m, active, lpg, levels, kc, kqs, kzp, a.status);
+        quant4(v, active, lpg, levels, vc, vqs, vzp, a.status);
       }
     }
     // codebook accumulation, token order within this warp's fixed token sequence
@@ -193,12 +383,6 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) e[i] += kp[i];
       cnt[lane * 16 + code] += 1;
-    }
-    uint32_t kc[4] = {0, 0, 0, 0}, vc[4] = {0, 0, 0, 0};
-    __half kqs = __float2half(0.f), kzp = kqs, vqs = kqs, vzp = kqs;
-    if (a.bits > 0) {   // bits == 0: lossless mode, codes + codebook only
-      quant4(m, active, lpg, levels, kc, kqs, kzp, a.status);
-      quant4(v, active, lpg, levels, vc, vqs, vzp, a.status);
     }
 
     // -------- reference layout
@@ -299,12 +483,298 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------- K2': group-parallel quantiser
+// D = 128, group 32, bf16 / f32 inputs: one thread per (token, 32-channel group), the 4
+// threads of a token are adjacent lanes.  Same arithmetic contract as pack_kernel (float32
+// fast path with exact float64 fix-ups, see quant4_fast), but each thread owns a whole
+// quantisation group (no shuffles for min / max) and builds its share of the fast record in
+// registers; the codebook is accumulated by codebook_tile_kernel.
+constexpr int QG_TOK = 64;                 // tokens per 256-thread CTA
+
+__device__ __forceinline__ uint32_t or4(uint32_t v) {   // OR over the 4 lanes of a token
+  v |= __shfl_xor_sync(0xffffffffu, v, 1);
+  v |= __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+template <typename Exact>
+__device__ __forceinline__ void quant_group32(const float (&m32)[32], const float (&err)[32], Exact&& exact,
+                                              int levels, uint32_t (&code)[32], __half& qs16, __half& zp16,
+                                              int* status, bool valid) {
+  float umin = INFINITY, lmax = -INFINITY;
+#pragma unroll
+  for (int n = 0; n < 32; ++n) { umin = fminf(umin, m32[n] + err[n]); lmax = fmaxf(lmax, m32[n] - err[n]); }
+  double mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const bool cmin = m32[n] - err[n] <= umin, cmax = m32[n] + err[n] >= lmax;
+    if (cmin || cmax) {
+      const double e = exact(n);
+      if (cmin) mn = fmin(mn, e);
+      if (cmax) mx = fmax(mx, e);
+    }
+  }
+  const double qs = (mx - mn) / (double)levels;
+  qs16 = __double2half(qs);
+  zp16 = __double2half(mn);
+  double qsd = (double)__half2float(qs16);
+  const double zpd = (double)__half2float(zp16);
+  if (valid && (!isfinite(qsd) || !isfinite(zpd))) atomicOr(status, 1);
+  if (qs > 0.0 && qsd == 0.0) { qs16 = __float2half(5.9604644775390625e-08f); qsd = 5.9604644775390625e-08; }
+  const float zpf = (float)zpd, iqs = qsd > 0.0 ? 1.0f / (float)qsd : 0.f;
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    uint32_t c = 0;
+    if (qsd > 0.0) {
+      const float t = (m32[n] - zpf) * iqs;
+      const float b = (err[n] + fabsf(m32[n] - zpf) * 1.2e-7f) * iqs * 1.0001f + fabsf(t) * 5e-7f + 1e-6f;
+      const float lo = fminf(fmaxf(floorf(t + 0.5f - b), 0.f), (float)levels);
+      const float hi = fminf(fmaxf(floorf(t + 0.5f + b), 0.f), (float)levels);
+      if (lo == hi) {
+        c = (uint32_t)lo;
+      } else {
+        const double ce = floor((exact(n) - zpd) / qsd + 0.5);
+        c = (uint32_t)fmin(fmax(ce, 0.0), (double)levels);
+      }
+    }
+    code[n] = c;
+  }
+}
+
+template <int DTY>
+__global__ void __launch_bounds__(256) quant_group_kernel(PackArgs a) {
+  __shared__ float s_mu32[4][33], s_inva[4][33], s_e0[4][33];
+  __shared__ double s_mu[4][33], s_al[4][33];
+  const int tid = threadIdx.x, lane = tid & 31, j = tid & 3;
+  const int64_t u = blockIdx.y;
+  const int64_t t = (int64_t)blockIdx.x * QG_TOK + (tid >> 2);
+  const bool valid = t < a.L;
+  for (int c = tid; c < FD; c += 256) {
+    const double mu = a.mu64[u * FD + c], al = a.alpha64[u * FD + c];
+    const float m32 = (float)mu;
+    const float inva = al > 0.0 ? 1.0f / (float)al : 0.f;
+    s_mu[c >> 5][c & 31] = mu;
+    s_al[c >> 5][c & 31] = al;
+    s_mu32[c >> 5][c & 31] = m32;
+    s_inva[c >> 5][c & 31] = inva;
+    s_e0[c >> 5][c & 31] = (float)fabs(mu - (double)m32) * 1.0001f * inva * 1.0001f;
+  }
+  __syncthreads();
+  const int levels = (1 << a.bits) - 1;
+  const int64_t row = (u * a.L + (valid ? t : 0)) * FD + 32 * j;
+  float kf[32], vf[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float x[4], y[4];
+    load4<DTY>(a.keys, row + 4 * q, x);
+    load4<DTY>(a.values, row + 4 * q, y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { kf[4 * q + i] = x[i]; vf[4 * q + i] = y[i]; }
+  }
+  // sign codes (K >= mu exactly, decided in float32) -> 4 reference bytes = word j of the row
+  uint32_t cw = 0, negw = 0;   // negw: bit n = channel 32j + n is negative
+#pragma unroll
+  for (int n = 0; n < 32; ++n) {
+    const float m32 = s_mu32[j][n];
+    const bool ge = kf[n] > m32 || (kf[n] == m32 && s_mu[j][n] <= (double)m32);
+    cw |= (ge ? 1u : 0u) << (4 * (n >> 2) + 3 - (n & 3));
+    negw |= (ge ? 0u : 1u) << n;
+  }
+  uint32_t kc[32], vc[32];
+  __half kqs = __float2half(0.f), kzp = kqs, vqs = kqs, vzp = kqs;
+  if (a.bits > 0) {
+    float m32[32], e32[32];
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float d = kf[n] - s_mu32[j][n];
+      if (a.siq) {
+        const float inva = s_inva[j][n];
+        m32[n] = fabsf(d) * inva;
+        e32[n] = s_e0[j][n] + fabsf(d) * 2.4e-7f * inva * 1.0001f + m32[n] * 5e-7f + 1e-37f;
+        if (inva == 0.f) { m32[n] = 0.f; e32[n] = 0.f; }
+      } else {
+        m32[n] = d;
+        e32[n] = s_e0[j][n] / (s_inva[j][n] > 0.f ? s_inva[j][n] : 1.f) + fabsf(d) * 1.2e-7f + 1e-37f;
+      }
+    }
+    auto kexact = [&](int n) -> double {
+      const double kd = (double)kf[n] - s_mu[j][n];
+      if (!a.siq) return kd;
+      const double al = s_al[j][n];
+      return al == 0.0 ? 0.0 : fabs(kd) / al;
+    };
+    if (a.siq && valid) {
+#pragma unroll
+      for (int n = 0; n < 32; ++n)
+        if (m32[n] + e32[n] > 1.0f + 1e-9f && kexact(n) > 1.0 + 1e-9) atomicOr(a.status, 2);
+    }
+    quant_group32(m32, e32, kexact, levels, kc, kqs, kzp, a.status, valid);
+    float z32[32];
+#pragma unroll
+    for (int n = 0; n < 32; ++n) z32[n] = 0.f;
+    quant_group32(vf, z32, [&](int n) -> double { return (double)vf[n]; }, levels, vc, vqs, vzp, a.status,
+                  valid);
+  }
+  const int64_t tok = u * a.L + t;
+  // ---------------- reference layout
+  if (valid && a.codes_ref) reinterpret_cast<uint32_t*>(a.codes_ref + tok * 16)[j] = cw;
+  if (valid && a.bits > 0) {
+    // group j's payload = bytes [4 bits j, 4 bits (j + 1)) of the row; element n at
+    // bit (n * bits) of that little-endian byte string
+    auto put = [&](uint8_t* dst, const uint32_t (&cc)[32]) {
+      if (!dst) return;
+      uint32_t* r = reinterpret_cast<uint32_t*>(dst + tok * (16 * a.bits) + 4 * a.bits * j);
+      switch (a.bits) {
+        case 1: { uint32_t w = 0;
+#pragma unroll
+                  for (int n = 0; n < 32; ++n) w |= cc[n] << n;
+                  r[0] = w; break; }
+        case 2:
+#pragma unroll
+          for (int q = 0; q < 2; ++q) { uint32_t w = 0;
+#pragma unroll
+            for (int n = 0; n < 16; ++n) w |= cc[16 * q + n] << (2 * n);
+            r[q] = w; }
+          break;
+        case 4:
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { uint32_t w = 0;
+#pragma unroll
+            for (int n = 0; n < 8; ++n) w |= cc[8 * q + n] << (4 * n);
+            r[q] = w; }
+          break;
+        default:
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { uint32_t w = 0;
+#pragma unroll
+            for (int n = 0; n < 4; ++n) w |= cc[4 * q + n] << (8 * n);
+            r[q] = w; }
+      }
+    };
+    put(a.kq_ref, kc);
+    put(a.vq_ref, vc);
+    const int64_t pi = tok * 4 + j;
+    if (a.ks_ref) { a.ks_ref[pi] = kqs; a.kz_ref[pi] = kzp; }
+    if (a.vs_ref) { a.vs_ref[pi] = vqs; a.vz_ref[pi] = vzp; }
+  }
+  // ---------------- fast layout (bits = 2, sign-in-quant)
+  if (a.signs_fast) {
+    // rotated sign row: byte i of token t = reference byte (t + i) mod 16
+    const int rot = (int)(t & 15), base = lane & ~3;
+    const int wsh = rot >> 2, bsh = 8 * (rot & 3);
+    const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
+    const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
+    const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
+    // K payload: channel 32j + n -> word 2*t4(n) + (j >> 1), bit 8(j&1) + 4(n>>4) + 2e(n) + 16hi(n)
+    uint32_t kp4[4] = {0, 0, 0, 0}, vp8[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sg4[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const int r = n & 15, e = r >> 3, rr = r & 7, t4 = rr >> 1, hb = rr & 1;
+      kp4[t4] |= kc[n] << (4 * (n >> 4) + 2 * e + 16 * hb);
+      vp8[r & 7] |= vc[n] << (4 * (n >> 4) + 2 * e);
+      sg4[t4] |= ((negw >> n) & 1u) << ((((n >> 4) << 1) | e) + 16 * hb);
+    }
+    uint32_t out[8];
+    // K payload words 2*t4 + u (u = j >> 1): combine the two groups of this u (lanes j, j^1)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t mine = kp4[q] << (8 * (j & 1));
+      kp4[q] = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
+    }
+    // V payload words g: byte j of every word comes from group j
+#pragma unroll
+    for (int q = 0; q < 8; ++q) vp8[q] = or4(vp8[q] << (8 * j));
+    // K sign words t4: bit 8u + i + 16hi, u = j >> 1, i = (2(j&1) + (n>>4)) << 1 | e
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sg4[q] = or4(sg4[q] << (8 * (j >> 1) + 4 * (j & 1)));
+    const uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
+    const uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
+    // record words: 0-7 K payload, 8-15 V payload, 16-19 K params, 20-23 V params, 24-27 K signs
+    // thread j writes words {2*t4 + u : t4 in {2(j&1), 2(j&1)+1}}, 8 + 2j, 9 + 2j, 16 + j, 20 + j,
+    // 24 + j, 28 + j
+    auto pick4 = [&](const uint32_t (&v)[4], int i) {
+      return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
+    };
+    auto pick8 = [&](const uint32_t (&v)[8], int i) {
+      uint32_t r = v[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) r = i == q ? v[q] : r;
+      return r;
+    };
+    out[0] = pick4(kp4, 2 * (j & 1));
+    out[1] = pick4(kp4, 2 * (j & 1) + 1);
+    out[2] = pick8(vp8, 2 * j);
+    out[3] = pick8(vp8, 2 * j + 1);
+    out[4] = kpar;
+    out[5] = vpar;
+    out[6] = pick4(sg4, j);
+    out[7] = 0u;
+    if (valid) {
+      reinterpret_cast<uint32_t*>(a.signs_fast + tok * FSIGN)[j] = rw;
+      uint32_t* rec = reinterpret_cast<uint32_t*>(a.recs_fast + tok * FREC);
+      const int uu = j >> 1;
+      rec[2 * (2 * (j & 1)) + uu] = out[0];
+      rec[2 * (2 * (j & 1) + 1) + uu] = out[1];
+      rec[8 + 2 * j] = out[2];
+      rec[9 + 2 * j] = out[3];
+      rec[16 + j] = out[4];
+      rec[20 + j] = out[5];
+      rec[24 + j] = out[6];
+      rec[28 + j] = out[7];
+    }
+  }
+}
+
+// Codebook partial sums for one token tile: thread (sign group g, channel i) accumulates
+// K' = fl64(K - mu) into its private accumulator of the token's code, in token order.
+// Deterministic; the fixed-order tile combine happens in codebook_final_kernel.
+template <int DTY>
+__global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restrict__ keys, int64_t L,
+                                                            const double* __restrict__ mu64, int tile,
+                                                            int ntiles, double* __restrict__ part,
+                                                            int* __restrict__ cntp) {
+  __shared__ double acc[16][128];
+  __shared__ int cnt[16][32];
+  const int c = threadIdx.x, lane = c & 31, g = c >> 2;
+  const int64_t u = blockIdx.y;
+  const int tl = blockIdx.x;
+  for (int q = 0; q < 16; ++q) acc[q][c] = 0.0;
+  for (int q = c; q < 16 * 32; q += 128) cnt[q >> 5][q & 31] = 0;
+  const double mu = mu64[u * FD + c];
+  const float mu32 = (float)mu;
+  const bool mule = mu <= (double)mu32;
+  __syncthreads();
+  const int64_t t0 = (int64_t)tl * tile, t1 = min(L, t0 + tile);
+  for (int64_t t = t0; t < t1; ++t) {
+    float x;
+    if (DTY == IN_BF16)
+      x = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(keys)[(u * L + t) * FD + c]);
+    else
+      x = reinterpret_cast<const float*>(keys)[(u * L + t) * FD + c];
+    const bool ge = x > mu32 || (x == mu32 && mule);
+    // the 4 channels of sign group g are lanes 4(g & 7) .. +3 of this warp
+    uint32_t bit = (ge ? 1u : 0u) << (3 - (c & 3));
+    bit |= __shfl_xor_sync(0xffffffffu, bit, 1);
+    bit |= __shfl_xor_sync(0xffffffffu, bit, 2);
+    acc[bit][c] += (double)x - mu;
+    if ((c & 3) == 0) cnt[bit][g] += 1;
+  }
+  __syncthreads();
+  double* outp = part + (u * ntiles + tl) * (int64_t)(32 * 64);
+  int* outc = cntp + (u * ntiles + tl) * (int64_t)(32 * 16);
+  // partial layout [g][code][i]
+  for (int q = 0; q < 16; ++q) outp[(g * 16 + q) * 4 + (c & 3)] = acc[q][c];
+  for (int q = c; q < 32 * 16; q += 128) outc[q] = cnt[q & 15][q >> 4];
+  (void)lane;
+}
+
 // ---------------------------------------------------------------- K3: codebook finalise
 __global__ void codebook_final_kernel(int G, int ntiles, const double* __restrict__ part,
                                       const int* __restrict__ cnt, double* __restrict__ c64,
                                       float* __restrict__ c32) {
   const int u = blockIdx.x;
-  for (int i = threadIdx.x; i < G * 64; i += blockDim.x) {
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < G * 64; i += blockDim.x * gridDim.y) {
     double s = 0.0;
     int n = 0;
     for (int t = 0; t < ntiles; ++t) {
@@ -352,7 +822,7 @@ __global__ void append_kernel(const void* __restrict__ k, const void* __restrict
 
 // ---------------------------------------------------------------- host launchers
 int stats_nsplit(int64_t L) { int64_t n = L / 512; if (n < 1) n = 1; if (n > 64) n = 64; return (int)n; }
-constexpr int PACK_TILE = 512;
+constexpr int PACK_TILE = 2048;
 int pack_ntiles(int64_t L) { return (int)((L + PACK_TILE - 1) / PACK_TILE); }
 
 size_t encode_workspace_bytes(int64_t U, int64_t L, int D) {
@@ -382,7 +852,12 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
 
   const int bs = D <= 128 ? 128 : 256;
   if (what & 1) {
-    stats_partial_kernel<<<dim3((unsigned)U, nsplit), bs, 0, st>>>(keys, dt, L, D, nsplit, spart, status);
+    if (dt == IN_BF16 && D % 4 == 0 && D <= 128)
+      stats_partial_fast_kernel<IN_BF16><<<dim3((unsigned)U, nsplit), 256, 0, st>>>(keys, L, D, nsplit, spart, status);
+    else if (dt == IN_F32 && D % 4 == 0 && D <= 128)
+      stats_partial_fast_kernel<IN_F32><<<dim3((unsigned)U, nsplit), 256, 0, st>>>(keys, L, D, nsplit, spart, status);
+    else
+      stats_partial_kernel<<<dim3((unsigned)U, nsplit), bs, 0, st>>>(keys, dt, L, D, nsplit, spart, status);
     stats_final_kernel<<<(unsigned)U, bs, 0, st>>>(keys, dt, L, D, nsplit, spart, mu64, alpha64, mu32,
                                                    alpha32, status);
   }
@@ -390,10 +865,33 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
   PackArgs pa{keys, values, dt, L, D, bits, gs, siq, mu64, alpha64, codes_ref, kq_ref, ks, kz,
               vq_ref, vs, vz, signs_fast, recs_fast, cbp, cbc, ntiles, PACK_TILE, status, codes_in};
   size_t smem = (size_t)PACK_WARPS * G * 64 * sizeof(double) + (size_t)PACK_WARPS * G * 16 * sizeof(int);
-  cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (D == FD && gs == 32 && (bits == 1 || bits == 2 || bits == 4 || bits == 8) && dt != IN_F64 && !codes_in) {
+    const int ctile = 4096, cnt_tiles = (int)((L + ctile - 1) / ctile);
+    if (cnt_tiles > ntiles) return cudaErrorInvalidValue;   // workspace sized for pack tiles
+    dim3 qg((unsigned)((L + QG_TOK - 1) / QG_TOK), (unsigned)U);
+    if (dt == IN_BF16) {
+      quant_group_kernel<IN_BF16><<<qg, 256, 0, st>>>(pa);
+      codebook_tile_kernel<IN_BF16><<<dim3(cnt_tiles, (unsigned)U), 128, 0, st>>>(keys, L, mu64, ctile, cnt_tiles,
+                                                                              cbp, cbc);
+    } else {
+      quant_group_kernel<IN_F32><<<qg, 256, 0, st>>>(pa);
+      codebook_tile_kernel<IN_F32><<<dim3(cnt_tiles, (unsigned)U), 128, 0, st>>>(keys, L, mu64, ctile, cnt_tiles,
+                                                                             cbp, cbc);
+    }
+    codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, cnt_tiles, cbp, cbc, c64,
+                                                                                  c32);
+    return cudaGetLastError();
+  }
+  auto launch = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<dim3(ntiles, (unsigned)U), PACK_WARPS * 32, smem, st>>>(pa);
+    return cudaSuccess;
+  };
+  cudaError_t e = dt == IN_BF16 ? launch(pack_kernel<IN_BF16>) : dt == IN_F32 ? launch(pack_kernel<IN_F32>)
+                                                                               : launch(pack_kernel<IN_F64>);
   if (e != cudaSuccess) return e;
-  pack_kernel<<<dim3(ntiles, (unsigned)U), PACK_WARPS * 32, smem, st>>>(pa);
-  codebook_final_kernel<<<(unsigned)U, 256, 0, st>>>(G, ntiles, cbp, cbc, c64, c32);
+  codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, ntiles, cbp, cbc, c64, c32);
   return cudaGetLastError();
 }
 

@@ -411,3 +411,61 @@ class TestCacheAttention:   # test_cache.py, test_attention.py
         mu, al = O.channel_stats(K)
         np.testing.assert_array_equal(N(st.mu), mu)
         np.testing.assert_array_equal(N(st.alpha), al)
+
+
+class TestFastEncoderPath:
+    """bf16 / f32 inputs take the encoder's float32 fast path with exact float64 fix-ups;
+    its planes must equal the oracle's (float64 reference arithmetic) bit for bit."""
+
+    @pytest.mark.parametrize("bits", [1, 2, 4, 8])
+    @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+    def test_quantize_values(self, bits, dtype):
+        rng = np.random.default_rng(bits)
+        V = rng.standard_normal((300, 64)) * rng.uniform(0.01, 30, size=(300, 1))
+        Vt = torch.tensor(V, dtype=dtype, device="cuda")
+        Vd = Vt.double().cpu().numpy()
+        q = sk.quantize_values(Vt, sk.QuantConfig(bits=bits, group_size=32))
+        o = O.quantize(Vd, bits, 32)
+        np.testing.assert_array_equal(N(q.packed), o.packed)
+        np.testing.assert_array_equal(N(q.scales), o.scales)
+        np.testing.assert_array_equal(N(q.zeros), o.zeros)
+
+    @pytest.mark.parametrize("bits,siq", [(2, True), (4, True), (8, True), (2, False), (1, True)])
+    @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+    def test_prefill_planes(self, bits, siq, dtype):
+        u = gen_unit(2000, 128, 2, 40 + bits, bf16=False)
+        K = torch.tensor(u.keys, dtype=dtype, device="cuda")
+        V = torch.tensor(u.values * 3.0, dtype=dtype, device="cuda")
+        cache = sk.prefill(K, V, config=sk.CacheConfig(bits=bits, group_size=32, sink_count=16, sign_in_quant=siq))
+        oc = O.prefill(K.double().cpu().numpy(), V.double().cpu().numpy(), bits=bits, group=32, sink_count=16,
+                       sign_in_quant=siq)
+        np.testing.assert_array_equal(N(cache.norm.mu), oc.mu)
+        np.testing.assert_array_equal(N(cache.norm.alpha), oc.alpha)
+        np.testing.assert_array_equal(N(cache.codes.packed), oc.packed_codes)
+        kq = cache.key_mag if siq else cache.key_direct
+        ko = oc.kmag if siq else oc.kdirect
+        np.testing.assert_array_equal(N(kq.packed), ko.packed)
+        np.testing.assert_array_equal(N(kq.scales), ko.scales)
+        np.testing.assert_array_equal(N(kq.zeros), ko.zeros)
+        np.testing.assert_array_equal(N(cache.values.packed), oc.vq.packed)
+        np.testing.assert_array_equal(N(cache.values.scales), oc.vq.scales)
+        np.testing.assert_array_equal(N(cache.values.zeros), oc.vq.zeros)
+        np.testing.assert_array_equal(N(cache.codebook.centroids).astype(np.float32), oc.centroids.astype(np.float32))
+
+    def test_constant_and_offset_channels(self):
+        """Degenerate groups, alpha = 0 channels and large offsets (mu far from 0)."""
+        rng = np.random.default_rng(3)
+        K = (rng.standard_normal((777, 128)) * 0.01 + 1000.0).astype(np.float32)
+        K[:, 5] = 7.25
+        K[:, 64:96] = 3.0
+        V = np.repeat(rng.standard_normal((777, 1)), 128, axis=1).astype(np.float32)
+        Kt = torch.tensor(K, device="cuda")
+        Vt = torch.tensor(V, device="cuda")
+        cache = sk.prefill(Kt, Vt, config=sk.CacheConfig(sink_count=8))
+        oc = O.prefill(K.astype(np.float64), V.astype(np.float64), sink_count=8)
+        np.testing.assert_array_equal(N(cache.codes.packed), oc.packed_codes)
+        np.testing.assert_array_equal(N(cache.key_mag.packed), oc.kmag.packed)
+        np.testing.assert_array_equal(N(cache.key_mag.scales), oc.kmag.scales)
+        np.testing.assert_array_equal(N(cache.key_mag.zeros), oc.kmag.zeros)
+        np.testing.assert_array_equal(N(cache.values.packed), oc.vq.packed)
+        np.testing.assert_array_equal(N(cache.values.scales), oc.vq.scales)
