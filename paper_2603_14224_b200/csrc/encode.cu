@@ -14,6 +14,7 @@
 // failing this certificate are re-summed sequentially in row order (reference order).
 #include "common.cuh"
 #include <math.h>
+#include <type_traits>
 
 namespace sikv {
 
@@ -487,9 +488,14 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
 // ---------------------------------------------------------------- K2': group-parallel quantiser
 // D = 128, group 32, bf16 / f32 inputs: one thread per (token, 32-channel group), the 4
 // threads of a token are adjacent lanes.  Same arithmetic contract as pack_kernel (float32
-// fast path with exact float64 fix-ups, see quant4_fast), but each thread owns a whole
-// quantisation group (no shuffles for min / max) and builds its share of the fast record in
+// estimates with rigorous error bounds, exact float64 where an estimate is ambiguous), but
+// each thread owns a whole quantisation group and builds its share of the fast record in
 // registers; the codebook is accumulated by codebook_tile_kernel.
+//
+// Error model (see quant4_fast): every float32 magnitude estimate m_n of channel n satisfies
+// |m_n - exact_n| <= e0[n] + |m_n| * 7.5e-7, so the group-wide E = max e0 + max|m| * 7.5e-7
+// bounds all of them.  The exact group min (max) can only be attained by channels with
+// m_n <= min m + 2E (m_n >= max m - 2E); those few are evaluated in float64.
 constexpr int QG_TOK = 64;                 // tokens per 256-thread CTA
 
 __device__ __forceinline__ uint32_t or4(uint32_t v) {   // OR over the 4 lanes of a token
@@ -498,230 +504,256 @@ __device__ __forceinline__ uint32_t or4(uint32_t v) {   // OR over the 4 lanes o
   return v;
 }
 
-template <typename Exact>
-__device__ __forceinline__ void quant_group32(const float (&m32)[32], const float (&err)[32], Exact&& exact,
-                                              int levels, uint32_t (&code)[32], __half& qs16, __half& zp16,
-                                              int* status, bool valid) {
-  float umin = INFINITY, lmax = -INFINITY;
+// one thread's 32 consecutive input elements, kept packed until they are needed
+template <int DTY>
+struct Raw32 {
+  static constexpr int NW = DTY == IN_BF16 ? 16 : 32;
+  uint32_t w[NW];
+  __device__ __forceinline__ void load(const void* p, int64_t idx) {
+    const uint4* q = DTY == IN_BF16
+                         ? reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p) + idx)
+                         : reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(p) + idx);
 #pragma unroll
-  for (int n = 0; n < 32; ++n) { umin = fminf(umin, m32[n] + err[n]); lmax = fmaxf(lmax, m32[n] - err[n]); }
-  double mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const bool cmin = m32[n] - err[n] <= umin, cmax = m32[n] + err[n] >= lmax;
-    if (cmin || cmax) {
-      const double e = exact(n);
-      if (cmin) mn = fmin(mn, e);
-      if (cmax) mx = fmax(mx, e);
+    for (int k = 0; k < NW / 4; ++k) {
+      const uint4 v = __ldg(q + k);
+      w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
     }
   }
+  __device__ __forceinline__ float operator[](int n) const {
+    if (DTY == IN_BF16) return __uint_as_float((n & 1) ? (w[n >> 1] & 0xFFFF0000u) : (w[n >> 1] << 16));
+    return __uint_as_float(w[n]);
+  }
+};
+
+template <int DTY>
+__device__ __forceinline__ float load1(const void* p, int64_t idx) {
+  if (DTY == IN_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+  return reinterpret_cast<const float*>(p)[idx];
+}
+
+// Quantise one 32-element group (quantizer.py:119-130).  m: float32 estimates, E: group error
+// bound (0 = the estimates are exact), [mmin, mmax]: range of m, exact(n): float64 value.
+// emit(n, code) is called once per element with a compile-time n.
+template <int BITS, typename Exact, typename Emit>
+__device__ __forceinline__ void quant_group32(const float (&m)[32], float E, float mmin, float mmax, Exact&& exact,
+                                              Emit&& emit, __half& qs16, __half& zp16, double& mxo) {
+  constexpr int levels = (1 << BITS) - 1;
+  double mn, mx;
+  if (E == 0.f) {
+    mn = (double)mmin;
+    mx = (double)mmax;
+  } else {
+    const float thr_lo = __fadd_ru(mmin, 2.f * E), thr_hi = __fsub_rd(mmax, 2.f * E);
+    uint32_t cmin = 0, cmax = 0;
+#pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      cmin |= (m[n] <= thr_lo ? 1u : 0u) << n;
+      cmax |= (m[n] >= thr_hi ? 1u : 0u) << n;
+    }
+    mn = INFINITY;
+    mx = -INFINITY;
+    for (uint32_t c = cmin | cmax; c; c &= c - 1) {
+      const int n = __ffs((int)c) - 1;
+      const double e = exact(n);
+      if ((cmin >> n) & 1u) mn = fmin(mn, e);
+      if ((cmax >> n) & 1u) mx = fmax(mx, e);
+    }
+  }
+  mxo = mx;
   const double qs = (mx - mn) / (double)levels;
   qs16 = __double2half(qs);
   zp16 = __double2half(mn);
   double qsd = (double)__half2float(qs16);
   const double zpd = (double)__half2float(zp16);
-  if (valid && (!isfinite(qsd) || !isfinite(zpd))) atomicOr(status, 1);
   if (qs > 0.0 && qsd == 0.0) { qs16 = __float2half(5.9604644775390625e-08f); qsd = 5.9604644775390625e-08; }
-  const float zpf = (float)zpd, iqs = qsd > 0.0 ? 1.0f / (float)qsd : 0.f;
+  if (!(qsd > 0.0)) return;                        // all codes 0
+  const float zpf = (float)zpd, iqs = 1.0f / (float)qsd;
+  // group-wide ambiguity margin >= the per-element bound of quant4_fast
+  const float dev = fmaxf(fabsf(mmax - zpf), fabsf(zpf - mmin)) * 1.0001f;
+  const float B = (E + dev * 1.2e-7f) * iqs * 1.0001f + dev * iqs * 5.01e-7f + 1e-6f;
 #pragma unroll
   for (int n = 0; n < 32; ++n) {
-    uint32_t c = 0;
-    if (qsd > 0.0) {
-      const float t = (m32[n] - zpf) * iqs;
-      const float b = (err[n] + fabsf(m32[n] - zpf) * 1.2e-7f) * iqs * 1.0001f + fabsf(t) * 5e-7f + 1e-6f;
-      const float lo = fminf(fmaxf(floorf(t + 0.5f - b), 0.f), (float)levels);
-      const float hi = fminf(fmaxf(floorf(t + 0.5f + b), 0.f), (float)levels);
-      if (lo == hi) {
-        c = (uint32_t)lo;
-      } else {
-        const double ce = floor((exact(n) - zpd) / qsd + 0.5);
-        c = (uint32_t)fmin(fmax(ce, 0.0), (double)levels);
-      }
+    const float x = (m[n] - zpf) * iqs + 0.5f;
+    const float f = floorf(x), fr = x - f;
+    uint32_t c = (uint32_t)fminf(fmaxf(f, 0.f), (float)levels);
+    if (fminf(fr, 1.f - fr) < B) {
+      const double ce = floor((exact(n) - zpd) / qsd + 0.5);
+      c = (uint32_t)fmin(fmax(ce, 0.0), (double)levels);
     }
-    code[n] = c;
+    emit(n, c);
   }
 }
 
-template <int DTY>
-__global__ void __launch_bounds__(256) quant_group_kernel(PackArgs a) {
-  __shared__ float s_mu32[4][33], s_inva[4][33], s_e0[4][33];
+template <int DTY, int BITS>
+__global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
+  __shared__ float2 s_c[4][33];                   // (mu32, 1/alpha or 1) per channel
+  __shared__ float s_e0[4][33];
   __shared__ double s_mu[4][33], s_al[4][33];
+  __shared__ uint32_t s_mule[4];                  // bit n: mu <= fl32(mu) for channel 32j + n
+  __shared__ float s_e0max[4];
   const int tid = threadIdx.x, lane = tid & 31, j = tid & 3;
   const int64_t u = blockIdx.y;
   const int64_t t = (int64_t)blockIdx.x * QG_TOK + (tid >> 2);
   const bool valid = t < a.L;
-  for (int c = tid; c < FD; c += 256) {
+  const bool siq = a.siq != 0;
+  if (tid < FD) {
+    const int c = tid, g = c >> 5, n = c & 31;   // warp g holds group g
     const double mu = a.mu64[u * FD + c], al = a.alpha64[u * FD + c];
     const float m32 = (float)mu;
-    const float inva = al > 0.0 ? 1.0f / (float)al : 0.f;
-    s_mu[c >> 5][c & 31] = mu;
-    s_al[c >> 5][c & 31] = al;
-    s_mu32[c >> 5][c & 31] = m32;
-    s_inva[c >> 5][c & 31] = inva;
-    s_e0[c >> 5][c & 31] = (float)fabs(mu - (double)m32) * 1.0001f * inva * 1.0001f;
+    const float inva = siq ? (al > 0.0 ? 1.0f / (float)al : 0.f) : 1.f;
+    const float dmu = (float)fabs(mu - (double)m32) * 1.0001f;
+    const float e0 = (siq ? dmu * inva * 1.0001f : dmu) + 1e-37f;
+    s_c[g][n] = make_float2(m32, inva);
+    s_e0[g][n] = e0;
+    s_mu[g][n] = mu;
+    s_al[g][n] = al;
+    const uint32_t mule = __ballot_sync(0xffffffffu, mu <= (double)m32);
+    const uint32_t emax = __reduce_max_sync(0xffffffffu, __float_as_uint(e0));
+    if (n == 0) { s_mule[g] = mule; s_e0max[g] = __uint_as_float(emax); }
   }
   __syncthreads();
-  const int levels = (1 << a.bits) - 1;
   const int64_t row = (u * a.L + (valid ? t : 0)) * FD + 32 * j;
-  float kf[32], vf[32];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float x[4], y[4];
-    load4<DTY>(a.keys, row + 4 * q, x);
-    load4<DTY>(a.values, row + 4 * q, y);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { kf[4 * q + i] = x[i]; vf[4 * q + i] = y[i]; }
-  }
-  // sign codes (K >= mu exactly, decided in float32) -> 4 reference bytes = word j of the row
-  uint32_t cw = 0, negw = 0;   // negw: bit n = channel 32j + n is negative
+  Raw32<DTY> kr;
+  kr.load(a.keys, row);
+  // sign codes (K >= mu exactly, decided in float32) and key magnitudes
+  const uint32_t mule = s_mule[j], absmask = siq ? 0x7fffffffu : 0xffffffffu;
+  uint32_t cw = 0, negw = 0;                      // cw: word j of the reference code row
+  float km[32];
+  float kmin = INFINITY, kmax = -INFINITY;
 #pragma unroll
   for (int n = 0; n < 32; ++n) {
-    const float m32 = s_mu32[j][n];
-    const bool ge = kf[n] > m32 || (kf[n] == m32 && s_mu[j][n] <= (double)m32);
+    const float2 c = s_c[j][n];
+    const float x = kr[n];
+    const bool ge = x > c.x || (x == c.x && ((mule >> n) & 1u));
     cw |= (ge ? 1u : 0u) << (4 * (n >> 2) + 3 - (n & 3));
     negw |= (ge ? 0u : 1u) << n;
+    km[n] = __uint_as_float(__float_as_uint(x - c.x) & absmask) * c.y;
+    kmin = fminf(kmin, km[n]);
+    kmax = fmaxf(kmax, km[n]);
   }
-  uint32_t kc[32], vc[32];
+  // packed codes: reference words (element n at bit BITS*n of the group's byte string) and,
+  // for BITS == 2, this group's share of the fast record words
+  constexpr int PER = BITS > 0 ? 32 / BITS : 32;
+  uint32_t kref[BITS > 0 ? BITS : 1], vref[BITS > 0 ? BITS : 1];
+  uint32_t kp4[4] = {0, 0, 0, 0}, vp8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   __half kqs = __float2half(0.f), kzp = kqs, vqs = kqs, vzp = kqs;
-  if (a.bits > 0) {
-    float m32[32], e32[32];
+  if (BITS > 0) {
 #pragma unroll
-    for (int n = 0; n < 32; ++n) {
-      const float d = kf[n] - s_mu32[j][n];
-      if (a.siq) {
-        const float inva = s_inva[j][n];
-        m32[n] = fabsf(d) * inva;
-        e32[n] = s_e0[j][n] + fabsf(d) * 2.4e-7f * inva * 1.0001f + m32[n] * 5e-7f + 1e-37f;
-        if (inva == 0.f) { m32[n] = 0.f; e32[n] = 0.f; }
-      } else {
-        m32[n] = d;
-        e32[n] = s_e0[j][n] / (s_inva[j][n] > 0.f ? s_inva[j][n] : 1.f) + fabsf(d) * 1.2e-7f + 1e-37f;
-      }
+    for (int q = 0; q < (BITS > 0 ? BITS : 1); ++q) { kref[q] = 0; vref[q] = 0; }
+    {
+      const float E = __fmaf_ru(fmaxf(fabsf(kmin), fabsf(kmax)), 7.5e-7f, s_e0max[j]);
+      auto kexact = [&](int n) -> double {
+        const double kd = (double)load1<DTY>(a.keys, row + n) - s_mu[j][n];
+        if (!siq) return kd;
+        const double al = s_al[j][n];
+        return al == 0.0 ? 0.0 : fabs(kd) / al;
+      };
+      auto kemit = [&](int n, uint32_t c) {
+        kref[n / PER] |= c << (BITS * (n % PER));
+        if constexpr (BITS == 2) {
+          // channel 32j + n -> word 2*t4(n) + (j >> 1), bit 8(j&1) + 4(n>>4) + 2e(n) + 16hi(n)
+          const int r = n & 15, e = r >> 3, rr = r & 7;
+          kp4[rr >> 1] |= c << (4 * (n >> 4) + 2 * e + 16 * (rr & 1));
+        }
+      };
+      double kmx;
+      quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, kqs, kzp, kmx);
+      if (valid && siq && kmx > 1.0 + 1e-9) atomicOr(a.status, 2);
     }
-    auto kexact = [&](int n) -> double {
-      const double kd = (double)kf[n] - s_mu[j][n];
-      if (!a.siq) return kd;
-      const double al = s_al[j][n];
-      return al == 0.0 ? 0.0 : fabs(kd) / al;
-    };
-    if (a.siq && valid) {
+    {
+      Raw32<DTY> vr;
+      vr.load(a.values, row);
+      float vf[32];
+      float vmin = INFINITY, vmax = -INFINITY;
 #pragma unroll
-      for (int n = 0; n < 32; ++n)
-        if (m32[n] + e32[n] > 1.0f + 1e-9f && kexact(n) > 1.0 + 1e-9) atomicOr(a.status, 2);
+      for (int n = 0; n < 32; ++n) { vf[n] = vr[n]; vmin = fminf(vmin, vf[n]); vmax = fmaxf(vmax, vf[n]); }
+      auto vemit = [&](int n, uint32_t c) {
+        vref[n / PER] |= c << (BITS * (n % PER));
+        if constexpr (BITS == 2) vp8[n & 7] |= c << (4 * (n >> 4) + 2 * ((n >> 3) & 1));
+      };
+      double vmx;
+      quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
+                          vemit, vqs, vzp, vmx);
     }
-    quant_group32(m32, e32, kexact, levels, kc, kqs, kzp, a.status, valid);
-    float z32[32];
-#pragma unroll
-    for (int n = 0; n < 32; ++n) z32[n] = 0.f;
-    quant_group32(vf, z32, [&](int n) -> double { return (double)vf[n]; }, levels, vc, vqs, vzp, a.status,
-                  valid);
+    if (valid) {
+      const bool kbad = !isfinite(__half2float(kqs)) || !isfinite(__half2float(kzp));
+      const bool vbad = !isfinite(__half2float(vqs)) || !isfinite(__half2float(vzp));
+      if (kbad || vbad) atomicOr(a.status, 1);
+    }
   }
   const int64_t tok = u * a.L + t;
   // ---------------- reference layout
   if (valid && a.codes_ref) reinterpret_cast<uint32_t*>(a.codes_ref + tok * 16)[j] = cw;
-  if (valid && a.bits > 0) {
-    // group j's payload = bytes [4 bits j, 4 bits (j + 1)) of the row; element n at
-    // bit (n * bits) of that little-endian byte string
-    auto put = [&](uint8_t* dst, const uint32_t (&cc)[32]) {
-      if (!dst) return;
-      uint32_t* r = reinterpret_cast<uint32_t*>(dst + tok * (16 * a.bits) + 4 * a.bits * j);
-      switch (a.bits) {
-        case 1: { uint32_t w = 0;
+  if (valid && BITS > 0) {
+    // group j's payload = bytes [4 BITS j, 4 BITS (j + 1)) of the row
+    if (a.kq_ref) {
+      uint32_t* r = reinterpret_cast<uint32_t*>(a.kq_ref + tok * (16 * BITS) + 4 * BITS * j);
 #pragma unroll
-                  for (int n = 0; n < 32; ++n) w |= cc[n] << n;
-                  r[0] = w; break; }
-        case 2:
+      for (int q = 0; q < BITS; ++q) r[q] = kref[q];
+    }
+    if (a.vq_ref) {
+      uint32_t* r = reinterpret_cast<uint32_t*>(a.vq_ref + tok * (16 * BITS) + 4 * BITS * j);
 #pragma unroll
-          for (int q = 0; q < 2; ++q) { uint32_t w = 0;
-#pragma unroll
-            for (int n = 0; n < 16; ++n) w |= cc[16 * q + n] << (2 * n);
-            r[q] = w; }
-          break;
-        case 4:
-#pragma unroll
-          for (int q = 0; q < 4; ++q) { uint32_t w = 0;
-#pragma unroll
-            for (int n = 0; n < 8; ++n) w |= cc[8 * q + n] << (4 * n);
-            r[q] = w; }
-          break;
-        default:
-#pragma unroll
-          for (int q = 0; q < 8; ++q) { uint32_t w = 0;
-#pragma unroll
-            for (int n = 0; n < 4; ++n) w |= cc[4 * q + n] << (8 * n);
-            r[q] = w; }
-      }
-    };
-    put(a.kq_ref, kc);
-    put(a.vq_ref, vc);
+      for (int q = 0; q < BITS; ++q) r[q] = vref[q];
+    }
     const int64_t pi = tok * 4 + j;
     if (a.ks_ref) { a.ks_ref[pi] = kqs; a.kz_ref[pi] = kzp; }
     if (a.vs_ref) { a.vs_ref[pi] = vqs; a.vz_ref[pi] = vzp; }
   }
   // ---------------- fast layout (bits = 2, sign-in-quant)
-  if (a.signs_fast) {
-    // rotated sign row: byte i of token t = reference byte (t + i) mod 16
-    const int rot = (int)(t & 15), base = lane & ~3;
-    const int wsh = rot >> 2, bsh = 8 * (rot & 3);
-    const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
-    const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
-    const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
-    // K payload: channel 32j + n -> word 2*t4(n) + (j >> 1), bit 8(j&1) + 4(n>>4) + 2e(n) + 16hi(n)
-    uint32_t kp4[4] = {0, 0, 0, 0}, vp8[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sg4[4] = {0, 0, 0, 0};
+  if constexpr (BITS == 2) {
+    if (a.signs_fast) {
+      // rotated sign row: byte i of token t = reference byte (t + i) mod 16
+      const int rot = (int)(t & 15), base = lane & ~3;
+      const int wsh = rot >> 2, bsh = 8 * (rot & 3);
+      const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
+      const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
+      const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
+      uint32_t sg4[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int n = 0; n < 32; ++n) {
-      const int r = n & 15, e = r >> 3, rr = r & 7, t4 = rr >> 1, hb = rr & 1;
-      kp4[t4] |= kc[n] << (4 * (n >> 4) + 2 * e + 16 * hb);
-      vp8[r & 7] |= vc[n] << (4 * (n >> 4) + 2 * e);
-      sg4[t4] |= ((negw >> n) & 1u) << ((((n >> 4) << 1) | e) + 16 * hb);
-    }
-    uint32_t out[8];
-    // K payload words 2*t4 + u (u = j >> 1): combine the two groups of this u (lanes j, j^1)
+      for (int n = 0; n < 32; ++n) {
+        const int r = n & 15, e = r >> 3, rr = r & 7;
+        sg4[rr >> 1] |= ((negw >> n) & 1u) << ((((n >> 4) << 1) | e) + 16 * (rr & 1));
+      }
+      // K payload words 2*t4 + u (u = j >> 1): combine the two groups of this u (lanes j, j^1)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t mine = kp4[q] << (8 * (j & 1));
-      kp4[q] = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
-    }
-    // V payload words g: byte j of every word comes from group j
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t mine = kp4[q] << (8 * (j & 1));
+        kp4[q] = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
+      }
+      // V payload words g: byte j of every word comes from group j
 #pragma unroll
-    for (int q = 0; q < 8; ++q) vp8[q] = or4(vp8[q] << (8 * j));
-    // K sign words t4: bit 8u + i + 16hi, u = j >> 1, i = (2(j&1) + (n>>4)) << 1 | e
+      for (int q = 0; q < 8; ++q) vp8[q] = or4(vp8[q] << (8 * j));
+      // K sign words t4: bit 8u + i + 16hi, u = j >> 1, i = (2(j&1) + (n>>4)) << 1 | e
 #pragma unroll
-    for (int q = 0; q < 4; ++q) sg4[q] = or4(sg4[q] << (8 * (j >> 1) + 4 * (j & 1)));
-    const uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
-    const uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
-    // record words: 0-7 K payload, 8-15 V payload, 16-19 K params, 20-23 V params, 24-27 K signs
-    // thread j writes words {2*t4 + u : t4 in {2(j&1), 2(j&1)+1}}, 8 + 2j, 9 + 2j, 16 + j, 20 + j,
-    // 24 + j, 28 + j
-    auto pick4 = [&](const uint32_t (&v)[4], int i) {
-      return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
-    };
-    auto pick8 = [&](const uint32_t (&v)[8], int i) {
-      uint32_t r = v[0];
+      for (int q = 0; q < 4; ++q) sg4[q] = or4(sg4[q] << (8 * (j >> 1) + 4 * (j & 1)));
+      const uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
+      const uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
+      // record words: 0-7 K payload, 8-15 V payload, 16-19 K params, 20-23 V params, 24-27 K signs;
+      // thread j writes K words 4(j&1) + (j>>1) and 4(j&1) + 2 + (j>>1), V words 8 + 2j, 9 + 2j,
+      // and words 16 + j, 20 + j, 24 + j, 28 + j
+      auto pick4 = [](const uint32_t (&v)[4], int i) {
+        return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
+      };
+      auto pick8 = [](const uint32_t (&v)[8], int i) {
+        uint32_t r = v[0];
 #pragma unroll
-      for (int q = 1; q < 8; ++q) r = i == q ? v[q] : r;
-      return r;
-    };
-    out[0] = pick4(kp4, 2 * (j & 1));
-    out[1] = pick4(kp4, 2 * (j & 1) + 1);
-    out[2] = pick8(vp8, 2 * j);
-    out[3] = pick8(vp8, 2 * j + 1);
-    out[4] = kpar;
-    out[5] = vpar;
-    out[6] = pick4(sg4, j);
-    out[7] = 0u;
-    if (valid) {
-      reinterpret_cast<uint32_t*>(a.signs_fast + tok * FSIGN)[j] = rw;
-      uint32_t* rec = reinterpret_cast<uint32_t*>(a.recs_fast + tok * FREC);
-      const int uu = j >> 1;
-      rec[2 * (2 * (j & 1)) + uu] = out[0];
-      rec[2 * (2 * (j & 1) + 1) + uu] = out[1];
-      rec[8 + 2 * j] = out[2];
-      rec[9 + 2 * j] = out[3];
-      rec[16 + j] = out[4];
-      rec[20 + j] = out[5];
-      rec[24 + j] = out[6];
-      rec[28 + j] = out[7];
+        for (int q = 1; q < 8; ++q) r = i == q ? v[q] : r;
+        return r;
+      };
+      if (valid) {
+        reinterpret_cast<uint32_t*>(a.signs_fast + tok * FSIGN)[j] = rw;
+        uint32_t* rec = reinterpret_cast<uint32_t*>(a.recs_fast + tok * FREC);
+        const int uu = j >> 1;
+        rec[4 * (j & 1) + uu] = pick4(kp4, 2 * (j & 1));
+        rec[4 * (j & 1) + 2 + uu] = pick4(kp4, 2 * (j & 1) + 1);
+        rec[8 + 2 * j] = pick8(vp8, 2 * j);
+        rec[9 + 2 * j] = pick8(vp8, 2 * j + 1);
+        rec[16 + j] = kpar;
+        rec[20 + j] = vpar;
+        rec[24 + j] = pick4(sg4, j);
+        rec[28 + j] = 0u;
+      }
     }
   }
 }
@@ -729,6 +761,7 @@ __global__ void __launch_bounds__(256) quant_group_kernel(PackArgs a) {
 // Codebook partial sums for one token tile: thread (sign group g, channel i) accumulates
 // K' = fl64(K - mu) into its private accumulator of the token's code, in token order.
 // Deterministic; the fixed-order tile combine happens in codebook_final_kernel.
+constexpr int CB_TILE = 1024;
 template <int DTY>
 __global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restrict__ keys, int64_t L,
                                                             const double* __restrict__ mu64, int tile,
@@ -736,7 +769,7 @@ __global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restri
                                                             int* __restrict__ cntp) {
   __shared__ double acc[16][128];
   __shared__ int cnt[16][32];
-  const int c = threadIdx.x, lane = c & 31, g = c >> 2;
+  const int c = threadIdx.x, g = c >> 2;
   const int64_t u = blockIdx.y;
   const int tl = blockIdx.x;
   for (int q = 0; q < 16; ++q) acc[q][c] = 0.0;
@@ -746,19 +779,22 @@ __global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restri
   const bool mule = mu <= (double)mu32;
   __syncthreads();
   const int64_t t0 = (int64_t)tl * tile, t1 = min(L, t0 + tile);
-  for (int64_t t = t0; t < t1; ++t) {
-    float x;
-    if (DTY == IN_BF16)
-      x = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(keys)[(u * L + t) * FD + c]);
-    else
-      x = reinterpret_cast<const float*>(keys)[(u * L + t) * FD + c];
-    const bool ge = x > mu32 || (x == mu32 && mule);
-    // the 4 channels of sign group g are lanes 4(g & 7) .. +3 of this warp
-    uint32_t bit = (ge ? 1u : 0u) << (3 - (c & 3));
-    bit |= __shfl_xor_sync(0xffffffffu, bit, 1);
-    bit |= __shfl_xor_sync(0xffffffffu, bit, 2);
-    acc[bit][c] += (double)x - mu;
-    if ((c & 3) == 0) cnt[bit][g] += 1;
+  constexpr int UN = 8;
+  for (int64_t tb = t0; tb < t1; tb += UN) {
+    float x[UN];
+#pragma unroll
+    for (int i = 0; i < UN; ++i) x[i] = tb + i < t1 ? load1<DTY>(keys, (u * L + tb + i) * FD + c) : 0.f;
+#pragma unroll
+    for (int i = 0; i < UN; ++i) {
+      if (tb + i >= t1) break;
+      const bool ge = x[i] > mu32 || (x[i] == mu32 && mule);
+      // the 4 channels of sign group g are lanes 4(g & 7) .. +3 of this warp
+      uint32_t bit = (ge ? 1u : 0u) << (3 - (c & 3));
+      bit |= __shfl_xor_sync(0xffffffffu, bit, 1);
+      bit |= __shfl_xor_sync(0xffffffffu, bit, 2);
+      acc[bit][c] += (double)x[i] - mu;
+      if ((c & 3) == 0) cnt[bit][g] += 1;
+    }
   }
   __syncthreads();
   double* outp = part + (u * ntiles + tl) * (int64_t)(32 * 64);
@@ -766,7 +802,6 @@ __global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restri
   // partial layout [g][code][i]
   for (int q = 0; q < 16; ++q) outp[(g * 16 + q) * 4 + (c & 3)] = acc[q][c];
   for (int q = c; q < 32 * 16; q += 128) outc[q] = cnt[q & 15][q >> 4];
-  (void)lane;
 }
 
 // ---------------------------------------------------------------- K3: codebook finalise
@@ -823,7 +858,11 @@ __global__ void append_kernel(const void* __restrict__ k, const void* __restrict
 // ---------------------------------------------------------------- host launchers
 int stats_nsplit(int64_t L) { int64_t n = L / 512; if (n < 1) n = 1; if (n > 64) n = 64; return (int)n; }
 constexpr int PACK_TILE = 2048;
-int pack_ntiles(int64_t L) { return (int)((L + PACK_TILE - 1) / PACK_TILE); }
+// partial-sum tiles: enough for both the generic pack tiles and the codebook tiles
+int pack_ntiles(int64_t L) {
+  const int64_t a = (L + PACK_TILE - 1) / PACK_TILE, b = (L + CB_TILE - 1) / CB_TILE;
+  return (int)(a > b ? a : b);
+}
 
 size_t encode_workspace_bytes(int64_t U, int64_t L, int D) {
   size_t a = (size_t)U * stats_nsplit(L) * D * 5 * sizeof(double);
@@ -844,7 +883,7 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
   double* spart = reinterpret_cast<double*>(w);
   size_t a = (size_t)U * nsplit * D * 5 * sizeof(double);
   w += (a + 255) & ~(size_t)255;
-  const int G = D / 4, ntiles = pack_ntiles(L);
+  const int G = D / 4, ntiles = pack_ntiles(L), ptiles = (int)((L + PACK_TILE - 1) / PACK_TILE);
   double* cbp = reinterpret_cast<double*>(w);
   size_t b = (size_t)U * ntiles * G * 64 * sizeof(double);
   w += (b + 255) & ~(size_t)255;
@@ -863,21 +902,27 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
   }
   if (!(what & 2)) return cudaGetLastError();
   PackArgs pa{keys, values, dt, L, D, bits, gs, siq, mu64, alpha64, codes_ref, kq_ref, ks, kz,
-              vq_ref, vs, vz, signs_fast, recs_fast, cbp, cbc, ntiles, PACK_TILE, status, codes_in};
+              vq_ref, vs, vz, signs_fast, recs_fast, cbp, cbc, ptiles, PACK_TILE, status, codes_in};
   size_t smem = (size_t)PACK_WARPS * G * 64 * sizeof(double) + (size_t)PACK_WARPS * G * 16 * sizeof(int);
-  if (D == FD && gs == 32 && (bits == 1 || bits == 2 || bits == 4 || bits == 8) && dt != IN_F64 && !codes_in) {
-    const int ctile = 4096, cnt_tiles = (int)((L + ctile - 1) / ctile);
-    if (cnt_tiles > ntiles) return cudaErrorInvalidValue;   // workspace sized for pack tiles
+  const bool al16 = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(values)) & 15) == 0;
+  if (D == FD && gs == 32 && (bits == 1 || bits == 2 || bits == 4 || bits == 8) && dt != IN_F64 && !codes_in &&
+      al16) {
+    const int cnt_tiles = (int)((L + CB_TILE - 1) / CB_TILE);
+    if (cnt_tiles > ntiles) return cudaErrorInvalidValue;   // workspace sized by encode_tiles()
     dim3 qg((unsigned)((L + QG_TOK - 1) / QG_TOK), (unsigned)U);
-    if (dt == IN_BF16) {
-      quant_group_kernel<IN_BF16><<<qg, 256, 0, st>>>(pa);
-      codebook_tile_kernel<IN_BF16><<<dim3(cnt_tiles, (unsigned)U), 128, 0, st>>>(keys, L, mu64, ctile, cnt_tiles,
-                                                                              cbp, cbc);
-    } else {
-      quant_group_kernel<IN_F32><<<qg, 256, 0, st>>>(pa);
-      codebook_tile_kernel<IN_F32><<<dim3(cnt_tiles, (unsigned)U), 128, 0, st>>>(keys, L, mu64, ctile, cnt_tiles,
-                                                                             cbp, cbc);
-    }
+    auto run = [&](auto dty) {
+      constexpr int DTY = decltype(dty)::value;
+      switch (bits) {
+        case 1: quant_group_kernel<DTY, 1><<<qg, 256, 0, st>>>(pa); break;
+        case 2: quant_group_kernel<DTY, 2><<<qg, 256, 0, st>>>(pa); break;
+        case 4: quant_group_kernel<DTY, 4><<<qg, 256, 0, st>>>(pa); break;
+        default: quant_group_kernel<DTY, 8><<<qg, 256, 0, st>>>(pa); break;
+      }
+      codebook_tile_kernel<DTY><<<dim3(cnt_tiles, (unsigned)U), 128, 0, st>>>(keys, L, mu64, CB_TILE, cnt_tiles,
+                                                                           cbp, cbc);
+    };
+    if (dt == IN_BF16) run(std::integral_constant<int, IN_BF16>{});
+    else run(std::integral_constant<int, IN_F32>{});
     codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, cnt_tiles, cbp, cbc, c64,
                                                                                   c32);
     return cudaGetLastError();
@@ -885,13 +930,13 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
   auto launch = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3(ntiles, (unsigned)U), PACK_WARPS * 32, smem, st>>>(pa);
+    kern<<<dim3(ptiles, (unsigned)U), PACK_WARPS * 32, smem, st>>>(pa);
     return cudaSuccess;
   };
   cudaError_t e = dt == IN_BF16 ? launch(pack_kernel<IN_BF16>) : dt == IN_F32 ? launch(pack_kernel<IN_F32>)
                                                                                : launch(pack_kernel<IN_F64>);
   if (e != cudaSuccess) return e;
-  codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, ntiles, cbp, cbc, c64, c32);
+  codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, ptiles, cbp, cbc, c64, c32);
   return cudaGetLastError();
 }
 
