@@ -124,17 +124,27 @@ __global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __r
   int low[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
   bool bad = false;
   if (active) {
-    for (int64_t t = t0 + warp; t < t1; t += 8) {
-      float x[4];
-      load4<DTY>(keys, ((int64_t)u * L + t) * D + 4 * lane, x);
+    constexpr int UN = 8;                        // rows in flight per warp
+    for (int64_t tb = t0 + warp; tb < t1; tb += 8 * UN) {
+      float x[UN][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        bad |= !isfinite(x[i]);
-        sum[i] += (double)x[i];
-        sab[i] += (double)fabsf(x[i]);
-        mn[i] = fminf(mn[i], x[i]);
-        mx[i] = fmaxf(mx[i], x[i]);
-        if (x[i] != 0.f) low[i] = min(low[i], lowbit_f32(x[i]));
+      for (int r = 0; r < UN; ++r) {
+        const int64_t t = tb + 8 * r;
+        if (t < t1) load4<DTY>(keys, ((int64_t)u * L + t) * D + 4 * lane, x[r]);
+        else x[r][0] = x[r][1] = x[r][2] = x[r][3] = 0.f;   // zeros leave every statistic unchanged
+      }
+#pragma unroll
+      for (int r = 0; r < UN; ++r) {
+        const bool in = tb + 8 * r < t1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float v = x[r][i];
+          bad |= !isfinite(v);
+          sum[i] += (double)v;
+          sab[i] += (double)fabsf(v);
+          if (in) { mn[i] = fminf(mn[i], v); mx[i] = fmaxf(mx[i], v); }
+          if (v != 0.f) low[i] = min(low[i], lowbit_f32(v));
+        }
       }
     }
 #pragma unroll
@@ -533,10 +543,11 @@ __device__ __forceinline__ float load1(const void* p, int64_t idx) {
 
 // Quantise one 32-element group (quantizer.py:119-130).  m: float32 estimates, E: group error
 // bound (0 = the estimates are exact), [mmin, mmax]: range of m, exact(n): float64 value.
-// emit(n, code) is called once per element with a compile-time n.
+// emit(n, code) ORs a code into the caller's packed words (n is always a compile-time constant);
+// fix[32] is this thread's shared-memory scratch for the exact codes.
 template <int BITS, typename Exact, typename Emit>
 __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, float mmin, float mmax, Exact&& exact,
-                                              Emit&& emit, __half& qs16, __half& zp16, double& mxo) {
+                                              Emit&& emit, uint8_t* fix, __half& qs16, __half& zp16, double& mxo) {
   constexpr int levels = (1 << BITS) - 1;
   double mn, mx;
   if (E == 0.f) {
@@ -567,30 +578,46 @@ __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, flo
   const double zpd = (double)__half2float(zp16);
   if (qs > 0.0 && qsd == 0.0) { qs16 = __float2half(5.9604644775390625e-08f); qsd = 5.9604644775390625e-08; }
   if (!(qsd > 0.0)) return;                        // all codes 0
+  // x = m * iqs + (0.5 - zp * iqs) estimates T = (exact - zp) / qs + 0.5 with
+  // |x - T| <= E iqs (1+2^-23) + |m| iqs 2^-23 + |zp iqs| 2^-22.5 + |x| 2^-24 + 2^-25 < B;
+  // codes whose x lies within B of an integer are recomputed exactly afterwards.
   const float zpf = (float)zpd, iqs = 1.0f / (float)qsd;
-  // group-wide ambiguity margin >= the per-element bound of quant4_fast
-  const float dev = fmaxf(fabsf(mmax - zpf), fabsf(zpf - mmin)) * 1.0001f;
-  const float B = (E + dev * 1.2e-7f) * iqs * 1.0001f + dev * iqs * 5.01e-7f + 1e-6f;
+  const float zq = zpf * iqs, c0 = 0.5f - zq;
+  const float mabs = fmaxf(fabsf(mmin), fabsf(mmax)) + E;
+  const float B = (E * 1.0001f + mabs * 2.5e-7f) * iqs + fabsf(zq) * 3e-7f + 2e-6f;
+  const float omB = 1.f - B;
+  constexpr float kRnd = 12582912.f;               // 1.5 * 2^23: x + kRnd (round down) = floor(x)
+  uint32_t amb = 0;
 #pragma unroll
   for (int n = 0; n < 32; ++n) {
-    const float x = (m[n] - zpf) * iqs + 0.5f;
-    const float f = floorf(x), fr = x - f;
-    uint32_t c = (uint32_t)fminf(fmaxf(f, 0.f), (float)levels);
-    if (fminf(fr, 1.f - fr) < B) {
+    const float x = fmaf(m[n], iqs, c0);
+    const float y = __fadd_rd(x, kRnd);
+    const float fr = x - (y - kRnd);
+    const bool a_n = fr < B || fr > omB;
+    int ci = (int)(__float_as_uint(y) - 0x4B400000u);
+    ci = min(max(ci, 0), levels);
+    amb |= (a_n ? 1u : 0u) << n;
+    emit(n, a_n ? 0u : (uint32_t)ci);
+  }
+  if (amb) {                                       // rare: exact float64 codes via fix[]
+    for (uint32_t r = amb; r; r &= r - 1) {
+      const int n = __ffs((int)r) - 1;
       const double ce = floor((exact(n) - zpd) / qsd + 0.5);
-      c = (uint32_t)fmin(fmax(ce, 0.0), (double)levels);
+      fix[n] = (uint8_t)fmin(fmax(ce, 0.0), (double)levels);
     }
-    emit(n, c);
+#pragma unroll
+    for (int n = 0; n < 32; ++n)
+      if ((amb >> n) & 1u) emit(n, (uint32_t)fix[n]);
   }
 }
 
 template <int DTY, int BITS>
 __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
-  __shared__ float2 s_c[4][33];                   // (mu32, 1/alpha or 1) per channel
+  __shared__ float4 s_c[4][33];                   // (sign threshold, mu32, 1/alpha or 1, -) per channel
   __shared__ float s_e0[4][33];
   __shared__ double s_mu[4][33], s_al[4][33];
-  __shared__ uint32_t s_mule[4];                  // bit n: mu <= fl32(mu) for channel 32j + n
   __shared__ float s_e0max[4];
+  __shared__ uint8_t s_fix[256][32];
   const int tid = threadIdx.x, lane = tid & 31, j = tid & 3;
   const int64_t u = blockIdx.y;
   const int64_t t = (int64_t)blockIdx.x * QG_TOK + (tid >> 2);
@@ -603,34 +630,38 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
     const float inva = siq ? (al > 0.0 ? 1.0f / (float)al : 0.f) : 1.f;
     const float dmu = (float)fabs(mu - (double)m32) * 1.0001f;
     const float e0 = (siq ? dmu * inva * 1.0001f : dmu) + 1e-37f;
-    s_c[g][n] = make_float2(m32, inva);
+    // K >= mu  <=>  K >= thr for float32 K (no float32 lies strictly between mu and mu32)
+    const float thr = mu <= (double)m32 ? m32 : __int_as_float(__float_as_int(m32) + (m32 >= 0.f ? 1 : -1));
+    s_c[g][n] = make_float4(thr, m32, inva, 0.f);
     s_e0[g][n] = e0;
     s_mu[g][n] = mu;
     s_al[g][n] = al;
-    const uint32_t mule = __ballot_sync(0xffffffffu, mu <= (double)m32);
     const uint32_t emax = __reduce_max_sync(0xffffffffu, __float_as_uint(e0));
-    if (n == 0) { s_mule[g] = mule; s_e0max[g] = __uint_as_float(emax); }
+    if (n == 0) s_e0max[g] = __uint_as_float(emax);
   }
   __syncthreads();
   const int64_t row = (u * a.L + (valid ? t : 0)) * FD + 32 * j;
-  Raw32<DTY> kr;
+  Raw32<DTY> kr, vr;
   kr.load(a.keys, row);
+  vr.load(a.values, row);
   // sign codes (K >= mu exactly, decided in float32) and key magnitudes
-  const uint32_t mule = s_mule[j], absmask = siq ? 0x7fffffffu : 0xffffffffu;
-  uint32_t cw = 0, negw = 0;                      // cw: word j of the reference code row
+  const uint32_t absmask = siq ? 0x7fffffffu : 0xffffffffu;
+  uint32_t geb = 0;                               // bit n: K >= mu for channel 32j + n
   float km[32];
   float kmin = INFINITY, kmax = -INFINITY;
 #pragma unroll
   for (int n = 0; n < 32; ++n) {
-    const float2 c = s_c[j][n];
+    const float4 c = s_c[j][n];
     const float x = kr[n];
-    const bool ge = x > c.x || (x == c.x && ((mule >> n) & 1u));
-    cw |= (ge ? 1u : 0u) << (4 * (n >> 2) + 3 - (n & 3));
-    negw |= (ge ? 0u : 1u) << n;
-    km[n] = __uint_as_float(__float_as_uint(x - c.x) & absmask) * c.y;
+    geb |= (x >= c.x ? 1u : 0u) << n;
+    km[n] = __uint_as_float(__float_as_uint(x - c.y) & absmask) * c.z;
     kmin = fminf(kmin, km[n]);
     kmax = fmaxf(kmax, km[n]);
   }
+  const uint32_t negw = ~geb;
+  // cw: word j of the reference code row, channel n at bit 4(n>>2) + 3 - (n&3)
+  uint32_t cw = __byte_perm(__brev(geb), 0, 0x0123);
+  cw = ((cw >> 4) & 0x0F0F0F0Fu) | ((cw & 0x0F0F0F0Fu) << 4);
   // packed codes: reference words (element n at bit BITS*n of the group's byte string) and,
   // for BITS == 2, this group's share of the fast record words
   constexpr int PER = BITS > 0 ? 32 / BITS : 32;
@@ -657,12 +688,10 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         }
       };
       double kmx;
-      quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, kqs, kzp, kmx);
+      quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, s_fix[tid], kqs, kzp, kmx);
       if (valid && siq && kmx > 1.0 + 1e-9) atomicOr(a.status, 2);
     }
     {
-      Raw32<DTY> vr;
-      vr.load(a.values, row);
       float vf[32];
       float vmin = INFINITY, vmax = -INFINITY;
 #pragma unroll
@@ -673,7 +702,7 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
       };
       double vmx;
       quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
-                          vemit, vqs, vzp, vmx);
+                          vemit, s_fix[tid], vqs, vzp, vmx);
     }
     if (valid) {
       const bool kbad = !isfinite(__half2float(kqs)) || !isfinite(__half2float(kzp));
@@ -776,10 +805,10 @@ __global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restri
   for (int q = c; q < 16 * 32; q += 128) cnt[q >> 5][q & 31] = 0;
   const double mu = mu64[u * FD + c];
   const float mu32 = (float)mu;
-  const bool mule = mu <= (double)mu32;
+  const float thr = mu <= (double)mu32 ? mu32 : __int_as_float(__float_as_int(mu32) + (mu32 >= 0.f ? 1 : -1));
   __syncthreads();
   const int64_t t0 = (int64_t)tl * tile, t1 = min(L, t0 + tile);
-  constexpr int UN = 8;
+  constexpr int UN = 32;
   for (int64_t tb = t0; tb < t1; tb += UN) {
     float x[UN];
 #pragma unroll
@@ -787,7 +816,7 @@ __global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restri
 #pragma unroll
     for (int i = 0; i < UN; ++i) {
       if (tb + i >= t1) break;
-      const bool ge = x[i] > mu32 || (x[i] == mu32 && mule);
+      const bool ge = x[i] >= thr;               // K >= mu
       // the 4 channels of sign group g are lanes 4(g & 7) .. +3 of this warp
       uint32_t bit = (ge ? 1u : 0u) << (3 - (c & 3));
       bit |= __shfl_xor_sync(0xffffffffu, bit, 1);

@@ -469,3 +469,26 @@ class TestFastEncoderPath:
         np.testing.assert_array_equal(N(cache.key_mag.zeros), oc.kmag.zeros)
         np.testing.assert_array_equal(N(cache.values.packed), oc.vq.packed)
         np.testing.assert_array_equal(N(cache.values.scales), oc.vq.scales)
+
+    @pytest.mark.parametrize("bits", [2, 4])
+    @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+    def test_grid_midpoints_and_ties(self, bits, dtype):
+        """Integer-valued K / V: many values sit exactly on quantisation midpoints, many keys
+        equal mu, and magnitudes tie; every such code takes the exact float64 fix-up path."""
+        rng = np.random.default_rng(11 + bits)
+        L = 1500
+        K = rng.integers(-4, 5, size=(L, 128)).astype(np.float64)
+        K[:, 7] = 2.0                                   # constant channel: K == mu, alpha = 0
+        V = rng.integers(0, 7, size=(L, 128)).astype(np.float64)
+        V[:, 0::32] = 0.0
+        V[:, 1::32] = 6.0                               # every group spans [0, 6]: qs = 2 (2-bit)
+        Kt = torch.tensor(K, dtype=dtype, device="cuda")
+        Vt = torch.tensor(V, dtype=dtype, device="cuda")
+        cache = sk.prefill(Kt, Vt, config=sk.CacheConfig(bits=bits, group_size=32, sink_count=8))
+        oc = O.prefill(K, V, bits=bits, group=32, sink_count=8)
+        np.testing.assert_array_equal(N(cache.codes.packed), oc.packed_codes)
+        for got, ref in ((cache.key_mag, oc.kmag), (cache.values, oc.vq)):
+            np.testing.assert_array_equal(N(got.packed), ref.packed)
+            np.testing.assert_array_equal(N(got.scales), ref.scales)
+            np.testing.assert_array_equal(N(got.zeros), ref.zeros)
+        np.testing.assert_array_equal(N(cache.codebook.centroids).astype(np.float32), oc.centroids.astype(np.float32))
