@@ -56,34 +56,56 @@ __global__ void stats_partial_kernel(const void* __restrict__ keys, int dt, int6
   }
 }
 
-__global__ void stats_final_kernel(const void* __restrict__ keys, int dt, int64_t L, int D, int nsplit,
-                                   const double* __restrict__ part, double* __restrict__ mu64,
-                                   double* __restrict__ alpha64, float* __restrict__ mu32,
-                                   float* __restrict__ alpha32, int* __restrict__ status) {
-  const int u = blockIdx.x;
-  for (int c = threadIdx.x; c < D; c += blockDim.x) {
-    double sum = -0.0, sab = 0.0, mn = INFINITY, mx = -INFINITY;
-    int low = 0x7fffffff;
-    for (int s = 0; s < nsplit; ++s) {
-      const double* p = part + (((int64_t)u * nsplit + s) * D + c) * 5;
-      sum += p[0]; sab += p[1]; mn = fmin(mn, p[2]); mx = fmax(mx, p[3]);
-      low = min(low, (int)__double_as_longlong(p[4]));
-    }
-    bool exact = (low == 0x7fffffff) || (low + 52 < 1023 && sab < ldexp(1.0, low + 52));
-    if (!exact) {
-      // certificate failed: replay the reference's sequential row order
-      atomicOr(status, 8);
-      const int64_t base = (int64_t)u * L * D + c;
-      sum = load_in(keys, dt, base);
-      for (int64_t t = 1; t < L; ++t) sum += load_in(keys, dt, base + t * D);
-    }
-    double mu = sum / (double)L;
-    double a = fmax(fabs(mx - mu), fabs(mn - mu));
-    mu64[(int64_t)u * D + c] = mu;
-    alpha64[(int64_t)u * D + c] = a;
-    if (mu32) mu32[(int64_t)u * D + c] = (float)mu;
-    if (alpha32) alpha32[(int64_t)u * D + c] = (float)a;
+// One warp per (unit, channel): lanes combine the split partials (exact under the
+// certificate, so the combine order is free), lane 0 finalises.
+__global__ void __launch_bounds__(256) stats_final_kernel(const void* __restrict__ keys, int dt, int64_t L, int D,
+                                                          int nsplit, const double* __restrict__ part,
+                                                          double* __restrict__ mu64, double* __restrict__ alpha64,
+                                                          float* __restrict__ mu32, float* __restrict__ alpha32,
+                                                          int* __restrict__ status) {
+  const int u = blockIdx.x, lane = threadIdx.x & 31;
+  const int c = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (c >= D) return;
+  double sum = -0.0, sab = 0.0, mn = INFINITY, mx = -INFINITY;
+  int low = 0x7fffffff;
+  for (int s = lane; s < nsplit; s += 32) {
+    const double* p = part + (((int64_t)u * nsplit + s) * D + c) * 5;
+    sum += p[0]; sab += p[1]; mn = fmin(mn, p[2]); mx = fmax(mx, p[3]);
+    low = min(low, (int)__double_as_longlong(p[4]));
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    sab += __shfl_xor_sync(0xffffffffu, sab, o);
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    low = min(low, __shfl_xor_sync(0xffffffffu, low, o));
+  }
+  if (lane) return;
+  sab *= 1.0 + 0x1p-40;                          // covers the rounding of the combine
+  const bool exact = (low == 0x7fffffff) || (low + 52 < 1023 && sab < ldexp(1.0, low + 52));
+  if (!exact) {
+    // certificate failed: replay the reference's sequential row order (loads batched ahead)
+    atomicOr(status, 8);
+    const int64_t base = (int64_t)u * L * D + c;
+    sum = load_in(keys, dt, base);
+    int64_t t = 1;
+    constexpr int RU = 16;
+    for (; t + RU <= L; t += RU) {
+      double v[RU];
+#pragma unroll
+      for (int k = 0; k < RU; ++k) v[k] = load_in(keys, dt, base + (t + k) * D);
+#pragma unroll
+      for (int k = 0; k < RU; ++k) sum += v[k];
+    }
+    for (; t < L; ++t) sum += load_in(keys, dt, base + t * D);
+  }
+  const double mu = sum / (double)L;
+  const double a = fmax(fabs(mx - mu), fabs(mn - mu));
+  mu64[(int64_t)u * D + c] = mu;
+  alpha64[(int64_t)u * D + c] = a;
+  if (mu32) mu32[(int64_t)u * D + c] = (float)mu;
+  if (alpha32) alpha32[(int64_t)u * D + c] = (float)a;
 }
 
 
@@ -119,10 +141,13 @@ __global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __r
   const int64_t per = (L + nsplit - 1) / nsplit;
   const int64_t t0 = s * per, t1 = min(L, t0 + per);
   const bool active = 4 * lane < D;
-  double sum[4] = {-0.0, -0.0, -0.0, -0.0}, sab[4] = {0.0, 0.0, 0.0, 0.0};
+  // sum: exact float64 (certificate in stats_final); sab: float32 rounded up, an upper bound
+  // on sum|x|; low: lowest set-bit exponent (bf16: a lower bound from the exponent field)
+  double sum[4] = {-0.0, -0.0, -0.0, -0.0};
+  float sab[4] = {0.f, 0.f, 0.f, 0.f};
   float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   int low[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-  bool bad = false;
+  uint32_t emin[4] = {0x7F800000u, 0x7F800000u, 0x7F800000u, 0x7F800000u};
   if (active) {
     constexpr int UN = 8;                        // rows in flight per warp
     for (int64_t tb = t0 + warp; tb < t1; tb += 8 * UN) {
@@ -131,7 +156,7 @@ __global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __r
       for (int r = 0; r < UN; ++r) {
         const int64_t t = tb + 8 * r;
         if (t < t1) load4<DTY>(keys, ((int64_t)u * L + t) * D + 4 * lane, x[r]);
-        else x[r][0] = x[r][1] = x[r][2] = x[r][3] = 0.f;   // zeros leave every statistic unchanged
+        else x[r][0] = x[r][1] = x[r][2] = x[r][3] = -0.f;  // -0 leaves sum / sab / low unchanged
       }
 #pragma unroll
       for (int r = 0; r < UN; ++r) {
@@ -139,21 +164,29 @@ __global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __r
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float v = x[r][i];
-          bad |= !isfinite(v);
           sum[i] += (double)v;
-          sab[i] += (double)fabsf(v);
+          sab[i] = __fadd_ru(sab[i], fabsf(v));
           if (in) { mn[i] = fminf(mn[i], v); mx[i] = fmaxf(mx[i], v); }
-          if (v != 0.f) low[i] = min(low[i], lowbit_f32(v));
+          if (DTY == IN_BF16) {
+            const uint32_t eb = __float_as_uint(v) & 0x7F800000u;
+            emin[i] = min(emin[i], v != 0.f ? eb : 0x7F800000u);
+          } else if (v != 0.f) {
+            low[i] = min(low[i], lowbit_f32(v));
+          }
         }
       }
     }
+    bool bad = false;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
+      bad |= !isfinite(sum[i]) || mx[i] == INFINITY || mn[i] == -INFINITY;
+      // bf16 values are multiples of 2^(e - 134) (normal, biased exponent e) or 2^-133
+      if (DTY == IN_BF16 && emin[i] != 0x7F800000u) low[i] = emin[i] ? (int)(emin[i] >> 23) - 134 : -133;
       double* r = red[warp][4 * lane + i];
-      r[0] = sum[i]; r[1] = sab[i]; r[2] = mn[i]; r[3] = mx[i]; r[4] = __longlong_as_double((long long)low[i]);
+      r[0] = sum[i]; r[1] = (double)sab[i]; r[2] = mn[i]; r[3] = mx[i]; r[4] = __longlong_as_double((long long)low[i]);
     }
+    if (bad) atomicOr(status, 4);
   }
-  if (bad) atomicOr(status, 4);
   __syncthreads();
   for (int c = threadIdx.x; c < D; c += 256) {
     double a0 = -0.0, a1 = 0.0, a2 = INFINITY, a3 = -INFINITY;
@@ -163,7 +196,7 @@ __global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __r
       lo = min(lo, (int)__double_as_longlong(red[w][c][4]));
     }
     double* p = part + (((int64_t)u * nsplit + s) * D + c) * 5;
-    p[0] = a0; p[1] = a1; p[2] = a2; p[3] = a3; p[4] = __longlong_as_double((long long)lo);
+    p[0] = a0; p[1] = a1 * (1.0 + 0x1p-40); p[2] = a2; p[3] = a3; p[4] = __longlong_as_double((long long)lo);
   }
 }
 
@@ -500,13 +533,15 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
 // threads of a token are adjacent lanes.  Same arithmetic contract as pack_kernel (float32
 // estimates with rigorous error bounds, exact float64 where an estimate is ambiguous), but
 // each thread owns a whole quantisation group and builds its share of the fast record in
-// registers; the codebook is accumulated by codebook_tile_kernel.
+// registers.  Each CTA loops over a tile of CB_TILE tokens in 64-token blocks and also
+// accumulates the tile's codebook partial sums (deterministic order, see the walk below).
 //
 // Error model (see quant4_fast): every float32 magnitude estimate m_n of channel n satisfies
 // |m_n - exact_n| <= e0[n] + |m_n| * 7.5e-7, so the group-wide E = max e0 + max|m| * 7.5e-7
 // bounds all of them.  The exact group min (max) can only be attained by channels with
 // m_n <= min m + 2E (m_n >= max m - 2E); those few are evaluated in float64.
-constexpr int QG_TOK = 64;                 // tokens per 256-thread CTA
+constexpr int QG_TOK = 64;                 // tokens per 256-thread CTA block
+constexpr int CB_TILE = 512;               // tokens per quant_group CTA (one codebook partial each)
 
 __device__ __forceinline__ uint32_t or4(uint32_t v) {   // OR over the 4 lanes of a token
   v |= __shfl_xor_sync(0xffffffffu, v, 1);
@@ -611,17 +646,26 @@ __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, flo
   }
 }
 
+struct QgSmem {
+  float x[QG_TOK][130];                           // staged K of one 64-token block (skewed columns)
+  uint32_t cw[QG_TOK][4];                         // reference code words of the block
+  double acc[4][16][FD];                          // codebook sums per token quarter
+  int cnt[16][32];
+};
+
 template <int DTY, int BITS>
 __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
+  extern __shared__ __align__(16) unsigned char qg_smem[];
+  QgSmem& S = *reinterpret_cast<QgSmem*>(qg_smem);
+  auto& s_x = S.x;
+  auto& s_cw = S.cw;
   __shared__ float4 s_c[4][33];                   // (sign threshold, mu32, 1/alpha or 1, -) per channel
-  __shared__ float s_e0[4][33];
   __shared__ double s_mu[4][33], s_al[4][33];
   __shared__ float s_e0max[4];
   __shared__ uint8_t s_fix[256][32];
   const int tid = threadIdx.x, lane = tid & 31, j = tid & 3;
   const int64_t u = blockIdx.y;
-  const int64_t t = (int64_t)blockIdx.x * QG_TOK + (tid >> 2);
-  const bool valid = t < a.L;
+  const int tl = tid >> 2;                        // token slot within a 64-token block
   const bool siq = a.siq != 0;
   if (tid < FD) {
     const int c = tid, g = c >> 5, n = c & 31;   // warp g holds group g
@@ -633,219 +677,247 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
     // K >= mu  <=>  K >= thr for float32 K (no float32 lies strictly between mu and mu32)
     const float thr = mu <= (double)m32 ? m32 : __int_as_float(__float_as_int(m32) + (m32 >= 0.f ? 1 : -1));
     s_c[g][n] = make_float4(thr, m32, inva, 0.f);
-    s_e0[g][n] = e0;
     s_mu[g][n] = mu;
     s_al[g][n] = al;
     const uint32_t emax = __reduce_max_sync(0xffffffffu, __float_as_uint(e0));
     if (n == 0) s_e0max[g] = __uint_as_float(emax);
   }
+  for (int q = tid; q < 4 * 16 * FD; q += 256) (&S.acc[0][0][0])[q] = 0.0;
+  for (int q = tid; q < 16 * 32; q += 256) (&S.cnt[0][0])[q] = 0;
+  // codebook walk: thread (channel pair wp, token quarter wq)
+  const int wp = tid & 63, wq = tid >> 6;
+  const double wmu0 = a.mu64[u * FD + 2 * wp], wmu1 = a.mu64[u * FD + 2 * wp + 1];
+  const int64_t tile0 = (int64_t)blockIdx.x * a.tile, tile1 = min(a.L, tile0 + a.tile);
   __syncthreads();
-  const int64_t row = (u * a.L + (valid ? t : 0)) * FD + 32 * j;
-  Raw32<DTY> kr, vr;
-  kr.load(a.keys, row);
-  vr.load(a.values, row);
-  // sign codes (K >= mu exactly, decided in float32) and key magnitudes
-  const uint32_t absmask = siq ? 0x7fffffffu : 0xffffffffu;
-  uint32_t geb = 0;                               // bit n: K >= mu for channel 32j + n
-  float km[32];
-  float kmin = INFINITY, kmax = -INFINITY;
-#pragma unroll
-  for (int n = 0; n < 32; ++n) {
-    const float4 c = s_c[j][n];
-    const float x = kr[n];
-    geb |= (x >= c.x ? 1u : 0u) << n;
-    km[n] = __uint_as_float(__float_as_uint(x - c.y) & absmask) * c.z;
-    kmin = fminf(kmin, km[n]);
-    kmax = fmaxf(kmax, km[n]);
-  }
-  const uint32_t negw = ~geb;
-  // cw: word j of the reference code row, channel n at bit 4(n>>2) + 3 - (n&3)
-  uint32_t cw = __byte_perm(__brev(geb), 0, 0x0123);
-  cw = ((cw >> 4) & 0x0F0F0F0Fu) | ((cw & 0x0F0F0F0Fu) << 4);
-  // packed codes: reference words (element n at bit BITS*n of the group's byte string) and,
-  // for BITS == 2, this group's share of the fast record words
-  constexpr int PER = BITS > 0 ? 32 / BITS : 32;
-  uint32_t kref[BITS > 0 ? BITS : 1], vref[BITS > 0 ? BITS : 1];
-  uint32_t kp4[4] = {0, 0, 0, 0}, vp8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  __half kqs = __float2half(0.f), kzp = kqs, vqs = kqs, vzp = kqs;
-  if (BITS > 0) {
-#pragma unroll
-    for (int q = 0; q < (BITS > 0 ? BITS : 1); ++q) { kref[q] = 0; vref[q] = 0; }
-    {
-      const float E = __fmaf_ru(fmaxf(fabsf(kmin), fabsf(kmax)), 7.5e-7f, s_e0max[j]);
-      auto kexact = [&](int n) -> double {
-        const double kd = (double)load1<DTY>(a.keys, row + n) - s_mu[j][n];
-        if (!siq) return kd;
-        const double al = s_al[j][n];
-        return al == 0.0 ? 0.0 : fabs(kd) / al;
-      };
-      auto kemit = [&](int n, uint32_t c) {
-        kref[n / PER] |= c << (BITS * (n % PER));
-        if constexpr (BITS == 2) {
-          // channel 32j + n -> word 2*t4(n) + (j >> 1), bit 8(j&1) + 4(n>>4) + 2e(n) + 16hi(n)
-          const int r = n & 15, e = r >> 3, rr = r & 7;
-          kp4[rr >> 1] |= c << (4 * (n >> 4) + 2 * e + 16 * (rr & 1));
-        }
-      };
-      double kmx;
-      quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, s_fix[tid], kqs, kzp, kmx);
-      if (valid && siq && kmx > 1.0 + 1e-9) atomicOr(a.status, 2);
+  for (int64_t b0 = tile0; b0 < tile1; b0 += QG_TOK) {
+    const int64_t t = b0 + tl;
+    const bool valid = t < tile1;
+    const int64_t row = (u * a.L + (valid ? t : 0)) * FD + 32 * j;
+    Raw32<DTY> kr, vr;
+    kr.load(a.keys, row);
+    vr.load(a.values, row);
+    // sign codes (K >= mu exactly, decided in float32) and key magnitudes
+    const uint32_t absmask = siq ? 0x7fffffffu : 0xffffffffu;
+    uint32_t geb = 0;                               // bit n: K >= mu for channel 32j + n
+    float km[32];
+    float kmin = INFINITY, kmax = -INFINITY;
+  #pragma unroll
+    for (int n = 0; n < 32; ++n) {
+      const float4 c = s_c[j][n];
+      const float x = kr[n];
+      geb |= (x >= c.x ? 1u : 0u) << n;
+      km[n] = __uint_as_float(__float_as_uint(x - c.y) & absmask) * c.z;
+      kmin = fminf(kmin, km[n]);
+      kmax = fmaxf(kmax, km[n]);
     }
-    {
-      float vf[32];
-      float vmin = INFINITY, vmax = -INFINITY;
+    const uint32_t negw = ~geb;
+    // cw: word j of the reference code row, channel n at bit 4(n>>2) + 3 - (n&3)
+    uint32_t cw = __byte_perm(__brev(geb), 0, 0x0123);
+    cw = ((cw >> 4) & 0x0F0F0F0Fu) | ((cw & 0x0F0F0F0Fu) << 4);
+    // stage K and the codes for the codebook walk (channel 32j + n at 32j + ((n + 8j) & 31))
+    s_cw[tl][j] = cw;
 #pragma unroll
-      for (int n = 0; n < 32; ++n) { vf[n] = vr[n]; vmin = fminf(vmin, vf[n]); vmax = fmaxf(vmax, vf[n]); }
-      auto vemit = [&](int n, uint32_t c) {
-        vref[n / PER] |= c << (BITS * (n % PER));
-        if constexpr (BITS == 2) vp8[n & 7] |= c << (4 * (n >> 4) + 2 * ((n >> 3) & 1));
-      };
-      double vmx;
-      quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
-                          vemit, s_fix[tid], vqs, vzp, vmx);
-    }
-    if (valid) {
-      const bool kbad = !isfinite(__half2float(kqs)) || !isfinite(__half2float(kzp));
-      const bool vbad = !isfinite(__half2float(vqs)) || !isfinite(__half2float(vzp));
-      if (kbad || vbad) atomicOr(a.status, 1);
-    }
-  }
-  const int64_t tok = u * a.L + t;
-  // ---------------- reference layout
-  if (valid && a.codes_ref) reinterpret_cast<uint32_t*>(a.codes_ref + tok * 16)[j] = cw;
-  if (valid && BITS > 0) {
-    // group j's payload = bytes [4 BITS j, 4 BITS (j + 1)) of the row
-    if (a.kq_ref) {
-      uint32_t* r = reinterpret_cast<uint32_t*>(a.kq_ref + tok * (16 * BITS) + 4 * BITS * j);
-#pragma unroll
-      for (int q = 0; q < BITS; ++q) r[q] = kref[q];
-    }
-    if (a.vq_ref) {
-      uint32_t* r = reinterpret_cast<uint32_t*>(a.vq_ref + tok * (16 * BITS) + 4 * BITS * j);
-#pragma unroll
-      for (int q = 0; q < BITS; ++q) r[q] = vref[q];
-    }
-    const int64_t pi = tok * 4 + j;
-    if (a.ks_ref) { a.ks_ref[pi] = kqs; a.kz_ref[pi] = kzp; }
-    if (a.vs_ref) { a.vs_ref[pi] = vqs; a.vz_ref[pi] = vzp; }
-  }
-  // ---------------- fast layout (bits = 2, sign-in-quant)
-  if constexpr (BITS == 2) {
-    if (a.signs_fast) {
-      // rotated sign row: byte i of token t = reference byte (t + i) mod 16
-      const int rot = (int)(t & 15), base = lane & ~3;
-      const int wsh = rot >> 2, bsh = 8 * (rot & 3);
-      const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
-      const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
-      const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
-      uint32_t sg4[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int n = 0; n < 32; ++n) {
-        const int r = n & 15, e = r >> 3, rr = r & 7;
-        sg4[rr >> 1] |= ((negw >> n) & 1u) << ((((n >> 4) << 1) | e) + 16 * (rr & 1));
+    for (int n = 0; n < 32; ++n) s_x[tl][32 * j + ((n + 8 * j) & 31)] = kr[n];   // 2-way bank conflict at most
+    // packed codes: reference words (element n at bit BITS*n of the group's byte string) and,
+    // for BITS == 2, this group's share of the fast record words
+    constexpr int PER = BITS > 0 ? 32 / BITS : 32;
+    uint32_t kref[BITS > 0 ? BITS : 1], vref[BITS > 0 ? BITS : 1];
+    uint32_t kp4[4] = {0, 0, 0, 0}, vp8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    __half kqs = __float2half(0.f), kzp = kqs, vqs = kqs, vzp = kqs;
+    if (BITS > 0) {
+  #pragma unroll
+      for (int q = 0; q < (BITS > 0 ? BITS : 1); ++q) { kref[q] = 0; vref[q] = 0; }
+      {
+        const float E = __fmaf_ru(fmaxf(fabsf(kmin), fabsf(kmax)), 7.5e-7f, s_e0max[j]);
+        auto kexact = [&](int n) -> double {
+          const double kd = (double)load1<DTY>(a.keys, row + n) - s_mu[j][n];
+          if (!siq) return kd;
+          const double al = s_al[j][n];
+          return al == 0.0 ? 0.0 : fabs(kd) / al;
+        };
+        auto kemit = [&](int n, uint32_t c) {
+          kref[n / PER] |= c << (BITS * (n % PER));
+          if constexpr (BITS == 2) {
+            // channel 32j + n -> word 2*t4(n) + (j >> 1), bit 8(j&1) + 4(n>>4) + 2e(n) + 16hi(n)
+            const int r = n & 15, e = r >> 3, rr = r & 7;
+            kp4[rr >> 1] |= c << (4 * (n >> 4) + 2 * e + 16 * (rr & 1));
+          }
+        };
+        double kmx;
+        quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, s_fix[tid], kqs, kzp, kmx);
+        if (valid && siq && kmx > 1.0 + 1e-9) atomicOr(a.status, 2);
       }
-      // K payload words 2*t4 + u (u = j >> 1): combine the two groups of this u (lanes j, j^1)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t mine = kp4[q] << (8 * (j & 1));
-        kp4[q] = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
+      {
+        float vf[32];
+        float vmin = INFINITY, vmax = -INFINITY;
+  #pragma unroll
+        for (int n = 0; n < 32; ++n) { vf[n] = vr[n]; vmin = fminf(vmin, vf[n]); vmax = fmaxf(vmax, vf[n]); }
+        auto vemit = [&](int n, uint32_t c) {
+          vref[n / PER] |= c << (BITS * (n % PER));
+          if constexpr (BITS == 2) vp8[n & 7] |= c << (4 * (n >> 4) + 2 * ((n >> 3) & 1));
+        };
+        double vmx;
+        quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
+                            vemit, s_fix[tid], vqs, vzp, vmx);
       }
-      // V payload words g: byte j of every word comes from group j
-#pragma unroll
-      for (int q = 0; q < 8; ++q) vp8[q] = or4(vp8[q] << (8 * j));
-      // K sign words t4: bit 8u + i + 16hi, u = j >> 1, i = (2(j&1) + (n>>4)) << 1 | e
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sg4[q] = or4(sg4[q] << (8 * (j >> 1) + 4 * (j & 1)));
-      const uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
-      const uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
-      // record words: 0-7 K payload, 8-15 V payload, 16-19 K params, 20-23 V params, 24-27 K signs;
-      // thread j writes K words 4(j&1) + (j>>1) and 4(j&1) + 2 + (j>>1), V words 8 + 2j, 9 + 2j,
-      // and words 16 + j, 20 + j, 24 + j, 28 + j
-      auto pick4 = [](const uint32_t (&v)[4], int i) {
-        return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
-      };
-      auto pick8 = [](const uint32_t (&v)[8], int i) {
-        uint32_t r = v[0];
-#pragma unroll
-        for (int q = 1; q < 8; ++q) r = i == q ? v[q] : r;
-        return r;
-      };
       if (valid) {
-        reinterpret_cast<uint32_t*>(a.signs_fast + tok * FSIGN)[j] = rw;
-        uint32_t* rec = reinterpret_cast<uint32_t*>(a.recs_fast + tok * FREC);
-        const int uu = j >> 1;
-        rec[4 * (j & 1) + uu] = pick4(kp4, 2 * (j & 1));
-        rec[4 * (j & 1) + 2 + uu] = pick4(kp4, 2 * (j & 1) + 1);
-        rec[8 + 2 * j] = pick8(vp8, 2 * j);
-        rec[9 + 2 * j] = pick8(vp8, 2 * j + 1);
-        rec[16 + j] = kpar;
-        rec[20 + j] = vpar;
-        rec[24 + j] = pick4(sg4, j);
-        rec[28 + j] = 0u;
+        const bool kbad = !isfinite(__half2float(kqs)) || !isfinite(__half2float(kzp));
+        const bool vbad = !isfinite(__half2float(vqs)) || !isfinite(__half2float(vzp));
+        if (kbad || vbad) atomicOr(a.status, 1);
       }
     }
-  }
-}
-
-// Codebook partial sums for one token tile: thread (sign group g, channel i) accumulates
-// K' = fl64(K - mu) into its private accumulator of the token's code, in token order.
-// Deterministic; the fixed-order tile combine happens in codebook_final_kernel.
-constexpr int CB_TILE = 1024;
-template <int DTY>
-__global__ void __launch_bounds__(128) codebook_tile_kernel(const void* __restrict__ keys, int64_t L,
-                                                            const double* __restrict__ mu64, int tile,
-                                                            int ntiles, double* __restrict__ part,
-                                                            int* __restrict__ cntp) {
-  __shared__ double acc[16][128];
-  __shared__ int cnt[16][32];
-  const int c = threadIdx.x, g = c >> 2;
-  const int64_t u = blockIdx.y;
-  const int tl = blockIdx.x;
-  for (int q = 0; q < 16; ++q) acc[q][c] = 0.0;
-  for (int q = c; q < 16 * 32; q += 128) cnt[q >> 5][q & 31] = 0;
-  const double mu = mu64[u * FD + c];
-  const float mu32 = (float)mu;
-  const float thr = mu <= (double)mu32 ? mu32 : __int_as_float(__float_as_int(mu32) + (mu32 >= 0.f ? 1 : -1));
-  __syncthreads();
-  const int64_t t0 = (int64_t)tl * tile, t1 = min(L, t0 + tile);
-  constexpr int UN = 32;
-  for (int64_t tb = t0; tb < t1; tb += UN) {
-    float x[UN];
-#pragma unroll
-    for (int i = 0; i < UN; ++i) x[i] = tb + i < t1 ? load1<DTY>(keys, (u * L + tb + i) * FD + c) : 0.f;
-#pragma unroll
-    for (int i = 0; i < UN; ++i) {
-      if (tb + i >= t1) break;
-      const bool ge = x[i] >= thr;               // K >= mu
-      // the 4 channels of sign group g are lanes 4(g & 7) .. +3 of this warp
-      uint32_t bit = (ge ? 1u : 0u) << (3 - (c & 3));
-      bit |= __shfl_xor_sync(0xffffffffu, bit, 1);
-      bit |= __shfl_xor_sync(0xffffffffu, bit, 2);
-      acc[bit][c] += (double)x[i] - mu;
-      if ((c & 3) == 0) cnt[bit][g] += 1;
+    const int64_t tok = u * a.L + t;
+    // ---------------- reference layout
+    if (valid && a.codes_ref) reinterpret_cast<uint32_t*>(a.codes_ref + tok * 16)[j] = cw;
+    if (valid && BITS > 0) {
+      // group j's payload = bytes [4 BITS j, 4 BITS (j + 1)) of the row
+      if (a.kq_ref) {
+        uint32_t* r = reinterpret_cast<uint32_t*>(a.kq_ref + tok * (16 * BITS) + 4 * BITS * j);
+  #pragma unroll
+        for (int q = 0; q < BITS; ++q) r[q] = kref[q];
+      }
+      if (a.vq_ref) {
+        uint32_t* r = reinterpret_cast<uint32_t*>(a.vq_ref + tok * (16 * BITS) + 4 * BITS * j);
+  #pragma unroll
+        for (int q = 0; q < BITS; ++q) r[q] = vref[q];
+      }
+      const int64_t pi = tok * 4 + j;
+      if (a.ks_ref) { a.ks_ref[pi] = kqs; a.kz_ref[pi] = kzp; }
+      if (a.vs_ref) { a.vs_ref[pi] = vqs; a.vz_ref[pi] = vzp; }
     }
+    // ---------------- fast layout (bits = 2, sign-in-quant)
+    if constexpr (BITS == 2) {
+      if (a.signs_fast) {
+        // rotated sign row: byte i of token t = reference byte (t + i) mod 16
+        const int rot = (int)(t & 15), base = lane & ~3;
+        const int wsh = rot >> 2, bsh = 8 * (rot & 3);
+        const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
+        const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
+        const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
+        uint32_t sg4[4] = {0, 0, 0, 0};
+  #pragma unroll
+        for (int n = 0; n < 32; ++n) {
+          const int r = n & 15, e = r >> 3, rr = r & 7;
+          sg4[rr >> 1] |= ((negw >> n) & 1u) << ((((n >> 4) << 1) | e) + 16 * (rr & 1));
+        }
+        // K payload words 2*t4 + u (u = j >> 1): combine the two groups of this u (lanes j, j^1)
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t mine = kp4[q] << (8 * (j & 1));
+          kp4[q] = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
+        }
+        // V payload words g: byte j of every word comes from group j
+  #pragma unroll
+        for (int q = 0; q < 8; ++q) vp8[q] = or4(vp8[q] << (8 * j));
+        // K sign words t4: bit 8u + i + 16hi, u = j >> 1, i = (2(j&1) + (n>>4)) << 1 | e
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) sg4[q] = or4(sg4[q] << (8 * (j >> 1) + 4 * (j & 1)));
+        const uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
+        const uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
+        // record words: 0-7 K payload, 8-15 V payload, 16-19 K params, 20-23 V params, 24-27 K signs;
+        // thread j writes K words 4(j&1) + (j>>1) and 4(j&1) + 2 + (j>>1), V words 8 + 2j, 9 + 2j,
+        // and words 16 + j, 20 + j, 24 + j, 28 + j
+        auto pick4 = [](const uint32_t (&v)[4], int i) {
+          return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
+        };
+        auto pick8 = [](const uint32_t (&v)[8], int i) {
+          uint32_t r = v[0];
+  #pragma unroll
+          for (int q = 1; q < 8; ++q) r = i == q ? v[q] : r;
+          return r;
+        };
+        if (valid) {
+          reinterpret_cast<uint32_t*>(a.signs_fast + tok * FSIGN)[j] = rw;
+          uint32_t* rec = reinterpret_cast<uint32_t*>(a.recs_fast + tok * FREC);
+          const int uu = j >> 1;
+          rec[4 * (j & 1) + uu] = pick4(kp4, 2 * (j & 1));
+          rec[4 * (j & 1) + 2 + uu] = pick4(kp4, 2 * (j & 1) + 1);
+          rec[8 + 2 * j] = pick8(vp8, 2 * j);
+          rec[9 + 2 * j] = pick8(vp8, 2 * j + 1);
+          rec[16 + j] = kpar;
+          rec[20 + j] = vpar;
+          rec[24 + j] = pick4(sg4, j);
+          rec[28 + j] = 0u;
+        }
+      }
+    }
+    // codebook walk: thread (channel pair wp, quarter wq) adds K' = fl64(K - mu) of its 16
+    // tokens, in token order, to the accumulators of each token's code (codebook.py:128-160)
+    __syncthreads();
+    {
+      const int nt = (int)min((int64_t)QG_TOK, tile1 - b0);
+      const int jw = wp >> 4, nw = 2 * (wp & 15);
+      const int pos = 32 * jw + ((nw + 8 * jw) & 31), sh = 4 * (nw >> 2);
+      double2* accw = reinterpret_cast<double2*>(&S.acc[wq][0][2 * wp]);
+      int* cntw = &S.cnt[0][wp >> 1];
+      const bool counter = (wp & 1) == 0;
+      auto step = [&](int i) {
+        const uint32_t code = (s_cw[i][jw] >> sh) & 15u;
+        const float2 x = *reinterpret_cast<const float2*>(&s_x[i][pos]);
+        double2 v = accw[code * (FD / 2)];
+        v.x += (double)x.x - wmu0;
+        v.y += (double)x.y - wmu1;
+        accw[code * (FD / 2)] = v;
+        if (counter) atomicAdd(&cntw[code * 32], 1);
+      };
+      if (nt == QG_TOK) {
+#pragma unroll 8
+        for (int i = 16 * wq; i < 16 * wq + 16; ++i) step(i);
+      } else {
+        for (int i = 16 * wq; i < 16 * wq + 16 && i < nt; ++i) step(i);
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  double* outp = part + (u * ntiles + tl) * (int64_t)(32 * 64);
-  int* outc = cntp + (u * ntiles + tl) * (int64_t)(32 * 16);
-  // partial layout [g][code][i]
-  for (int q = 0; q < 16; ++q) outp[(g * 16 + q) * 4 + (c & 3)] = acc[q][c];
-  for (int q = c; q < 32 * 16; q += 128) outc[q] = cnt[q & 15][q >> 4];
+  // this tile's partial sums, layout [g][code][i], quarters combined in fixed order
+  double* outp = a.cb_part + (u * a.ntiles + blockIdx.x) * (int64_t)(32 * 64);
+  int* outc = a.cb_cnt + (u * a.ntiles + blockIdx.x) * (int64_t)(32 * 16);
+  for (int q = 0; q < 16; ++q) {
+    const int c = tid & (FD - 1);
+    if (tid < FD) outp[((c >> 2) * 16 + q) * 4 + (c & 3)] = ((S.acc[0][q][c] + S.acc[1][q][c]) + S.acc[2][q][c]) + S.acc[3][q][c];
+  }
+  for (int q = tid; q < 32 * 16; q += 256) outc[q] = S.cnt[q & 15][q >> 4];
 }
 
 // ---------------------------------------------------------------- K3: codebook finalise
-__global__ void codebook_final_kernel(int G, int ntiles, const double* __restrict__ part,
-                                      const int* __restrict__ cnt, double* __restrict__ c64,
-                                      float* __restrict__ c32) {
-  const int u = blockIdx.x;
-  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < G * 64; i += blockDim.x * gridDim.y) {
-    double s = 0.0;
-    int n = 0;
-    for (int t = 0; t < ntiles; ++t) {
-      s += part[((int64_t)u * ntiles + t) * G * 64 + i];
-      n += cnt[((int64_t)u * ntiles + t) * G * 16 + i / 4];
+// 256 threads per (unit, 32 consecutive entries): warp w sums tiles w, w + 8, ... in order,
+// then the 8 warp sums are combined in warp order (deterministic).
+__global__ void __launch_bounds__(256) codebook_final_kernel(int G, int ntiles, const double* __restrict__ part,
+                                                             const int* __restrict__ cnt, double* __restrict__ c64,
+                                                             float* __restrict__ c32) {
+  __shared__ double ws[8][32];
+  __shared__ int wn[8][32];
+  const int u = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.y * 32 + lane;
+  const bool act = i < G * 64;
+  double s = 0.0;
+  int n = 0;
+  if (act) {
+    const double* pp = part + (int64_t)u * ntiles * G * 64 + i;
+    const int* cp = cnt + (int64_t)u * ntiles * G * 16 + i / 4;
+    int t = warp;
+    constexpr int UN = 4;
+    for (; t + 8 * (UN - 1) < ntiles; t += 8 * UN) {
+      double v[UN];
+      int c[UN];
+#pragma unroll
+      for (int k = 0; k < UN; ++k) {
+        v[k] = pp[(int64_t)(t + 8 * k) * G * 64];
+        c[k] = cp[(int64_t)(t + 8 * k) * G * 16];
+      }
+#pragma unroll
+      for (int k = 0; k < UN; ++k) { s += v[k]; n += c[k]; }
     }
-    double c = n > 0 ? s / (double)n : 0.0;
+    for (; t < ntiles; t += 8) { s += pp[(int64_t)t * G * 64]; n += cp[(int64_t)t * G * 16]; }
+  }
+  ws[warp][lane] = s;
+  wn[warp][lane] = n;
+  __syncthreads();
+  if (warp == 0 && act) {
+    s = 0.0;
+    n = 0;
+    for (int w = 0; w < 8; ++w) { s += ws[w][lane]; n += wn[w][lane]; }
+    const double c = n > 0 ? s / (double)n : 0.0;
     if (c64) c64[(int64_t)u * G * 64 + i] = c;
     if (c32) c32[(int64_t)u * G * 64 + i] = (float)c;
   }
@@ -926,8 +998,8 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
       stats_partial_fast_kernel<IN_F32><<<dim3((unsigned)U, nsplit), 256, 0, st>>>(keys, L, D, nsplit, spart, status);
     else
       stats_partial_kernel<<<dim3((unsigned)U, nsplit), bs, 0, st>>>(keys, dt, L, D, nsplit, spart, status);
-    stats_final_kernel<<<(unsigned)U, bs, 0, st>>>(keys, dt, L, D, nsplit, spart, mu64, alpha64, mu32,
-                                                   alpha32, status);
+    stats_final_kernel<<<dim3((unsigned)U, (D + 7) / 8), 256, 0, st>>>(keys, dt, L, D, nsplit, spart, mu64, alpha64,
+                                                                     mu32, alpha32, status);
   }
   if (!(what & 2)) return cudaGetLastError();
   PackArgs pa{keys, values, dt, L, D, bits, gs, siq, mu64, alpha64, codes_ref, kq_ref, ks, kz,
@@ -937,22 +1009,31 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
   if (D == FD && gs == 32 && (bits == 1 || bits == 2 || bits == 4 || bits == 8) && dt != IN_F64 && !codes_in &&
       al16) {
     const int cnt_tiles = (int)((L + CB_TILE - 1) / CB_TILE);
-    if (cnt_tiles > ntiles) return cudaErrorInvalidValue;   // workspace sized by encode_tiles()
-    dim3 qg((unsigned)((L + QG_TOK - 1) / QG_TOK), (unsigned)U);
+    if (cnt_tiles > ntiles) return cudaErrorInvalidValue;   // workspace sized by pack_ntiles()
+    PackArgs qa = pa;
+    qa.tile = CB_TILE;
+    qa.ntiles = cnt_tiles;
+    const dim3 qg((unsigned)cnt_tiles, (unsigned)U);
+    const int qsm = (int)sizeof(QgSmem);
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kern) {
+      if (e != cudaSuccess) return;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, qsm);
+      if (e == cudaSuccess) kern<<<qg, 256, qsm, st>>>(qa);
+    };
     auto run = [&](auto dty) {
       constexpr int DTY = decltype(dty)::value;
       switch (bits) {
-        case 1: quant_group_kernel<DTY, 1><<<qg, 256, 0, st>>>(pa); break;
-        case 2: quant_group_kernel<DTY, 2><<<qg, 256, 0, st>>>(pa); break;
-        case 4: quant_group_kernel<DTY, 4><<<qg, 256, 0, st>>>(pa); break;
-        default: quant_group_kernel<DTY, 8><<<qg, 256, 0, st>>>(pa); break;
+        case 1: go(quant_group_kernel<DTY, 1>); break;
+        case 2: go(quant_group_kernel<DTY, 2>); break;
+        case 4: go(quant_group_kernel<DTY, 4>); break;
+        default: go(quant_group_kernel<DTY, 8>); break;
       }
-      codebook_tile_kernel<DTY><<<dim3(cnt_tiles, (unsigned)U), 128, 0, st>>>(keys, L, mu64, CB_TILE, cnt_tiles,
-                                                                           cbp, cbc);
     };
     if (dt == IN_BF16) run(std::integral_constant<int, IN_BF16>{});
     else run(std::integral_constant<int, IN_F32>{});
-    codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, cnt_tiles, cbp, cbc, c64,
+    if (e != cudaSuccess) return e;
+    codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 31) / 32), 256, 0, st>>>(G, cnt_tiles, cbp, cbc, c64,
                                                                                   c32);
     return cudaGetLastError();
   }
@@ -965,7 +1046,7 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
   cudaError_t e = dt == IN_BF16 ? launch(pack_kernel<IN_BF16>) : dt == IN_F32 ? launch(pack_kernel<IN_F32>)
                                                                                : launch(pack_kernel<IN_F64>);
   if (e != cudaSuccess) return e;
-  codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 255) / 256), 256, 0, st>>>(G, ptiles, cbp, cbc, c64, c32);
+  codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 31) / 32), 256, 0, st>>>(G, ptiles, cbp, cbc, c64, c32);
   return cudaGetLastError();
 }
 
