@@ -40,10 +40,10 @@ def test_host_queries():
 def test_argument_validation_without_gpu():
     with pytest.raises(ValueError, match="null"):
         _lib.call("sikv_decode_step", *([None] * 5), 0, None, 1, 0, None, 1, 10, 4, 1, 0, None, None, None, 0,
-                  None, None, None)
+                  None, None, None, 0, 0, None)
     with pytest.raises(NotImplementedError, match="query heads"):
         _lib.call("sikv_decode_step", *([_lib.ptr(8)] * 5), 0, None, 1, 0, _lib.ptr(8), 1, 10, 9, 1, 0,
-                  _lib.ptr(8), None, None, 0, None, None, None)
+                  _lib.ptr(8), None, None, 0, None, None, None, 0, 0, None)
     with pytest.raises(ValueError, match="non-negative"):
         _lib.call("sikv_topk", _lib.ptr(8), 0, 1, 10, None, 0, -1, _lib.ptr(8), _lib.ptr(8), 10, _lib.ptr(8), None)
 
