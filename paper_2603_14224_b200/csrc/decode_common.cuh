@@ -431,7 +431,15 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
   }
 }
 
-// th / tmin: 256 + 256 words of scratch for the threshold histogram
+// th / tmin: 256 + 256 words of scratch for the threshold histogram (may alias cand: the
+// histogram is rebuilt from the register-resident sample keys for every attempt).
+//
+// The sampled threshold is the sample key of rank r = e + 4 sqrt(e) + 16 (e = expected
+// sample items in the top-k).  When the scan then overflows a warp segment (tau too low) or
+// yields fewer than k candidates (tau too high), r is rescaled from the observed counts and
+// the scan is repeated (at most kRetries times) before falling back to the exact path.
+constexpr int kRetries = 2;
+
 template <class Grp>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
@@ -441,13 +449,12 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
   const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
   const int capw = g.capw;
   uint32_t* seg = cand + 2 * warp * capw;
-  int wc = 0;
-  uint32_t mx = 0;
-  uint32_t tau = 1;
+  uint32_t sk[MAX_SAMPLE_CHUNKS];
+  int nsv = 0, r = 0;
+  uint32_t kmx = 0, kmn = 0;
   if (tid == 0) { ms->maxx = 0; ms->bad = 0; }
   if (g.mode == 3) {
     // ---------------- B1: score the sample chunks (kept in registers)
-    uint32_t sk[MAX_SAMPLE_CHUNKS];
     float sv[MAX_SAMPLE_CHUNKS];
     score_batch(wsamp, lb, T, sv);
     int nv = 0;
@@ -468,82 +475,20 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
       smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
     }
-    for (int i = tid; i < 256; i += DT) { th[i] = 0; tmin[i] = 0xFFFFFFFFu; }
     if (tid == 0) { ms->nsv = 0; ms->tau = 0xFFFFFFFFu; }
     Grp::sync();
     if (lane == 0) { atomicAdd(&ms->nsv, nv); atomicMax(&ms->maxx, smax); atomicMin(&ms->tau, smin); }
     Grp::sync();
-    const int nsv = ms->nsv;
+    nsv = ms->nsv;
+    kmx = ms->maxx;
+    kmn = ms->tau;
     const double e = (double)g.keff * (double)nsv / (double)(g.L - g.S);
-    int r = (int)ceil(e + 4.0 * sqrt(e) + 16.0);
-    r = min(r, nsv);
-    if (r >= 1) {
-      const uint32_t kmx = ms->maxx, kmn = ms->tau;
-      const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
-      const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
-#pragma unroll
-      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-        if (sk[x]) {
-          const int b = min(255, (int)((__uint_as_float(unkey_bits(sk[x])) - fmn) * scale));
-          atomicAdd(&th[b], 1);
-          atomicMin(&tmin[b], sk[x]);
-        }
-      }
-      Grp::sync();
-      if (warp == 0) {
-        int loc[8], s8 = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) { loc[i] = th[255 - 8 * lane - i]; s8 += loc[i]; }
-        int inc = s8;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += v;
-        }
-        int c = inc - s8;
-        if (c < r && r <= inc) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (c < r && r <= c + loc[i]) ms->digit = 255 - 8 * lane - i;
-            c += loc[i];
-          }
-        }
-      }
-      Grp::sync();
-      tau = tmin[ms->digit];          // smallest sample key in the boundary bin
-    }
-    Grp::sync();
-    if (tid == 0) ms->maxx = 0;
-    Grp::sync();
-    uint32_t bits = 0;
-#pragma unroll
-    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x)
-      if (x < g.nsc && sk[x] != 0 && sk[x] >= tau) bits |= 1u << x;
-    const int cnt = __popc(bits);
-    int inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    int pos = wc + inc - cnt;
-    wc += __shfl_sync(0xffffffffu, inc, 31);
-#pragma unroll
-    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-      if ((bits >> x) & 1u) {
-        const uint32_t xk = sk[x] - tau;
-        if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(x * g.sstride * 256 + tid); }
-        mx = max(mx, xk);
-        ++pos;
-      }
-    }
+    r = min((int)ceil(e + 4.0 * sqrt(e) + 16.0), nsv);
   }
-  // ---------------- B2: score everything else, keep score >= tau (compared as floats)
-  const float tauf = g.mode == 2 ? -INFINITY : __uint_as_float(unkey_bits(tau));
+  const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
+  const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
   const int Li = (int)g.L;
-  int next_s = g.mode == 3 ? 0 : 0x7fffffff;      // next sample chunk (already scored in B1)
   const int end_s = g.nsc * g.sstride;
-  // register double buffer: the loads of batch c0 + NB are in flight while batch c0 scores
   auto load_batch = [&](int c0, uint4 (&w)[NB]) {
     const int t0 = c0 * 256 + tid;
     if ((c0 + NB) * 256 <= Li) {
@@ -554,60 +499,139 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       for (int x = 0; x < NB; ++x) w[x] = t0 + 256 * x < Li ? __ldg(signs + t0 + 256 * x) : make_uint4(0, 0, 0, 0);
     }
   };
-  uint4 wn[NB];
-  load_batch(0, wn);
-  for (int c0 = 0; c0 < g.nchunks; c0 += NB) {
-    int xs = -1;
-    if (next_s < c0 + NB && next_s < end_s) { xs = next_s - c0; next_s += g.sstride; }
-    const int t0 = c0 * 256 + tid;
-    const bool full = (c0 + NB) * 256 <= Li;
-    uint4 w[NB];
+  for (int attempt = 0;; ++attempt) {
+    int wc = 0;
+    uint32_t mx = 0;
+    uint32_t tau = 1;
+    if (g.mode == 3) {
+      if (r >= 1) {
+        // threshold histogram of the sample keys (256 value bins), rank r from the top
+        for (int i = tid; i < 256; i += DT) { th[i] = 0; tmin[i] = 0xFFFFFFFFu; }
+        Grp::sync();
 #pragma unroll
-    for (int x = 0; x < NB; ++x) w[x] = wn[x];
-    if (c0 + NB < g.nchunks) load_batch(c0 + NB, wn);
-    float sv[NB];
-    score_batch(w, lb, T, sv);
-    uint32_t bits = 0;
+        for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+          if (sk[x]) {
+            const int b = min(255, (int)((__uint_as_float(unkey_bits(sk[x])) - fmn) * scale));
+            atomicAdd(&th[b], 1);
+            atomicMin(&tmin[b], sk[x]);
+          }
+        }
+        Grp::sync();
+        if (warp == 0) {
+          int loc[8], s8 = 0;
 #pragma unroll
-    for (int x = 0; x < NB; ++x)
-      if (sv[x] >= tauf) bits |= 1u << x;
-    if (xs >= 0) bits &= ~(1u << xs);
-    if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NB ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
-    if (c0 * 256 < g.flim) {
+          for (int i = 0; i < 8; ++i) { loc[i] = th[255 - 8 * lane - i]; s8 += loc[i]; }
+          int inc = s8;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+          }
+          int c = inc - s8;
+          if (c < r && r <= inc) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (c < r && r <= c + loc[i]) ms->digit = 255 - 8 * lane - i;
+              c += loc[i];
+            }
+          }
+        }
+        Grp::sync();
+        tau = tmin[ms->digit];          // smallest sample key in the boundary bin
+      }
+      Grp::sync();
+      if (tid == 0) { ms->maxx = 0; ms->bad = 0; }
+      Grp::sync();
+      uint32_t bits = 0;
+#pragma unroll
+      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x)
+        if (x < g.nsc && sk[x] != 0 && sk[x] >= tau) bits |= 1u << x;
+      const int cnt = __popc(bits);
+      int inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int pos = wc + inc - cnt;
+      wc += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+        if ((bits >> x) & 1u) {
+          const uint32_t xk = sk[x] - tau;
+          if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(x * g.sstride * 256 + tid); }
+          mx = max(mx, xk);
+          ++pos;
+        }
+      }
+    }
+    // ---------------- B2: score everything else, keep score >= tau (compared as floats)
+    const float tauf = g.mode == 2 ? -INFINITY : __uint_as_float(unkey_bits(tau));
+    int next_s = g.mode == 3 ? 0 : 0x7fffffff;      // next sample chunk (already scored in B1)
+    // register double buffer: the loads of batch c0 + NB are in flight while batch c0 scores
+    uint4 wn[NB];
+    load_batch(0, wn);
+    for (int c0 = 0; c0 < g.nchunks; c0 += NB) {
+      int xs = -1;
+      if (next_s < c0 + NB && next_s < end_s) { xs = next_s - c0; next_s += g.sstride; }
+      const int t0 = c0 * 256 + tid;
+      const bool full = (c0 + NB) * 256 <= Li;
+      uint4 w[NB];
+#pragma unroll
+      for (int x = 0; x < NB; ++x) w[x] = wn[x];
+      if (c0 + NB < g.nchunks) load_batch(c0 + NB, wn);
+      float sv[NB];
+      score_batch(w, lb, T, sv);
+      uint32_t bits = 0;
 #pragma unroll
       for (int x = 0; x < NB; ++x)
-        if (t0 + 256 * x < Li && forced_bit(forced, t0 + 256 * x)) bits &= ~(1u << x);
-    }
-    // warp-compacted append: one scan per batch
-    const int cnt = __popc(bits);
-    int inc = cnt;
+        if (sv[x] >= tauf) bits |= 1u << x;
+      if (xs >= 0) bits &= ~(1u << xs);
+      if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NB ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
+      if (c0 * 256 < g.flim) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    int pos = wc + inc - cnt;
-    wc += __shfl_sync(0xffffffffu, inc, 31);
-    while (bits) {
-      const int x = __ffs(bits) - 1;
-      bits &= bits - 1;
-      float v = sv[0];
+        for (int x = 0; x < NB; ++x)
+          if (t0 + 256 * x < Li && forced_bit(forced, t0 + 256 * x)) bits &= ~(1u << x);
+      }
+      // warp-compacted append: one scan per batch
+      const int cnt = __popc(bits);
+      int inc = cnt;
 #pragma unroll
-      for (int y = 1; y < NB; ++y) v = (x == y) ? sv[y] : v;
-      const uint32_t xk = f32_key(v) - tau;
-      if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(t0 + 256 * x); }
-      mx = max(mx, xk);
-      ++pos;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int pos = wc + inc - cnt;
+      wc += __shfl_sync(0xffffffffu, inc, 31);
+      while (bits) {
+        const int x = __ffs(bits) - 1;
+        bits &= bits - 1;
+        float v = sv[0];
+#pragma unroll
+        for (int y = 1; y < NB; ++y) v = (x == y) ? sv[y] : v;
+        const uint32_t xk = f32_key(v) - tau;
+        if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(t0 + 256 * x); }
+        mx = max(mx, xk);
+        ++pos;
+      }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) { ms->wcnt[warp] = wc; atomicMax(&ms->maxx, mx); if (wc > capw) ms->bad = 1; }
+    Grp::sync();
+    int total = 0, maxwc = 0;
+    for (int w2 = 0; w2 < DW; ++w2) { total += ms->wcnt[w2]; maxwc = max(maxwc, ms->wcnt[w2]); }
+    tau_out = tau;
+    const bool bad = ms->bad != 0;
+    if (!bad && total >= g.keff) return false;
+    if (g.mode != 3 || attempt >= kRetries || r < 1) return true;
+    // rescale the sample rank from the observed candidate counts and scan again
+    const int r2 = bad ? (int)((double)r * 0.85 * (double)capw / (double)maxwc)
+                       : min(nsv, (int)ceil((double)r * 1.25 * (double)g.keff / (double)max(total, 1)) + 8);
+    if (r2 < 1 || r2 == r) return true;
+    r = r2;
+    Grp::sync();                          // every thread has read ms before it is reset
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) { ms->wcnt[warp] = wc; atomicMax(&ms->maxx, mx); if (wc > capw) ms->bad = 1; }
-  Grp::sync();
-  int total = 0;
-  for (int w2 = 0; w2 < DW; ++w2) total += ms->wcnt[w2];
-  tau_out = tau;
-  return ms->bad || total < g.keff;
 }
 
 // Exact fallback: multi-pass radix select over rescored keys, then gt / eq bitmaps (zeroed
