@@ -197,7 +197,8 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
                 sel_buf: torch.Tensor | None = None, kernel: int = 0) -> DecodeOutput:
     """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
 
-    kernel: 0 auto, 1 one CTA per unit, 2 warp-specialised persistent kernel."""
+    kernel: 0 auto, 1 one CTA per unit, 2 warp-specialised persistent kernel, 3 each unit split
+    across a CTA cluster (long contexts, few units)."""
     U = cb.units
     if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
         raise ValueError(f"q must be [{U}, Gq, {FD}], got {tuple(q.shape)}")

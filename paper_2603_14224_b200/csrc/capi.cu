@@ -31,6 +31,11 @@ cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, i
                               cudaStream_t);
 cudaError_t set_decode_profile(long long*);
 int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap);
+int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
+int split_default_cap(int64_t L, int k, int S, int ns);
+cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
+                                const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, int, float*,
+                                float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t);
 size_t ws_workspace_bytes(int64_t U, int64_t L);
 cudaError_t launch_decode_ws(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                              const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*,
@@ -206,8 +211,33 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   const int64_t keff = std::min<int64_t>(k, tokens - sinks);
   REQUIRE(sinks + keff + recent >= 1, SIKV_EINVAL, "selection is empty");
   REQUIRE(!sel || sel_stride >= sinks + keff + recent, SIKV_EINVAL, "sel_stride too small");
-  // kernel: 0 = auto, 1 = one CTA per unit, 2 = warp-specialised persistent
-  REQUIRE(kernel >= 0 && kernel <= 2, SIKV_EINVAL, "kernel must be 0, 1 or 2");
+  // kernel: 0 = auto, 1 = one CTA per unit, 2 = warp-specialised persistent, 3 = split units
+  // (a CTA cluster per unit)
+  REQUIRE(kernel >= 0 && kernel <= 3, SIKV_EINVAL, "kernel must be 0, 1, 2 or 3");
+  // few long units: split each across a cluster of 2 / 4 / 8 CTAs so every SM has work
+  if (kernel == 3 || (kernel == 0 && units < num_sms() && tokens >= 16384)) {
+    int pick = 0, pick_cap = 0;
+    for (int ns : {2, 4, 8}) {
+      if ((tokens + 255) / 256 < (kernel == 3 ? 1 : 4) * ns) break;   // chunks per CTA
+      const int c = cap > 0 ? cap : split_default_cap(tokens, k, sinks, ns);
+      const int need = split_smem_bytes(tokens, k, sinks, gq, c, ns);
+      if (need > max_smem()) continue;
+      const bool two_per_sm = need <= 113 * 1024;
+      if (!pick || (two_per_sm && units * ns <= 2 * num_sms()) ||
+          (two_per_sm && split_smem_bytes(tokens, k, sinks, gq, pick_cap, pick) > 113 * 1024)) {
+        pick = ns;
+        pick_cap = c;
+      }
+      if (two_per_sm && units * ns >= num_sms()) break;
+    }
+    REQUIRE(pick || kernel != 3, SIKV_EUNSUPPORTED, "the split kernel does not fit this configuration");
+    if (pick) {
+      return cuda_ret(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
+                                          frag_blocks, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
+                                          sel, sel_stride, sel_count, diag, (cudaStream_t)stream),
+                      "sikv_decode_step");
+    }
+  }
   if (kernel != 1 && workspace && workspace_bytes >= ws_workspace_bytes(units, tokens)) {
     int wcap = cap > 0 ? cap : sikv_decode_default_cap(tokens, k, sinks);
     // the persistent kernel keeps two hand-off slots; shrink the candidate buffer to fit

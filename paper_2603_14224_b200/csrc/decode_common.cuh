@@ -399,7 +399,8 @@ namespace sikv {
 // `fallback` = the segments are unusable (overflow or too few).  In that case the caller
 // runs produce_exact().
 struct UnitGeom {
-  int64_t L;
+  int64_t L;           // tokens this group scans (a slice of the unit for split units)
+  int64_t ncand;       // selectable tokens of the whole unit (L_unit - S)
   int S, keff, mode, nchunks, capw, sstride, nsc;
   int64_t flim;        // tokens below flim may be sinks
 };
@@ -409,6 +410,7 @@ __device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw,
   g.L = L;
   g.S = S;
   const int64_t ncand = L - S;
+  g.ncand = ncand;
   g.keff = (int)((int64_t)k < ncand ? (int64_t)k : ncand);
   g.nchunks = (int)((L + 255) >> 8);
   g.capw = capw;
@@ -440,11 +442,11 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
 // the scan is repeated (at most kRetries times) before falling back to the exact path.
 constexpr int kRetries = 2;
 
-template <class Grp>
+template <class Grp, class Xch = NoX>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
                                                    uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
-                                                   uint32_t& tau_out) {
+                                                   uint32_t& tau_out, const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
   const int capw = g.capw;
@@ -482,7 +484,8 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     nsv = ms->nsv;
     kmx = ms->maxx;
     kmn = ms->tau;
-    const double e = (double)g.keff * (double)nsv / (double)(g.L - g.S);
+    xch.sample(nsv, kmx, kmn);            // cluster: the whole unit's sample
+    const double e = (double)g.keff * (double)nsv / (double)(g.ncand);
     r = min((int)ceil(e + 4.0 * sqrt(e) + 16.0), nsv);
   }
   const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
@@ -517,10 +520,13 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
           }
         }
         Grp::sync();
+        const int* thm = th;
+        const uint32_t* tminm = tmin;
+        xch.hist256(thm, tminm);              // cluster: merged over the CTAs
         if (warp == 0) {
           int loc[8], s8 = 0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) { loc[i] = th[255 - 8 * lane - i]; s8 += loc[i]; }
+          for (int i = 0; i < 8; ++i) { loc[i] = thm[255 - 8 * lane - i]; s8 += loc[i]; }
           int inc = s8;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -537,7 +543,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
           }
         }
         Grp::sync();
-        tau = tmin[ms->digit];          // smallest sample key in the boundary bin
+        tau = tminm[ms->digit];         // smallest sample key in the boundary bin
       }
       Grp::sync();
       if (tid == 0) { ms->maxx = 0; ms->bad = 0; }
@@ -622,7 +628,8 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     int total = 0, maxwc = 0;
     for (int w2 = 0; w2 < DW; ++w2) { total += ms->wcnt[w2]; maxwc = max(maxwc, ms->wcnt[w2]); }
     tau_out = tau;
-    const bool bad = ms->bad != 0;
+    bool bad = ms->bad != 0;
+    xch.counts(total, maxwc, bad);        // cluster: unit totals, any CTA overflowing
     if (!bad && total >= g.keff) return false;
     if (g.mode != 3 || attempt >= kRetries || r < 1) return true;
     // rescale the sample rank from the observed candidate counts and scan again
@@ -636,20 +643,21 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
 
 // Exact fallback: multi-pass radix select over rescored keys, then gt / eq bitmaps (zeroed
 // here; smem or global) of key > K* and key == K*.  hist needs NBIN + 33 ints.
-template <class Grp>
+template <class Grp, class Xch = NoX>
 __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* signs, const char* T,
                                               const uint32_t* forced, int* hist, Misc* ms, uint32_t* gt,
-                                              uint32_t* eq, uint32_t& kstar, int& need_eq, int& eq_count) {
+                                              uint32_t* eq, uint32_t& kstar, int& need_eq, int& eq_count,
+                                              const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31;
   const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
   const int64_t L = g.L;
   const int nchunks = g.nchunks;
-  radix_kth<Grp>([&](auto f) {
+  radix_kth<Grp, Xch>([&](auto f) {
     for (int c = 0; c < nchunks; ++c) {
       const int64_t t = (int64_t)c * 256 + tid;
       if (t < L && !forced_bit(forced, t)) f(f32_key(score_token(__ldg(signs + t), lb, T)));
     }
-  }, 0xFFFFFFFFu, g.keff, hist, ms, kstar, need_eq);
+  }, 0xFFFFFFFFu, g.keff, hist, ms, kstar, need_eq, xch);
   const int W = (int)((L + 31) >> 5);
   for (int i = tid; i < 2 * W; i += DT) (i < W ? gt[i] : eq[i - W]) = 0u;
   if (tid == 0) ms->nsv = 0;
@@ -669,18 +677,19 @@ __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* si
 }
 
 // Exact k-th key among the candidate segments, then the gt / eq bitmaps (zeroed here).
-template <class Grp>
+template <class Grp, class Xch = NoX>
 __device__ __forceinline__ void select_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
                                                        uint32_t maxx, uint32_t tau, int* hist, Misc* ms,
                                                        uint32_t* gt, uint32_t* eq, uint32_t& kstar,
-                                                       int& need_eq, int& eq_count) {
+                                                       int& need_eq, int& eq_count, const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const uint32_t* seg = cand + 2 * warp * g.capw;
   const int n = wcnt[warp];
   uint32_t xk;
-  radix_kth<Grp>([&](auto f) {
+  maxx = xch.maxu(maxx);
+  radix_kth<Grp, Xch>([&](auto f) {
     for (int i = lane; i < n; i += 32) f(seg[2 * i]);
-  }, maxx, g.keff, hist, ms, xk, need_eq);
+  }, maxx, g.keff, hist, ms, xk, need_eq, xch);
   kstar = xk + tau;
   const int W = (int)((g.L + 31) >> 5);
   for (int i = tid; i < W; i += DT) { gt[i] = 0u; eq[i] = 0u; }

@@ -19,6 +19,18 @@ struct NamedGroup {                // threads [BASE, BASE + 256) of the CTA, bar
   static __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, 256;\n" ::"n"(ID) : "memory"); }
 };
 
+// Cross-CTA exchange policy for split units (a CTA cluster sharing one unit).  NoX: the
+// group owns the whole unit, every "global" value is the local one.  Each hook is called by
+// every thread of the group after the group has synchronised on the local value.
+struct NoX {
+  static constexpr bool kCluster = false;
+  __device__ __forceinline__ void sample(int&, uint32_t&, uint32_t&) const {}
+  __device__ __forceinline__ void hist256(const int*&, const uint32_t*&) const {}
+  __device__ __forceinline__ void counts(int&, int&, bool&) const {}
+  __device__ __forceinline__ const int* hist4k(const int* h) const { return h; }
+  __device__ __forceinline__ uint32_t maxu(uint32_t v) const { return v; }
+};
+
 // ---------------------------------------------------------------- small group utilities
 struct Misc {                      // scalars in shared memory
   int ncand, nsv, digit, rem_sel, cnt_above, total, fb, bad;
@@ -109,9 +121,9 @@ __device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
 // f(x) once per item on the calling thread (every thread of the group calls each()).
 // Returns the k-th value and how many items equal to it belong to the top `rank` (ties
 // are then resolved by index by the caller).  hist must hold NBIN + 33 ints.
-template <class Grp = Cta256, typename Each>
+template <class Grp = Cta256, class Xch = NoX, typename Each>
 __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, int* hist, Misc* ms,
-                                          uint32_t& kth, int& need_eq) {
+                                          uint32_t& kth, int& need_eq, const Xch& xch = Xch()) {
   const int tid = Grp::tid();
   const int nbits = maxx ? 32 - __clz(maxx) : 0;
   int* list = hist + NBIN;           // up to 32 items of a small boundary bin (+ counter)
@@ -132,14 +144,15 @@ __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, in
       if ((hi >= 32 ? 0u : (x >> hi)) == want) atomicAdd(&hist[(x >> sh) & (NBIN - 1)], 1);
     });
     Grp::sync();
-    pick_digit_big<Grp>(hist, ms);
+    const int* mh = xch.hist4k(hist);   // cluster: the sum of every CTA's histogram
+    pick_digit_big<Grp>(mh, ms);
     const uint32_t d = (uint32_t)ms->digit;
     prefix |= d << shift;
-    const int nb = hist[d];
+    const int nb = mh[d];
     Grp::sync();
     if (tid == 0) ms->rem_sel -= ms->cnt_above;
     Grp::sync();
-    if (shift > 0 && nb <= 32) {
+    if (!Xch::kCluster && shift > 0 && nb <= 32) {
       // finish inside one warp: exact rank among the few items of the boundary bin
       const uint32_t w2 = prefix >> shift;
       each([&](uint32_t x) {

@@ -116,7 +116,7 @@ def _check_decode(units, cb, oc, q, k, **kw):
     return res
 
 
-KERNELS = [1, 2]    # one CTA per unit / warp-specialised persistent
+KERNELS = [1, 2, 3]    # one CTA per unit / warp-specialised persistent / split across a cluster
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -140,7 +140,9 @@ def test_decode_matches_reference_selection(c1, golden):
 def test_decode_fallback_path(c1, kernel):
     """A tiny candidate buffer forces the exact multi-pass rescoring path."""
     units, cb, oc, q = c1
-    res = _check_decode(units, cb, oc, q, 256, cap=300, kernel=kernel)
+    # the split kernel's buffer is per CTA: ask for more than one CTA's share can hold
+    k, cap = (3500, 40) if kernel == 3 else (256, 300)
+    res = _check_decode(units, cb, oc, q, k, cap=cap, kernel=kernel)
     assert (res.diag.cpu().numpy() & 4).all()
 
 
@@ -164,6 +166,20 @@ def test_kernels_agree_bitwise(c32k):
     r2 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=2)
     assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.counts, r2.counts)
     assert torch.equal(r1.out, r2.out) and torch.equal(r1.lse, r2.lse)
+
+
+def test_split_kernel_matches_single_cta(c32k):
+    """The cluster-split kernel selects exactly what the one-CTA kernel selects."""
+    units, cb, oc, q = c32k
+    r1 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, with_diag=True, kernel=1)
+    r3 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, with_diag=True, kernel=3)
+    assert torch.equal(r1.selection, r3.selection) and torch.equal(r1.counts, r3.counts)
+    assert (r3.diag.cpu().numpy() & 8).all()
+    # P is rounded to fp16 against each CTA's own running max, so outputs agree to the fp16
+    # probability rounding (both are also checked against the float64 oracle above)
+    rel = (r3.out - r1.out).norm(dim=-1) / r1.out.norm(dim=-1)
+    assert rel.max().item() <= 1e-3, rel.max().item()
+    torch.testing.assert_close(r3.lse, r1.lse, rtol=1e-5, atol=1e-4)
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -207,7 +223,8 @@ def test_decode_ties_lowest_index_first():
     cb = B.prefill_batch(K_t, V_t, sink_count=64)
     c = O.prefill(reps, V, sink_count=64)
     q = torch.tensor(base.queries[None, :4], dtype=torch.float32, device="cuda")
-    for k, cap, kern in ((500, 0, 1), (500, 200, 1), (333, 0, 1), (500, 0, 2), (500, 200, 2)):
+    for k, cap, kern in ((500, 0, 1), (500, 200, 1), (333, 0, 1), (500, 0, 2), (500, 200, 2), (500, 0, 3),
+                         (500, 200, 3), (333, 0, 3)):
         res = B.decode_step(cb, q, k, cap=cap, with_selection=True, kernel=kern)
         idx = R.select32(c, base.queries[:4].astype(np.float32), k)[0]
         got = res.selection[0, : res.counts[0]].cpu().numpy()
