@@ -115,6 +115,10 @@ int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const 
  * subsequent sikv_decode_step; NULL disables. */
 int sikv_debug_set_decode_profile(void* clocks);
 
+/* debug: bit 0 makes the persistent decode kernel skip sparse attention (phase timing of
+ * the scoring / selection half alone); 0 restores normal operation. */
+int sikv_debug_set_ws_skip(int bits);
+
 /* fast-path float32 scores only (the decode kernel's scoring, for verification / API).
  * replaces: build_lut + score_tokens on the group-summed query, retrieval.py:46-77 */
 int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq,

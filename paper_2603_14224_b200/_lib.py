@@ -38,6 +38,7 @@ _SIGS = {
     "sikv_pack_forced": (I, [P, P, I, P, P, I64, I, P, I64, P, I, I, I, P]),
     "sikv_score_fast": (I, [P, P, P, I, I64, I64, P, P]),
     "sikv_debug_set_decode_profile": (I, [P]),
+    "sikv_debug_set_ws_skip": (I, [I]),
     "sikv_build_lut_f64": (I, [P, P, I64, I, I, P, P]),
     "sikv_score_f64": (I, [P, P, I64, I, I64, P, P]),
     "sikv_topk_workspace_bytes": (SZ, [I64, I64]),

@@ -30,6 +30,8 @@ cudaError_t launch_pack_forced(const float*, const float*, int, const float*, co
 cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
                               cudaStream_t);
 cudaError_t set_decode_profile(long long*);
+cudaError_t set_decode_ws_profile(long long*);
+cudaError_t set_decode_ws_skip(int);
 int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap);
 int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
@@ -201,6 +203,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
+  REQUIRE(tokens <= (1ll << 25), SIKV_EUNSUPPORTED, "fast decode supports at most 2^25 tokens per unit");
   REQUIRE(gq >= 1 && gq <= 8, SIKV_EUNSUPPORTED, "fast decode supports 1..8 query heads per KV head");
   REQUIRE(k >= 0, SIKV_EINVAL, "k must be non-negative");
   REQUIRE(sinks >= 0 && sinks <= tokens, SIKV_EINVAL, "sink count out of range");
@@ -264,8 +267,12 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   return cuda_ret(e, "sikv_decode_step");
 }
 
+int sikv_debug_set_ws_skip(int v) { return cuda_ret(set_decode_ws_skip(v), "sikv_debug_set_ws_skip"); }
+
 int sikv_debug_set_decode_profile(void* clocks) {
-  return cuda_ret(set_decode_profile((long long*)clocks), "sikv_debug_set_decode_profile");
+  cudaError_t e = set_decode_profile((long long*)clocks);
+  if (e == cudaSuccess) e = set_decode_ws_profile((long long*)clocks);
+  return cuda_ret(e, "sikv_debug_set_decode_profile");
 }
 
 int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq, int64_t units,

@@ -36,32 +36,22 @@ constexpr int FD = 128;
 constexpr int FSIGN = 16;      // bytes per token in the sign plane
 constexpr int FREC = 128;      // bytes per token record
 // record byte offsets
-constexpr int R_KPAY = 0;      // 32 B K magnitude payload, MMA-permuted
-constexpr int R_VPAY = 32;     // 32 B V payload, MMA-permuted
-constexpr int R_KPAR = 64;     // 4 x (qs, zp) fp16
-constexpr int R_VPAR = 80;     // 4 x (qs, zp) fp16
-constexpr int R_KSGN = 96;     // 4 x u32 negative-sign words, MMA-permuted
+constexpr int R_K4 = 0;        // 64 B K as e2m1 nibbles (sign | 2-bit code), MMA-permuted
+constexpr int R_VPAY = 64;     // 32 B V payload, MMA-permuted
+constexpr int R_KPAR = 96;     // 4 x (2 qs, zp) fp16
+constexpr int R_VPAR = 112;    // 4 x (qs, zp) fp16
 
-// ---- K payload permutation (B operand of q~ K^T, m16n8k16, one token per n column)
-// thread t4 of a quad owns words 2*t4 + u (u = 0,1).  Slot i (0..7) of word u holds
-// pair (s = 4u + (i>>1), e = i&1): lo half bits [2i,2i+2) = channel 16s+2t4+8e,
-// hi half bits [16+2i, 16+2i+2) = channel 16s+2t4+8e+1.
-__host__ __device__ __forceinline__ void kpay_pos(int ch, int& word, int& bit) {
-  int s = ch >> 4, r = ch & 15;
-  int e = (r >> 3) & 1, rr = r & 7;        // rr = 2*t4 + hi
-  int t4 = rr >> 1, hi = rr & 1;
-  int u = s >> 2, i = ((s & 3) << 1) | e;
-  word = 2 * t4 + u;
-  bit = 2 * i + 16 * hi;
-}
-// ---- K sign permutation: word t4, pair P = 8u + i  -> lo sign at bit P, hi at 16+P
-__host__ __device__ __forceinline__ void ksgn_pos(int ch, int& word, int& bit) {
-  int s = ch >> 4, r = ch & 15;
-  int e = (r >> 3) & 1, rr = r & 7;
-  int t4 = rr >> 1, hi = rr & 1;
-  int u = s >> 2, i = ((s & 3) << 1) | e;
-  word = t4;
-  bit = 8 * u + i + 16 * hi;
+// ---- K nibble permutation (B operand of q~ K^T, m16n8k16, one token per n column).
+// A nibble is an e2m1 value: bit 3 = sign of K' (1 = negative), bits 0-1 = the 2-bit
+// magnitude code c, bit 2 = 0, so it decodes (cvt.rn.f16x2.e2m1x2) to sign * c / 2 and
+// K^ = (2 qs) x + copysign(zp, x).  Thread t4 of a quad owns the 16-byte chunk t4 (words
+// 4 t4 .. 4 t4 + 3); byte 2s + e of the chunk holds channels 16s + 8e + 2t4 (lo nibble) and
+// +1 (hi nibble).  Group j's channels fill exactly word 4 t4 + j.
+__host__ __device__ __forceinline__ void k4_pos(int ch, int& word, int& bit) {
+  const int j = ch >> 5, n = ch & 31;
+  const int ss = n >> 4, e = (n >> 3) & 1, rr = n & 7;
+  word = 4 * (rr >> 1) + j;
+  bit = 16 * ss + 8 * e + 4 * (rr & 1);
 }
 // ---- V payload permutation (A operand of V^T P^T, m16n8k16, one channel per m row)
 // word g (0..7) holds channels 16m + g + 8e (m = 0..7, e = 0,1):

@@ -97,14 +97,18 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   uint32_t* eq = gt + W;
   uint32_t kstar = 0;
   int need_eq = 0, eq_count = 0;
+  int ndyn = -1;
+  int32_t* sel_u = a.sel ? a.sel + u * a.sel_stride : nullptr;
+  int32_t* sel_count_u = a.sel_count ? a.sel_count + u : nullptr;
   if (mode >= 2) {
     uint32_t tau;
     const bool fb = produce_candidates<Cta256>(g, signs, T, forced, wsamp, cand, reinterpret_cast<int*>(cand),
                                                cand + 256, ms, tau);
     PROF(3);
     if (!fb) {
-      select_from_candidates<Cta256>(g, cand, ms->wcnt, ms->maxx, tau, reinterpret_cast<int*>(T), ms, gt, eq,
-                                     kstar, need_eq, eq_count);
+      ndyn = select_emit_candidates<Cta256>(g, forced, cand, ms->wcnt, ms->maxx, tau, reinterpret_cast<int*>(T), ms,
+                                            gt, eq, reinterpret_cast<int32_t*>(sm + a.off_dyn), sel_u, R,
+                                            sel_count_u, kstar);
     } else {
       if (tid == 0) ms->fb = 1;
       gt = cand + NBIN + 64;                                      // R1: candidates are void
@@ -114,10 +118,9 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     }
   }
   PROF(4);
-  const int ndyn = emit_selection<Cta256>(g, mode, forced, gt, eq, need_eq, eq_count,
-                                          reinterpret_cast<int32_t*>(sm + a.off_dyn),
-                                          a.sel ? a.sel + u * a.sel_stride : nullptr, R,
-                                          a.sel_count ? a.sel_count + u : nullptr, ms);
+  if (ndyn < 0)
+    ndyn = emit_selection<Cta256>(g, mode, forced, gt, eq, need_eq, eq_count,
+                                  reinterpret_cast<int32_t*>(sm + a.off_dyn), sel_u, R, sel_count_u, ms);
   if (tid == 0 && a.diag) a.diag[u] = (mode & 3) | (ms->fb ? 4 : 0);
 
   PROF(5);
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   float* pl = pm + DW * Gq;                                // [DW][Gq]
   attn_write_partial(A, part, pm, pl, warp, Gq, lane);
   __syncthreads();
-  attn_merge(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+  attn_merge<Cta256>(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
   PROF(9);
 #undef PROF
 }
@@ -190,7 +193,7 @@ DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap) {
   // R0: pair table while scoring; afterwards hist | gt | eq | dynamic list | staging
   d.off_bits = align128(NBIN * 4);
   d.off_dyn = align128(d.off_bits + 2 * W * 4);
-  d.off_stage = align128(d.off_dyn + std::max(keff, 1) * 4);
+  d.off_stage = align128(d.off_dyn + (std::max(keff, 1) + 16) * 4);
   const int r0 = std::max(TBL_BYTES, d.off_stage + DW * 2 * STAGE_BYTES);
   // R1: per-warp candidate segments; at other times the tau histogram, the fallback
   // histogram + bitmaps, and the attention partials

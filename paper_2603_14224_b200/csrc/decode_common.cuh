@@ -115,19 +115,35 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// stage the 16 records of one dynamic block into shared memory, 16-byte chunk k of token j
-// stored at chunk k ^ (j & 7) so the fragment reads below are bank-conflict free
-__device__ __forceinline__ void stage_block(char* buf, const uint8_t* recs, const int32_t* dyn, int base,
-                                            int ndyn, int lane) {
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int c = lane + 32 * r, j = c >> 3, kk = c & 7;
-    const int t = dyn[min(base + j, ndyn - 1)];
-    cp_async16(buf + j * FREC + 16 * (kk ^ (j & 7)), recs + (int64_t)t * FREC + 16 * kk);
-  }
+// staged-record swizzle: 16-byte chunk kk of block token j lives at slot kk ^ stage_sw(j).
+// Conflict-free for the fragment reads below: K4 chunks t4 of tokens 2p, 2p+1 fill all 8
+// slots of a quarter-warp phase; the V words / params of the 4 even (odd) tokens of a block
+// hit 4 distinct slot pairs.
+__host__ __device__ __forceinline__ int stage_sw(int j) { return (j & 6) ^ ((j & 1) << 2); }
+
+// two e2m1 nibbles (byte B of w) -> f16x2 (lo nibble -> low half)
+template <int B>
+__device__ __forceinline__ uint32_t e2m1x2_to_h2(uint32_t w) {
+  uint32_t r;
+  if constexpr (B == 0)
+    asm("{ .reg .b8 b0, b1, b2, b3; mov.b32 {b0, b1, b2, b3}, %1; cvt.rn.f16x2.e2m1x2 %0, b0; }" : "=r"(r) : "r"(w));
+  else if constexpr (B == 1)
+    asm("{ .reg .b8 b0, b1, b2, b3; mov.b32 {b0, b1, b2, b3}, %1; cvt.rn.f16x2.e2m1x2 %0, b1; }" : "=r"(r) : "r"(w));
+  else if constexpr (B == 2)
+    asm("{ .reg .b8 b0, b1, b2, b3; mov.b32 {b0, b1, b2, b3}, %1; cvt.rn.f16x2.e2m1x2 %0, b2; }" : "=r"(r) : "r"(w));
+  else
+    asm("{ .reg .b8 b0, b1, b2, b3; mov.b32 {b0, b1, b2, b3}, %1; cvt.rn.f16x2.e2m1x2 %0, b3; }" : "=r"(r) : "r"(w));
+  return r;
 }
-__device__ __forceinline__ const char* chunk(const char* buf, int j, int kk) {
-  return buf + j * FREC + 16 * (kk ^ (j & 7));
+
+// K^ for two channels from their e2m1 byte: (2 qs) x + copysign(zp, x), x = sign * code / 2.
+// Bit-identical to sign * fl16(qs c + zp) (c/2 * 2qs is exact; one rounding, symmetric).
+template <int B>
+__device__ __forceinline__ uint32_t k_dequant2(uint32_t w, __half2 qs2, uint32_t zp2) {
+  const uint32_t x = e2m1x2_to_h2<B>(w);
+  uint32_t z;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(z) : "r"(x), "r"(0x80008000u), "r"(zp2));   // (x & m) | zp
+  return h2u(__hfma2(u2h(x), qs2, u2h(z)));
 }
 
 // ---------------------------------------------------------------- sparse attention
@@ -157,28 +173,35 @@ __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float*
 }
 
 constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;   // log2(e) / sqrt(128)
+// 2^x on the SFU (x <= 0 here: logits minus the running max; -inf -> +0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 // fp16 magic for a 2-bit code at bits [2i, 2i+2) of each half: 2^(10-2i), so that
 // (w & mask_i) | magic_i is the half 2^(10-2i) + code exactly
 __host__ __device__ constexpr uint32_t kMagic(int i) { return ((25u - 2u * (uint32_t)i) << 10) * 0x00010001u; }
 
-// online softmax update + P V for one 16-token block (scores for head g in sacc)
+// online softmax update + P V for one 16-token block (scores for head g in sacc); rows at
+// block offsets >= rem are padding
 template <typename VFrag>
-__device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][4], const bool (&valid)[2][2],
-                                                int lane, VFrag&& vfrag) {
+__device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][4], int rem, int lane,
+                                                VFrag&& vfrag) {
   const int t4 = lane & 3;
   float x[4];
-  x[0] = valid[0][0] ? sacc[0][0] * kSoftmaxScale : -INFINITY;
-  x[1] = valid[0][1] ? sacc[0][1] * kSoftmaxScale : -INFINITY;
-  x[2] = valid[1][0] ? sacc[1][0] * kSoftmaxScale : -INFINITY;
-  x[3] = valid[1][1] ? sacc[1][1] * kSoftmaxScale : -INFINITY;
+  x[0] = 2 * t4 < rem ? sacc[0][0] * kSoftmaxScale : -INFINITY;
+  x[1] = 2 * t4 + 1 < rem ? sacc[0][1] * kSoftmaxScale : -INFINITY;
+  x[2] = 2 * t4 + 8 < rem ? sacc[1][0] * kSoftmaxScale : -INFINITY;
+  x[3] = 2 * t4 + 9 < rem ? sacc[1][1] * kSoftmaxScale : -INFINITY;
   float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
   bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
   bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
   const float mnew = fmaxf(A.mrun, bm);
-  const float fac = exp2f(A.mrun - mnew);
+  const float fac = ex2(A.mrun - mnew);
   A.mrun = mnew;
-  const __half2 p01 = __floats2half2_rn(exp2f(x[0] - mnew), exp2f(x[1] - mnew));
-  const __half2 p23 = __floats2half2_rn(exp2f(x[2] - mnew), exp2f(x[3] - mnew));
+  const __half2 p01 = __floats2half2_rn(ex2(x[0] - mnew), ex2(x[1] - mnew));
+  const __half2 p23 = __floats2half2_rn(ex2(x[2] - mnew), ex2(x[3] - mnew));
   const float2 f01 = __half22float2(p01), f23 = __half22float2(p23);
   A.lrun = A.lrun * fac + ((f01.x + f01.y) + (f23.x + f23.y));
   if (!__all_sync(0xffffffffu, fac == 1.0f)) {   // the running max moved for some head
@@ -199,7 +222,6 @@ __device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][
 // forced rows (sinks then recents), pre-packed as fp16 fragments; this warp takes blocks
 // wi, wi + nw, ... of [0, nbf)
 __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, int nf, int wi, int nw, int lane) {
-  const int t4 = lane & 3;
   const int nbf = (nf + 15) >> 4;
   for (int blk = wi; blk < nbf; blk += nw) {
     const int base = blk * 16;
@@ -217,17 +239,14 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
       vwd[4 * i] = t.x; vwd[4 * i + 1] = t.y; vwd[4 * i + 2] = t.z; vwd[4 * i + 3] = t.w;
     }
     float sacc[2][4];
-    bool valid[2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
 #pragma unroll
       for (int s = 0; s < 8; ++s)
         mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, kwd[nt * 16 + 2 * s], kwd[nt * 16 + 2 * s + 1]);
-      valid[nt][0] = base + 2 * t4 + 8 * nt < nf;
-      valid[nt][1] = base + 2 * t4 + 1 + 8 * nt < nf;
     }
-    attn_softmax_pv(A, sacc, valid, lane, [&](int mp, uint32_t (&v)[2][4]) {
+    attn_softmax_pv(A, sacc, nf - base, lane, [&](int mp, uint32_t (&v)[2][4]) {
 #pragma unroll
       for (int mm = 0; mm < 2; ++mm)
 #pragma unroll
@@ -237,9 +256,10 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
 }
 
 // dynamic rows: blocks first, first + nw, ... of [0, nbd), staged by cp.async (double
-// buffered) and dequantised into mma fragments.  Every lane's shared-memory offsets are
-// fixed for the whole unit (16-byte chunk k of token j lives at chunk k ^ (j & 7)), so they
-// are computed once; token g and g + 8 (and 2t4 + x and 2t4 + x + 8) differ by 1 KiB.
+// buffered) and dequantised into mma fragments.  The list is padded to a multiple of 16
+// (pad_dyn), so staging needs no bounds.  Every lane's shared-memory offsets are fixed for
+// the whole unit (16-byte chunk k of token j lives at chunk k ^ (j & 7)), so they are
+// computed once; token g and g + 8 (and 2t4 + x and 2t4 + x + 8) differ by 1 KiB.
 __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, const int32_t* dyn, int ndyn,
                                              int first, int nw, char* stage, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
@@ -251,25 +271,25 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int j = jb + 4 * r;
-    dst[r] = (uint32_t)(j * FREC + 16 * (kk ^ (j & 7)));
+    dst[r] = (uint32_t)(j * FREC + 16 * (kk ^ stage_sw(j)));
   }
+  const uint8_t* src0 = recs_u + 16 * kk;
   auto stage_blk = [&](uint32_t buf, int base) {
+    const int32_t* dl = dyn + base + jb;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const int t = dyn[min(base + jb + 4 * r, ndyn - 1)];
-      const uint8_t* src = recs_u + (int64_t)t * FREC + 16 * kk;
+      const uint8_t* src = src0 + (size_t)((uint32_t)dl[4 * r] * (uint32_t)FREC);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + buf + dst[r]), "l"(src));
     }
   };
   // fragment offsets (token g for K, tokens 2t4 / 2t4 + 1 for V; +1 KiB for the +8 tokens)
   const int jk = g, jv0 = 2 * t4, jv1 = 2 * t4 + 1;
-  const int off_kw = jk * FREC + 16 * ((t4 >> 1) ^ (jk & 7)) + 8 * (t4 & 1);
-  const int off_kp = jk * FREC + 16 * (4 ^ (jk & 7));
-  const int off_ks = jk * FREC + 16 * (6 ^ (jk & 7)) + 4 * t4;
-  const int off_vw0 = jv0 * FREC + 16 * ((2 + (g >> 2)) ^ (jv0 & 7)) + 4 * (g & 3);
-  const int off_vw1 = jv1 * FREC + 16 * ((2 + (g >> 2)) ^ (jv1 & 7)) + 4 * (g & 3);
-  const int off_vp0 = jv0 * FREC + 16 * (5 ^ (jv0 & 7));
-  const int off_vp1 = jv1 * FREC + 16 * (5 ^ (jv1 & 7));
+  const int off_k4 = jk * FREC + 16 * (t4 ^ stage_sw(jk));
+  const int off_kp = jk * FREC + 16 * (6 ^ stage_sw(jk));
+  const int off_vw0 = jv0 * FREC + 16 * ((4 + (g >> 2)) ^ stage_sw(jv0)) + 4 * (g & 3);
+  const int off_vw1 = jv1 * FREC + 16 * ((4 + (g >> 2)) ^ stage_sw(jv1)) + 4 * (g & 3);
+  const int off_vp0 = jv0 * FREC + 16 * (7 ^ stage_sw(jv0));
+  const int off_vp1 = jv1 * FREC + 16 * (7 ^ stage_sw(jv1));
   constexpr int P8 = 8 * FREC;
   if (first < nbd) stage_blk(0, first * 16);
   cp_commit();
@@ -282,38 +302,23 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     const char* sb = stage + buf * STAGE_BYTES;
     const int base = db * 16;
     float sacc[2][4];
-    bool valid[2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const uint2 kw = *reinterpret_cast<const uint2*>(sb + off_kw + nt * P8);
+      const uint4 k4 = *reinterpret_cast<const uint4*>(sb + off_k4 + nt * P8);
       const uint4 kp = *reinterpret_cast<const uint4*>(sb + off_kp + nt * P8);
-      const uint32_t ks = *reinterpret_cast<const uint32_t*>(sb + off_ks + nt * P8);
+      const uint32_t kw[4] = {k4.x, k4.y, k4.z, k4.w};
       const uint32_t par[4] = {kp.x, kp.y, kp.z, kp.w};
-      const uint32_t wsrc[4] = {kw.x, kw.x >> 8, kw.y, kw.y >> 8};   // slots 0-3 / 4-7 of each word
       sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
 #pragma unroll
       for (int grp = 0; grp < 4; ++grp) {
         const __half2 qs2 = u2h(prmt(par[grp], par[grp], 0x1010u));
-        const __half2 zp2 = u2h(prmt(par[grp], par[grp], 0x3232u));
-#pragma unroll
-        for (int ss = 0; ss < 2; ++ss) {
-          const int s = 2 * grp + ss, uu = s >> 2;
-          uint32_t b[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = ((s & 3) << 1) | e;
-            const uint32_t src = wsrc[2 * uu + (i >> 2)];
-            const int ii = i & 3;
-            const uint32_t xx = lop3_and_or(src, 0x00030003u << (2 * ii), kMagic(ii));
-            const __half2 c = __hsub2(u2h(xx), u2h(kMagic(ii)));
-            const uint32_t v = h2u(__hfma2(c, qs2, zp2));
-            b[e] = lop3_xor_and(v, ks << (15 - (8 * uu + i)), 0x80008000u);
-          }
-          mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, b[0], b[1]);
-        }
+        const uint32_t zp2 = prmt(par[grp], par[grp], 0x3232u);
+        // k-steps s = 2 grp (bytes 0, 1 of word grp) and 2 grp + 1 (bytes 2, 3)
+        mma16816(sacc[nt], A.qa[2 * grp][0], 0u, A.qa[2 * grp][1], 0u, k_dequant2<0>(kw[grp], qs2, zp2),
+                 k_dequant2<1>(kw[grp], qs2, zp2));
+        mma16816(sacc[nt], A.qa[2 * grp + 1][0], 0u, A.qa[2 * grp + 1][1], 0u, k_dequant2<2>(kw[grp], qs2, zp2),
+                 k_dequant2<3>(kw[grp], qs2, zp2));
       }
-      valid[nt][0] = base + 2 * t4 + 8 * nt < ndyn;
-      valid[nt][1] = base + 2 * t4 + 1 + 8 * nt < ndyn;
     }
     // V words and params of tokens 2t4, 2t4+1, 2t4+8, 2t4+9
     uint32_t vw[4];
@@ -326,7 +331,7 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     vp[1] = *reinterpret_cast<const uint4*>(sb + off_vp1);
     vp[2] = *reinterpret_cast<const uint4*>(sb + off_vp0 + P8);
     vp[3] = *reinterpret_cast<const uint4*>(sb + off_vp1 + P8);
-    attn_softmax_pv(A, sacc, valid, lane, [&](int jg, uint32_t (&v)[2][4]) {
+    attn_softmax_pv(A, sacc, ndyn - base, lane, [&](int jg, uint32_t (&v)[2][4]) {
 #pragma unroll
       for (int pr = 0; pr < 2; ++pr) {
         const uint32_t pa[4] = {vp[2 * pr].x, vp[2 * pr].y, vp[2 * pr].z, vp[2 * pr].w};
@@ -366,23 +371,39 @@ __device__ __forceinline__ void attn_write_partial(const Attn& A, float* part, f
   }
 }
 
-// fixed-order merge of the nw partials (caller synchronises before)
-__device__ __forceinline__ void attn_merge(const float* part, const float* pm, const float* pl, int nw, int Gq,
-                                           int gtid, int gsize, float* out_u, float* lse_u) {
-  for (int e = gtid; e < Gq * FD; e += gsize) {
-    const int h = e / FD, d = e % FD;
+// fixed-order merge of the nw partials (caller synchronises before).  The per-(warp, head)
+// factors 2^(m_w - M) replace pm in place and the denominators replace pl[h] (one Grp sync).
+template <class Grp>
+__device__ __forceinline__ void attn_merge(const float* part, float* pm, float* pl, int nw, int Gq, int gtid,
+                                           int gsize, float* out_u, float* lse_u) {
+  if (gtid < Gq) {
+    const int h = gtid;
     float M = -INFINITY;
     for (int w = 0; w < nw; ++w) M = fmaxf(M, pm[w * Gq + h]);
-    float num = 0.f, den = 0.f;
+    float den = 0.f;
     for (int w = 0; w < nw; ++w) {
       const float mw = pm[w * Gq + h];
       const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
-      num += part[(w * Gq + h) * FD + d] * f;
       den += pl[w * Gq + h] * f;
+      pm[w * Gq + h] = f;
     }
-    out_u[h * FD + d] = num / den;
-    if (lse_u && d == 0) lse_u[h] = (M + log2f(den)) * 0.6931471805599453f;
+    pl[h] = den;
+    if (lse_u) lse_u[h] = (M + log2f(den)) * 0.6931471805599453f;
   }
+  Grp::sync();
+  for (int e = gtid; e < Gq * FD; e += gsize) {
+    const int h = e / FD, d = e % FD;
+    float num = 0.f;
+    for (int w = 0; w < nw; ++w) num += part[(w * Gq + h) * FD + d] * pm[w * Gq + h];
+    out_u[h * FD + d] = num / pl[h];
+  }
+}
+
+// pad the dynamic list [n, n rounded up to 16) with token 0 (masked in attention; it keeps
+// staging free of bounds checks).  Any thread may call it once n is known.
+__device__ __forceinline__ void pad_dyn(int32_t* dyn, int n, int tid) {
+  const int padded = (n + 15) & ~15;
+  if (tid < padded - n) dyn[n + tid] = 0;
 }
 
 }  // namespace sikv
@@ -492,14 +513,16 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
   const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
   const int Li = (int)g.L;
   const int end_s = g.nsc * g.sstride;
+  const uint4* pbase = signs + tid;
   auto load_batch = [&](int c0, uint4 (&w)[NB]) {
-    const int t0 = c0 * 256 + tid;
+    const uint4* p = pbase + (int64_t)c0 * 256;     // constant offsets 4 KiB apart: no per-load address math
     if ((c0 + NB) * 256 <= Li) {
 #pragma unroll
-      for (int x = 0; x < NB; ++x) w[x] = __ldg(signs + t0 + 256 * x);
+      for (int x = 0; x < NB; ++x) w[x] = __ldg(p + 256 * x);
     } else {
+      const int t0 = c0 * 256 + tid;
 #pragma unroll
-      for (int x = 0; x < NB; ++x) w[x] = t0 + 256 * x < Li ? __ldg(signs + t0 + 256 * x) : make_uint4(0, 0, 0, 0);
+      for (int x = 0; x < NB; ++x) w[x] = t0 + 256 * x < Li ? __ldg(p + 256 * x) : make_uint4(0, 0, 0, 0);
     }
   };
   for (int attempt = 0;; ++attempt) {
@@ -676,21 +699,29 @@ __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* si
   eq_count = ms->nsv;
 }
 
-// Exact k-th key among the candidate segments, then the gt / eq bitmaps (zeroed here).
+// Exact k-th key among the candidate segments: xk (relative to tau) and how many of the
+// items equal to it belong to the top keff.
 template <class Grp, class Xch = NoX>
-__device__ __forceinline__ void select_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
-                                                       uint32_t maxx, uint32_t tau, int* hist, Misc* ms,
-                                                       uint32_t* gt, uint32_t* eq, uint32_t& kstar,
-                                                       int& need_eq, int& eq_count, const Xch& xch = Xch()) {
+__device__ __forceinline__ void kth_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
+                                                    uint32_t maxx, int* hist, Misc* ms, uint32_t& xk,
+                                                    int& need_eq, const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const uint32_t* seg = cand + 2 * warp * g.capw;
   const int n = wcnt[warp];
-  uint32_t xk;
   maxx = xch.maxu(maxx);
   radix_kth<Grp, Xch>([&](auto f) {
     for (int i = lane; i < n; i += 32) f(seg[2 * i]);
   }, maxx, g.keff, hist, ms, xk, need_eq, xch);
-  kstar = xk + tau;
+}
+
+// gt / eq bitmaps (zeroed here) of the candidates above / at the k-th key xk
+template <class Grp>
+__device__ __forceinline__ void bitmaps_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
+                                                        uint32_t xk, Misc* ms, uint32_t* gt, uint32_t* eq,
+                                                        int& eq_count) {
+  const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
+  const uint32_t* seg = cand + 2 * warp * g.capw;
+  const int n = wcnt[warp];
   const int W = (int)((g.L + 31) >> 5);
   for (int i = tid; i < W; i += DT) { gt[i] = 0u; eq[i] = 0u; }
   if (tid == 0) ms->nsv = 0;
@@ -704,7 +735,53 @@ __device__ __forceinline__ void select_from_candidates(const UnitGeom& g, const 
   eq_count = ms->nsv;
 }
 
-// Ordered emission: dynamic list (smem) and the sorted selection (global, nullable).
+// Exact k-th key among the candidate segments, then the gt / eq bitmaps (zeroed here).
+template <class Grp, class Xch = NoX>
+__device__ __forceinline__ void select_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
+                                                       uint32_t maxx, uint32_t tau, int* hist, Misc* ms,
+                                                       uint32_t* gt, uint32_t* eq, uint32_t& kstar,
+                                                       int& need_eq, int& eq_count, const Xch& xch = Xch()) {
+  uint32_t xk;
+  kth_from_candidates<Grp, Xch>(g, cand, wcnt, maxx, hist, ms, xk, need_eq, xch);
+  kstar = xk + tau;
+  bitmaps_from_candidates<Grp>(g, cand, wcnt, xk, ms, gt, eq, eq_count);
+}
+
+// The dynamic list straight from the candidate segments, without bitmaps: every candidate
+// with x > xk plus the ties x == xk, in segment order (warp 0's segment first, each in
+// scan order — deterministic).  Valid only when every tie is taken; returns -1 when the
+// ties must be cut by token index (the caller then takes the bitmap path).
+template <class Grp>
+__device__ __forceinline__ int emit_from_segments(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
+                                                  uint32_t xk, int need_eq, int32_t* dyn, Misc* ms) {
+  const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
+  const uint32_t* seg = cand + 2 * warp * g.capw;
+  const int n = wcnt[warp];
+  int ngt = 0, neq = 0;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t x = seg[2 * i];
+    ngt += x > xk;
+    neq += x == xk;
+  }
+  ngt = warp_sum(ngt);
+  neq = warp_sum(neq);
+  int pos, epos, tot, etot;
+  block_exscan2<Grp>(lane == 0 ? ngt + neq : 0, lane == 0 ? neq : 0, pos, epos, tot, etot, ms->wsum);
+  if (etot != need_eq) return -1;
+  pad_dyn(dyn, tot, tid);
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  for (int b = 0; b < n; b += 32) {
+    const int i = b + lane;
+    const bool take = i < n && seg[2 * i] >= xk;
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (take) dyn[pos + __popc(m & ((1u << lane) - 1u))] = (int32_t)seg[2 * i + 1];
+    pos += __popc(m);
+  }
+  Grp::sync();
+  return tot;
+}
+
+// Ordered emission: dynamic list (smem, nullable) and the sorted selection (global, nullable).
 // Returns the dynamic count.
 template <class Grp>
 __device__ __forceinline__ int emit_selection(const UnitGeom& g, int mode, const uint32_t* forced,
@@ -749,11 +826,13 @@ __device__ __forceinline__ int emit_selection(const UnitGeom& g, int mode, const
   }
   int dpos, spos, dtot, stot;
   block_exscan2<Grp>(nd, nsl, dpos, spos, dtot, stot, ms->wsum);
+  if (dyn) pad_dyn(dyn, dtot, tid);
   eb = eq_before;
   for (int x = w0; x < w1; ++x) {
     uint32_t d = dbits(x, eb);
     uint32_t sb = d | forced[x];
-    while (d) { const int b = __ffs(d) - 1; d &= d - 1; dyn[dpos++] = x * 32 + b; }
+    if (dyn)
+      while (d) { const int b = __ffs(d) - 1; d &= d - 1; dyn[dpos++] = x * 32 + b; }
     if (sel_u)
       while (sb) { const int b = __ffs(sb) - 1; sb &= sb - 1; sel_u[spos++] = x * 32 + b; }
   }
@@ -762,6 +841,30 @@ __device__ __forceinline__ int emit_selection(const UnitGeom& g, int mode, const
   if (tid == 0 && sel_count_u) *sel_count_u = stot + R;
   Grp::sync();
   return dtot;
+}
+
+// Select + emit for a unit whose candidates sit in per-warp segments (mode >= 2, no
+// fallback): the exact k-th key, then the dynamic list from the segments.  The sorted
+// selection (sel_u / sel_count_u, optional) and the rare index-cut ties go through the
+// bitmaps.  Returns the dynamic count; kstar = absolute k-th key.
+template <class Grp>
+__device__ __forceinline__ int select_emit_candidates(const UnitGeom& g, const uint32_t* forced, const uint32_t* cand,
+                                                      const int* wcnt, uint32_t maxx, uint32_t tau, int* hist,
+                                                      Misc* ms, uint32_t* gt, uint32_t* eq, int32_t* dyn,
+                                                      int32_t* sel_u, int R, int32_t* sel_count_u, uint32_t& kstar) {
+  uint32_t xk;
+  int need_eq;
+  kth_from_candidates<Grp>(g, cand, wcnt, maxx, hist, ms, xk, need_eq);
+  kstar = xk + tau;
+  int ndyn = emit_from_segments<Grp>(g, cand, wcnt, xk, need_eq, dyn, ms);
+  if (ndyn < 0 || sel_u || sel_count_u) {
+    int eq_count;
+    bitmaps_from_candidates<Grp>(g, cand, wcnt, xk, ms, gt, eq, eq_count);
+    const int nd = emit_selection<Grp>(g, g.mode, forced, gt, eq, need_eq, eq_count, ndyn < 0 ? dyn : nullptr,
+                                       sel_u, R, sel_count_u, ms);
+    if (ndyn < 0) ndyn = nd;
+  }
+  return ndyn;
 }
 
 }  // namespace sikv

@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     }
     int dpos, spos, dtot, stot;
     block_exscan2<Cta256>(nd, nsl, dpos, spos, dtot, stot, ms->wsum);
+    pad_dyn(dyn, dtot, tid);
     if (tid == 0) slot->nsl = stot;
     ClusterX::csync();
     int soff = 0, sall = 0;
@@ -342,7 +343,7 @@ static SplitLayout split_layout(int64_t L, int k, int S, int Gq, int cap, int ns
   a.capw = std::max(32, cap / DW);
   // R0: pair table while scoring; then dyn | {hist, gt, eq} | later staging / partials
   a.off_dyn = 0;
-  int u0 = a128(std::max(keff, 1) * 4);
+  int u0 = a128((std::max(keff, 1) + 16) * 4);
   a.off_hist = u0;
   a.off_bits = a128(u0 + (NBIN + 64) * 4);
   const int sel_end = a.off_bits + 2 * W * 4;

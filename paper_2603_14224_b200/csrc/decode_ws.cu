@@ -18,6 +18,8 @@
 namespace sikv {
 
 constexpr int WS_THREADS = 512;
+__device__ long long* g_prof_ws = nullptr;   // optional per-unit phase clocks (profiling)
+__device__ int g_ws_skip = 0;                // debug: bit 0 skips attention, bit 1 skips scoring
 using PG = NamedGroup<1, 0>;
 using CG = NamedGroup<2, 256>;
 
@@ -102,7 +104,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
       float* qs = reinterpret_cast<float*>(slot + a.slot_q);
       float* ahat = reinterpret_cast<float*>(slot + a.slot_ahat);
       const int64_t u = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+      long long* prof = (g_prof_ws && u < a.U) ? g_prof_ws + u * 12 : nullptr;
+      const long long c0 = clock64();
       if (it >= 2) wait_empty(s);
+      if (prof && tid == 0) { prof[0] = c0; prof[1] = clock64(); }
       if (u >= a.U) {
         if (tid == 0) meta->unit = -1;
         __threadfence_block();
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
       }
       PG::sync();
       build_pair_rows<PG>(lut, T);
+      if (prof && tid == 0) prof[2] = clock64();
       prefetch(u + gridDim.x);       // next unit's inputs load while this unit streams
       int fb = 0, need_eq = 0, eq_count = 0;
       uint32_t tau = 1, kstar = 0;
@@ -153,6 +159,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
                             eq_count);
         }
       }
+      if (prof && tid == 0) prof[3] = clock64();
       if (tid == 0) {
         meta->unit = (int)u;
         meta->fb = fb;
@@ -185,26 +192,32 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
       const uint32_t* forced = reinterpret_cast<const uint32_t*>(slot + a.slot_forced);
       const float* qs = reinterpret_cast<const float*>(slot + a.slot_q);
       const float* ahat = reinterpret_cast<const float*>(slot + a.slot_ahat);
+      const long long c0 = clock64();
       wait_full(s);
       const int64_t u = meta->unit;
       if (u < 0) break;
+      long long* prof = g_prof_ws ? g_prof_ws + u * 12 : nullptr;
+      if (prof && tid == 0) { prof[4] = c0; prof[5] = clock64(); }
       const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
       const int mode = g.mode;
       uint32_t kstar = meta->kstar;
       int need_eq = meta->need_eq, eq_count = meta->eq_count;
-      if (mode >= 2) {
-        if (meta->fb) {             // the producer's exact path left the bitmaps in global memory
+      int32_t* sel_u = a.sel ? a.sel + u * a.sel_stride : nullptr;
+      int32_t* sel_count_u = a.sel_count ? a.sel_count + u : nullptr;
+      int ndyn;
+      if (mode >= 2 && !meta->fb) {
+        ndyn = select_emit_candidates<CG>(g, forced, cand, meta->wcnt, meta->maxx, meta->tau, hist, ms, gt, eq, dyn,
+                                          sel_u, R, sel_count_u, kstar);
+        if (prof && tid == 0) prof[6] = clock64();
+      } else {
+        if (mode >= 2) {            // the producer's exact path left the bitmaps in global memory
           const uint32_t* src = a.gbits + u * 2 * W;
           for (int i = tid; i < 2 * W; i += DT) (i < W ? gt[i] : eq[i - W]) = __ldcg(src + i);
           CG::sync();
-        } else {
-          select_from_candidates<CG>(g, cand, meta->wcnt, meta->maxx, meta->tau, hist, ms, gt, eq, kstar, need_eq,
-                                     eq_count);
         }
+        if (prof && tid == 0) prof[6] = clock64();
+        ndyn = emit_selection<CG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, R, sel_count_u, ms);
       }
-      const int ndyn = emit_selection<CG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn,
-                                          a.sel ? a.sel + u * a.sel_stride : nullptr, R,
-                                          a.sel_count ? a.sel_count + u : nullptr, ms);
       if (tid == 0 && a.diag) a.diag[u] = (mode & 3) | (meta->fb ? 4 : 0);
       Attn A;
       attn_init(A, qs, ahat, Gq, lane);
@@ -212,16 +225,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1) decode_ws_kernel(WsArgs a) {
       arrive_empty(s);
       const int nf = S + R;
       const int nbf = (nf + 15) >> 4;
+      if (prof && tid == 0) prof[7] = clock64();
+      if (!(g_ws_skip & 1)) {
       attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
       attn_dynamic(A, a.recs + u * L * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW, stage, lane);
+      }
       CG::sync();
+      if (prof && tid == 0) prof[8] = clock64();
       float* part = reinterpret_cast<float*>(creg);
       float* pm = part + DW * Gq * FD;
       float* pl = pm + DW * Gq;
       attn_write_partial(A, part, pm, pl, warp, Gq, lane);
       CG::sync();
-      attn_merge(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+      attn_merge<CG>(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
       CG::sync();                   // the region is reused by the next unit
+      if (prof && tid == 0) prof[9] = clock64();
     }
   }
 }
@@ -258,7 +276,7 @@ static WsLayout ws_layout(int64_t L, int k, int S, int Gq, int cap) {
   a.c_bits = co;
   co += a128(2 * W * 4);
   a.c_dyn = co;
-  co += a128(std::max(keff, 1) * 4);
+  co += a128((std::max(keff, 1) + 16) * 4);
   a.c_stage = co;
   co += DW * 2 * STAGE_BYTES;
   co = std::max(co, a128(DW * Gq * (FD + 2) * 4));
@@ -270,6 +288,8 @@ static WsLayout ws_layout(int64_t L, int k, int S, int Gq, int cap) {
 }
 
 int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap) { return ws_layout(L, k, S, Gq, cap).total; }
+cudaError_t set_decode_ws_profile(long long* p) { return cudaMemcpyToSymbol(g_prof_ws, &p, sizeof(p)); }
+cudaError_t set_decode_ws_skip(int v) { return cudaMemcpyToSymbol(g_ws_skip, &v, sizeof(v)); }
 size_t ws_workspace_bytes(int64_t U, int64_t L) { return 256 + (size_t)U * 2 * ((L + 31) / 32) * 4; }
 
 cudaError_t launch_decode_ws(const uint8_t* signs, const uint8_t* recs, const float* cent32, const float* alpha32,

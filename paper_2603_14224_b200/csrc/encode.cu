@@ -470,42 +470,39 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
         a.signs_fast[((int64_t)u * a.L + t) * FSIGN + pos] = (uint8_t)(code | (partner << 4));
       }
       uint32_t out = 0;
+      // K4 words 0-15: e2m1 nibbles (sign of K' at bit 3, magnitude code at bits 0-1)
 #pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        uint32_t ck = 0, cv = 0;
+      for (int w = 0; w < 16; ++w) {
+        uint32_t ck = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           int wd, bt;
-          kpay_pos(c0 + i, wd, bt);
-          if (wd == w) ck |= kc[i] << bt;
+          k4_pos(c0 + i, wd, bt);
+          if (wd == w) ck |= (kc[i] | (kp[i] < 0.0 ? 8u : 0u)) << bt;
+        }
+        ck = __reduce_or_sync(0xffffffffu, ck);
+        if (lane == w) out = ck;
+      }
+      // V payload words 16-23
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        uint32_t cv = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int wd, bt;
           vpay_pos(c0 + i, wd, bt);
           if (wd == w) cv |= vc[i] << bt;
         }
-        ck = __reduce_or_sync(0xffffffffu, ck);
         cv = __reduce_or_sync(0xffffffffu, cv);
-        if (lane == w) out = ck;
-        if (lane == 8 + w) out = cv;
+        if (lane == 16 + w) out = cv;
       }
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint32_t sg = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          int wd, bt;
-          ksgn_pos(c0 + i, wd, bt);
-          if (wd == w && kp[i] < 0.0) sg |= 1u << bt;   // 1 = negative
-        }
-        sg = __reduce_or_sync(0xffffffffu, sg);
-        if (lane == 24 + w) out = sg;
-      }
-      // params: group j lives on lanes 8j..8j+7
-      uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
+      // params: group j lives on lanes 8j..8j+7; K params carry 2 qs
+      uint32_t kpar = (uint32_t)__half_as_ushort(__hadd(kqs, kqs)) | ((uint32_t)__half_as_ushort(kzp) << 16);
       uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
-      uint32_t kpj = __shfl_sync(0xffffffffu, kpar, ((lane - 16) & 3) * 8);
-      uint32_t vpj = __shfl_sync(0xffffffffu, vpar, ((lane - 20) & 3) * 8);
-      if (lane >= 16 && lane < 20) out = kpj;
-      if (lane >= 20 && lane < 24) out = vpj;
-      if (lane >= 28) out = 0;
+      uint32_t kpj = __shfl_sync(0xffffffffu, kpar, ((lane - 24) & 3) * 8);
+      uint32_t vpj = __shfl_sync(0xffffffffu, vpar, ((lane - 28) & 3) * 8);
+      if (lane >= 24 && lane < 28) out = kpj;
+      if (lane >= 28) out = vpj;
       reinterpret_cast<uint32_t*>(a.recs_fast + ((int64_t)u * a.L + t) * FREC)[lane] = out;
     }
   }
@@ -738,9 +735,9 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         auto kemit = [&](int n, uint32_t c) {
           kref[n / PER] |= c << (BITS * (n % PER));
           if constexpr (BITS == 2) {
-            // channel 32j + n -> word 2*t4(n) + (j >> 1), bit 8(j&1) + 4(n>>4) + 2e(n) + 16hi(n)
+            // channel 32j + n -> K4 word 4 t4(n) + j, nibble at bit 16(n>>4) + 8e(n) + 4hi(n)
             const int r = n & 15, e = r >> 3, rr = r & 7;
-            kp4[rr >> 1] |= c << (4 * (n >> 4) + 2 * e + 16 * (rr & 1));
+            kp4[rr >> 1] |= c << (16 * (n >> 4) + 8 * e + 4 * (rr & 1));
           }
         };
         double kmx;
@@ -794,32 +791,20 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
         const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
         const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
-        uint32_t sg4[4] = {0, 0, 0, 0};
+        // K4 nibbles: bit 3 = sign of K' (1 = negative), bits 0-1 = magnitude code
   #pragma unroll
         for (int n = 0; n < 32; ++n) {
           const int r = n & 15, e = r >> 3, rr = r & 7;
-          sg4[rr >> 1] |= ((negw >> n) & 1u) << ((((n >> 4) << 1) | e) + 16 * (rr & 1));
-        }
-        // K payload words 2*t4 + u (u = j >> 1): combine the two groups of this u (lanes j, j^1)
-  #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t mine = kp4[q] << (8 * (j & 1));
-          kp4[q] = mine | __shfl_xor_sync(0xffffffffu, mine, 1);
+          kp4[rr >> 1] |= ((negw >> n) & 1u) << (16 * (n >> 4) + 8 * e + 4 * (rr & 1) + 3);
         }
         // V payload words g: byte j of every word comes from group j
   #pragma unroll
         for (int q = 0; q < 8; ++q) vp8[q] = or4(vp8[q] << (8 * j));
-        // K sign words t4: bit 8u + i + 16hi, u = j >> 1, i = (2(j&1) + (n>>4)) << 1 | e
-  #pragma unroll
-        for (int q = 0; q < 4; ++q) sg4[q] = or4(sg4[q] << (8 * (j >> 1) + 4 * (j & 1)));
-        const uint32_t kpar = (uint32_t)__half_as_ushort(kqs) | ((uint32_t)__half_as_ushort(kzp) << 16);
+        // K params carry 2 qs (the e2m1 nibble decodes to sign * code / 2); exact in fp16
+        const uint32_t kpar = (uint32_t)__half_as_ushort(__hadd(kqs, kqs)) | ((uint32_t)__half_as_ushort(kzp) << 16);
         const uint32_t vpar = (uint32_t)__half_as_ushort(vqs) | ((uint32_t)__half_as_ushort(vzp) << 16);
-        // record words: 0-7 K payload, 8-15 V payload, 16-19 K params, 20-23 V params, 24-27 K signs;
-        // thread j writes K words 4(j&1) + (j>>1) and 4(j&1) + 2 + (j>>1), V words 8 + 2j, 9 + 2j,
-        // and words 16 + j, 20 + j, 24 + j, 28 + j
-        auto pick4 = [](const uint32_t (&v)[4], int i) {
-          return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
-        };
+        // record words: 0-15 K4 (thread j: words 4 t4 + j), 16-23 V payload (thread j: 16 + 2j,
+        // 17 + 2j), 24-27 K params, 28-31 V params
         auto pick8 = [](const uint32_t (&v)[8], int i) {
           uint32_t r = v[0];
   #pragma unroll
@@ -829,15 +814,12 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         if (valid) {
           reinterpret_cast<uint32_t*>(a.signs_fast + tok * FSIGN)[j] = rw;
           uint32_t* rec = reinterpret_cast<uint32_t*>(a.recs_fast + tok * FREC);
-          const int uu = j >> 1;
-          rec[4 * (j & 1) + uu] = pick4(kp4, 2 * (j & 1));
-          rec[4 * (j & 1) + 2 + uu] = pick4(kp4, 2 * (j & 1) + 1);
-          rec[8 + 2 * j] = pick8(vp8, 2 * j);
-          rec[9 + 2 * j] = pick8(vp8, 2 * j + 1);
-          rec[16 + j] = kpar;
-          rec[20 + j] = vpar;
-          rec[24 + j] = pick4(sg4, j);
-          rec[28 + j] = 0u;
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) rec[4 * q + j] = kp4[q];
+          rec[16 + 2 * j] = pick8(vp8, 2 * j);
+          rec[17 + 2 * j] = pick8(vp8, 2 * j + 1);
+          rec[24 + j] = kpar;
+          rec[28 + j] = vpar;
         }
       }
     }

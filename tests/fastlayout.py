@@ -1,27 +1,18 @@
 """numpy inverse of the fast HBM layout (test helper): fast planes -> reference planes.
 
-Mirrors the permutations in paper_2603_14224_b200/csrc/common.cuh (kpay_pos, vpay_pos,
-ksgn_pos) and the rotated sign plane, so the tests can check the fast layout bit-exactly
-against the oracle's reference-layout planes.
+Mirrors the permutations in paper_2603_14224_b200/csrc/common.cuh (k4_pos, vpay_pos) and
+the rotated sign plane, so the tests can check the fast layout bit-exactly against the
+oracle's reference-layout planes.
 """
 
 import numpy as np
 
 
-def kpay_pos(ch):
-    s, r = ch >> 4, ch & 15
-    e, rr = (r >> 3) & 1, r & 7
-    t4, hi = rr >> 1, rr & 1
-    u, i = s >> 2, ((s & 3) << 1) | e
-    return 2 * t4 + u, 2 * i + 16 * hi
-
-
-def ksgn_pos(ch):
-    s, r = ch >> 4, ch & 15
-    e, rr = (r >> 3) & 1, r & 7
-    t4, hi = rr >> 1, rr & 1
-    u, i = s >> 2, ((s & 3) << 1) | e
-    return t4, 8 * u + i + 16 * hi
+def k4_pos(ch):
+    """K nibble (e2m1: sign at bit 3, code at bits 0-1) of channel ch: (word, bit)."""
+    j, n = ch >> 5, ch & 31
+    ss, e, rr = n >> 4, (n >> 3) & 1, n & 7
+    return 4 * (rr >> 1) + j, 16 * ss + 8 * e + 4 * (rr & 1)
 
 
 def vpay_pos(ch):
@@ -42,20 +33,24 @@ def unrotate_signs(signs_fast: np.ndarray) -> np.ndarray:
 
 def records_to_reference(recs: np.ndarray):
     """[L, 128] u8 records -> (kq codes [L,128], vq codes [L,128], kpar [L,4,2] u16,
-    vpar [L,4,2] u16, negative-sign mask [L,128] bool)."""
+    vpar [L,4,2] u16, negative-sign mask [L,128] bool).  K params are stored as (2 qs, zp)."""
     w = recs.view(np.uint32)           # [L, 32]
     L = recs.shape[0]
     kc = np.empty((L, 128), np.uint8)
     vc = np.empty((L, 128), np.uint8)
     neg = np.empty((L, 128), bool)
     for ch in range(128):
-        wd, bt = kpay_pos(ch)
-        kc[:, ch] = (w[:, wd] >> bt) & 3
+        wd, bt = k4_pos(ch)
+        nib = (w[:, wd] >> bt) & 15
+        assert ((nib & 4) == 0).all()
+        kc[:, ch] = nib & 3
+        neg[:, ch] = (nib & 8).astype(bool)
         wd, bt = vpay_pos(ch)
-        vc[:, ch] = (w[:, 8 + wd] >> bt) & 3
-        wd, bt = ksgn_pos(ch)
-        neg[:, ch] = ((w[:, 24 + wd] >> bt) & 1).astype(bool)
-    kpar = recs[:, 64:80].copy().view(np.uint16).reshape(L, 4, 2)
-    vpar = recs[:, 80:96].copy().view(np.uint16).reshape(L, 4, 2)
-    assert (w[:, 28:] == 0).all()
+        vc[:, ch] = (w[:, 16 + wd] >> bt) & 3
+    kp = recs[:, 96:112].copy().view(np.uint16).reshape(L, 4, 2)
+    qs2 = kp[..., 0].view(np.float16)
+    kpar = kp.copy()
+    kpar[..., 0] = (qs2 / np.float16(2)).astype(np.float16).view(np.uint16)
+    assert (kpar[..., 0].view(np.float16) * np.float16(2) == qs2).all()
+    vpar = recs[:, 112:128].copy().view(np.uint16).reshape(L, 4, 2)
     return kc, vc, kpar, vpar, neg
