@@ -67,15 +67,26 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
 #define PROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
   PROF(0);
   const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
+  // every small per-unit input is in flight at once, before any shared-memory step
+  float pq[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) pq[i] = tid + DT * i < Gq * FD ? a.q[u * Gq * FD + tid + DT * i] : 0.f;
+  const float pal = tid < FD ? a.alpha32[u * FD + tid] : 0.f;
+  const float4* c4 = reinterpret_cast<const float4*>(a.cent32 + u * 32 * 16 * 4);
+  const float4 pc0 = c4[tid], pc1 = c4[tid + DT];
+  const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
   uint4 wsamp[MAX_SAMPLE_CHUNKS];      // the sample's loads overlap the setup below
   load_sample(g, signs, tid, wsamp);
 
   // ---------------- A: queries, LUT, pair table, forced bitmap
-  for (int i = tid; i < Gq * FD; i += DT) qs[i] = a.q[u * Gq * FD + i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (tid + DT * i < Gq * FD) qs[tid + DT * i] = pq[i];
   for (int i = tid; i < W; i += DT) forced[i] = 0u;
   if (tid == 0) ms->fb = 0;
   __syncthreads();
-  for (int j = tid; j < S; j += DT) {
+  if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
+  for (int j = tid + DT; j < S; j += DT) {
     const int t = a.sink_idx[u * S + j];
     atomicOr(&forced[t >> 5], 1u << (t & 31));
   }
@@ -83,12 +94,20 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
     float s = qs[tid];
     for (int h = 1; h < Gq; ++h) s = __fadd_rn(s, qs[h * FD + tid]);
     qbar[tid] = s;
-    const float al = a.alpha32[u * FD + tid];
-    ahat[tid] = al > 0.f ? al : 1.0f;
+    ahat[tid] = pal > 0.f ? pal : 1.0f;
     inva[tid] = 1.0f / ahat[tid];
   }
   __syncthreads();
-  build_pair_table<Cta256>(a.cent32 + u * 32 * 16 * 4, qbar, lut, T);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int e = tid + DT * r, gg = e >> 4;
+    const float4 c = r ? pc1 : pc0;
+    const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
+    lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                                        __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+  }
+  __syncthreads();
+  build_pair_rows<Cta256>(lut, T);
   PROF(1);
 
   // ---------------- B/C: candidates, exact k-th key, tie-aware bitmaps
@@ -177,7 +196,7 @@ __global__ void score_fast_kernel(const uint8_t* __restrict__ signs_, const floa
   }
   __syncthreads();
   const uint4* signs = reinterpret_cast<const uint4*>(signs_ + u * L * FSIGN);
-  const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
+  const RepKey lb(lane);
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + tid; t < L; t += (int64_t)gridDim.x * blockDim.x)
     out[u * L + t] = score_token(__ldg(signs + t), lb, T);
 }

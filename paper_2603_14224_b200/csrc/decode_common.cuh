@@ -28,6 +28,22 @@ __device__ __forceinline__ void build_pair_rows(const float* lutT, char* T) {
   Grp::sync();
 }
 
+// 32-column variant (ColKey): T[b][16 h + p] (two copies, row stride 256 B; the caller
+// offsets T by 128 B for the second buffer).  Lanes 16-31 write the other copy first, so
+// both stores of a warp hit 32 distinct banks.
+template <class Grp>
+__device__ __forceinline__ void build_pair_rows_col(const float* lutT, char* T) {
+  const int tid = Grp::tid();
+  const int p = tid & 15, hh = (tid >> 4) & 1;
+  for (int b = tid >> 4; b < 256; b += DT / 16) {
+    const float v = __fadd_rn(lutT[(b & 15) * 32 + 2 * p], lutT[(b >> 4) * 32 + 2 * p + 1]);
+    float* row = reinterpret_cast<float*>(T) + b * 64;
+    row[p + 16 * hh] = v;
+    row[p + 16 * (1 - hh)] = v;
+  }
+  Grp::sync();
+}
+
 template <class Grp>
 __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent, const float* qbar, float* lut,
                                                  char* T) {
@@ -44,16 +60,49 @@ __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent,
 }
 
 // ---------------------------------------------------------------- scoring
-// score of the token whose 16-byte rotated sign record is w; lb = byte offset of this
-// lane's first column (64*half + 4*j); T = pair table (row stride 256 B).  Pairs are
-// summed left to right starting at pair (t mod 16) — the order oracle/restate32.py states.
-__device__ __forceinline__ float score_token(const uint4 w, uint32_t lb, const char* T) {
+// A lane's table addressing.  RepKey: the 64-column table of build_pair_rows (pair p
+// replicated at columns p, p+16, p+32), the lane's column at step i is lb + i (folded into
+// the LDS immediate).  ColKey: the 32-column table of build_pair_rows_col (two copies of the
+// 16 pairs, one per half warp); a row stride of 256 B leaves room for a second buffer, so
+// two tables interleave in one 64 KiB region.  The lane's 16 column offsets (pair (j+i) mod
+// 16 of its half-warp copy) sit in 4 registers and the PRMT that extracts the sign byte also
+// picks the column byte (sign-replicating selectors zero the high bytes: offsets < 128).
+// Both are bank-conflict free: the 32 lanes of a step hit 32 distinct columns mod 32.
+struct RepKey {
+  uint32_t lb;
+  __device__ __forceinline__ explicit RepKey(int lane) : lb((uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15))) {}
+  __device__ __forceinline__ uint32_t off(uint32_t w, int i) const {
+    return prmt(w, lb, 0x5504u | ((uint32_t)(i & 3) << 4)) + 4 * i;
+  }
+};
+struct ColKey {
+  uint32_t c[4];
+  __device__ __forceinline__ explicit ColKey(int lane) {
+    const int h = (lane >> 4) & 1, j = lane & 15;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) v |= (uint32_t)(4 * (16 * h + ((j + 4 * k + m) & 15))) << (8 * m);
+      c[k] = v;
+    }
+  }
+  __device__ __forceinline__ uint32_t off(uint32_t w, int i) const {
+    const uint32_t m = (uint32_t)(i & 3);
+    return prmt(w, c[i >> 2], (4u + m) | (m << 4) | ((12u + m) << 8) | ((12u + m) << 12));
+  }
+};
+
+// score of the token whose 16-byte rotated sign record is w; T = pair table (row stride
+// 256 B).  Pairs are summed left to right starting at pair (t mod 16) — the order
+// oracle/restate32.py states.
+template <class Key>
+__device__ __forceinline__ float score_token(const uint4 w, const Key& key, const char* T) {
   const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const uint32_t off = prmt(ww[i >> 2], lb, 0x5504u | ((uint32_t)(i & 3) << 4));
-    const float v = *reinterpret_cast<const float*>(T + off + 4 * i);
+    const float v = *reinterpret_cast<const float*>(T + key.off(ww[i >> 2], i));
     s = (i == 0) ? v : __fadd_rn(s, v);
   }
   return s;
@@ -76,8 +125,8 @@ __device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& 
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
 
-template <int N>
-__device__ __forceinline__ void score_batch(const uint4 (&w)[N], uint32_t lb, const char* T, float (&s)[N]) {
+template <int N, class Key>
+__device__ __forceinline__ void score_batch(const uint4 (&w)[N], const Key& key, const char* T, float (&s)[N]) {
   static_assert(N % 2 == 0, "tokens are scored in pairs");
   unsigned long long acc[N / 2];
 #pragma unroll
@@ -87,9 +136,8 @@ __device__ __forceinline__ void score_batch(const uint4 (&w)[N], uint32_t lb, co
       const uint32_t w0 = (i >> 2) == 0 ? w[x].x : (i >> 2) == 1 ? w[x].y : (i >> 2) == 2 ? w[x].z : w[x].w;
       const uint32_t w1 = (i >> 2) == 0 ? w[x + 1].x : (i >> 2) == 1 ? w[x + 1].y : (i >> 2) == 2 ? w[x + 1].z
                                                                                                : w[x + 1].w;
-      const uint32_t sel = 0x5504u | ((uint32_t)(i & 3) << 4);
-      const float v0 = *reinterpret_cast<const float*>(T + prmt(w0, lb, sel) + 4 * i);
-      const float v1 = *reinterpret_cast<const float*>(T + prmt(w1, lb, sel) + 4 * i);
+      const float v0 = *reinterpret_cast<const float*>(T + key.off(w0, i));
+      const float v1 = *reinterpret_cast<const float*>(T + key.off(w1, i));
       const unsigned long long v = pack2(v0, v1);
       acc[x / 2] = (i == 0) ? v : fadd2(acc[x / 2], v);
     }
@@ -463,13 +511,13 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
 // the scan is repeated (at most kRetries times) before falling back to the exact path.
 constexpr int kRetries = 2;
 
-template <class Grp, class Xch = NoX>
+template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
                                                    uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
                                                    uint32_t& tau_out, const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
-  const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
+  const Key lb(lane);
   const int capw = g.capw;
   uint32_t* seg = cand + 2 * warp * capw;
   uint32_t sk[MAX_SAMPLE_CHUNKS];
@@ -514,15 +562,15 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
   const int Li = (int)g.L;
   const int end_s = g.nsc * g.sstride;
   const uint4* pbase = signs + tid;
-  auto load_batch = [&](int c0, uint4 (&w)[NB]) {
+  auto load_batch = [&](int c0, uint4 (&w)[NBT]) {
     const uint4* p = pbase + (int64_t)c0 * 256;     // constant offsets 4 KiB apart: no per-load address math
-    if ((c0 + NB) * 256 <= Li) {
+    if ((c0 + NBT) * 256 <= Li) {
 #pragma unroll
-      for (int x = 0; x < NB; ++x) w[x] = __ldg(p + 256 * x);
+      for (int x = 0; x < NBT; ++x) w[x] = __ldg(p + 256 * x);
     } else {
       const int t0 = c0 * 256 + tid;
 #pragma unroll
-      for (int x = 0; x < NB; ++x) w[x] = t0 + 256 * x < Li ? __ldg(p + 256 * x) : make_uint4(0, 0, 0, 0);
+      for (int x = 0; x < NBT; ++x) w[x] = t0 + 256 * x < Li ? __ldg(p + 256 * x) : make_uint4(0, 0, 0, 0);
     }
   };
   for (int attempt = 0;; ++attempt) {
@@ -598,28 +646,28 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     const float tauf = g.mode == 2 ? -INFINITY : __uint_as_float(unkey_bits(tau));
     int next_s = g.mode == 3 ? 0 : 0x7fffffff;      // next sample chunk (already scored in B1)
     // register double buffer: the loads of batch c0 + NB are in flight while batch c0 scores
-    uint4 wn[NB];
+    uint4 wn[NBT];
     load_batch(0, wn);
-    for (int c0 = 0; c0 < g.nchunks; c0 += NB) {
+    for (int c0 = 0; c0 < g.nchunks; c0 += NBT) {
       int xs = -1;
-      if (next_s < c0 + NB && next_s < end_s) { xs = next_s - c0; next_s += g.sstride; }
+      if (next_s < c0 + NBT && next_s < end_s) { xs = next_s - c0; next_s += g.sstride; }
       const int t0 = c0 * 256 + tid;
-      const bool full = (c0 + NB) * 256 <= Li;
-      uint4 w[NB];
+      const bool full = (c0 + NBT) * 256 <= Li;
+      uint4 w[NBT];
 #pragma unroll
-      for (int x = 0; x < NB; ++x) w[x] = wn[x];
-      if (c0 + NB < g.nchunks) load_batch(c0 + NB, wn);
-      float sv[NB];
+      for (int x = 0; x < NBT; ++x) w[x] = wn[x];
+      if (c0 + NBT < g.nchunks) load_batch(c0 + NBT, wn);
+      float sv[NBT];
       score_batch(w, lb, T, sv);
       uint32_t bits = 0;
 #pragma unroll
-      for (int x = 0; x < NB; ++x)
+      for (int x = 0; x < NBT; ++x)
         if (sv[x] >= tauf) bits |= 1u << x;
       if (xs >= 0) bits &= ~(1u << xs);
-      if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NB ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
+      if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NBT ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
       if (c0 * 256 < g.flim) {
 #pragma unroll
-        for (int x = 0; x < NB; ++x)
+        for (int x = 0; x < NBT; ++x)
           if (t0 + 256 * x < Li && forced_bit(forced, t0 + 256 * x)) bits &= ~(1u << x);
       }
       // warp-compacted append: one scan per batch
@@ -637,7 +685,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
         bits &= bits - 1;
         float v = sv[0];
 #pragma unroll
-        for (int y = 1; y < NB; ++y) v = (x == y) ? sv[y] : v;
+        for (int y = 1; y < NBT; ++y) v = (x == y) ? sv[y] : v;
         const uint32_t xk = f32_key(v) - tau;
         if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(t0 + 256 * x); }
         mx = max(mx, xk);
@@ -666,13 +714,13 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
 
 // Exact fallback: multi-pass radix select over rescored keys, then gt / eq bitmaps (zeroed
 // here; smem or global) of key > K* and key == K*.  hist needs NBIN + 33 ints.
-template <class Grp, class Xch = NoX>
+template <class Grp, class Xch = NoX, class Key = RepKey>
 __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* signs, const char* T,
                                               const uint32_t* forced, int* hist, Misc* ms, uint32_t* gt,
                                               uint32_t* eq, uint32_t& kstar, int& need_eq, int& eq_count,
                                               const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31;
-  const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
+  const Key lb(lane);
   const int64_t L = g.L;
   const int nchunks = g.nchunks;
   radix_kth<Grp, Xch>([&](auto f) {
