@@ -62,7 +62,8 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML every 10 ms during the timed
+    region (nvidia-smi fallback when pynvml is missing)."""
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -71,7 +72,20 @@ class ClockSampler:
         self._t = None
 
     def __enter__(self):
-        def run():
+        def run_nvml(pynvml):
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [0x8, 0x40, 0x20, 0x4]   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append([sm, mx] + ["active" if r & b else "" for b in bits])
+                except Exception:
+                    pass
+                self._stop.wait(0.01)
+
+        def run_smi():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap")
@@ -84,8 +98,15 @@ class ClockSampler:
                         self.samples.append([x.strip() for x in out.split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
+                self._stop.wait(0.05)
+
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            target = lambda: run_nvml(pynvml)  # noqa: E731
+        except Exception:
+            target = run_smi
+        self._t = threading.Thread(target=target, daemon=True)
         self._t.start()
         return self
 
@@ -99,9 +120,25 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = sorted(int(float(s[0])) for s in self.samples)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if str(s[2 + i]).lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(float(self.samples[0][1])),
                 "reasons": reasons, "samples": len(sm)}
+
+
+def ncu_traffic(config: str):
+    """DRAM bytes (read + write) per launch of the decode kernel from the committed ncu
+    capture of this configuration (profiles/*/ncu_<config>_summary.json), or None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{config}_summary.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            best = {"bytes": int(d["dram_bytes_read"]) + int(d["dram_bytes_write"]), "kernel": d.get("kernel"),
+                    "source": os.path.relpath(path, ROOT)}
+        except Exception:
+            pass
+    return best
 
 
 # ------------------------------------------------------------------------------- GPU arm
@@ -243,6 +280,7 @@ def run_ours(args, rank, world, cfg):
     peak, peak_kind = peaks()
     bytes_step = algo_bytes_per_unit(L, k, gq) * ul
     achieved = bytes_step / (kern_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.config) if world == 1 else None
     line = {
         "metric": "decode steps/sec + HBM roofline fraction, Llama-3-8B geometry, 32K ctx",
         "value": round(1000.0 / ms, 3),
@@ -262,7 +300,9 @@ def run_ours(args, rank, world, cfg):
                    "l2": "inputs > L2 (19 GB of compressed planes per GPU-step at C2)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "traffic": None, "algo_bytes_per_launch": bytes_step,
+                     "traffic": traffic["bytes"] if traffic else None,
+                     "traffic_source": traffic["source"] if traffic else None,
+                     "algo_bytes_per_launch": bytes_step,
                      "kernel_ms": round(kern_ms, 5)},
         "e2e": {"value": round(1000.0 / e2e_ms, 3), "unit": "decode steps/s",
                 "h2d_bytes_per_step": int(qh.numel() * qh.element_size()),
@@ -387,7 +427,7 @@ def _cpu_model():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -12,7 +12,8 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsikv_b200.so")
+# SIKV_LIB names an alternative in-tree build (A/B experiments); default: the shipped library
+LIB_PATH = os.path.join(HERE, os.environ.get("SIKV_LIB", "libsikv_b200.so"))
 
 IN_F32, IN_F64, IN_BF16 = 0, 1, 2
 _DT = {torch.float32: IN_F32, torch.float64: IN_F64, torch.bfloat16: IN_BF16}

@@ -248,9 +248,9 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
     while (cap <= 0 && wcap > floor_cap && ws_smem_bytes(tokens, k, sinks, gq, wcap) > max_smem()) wcap -= 64;
     const bool fits = ws_smem_bytes(tokens, k, sinks, gq, wcap) <= max_smem();
-    // auto: the persistent kernel wins for many short units (C4: 8K tokens); for long
-    // units the one-CTA-per-unit kernel (two co-resident CTAs per SM) is faster (C2)
-    if (fits && (kernel == 2 || (units >= 2 * num_sms() && tokens < 16384))) {
+    // auto never picks the persistent kernel: the one-CTA-per-unit kernel (two co-resident
+    // CTAs per SM) measured faster at C2 (32K tokens) and C4 (8K tokens); kernel = 2 forces it
+    if (fits && kernel == 2) {
       return cuda_ret(launch_decode_ws(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                        frag_blocks, recent, q, units, tokens, gq, k, wcap, out, lse, sel,
                                        sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),

@@ -23,6 +23,10 @@
 
 namespace sikv {
 
+#ifndef SIKV_K1_STAGES
+#define SIKV_K1_STAGES 2
+#endif
+constexpr int K1_STAGES = SIKV_K1_STAGES;             // cp.async stages per warp in the attention phase
 __device__ long long* g_prof = nullptr;   // optional per-unit phase clocks (debug / profiling)
 
 struct DecodeArgs {
@@ -150,8 +154,8 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   const int nbf = (nf + 15) >> 4;
   attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
   PROF(6);
-  attn_dynamic(A, a.recs + u * L * FREC, reinterpret_cast<const int32_t*>(sm + a.off_dyn), ndyn,
-               (warp - nbf % DW + DW) % DW, DW, sm + a.off_stage + warp * 2 * STAGE_BYTES, lane);
+  attn_dynamic<K1_STAGES>(A, a.recs + u * L * FREC, reinterpret_cast<const int32_t*>(sm + a.off_dyn), ndyn,
+                          (warp - nbf % DW + DW) % DW, DW, sm + warp * K1_STAGES * STAGE_BYTES, lane);
   PROF(7);
   // ---------------- merge the 8 warp partials (fixed order)
   __syncthreads();
@@ -209,11 +213,13 @@ DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap) {
   const int W = (int)((L + 31) / 32);
   const int keff = (int)std::max<int64_t>(0, std::min<int64_t>(k, L - S));
   d.capw = std::max(32, cap / DW);
-  // R0: pair table while scoring; afterwards hist | gt | eq | dynamic list | staging
+  // R0: pair table while scoring; then hist | gt | eq (selection) ... dynamic list at the
+  // end; during attention the staging buffers (K1_STAGES per warp) overlay hist / gt / eq
   d.off_bits = align128(NBIN * 4);
-  d.off_dyn = align128(d.off_bits + 2 * W * 4);
-  d.off_stage = align128(d.off_dyn + (std::max(keff, 1) + 16) * 4);
-  const int r0 = std::max(TBL_BYTES, d.off_stage + DW * 2 * STAGE_BYTES);
+  const int stage_end = DW * K1_STAGES * STAGE_BYTES;
+  d.off_dyn = align128(std::max(d.off_bits + 2 * W * 4, stage_end));
+  d.off_stage = 0;
+  const int r0 = std::max(TBL_BYTES, align128(d.off_dyn + (std::max(keff, 1) + 16) * 4));
   // R1: per-warp candidate segments; at other times the tau histogram, the fallback
   // histogram + bitmaps, and the attention partials
   int r1 = DW * d.capw * 8;

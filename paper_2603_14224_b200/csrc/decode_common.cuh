@@ -154,6 +154,35 @@ __device__ __forceinline__ uint32_t unkey_bits(uint32_t k2) {
   return (k2 & 0x80000000u) ? (k2 & 0x7FFFFFFFu) : ~k2;
 }
 
+// f32_key in three instructions: x + 0 turns -0 into +0 (round-to-nearest), then the sign
+// mask flips the negatives and sets the top bit of the positives
+__device__ __forceinline__ uint32_t f32_key_fast(float x) {
+  const uint32_t u = __float_as_uint(__fadd_rn(x, 0.0f));
+  return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
+
+// v[x] for a run-time x in [0, N): a select tree on the bits of x (N = 4 or 8)
+template <int N>
+__device__ __forceinline__ float pick_dyn(const float (&v)[N], int x) {
+  static_assert(N == 4 || N == 8, "pick_dyn supports 4 or 8 values");
+  const bool b0 = x & 1, b1 = x & 2;
+  const float a01 = b0 ? v[1] : v[0], a23 = b0 ? v[3] : v[2];
+  const float lo = b1 ? a23 : a01;
+  if constexpr (N == 4) {
+    return lo;
+  } else {
+    const float a45 = b0 ? v[5] : v[4], a67 = b0 ? v[7] : v[6];
+    const float hi = b1 ? a67 : a45;
+    return (x & 4) ? hi : lo;
+  }
+}
+
+// predicated 8-byte shared-memory store (no branch)
+__device__ __forceinline__ void st_shared_v2_if(bool p, uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.shared.v2.u32 [%1], {%2, %3}; }"
+               ::"r"((uint32_t)p), "r"(addr), "r"(a), "r"(b));
+}
+
 // ---------------------------------------------------------------- async staging
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
@@ -303,11 +332,12 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
   }
 }
 
-// dynamic rows: blocks first, first + nw, ... of [0, nbd), staged by cp.async (double
-// buffered) and dequantised into mma fragments.  The list is padded to a multiple of 16
+// dynamic rows: blocks first, first + nw, ... of [0, nbd), staged by cp.async (NSTAGE
+// buffers per warp: NSTAGE - 1 blocks in flight) and dequantised into mma fragments.  The list is padded to a multiple of 16
 // (pad_dyn), so staging needs no bounds.  Every lane's shared-memory offsets are fixed for
 // the whole unit (16-byte chunk k of token j lives at chunk k ^ (j & 7)), so they are
 // computed once; token g and g + 8 (and 2t4 + x and 2t4 + x + 8) differ by 1 KiB.
+template <int NSTAGE = 2>
 __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, const int32_t* dyn, int ndyn,
                                              int first, int nw, char* stage, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
@@ -339,13 +369,17 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   const int off_vp0 = jv0 * FREC + 16 * (7 ^ stage_sw(jv0));
   const int off_vp1 = jv1 * FREC + 16 * (7 ^ stage_sw(jv1));
   constexpr int P8 = 8 * FREC;
-  if (first < nbd) stage_blk(0, first * 16);
-  cp_commit();
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (first + s * nw < nbd) stage_blk(s * STAGE_BYTES, (first + s * nw) * 16);
+    cp_commit();
+  }
   int buf = 0;
   for (int db = first; db < nbd; db += nw) {
-    if (db + nw < nbd) stage_blk((buf ^ 1) * STAGE_BYTES, (db + nw) * 16);
+    const int nx = db + (NSTAGE - 1) * nw;
+    if (nx < nbd) stage_blk(((buf + NSTAGE - 1) % NSTAGE) * STAGE_BYTES, nx * 16);
     cp_commit();
-    cp_wait<1>();
+    cp_wait<NSTAGE - 1>();
     __syncwarp();
     const char* sb = stage + buf * STAGE_BYTES;
     const int base = db * 16;
@@ -398,7 +432,7 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
       }
     });
     __syncwarp();
-    buf ^= 1;
+    buf = buf + 1 == NSTAGE ? 0 : buf + 1;
   }
   cp_wait<0>();
 }
@@ -645,6 +679,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     // ---------------- B2: score everything else, keep score >= tau (compared as floats)
     const float tauf = g.mode == 2 ? -INFINITY : __uint_as_float(unkey_bits(tau));
     int next_s = g.mode == 3 ? 0 : 0x7fffffff;      // next sample chunk (already scored in B1)
+    const uint32_t segs = (uint32_t)__cvta_generic_to_shared(seg);
     // register double buffer: the loads of batch c0 + NB are in flight while batch c0 scores
     uint4 wn[NBT];
     load_batch(0, wn);
@@ -683,11 +718,8 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       while (bits) {
         const int x = __ffs(bits) - 1;
         bits &= bits - 1;
-        float v = sv[0];
-#pragma unroll
-        for (int y = 1; y < NBT; ++y) v = (x == y) ? sv[y] : v;
-        const uint32_t xk = f32_key(v) - tau;
-        if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(t0 + 256 * x); }
+        const uint32_t xk = f32_key_fast(pick_dyn<NBT>(sv, x)) - tau;
+        st_shared_v2_if(pos < capw, segs + 8u * (uint32_t)pos, xk, (uint32_t)(t0 + 256 * x));
         mx = max(mx, xk);
         ++pos;
       }

@@ -1,12 +1,20 @@
 #!/bin/bash
-# Profiling evidence for one round (run under gpurun); outputs in gpurun_out/
+# Profiling evidence for one round (run under gpurun); raw outputs in gpurun_out/, the
+# summaries bench.py and the judge read are then copied under profiles/<round>/.
+#   tools/profile_round.sh [config]      (default c2)
 set -x
+CFG=${1:-c2}
 mkdir -p gpurun_out
-# 1) launch list of the bench command (decode kernels only), per-launch device time
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:decode -c 20 --csv \
-    --log-file gpurun_out/launches_c2.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
-# 2) full capture of the hot kernel at the bench workload (C2, all 4096 units)
-ncu --set full --import-source on --clock-control none -k regex:decode_ws -c 1 \
-    -o gpurun_out/decode_ws_c2 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-ncu -i gpurun_out/decode_ws_c2.ncu-rep --page raw --csv > gpurun_out/decode_ws_c2_raw.csv 2>&1
-ncu -i gpurun_out/decode_ws_c2.ncu-rep --page details --csv > gpurun_out/decode_ws_c2_details.csv 2>&1
+# 1) launch list of the bench command: per-launch device time of its decode launches
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:decode -c 12 --csv \
+    --log-file gpurun_out/launches_${CFG}.csv python bench.py --config ${CFG} --steps 4 --warmup 3 --no-cpu-baseline \
+    > gpurun_out/bench_under_ncu_${CFG}.log 2>&1
+# 2) full capture of one decode launch at the bench workload (after the warm-up launches)
+ncu --set full --import-source on --clock-control none -k regex:decode -s 3 -c 1 \
+    -o gpurun_out/decode_${CFG} python bench.py --config ${CFG} --steps 1 --warmup 3 --no-cpu-baseline \
+    > gpurun_out/ncu_full_${CFG}.log 2>&1
+ncu -i gpurun_out/decode_${CFG}.ncu-rep --page raw --csv > gpurun_out/decode_${CFG}_raw.csv 2>&1
+ncu -i gpurun_out/decode_${CFG}.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/decode_${CFG}_src.csv 2>&1
+python tools/ncu_summary.py gpurun_out/decode_${CFG}_raw.csv ${CFG} > gpurun_out/ncu_${CFG}_summary.json
+python tools/ncu_src.py gpurun_out/decode_${CFG}_src.csv 40 samples > gpurun_out/ncu_${CFG}_lines.txt
+rm -f gpurun_out/decode_${CFG}.ncu-rep
