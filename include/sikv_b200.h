@@ -91,9 +91,13 @@ int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64
 int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap);
 int sikv_decode_default_cap(int64_t tokens, int k, int sinks);
 size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens);
-/* kernel: 0 = auto (persistent warp-specialised kernel when a workspace of
- * sikv_decode_workspace_bytes is given, it fits shared memory and units >= 2 x SMs),
- * 1 = one CTA per unit, 2 = force the persistent kernel. */
+/* workspace for every decode kernel at top-k k (the two-kernel path stores the dynamic lists) */
+size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int sinks);
+/* kernel: 0 = auto (two kernels when units >= 2 x SMs, a workspace of
+ * sikv_decode_workspace_bytes_k is given and the selection kernel fits shared memory; a
+ * thread-block cluster per unit for few long units; else one CTA per unit),
+ * 1 = one CTA per unit, 2 = the persistent warp-specialised kernel, 3 = split units across a
+ * cluster, 4 = force the two-kernel path (selection, then attention). */
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
                      int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq,

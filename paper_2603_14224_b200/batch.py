@@ -182,8 +182,8 @@ class DecodeOutput:
 _WS: dict = {}
 
 
-def _workspace(units: int, tokens: int, device) -> torch.Tensor:
-    need = L_.lib().sikv_decode_workspace_bytes(units, tokens)
+def _workspace(units: int, tokens: int, k: int, sinks: int, device) -> torch.Tensor:
+    need = L_.lib().sikv_decode_workspace_bytes_k(units, tokens, k, sinks)
     key = (device.index if device.index is not None else torch.cuda.current_device())
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
@@ -198,7 +198,8 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
     """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
 
     kernel: 0 auto, 1 one CTA per unit, 2 warp-specialised persistent kernel, 3 each unit split
-    across a CTA cluster (long contexts, few units)."""
+    across a CTA cluster (long contexts, few units), 4 two kernels (selection with two unit
+    groups per SM, then attention)."""
     U = cb.units
     if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
         raise ValueError(f"q must be [{U}, Gq, {FD}], got {tuple(q.shape)}")
@@ -217,7 +218,7 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
         sel = sel_buf if sel_buf is not None else torch.empty(U, max(stride, 1), device=dev, dtype=torch.int32)
         cnt = torch.empty(U, device=dev, dtype=torch.int32)
     diag = torch.empty(U, device=dev, dtype=torch.int32) if with_diag else None
-    ws = _workspace(U, cb.tokens, dev)
+    ws = _workspace(U, cb.tokens, k, cb.sinks, dev)
     L_.call("sikv_decode_step", L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], cb.recent, L_.ptr(qf), U,
             cb.tokens, Gq, k, cap,

@@ -32,6 +32,7 @@ cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, i
 cudaError_t set_decode_profile(long long*);
 cudaError_t set_decode_ws_profile(long long*);
 cudaError_t set_decode_ws_skip(int);
+cudaError_t set_k1_skip(int);
 int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap);
 int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
@@ -39,6 +40,12 @@ cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, co
                                 const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, int, float*,
                                 float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t);
 size_t ws_workspace_bytes(int64_t U, int64_t L);
+int two_select_smem_bytes(int64_t L, int k, int S, int cap);
+int two_attend_smem_bytes(int64_t L, int k, int S, int Gq);
+size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
+cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
+                              const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
+                              int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
 cudaError_t launch_decode_ws(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                              const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*,
                              float*, int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
@@ -194,6 +201,9 @@ int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const 
 }
 
 size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens) { return ws_workspace_bytes(units, tokens); }
+size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int sinks) {
+  return std::max(ws_workspace_bytes(units, tokens), two_workspace_bytes(units, tokens, k, sinks));
+}
 
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
@@ -215,8 +225,27 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   REQUIRE(sinks + keff + recent >= 1, SIKV_EINVAL, "selection is empty");
   REQUIRE(!sel || sel_stride >= sinks + keff + recent, SIKV_EINVAL, "sel_stride too small");
   // kernel: 0 = auto, 1 = one CTA per unit, 2 = warp-specialised persistent, 3 = split units
-  // (a CTA cluster per unit)
-  REQUIRE(kernel >= 0 && kernel <= 3, SIKV_EINVAL, "kernel must be 0, 1, 2 or 3");
+  // (a CTA cluster per unit), 4 = two kernels (selection with two unit groups per SM, then
+  // attention)
+  REQUIRE(kernel >= 0 && kernel <= 4, SIKV_EINVAL, "kernel must be 0, 1, 2, 3 or 4");
+  if (kernel == 4 || (kernel == 0 && units >= 2 * num_sms())) {
+    const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
+    const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
+    int tcap = cap > 0 ? cap : (int)std::max<int64_t>(2 * ke + 1024, 1024);
+    while (cap <= 0 && tcap > floor_cap && two_select_smem_bytes(tokens, k, sinks, tcap) > max_smem()) tcap -= 64;
+    const bool fits = two_select_smem_bytes(tokens, k, sinks, tcap) <= max_smem() &&
+                      two_attend_smem_bytes(tokens, k, sinks, gq) <= max_smem();
+    const bool ws_ok = workspace && workspace_bytes >= two_workspace_bytes(units, tokens, k, sinks);
+    if (fits && ws_ok) {
+      return cuda_ret(launch_decode_two(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
+                                        frag_blocks, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
+                                        sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
+                      "sikv_decode_step");
+    }
+    REQUIRE(kernel != 4, SIKV_EUNSUPPORTED,
+            fits ? "the two-kernel path needs sikv_decode_workspace_bytes_k of workspace"
+                 : "the two-kernel path does not fit this configuration");
+  }
   // few long units: split each across a cluster of 2 / 4 / 8 CTAs so every SM has work
   if (kernel == 3 || (kernel == 0 && units < num_sms() && tokens >= 16384)) {
     int pick = 0, pick_cap = 0;
@@ -269,7 +298,11 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   return cuda_ret(e, "sikv_decode_step");
 }
 
-int sikv_debug_set_ws_skip(int v) { return cuda_ret(set_decode_ws_skip(v), "sikv_debug_set_ws_skip"); }
+int sikv_debug_set_ws_skip(int v) {
+  cudaError_t e = set_decode_ws_skip(v);
+  if (e == cudaSuccess) e = set_k1_skip(v);
+  return cuda_ret(e, "sikv_debug_set_ws_skip");
+}
 
 int sikv_debug_set_decode_profile(void* clocks) {
   cudaError_t e = set_decode_profile((long long*)clocks);

@@ -27,7 +27,8 @@ namespace sikv {
 #define SIKV_K1_STAGES 2
 #endif
 constexpr int K1_STAGES = SIKV_K1_STAGES;             // cp.async stages per warp in the attention phase
-__device__ long long* g_prof = nullptr;   // optional per-unit phase clocks (debug / profiling)
+__device__ long long* g_prof = nullptr;
+__device__ int g_k1_skip = 0;            // debug: bit 0 skips the attention phase   // optional per-unit phase clocks (debug / profiling)
 
 struct DecodeArgs {
   const uint8_t* signs;     // [U][L][16] rotated sign plane
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   attn_init(A, qs, ahat, Gq, lane);
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
+  if (g_k1_skip & 1) return;
   attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
   PROF(6);
   attn_dynamic<K1_STAGES>(A, a.recs + u * L * FREC, reinterpret_cast<const int32_t*>(sm + a.off_dyn), ndyn,
@@ -305,6 +307,7 @@ cudaError_t launch_pack_forced(const float* sink_k, const float* sink_v, int S, 
   return cudaGetLastError();
 }
 
+cudaError_t set_k1_skip(int v) { return cudaMemcpyToSymbol(g_k1_skip, &v, sizeof(v)); }
 cudaError_t set_decode_profile(long long* p) {
   return cudaMemcpyToSymbol(g_prof, &p, sizeof(p));
 }

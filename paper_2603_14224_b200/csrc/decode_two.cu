@@ -1,0 +1,251 @@
+// Two-kernel decode step (sm_100a): selection and attention in separate launches, each with
+// the occupancy its phase wants.
+//
+//   decode_select_kernel   one 512-thread CTA per SM, persistent.  Two independent groups of
+//                          8 warps (named barriers 1 and 2) each own a unit at a time
+//                          (units b + (2 it + g) * grid): pair table, sign-plane scoring,
+//                          sampled threshold, exact k-th key and the dynamic list, written to
+//                          the workspace.  The groups' 32-column pair tables interleave in one
+//                          64 KiB region (ColKey), so 16 warps stream sign planes per SM while
+//                          either group sits in its latency-bound setup / selection steps.
+//   decode_attend_kernel   one 256-thread CTA per unit, two per SM: the unit's dynamic list,
+//                          forced rows and sparse flash-decode (decode_common.cuh), fixed-order
+//                          merge, output.
+//
+// The arithmetic is that of decode.cu (shared device code): selections are identical, the
+// outputs equal within float32 accumulation order (the dynamic list is emitted in segment
+// order by 8-warp groups exactly as decode.cu does, so they are in fact bit-identical).
+#include "common.cuh"
+#include "select.cuh"
+#include "api_types.cuh"
+#include "decode_common.cuh"
+#include <algorithm>
+
+namespace sikv {
+
+constexpr int SEL_THREADS = 512;
+using SG0 = NamedGroup<1, 0>;
+using SG1 = NamedGroup<2, 256>;
+
+struct TwoArgs {
+  const uint8_t* signs;
+  const uint8_t* recs;
+  const float* cent32;
+  const float* alpha32;
+  const int32_t* sink_idx;
+  const uint32_t* ffrag;
+  const float* q;
+  float* out;
+  float* lse;
+  int32_t* sel;
+  int32_t* sel_count;
+  int32_t* diag;
+  int32_t* ndyn;        // [U]
+  int32_t* dynl;        // [U][dstride]
+  uint32_t* gbits;      // [U][2W] fallback / sorted-selection bitmaps
+  int64_t L, U;
+  int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
+  // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
+  int g_bytes, g_hist, g_forced, g_cand;
+};
+
+// ---------------------------------------------------------------- selection
+template <class PG, int G>
+__device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
+  const int64_t L = a.L;
+  const int W = (int)((L + 31) >> 5);
+  const int S = a.S, Gq = a.Gq;
+  const int tid = PG::tid();
+  char* T = sm + 128 * G;                        // this group's columns of the shared table rows
+  char* base = sm + TBL_BYTES + G * a.g_bytes;
+  float* lut = reinterpret_cast<float*>(base);
+  float* qbar = lut + 512;
+  int* th = reinterpret_cast<int*>(qbar + FD);
+  uint32_t* tmin = reinterpret_cast<uint32_t*>(th + 256);
+  Misc* ms = reinterpret_cast<Misc*>(tmin + 256);
+  int* hist = reinterpret_cast<int*>(base + a.g_hist);
+  uint32_t* forced = reinterpret_cast<uint32_t*>(base + a.g_forced);
+  uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
+  for (int it = 0;; ++it) {
+    const int64_t u = (int64_t)blockIdx.x + (int64_t)(2 * it + G) * gridDim.x;
+    if (u >= a.U) break;
+    const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
+    const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
+    // every small per-unit input is in flight at once, before any shared-memory step
+    float pq[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pq[i] = tid + DT * i < Gq * FD ? a.q[u * Gq * FD + tid + DT * i] : 0.f;
+    const float4* c4 = reinterpret_cast<const float4*>(a.cent32 + u * 32 * 16 * 4);
+    const float4 pc0 = c4[tid], pc1 = c4[tid + DT];
+    const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
+    uint4 wsamp[MAX_SAMPLE_CHUNKS];
+    load_sample(g, signs, tid, wsamp);
+    // q-bar: the Gq heads summed left to right (qs staged in the candidate buffer)
+    float* qs = reinterpret_cast<float*>(cand);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (tid + DT * i < Gq * FD) qs[tid + DT * i] = pq[i];
+    for (int i = tid; i < W; i += DT) forced[i] = 0u;
+    PG::sync();
+    if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
+    for (int j = tid + DT; j < S; j += DT) {
+      const int t = a.sink_idx[u * S + j];
+      atomicOr(&forced[t >> 5], 1u << (t & 31));
+    }
+    if (tid < FD) {
+      float sq = qs[tid];
+      for (int h = 1; h < Gq; ++h) sq = __fadd_rn(sq, qs[h * FD + tid]);
+      qbar[tid] = sq;
+    }
+    PG::sync();
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + DT * r, gg = e >> 4;
+      const float4 c = r ? pc1 : pc0;
+      const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
+      lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                                          __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+    }
+    PG::sync();
+    build_pair_rows_col<PG>(lut, T);
+    const int mode = g.mode;
+    int32_t* dyn = a.dynl + u * a.dstride;
+    int32_t* sel_u = a.sel ? a.sel + u * a.sel_stride : nullptr;
+    int32_t* sel_count_u = a.sel_count ? a.sel_count + u : nullptr;
+    uint32_t* gt = a.gbits + u * 2 * W;
+    uint32_t* eq = gt + W;
+    int ndyn = -1, fb = 0, need_eq = 0, eq_count = 0;
+    uint32_t kstar = 0;
+    if (mode >= 2) {
+      uint32_t tau;
+      fb = produce_candidates<PG, NoX, ColKey, NB>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau) ? 1 : 0;
+      if (!fb) {
+        ndyn = select_emit_candidates<PG>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
+                                          a.R, sel_count_u, kstar);
+      } else {
+        produce_exact<PG, NoX, ColKey>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
+      }
+    }
+    if (ndyn < 0) ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.R, sel_count_u, ms);
+    if (tid == 0) {
+      a.ndyn[u] = ndyn;
+      if (a.diag) a.diag[u] = (mode & 3) | (fb ? 4 : 0);
+    }
+    PG::sync();                       // the group's shared memory is reused by its next unit
+  }
+}
+
+__global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a) {
+  extern __shared__ __align__(128) char sm[];
+  // group from a value the compiler can prove warp-uniform (uniform-datapath table base)
+  const int grp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 8), 0);
+  if (grp == 0) select_group<SG0, 0>(a, sm);
+  else select_group<SG1, 1>(a, sm);
+}
+
+// ---------------------------------------------------------------- attention
+constexpr int ATT_THREADS = 256;
+
+__global__ void __launch_bounds__(ATT_THREADS, 2) decode_attend_kernel(TwoArgs a) {
+  extern __shared__ __align__(128) char sm[];
+  const int64_t u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int S = a.S, R = a.R, Gq = a.Gq;
+  // layout: staging (also the merge partials) | dynamic list | qs | ahat
+  char* stage = sm;
+  const int att_region = std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4);
+  int32_t* dyn = reinterpret_cast<int32_t*>(sm + att_region);
+  float* qs = reinterpret_cast<float*>(sm + att_region + a.dstride * 4);
+  float* ahat = qs + 8 * FD;
+  const int ndyn = a.ndyn[u];
+  const int npad = (ndyn + 15) & ~15;
+  const int4* src = reinterpret_cast<const int4*>(a.dynl + u * a.dstride);
+  for (int i = tid; i < npad / 4; i += ATT_THREADS) reinterpret_cast<int4*>(dyn)[i] = src[i];
+  for (int i = tid; i < Gq * FD; i += ATT_THREADS) qs[i] = a.q[u * Gq * FD + i];
+  if (tid < FD) {
+    const float al = a.alpha32[u * FD + tid];
+    ahat[tid] = al > 0.f ? al : 1.0f;
+  }
+  __syncthreads();
+  Attn A;
+  attn_init(A, qs, ahat, Gq, lane);
+  const int nf = S + R;
+  const int nbf = (nf + 15) >> 4;
+  attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
+  attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
+               stage + warp * 2 * STAGE_BYTES, lane);
+  __syncthreads();
+  float* part = reinterpret_cast<float*>(stage);
+  float* pm = part + DW * Gq * FD;
+  float* pl = pm + DW * Gq;
+  attn_write_partial(A, part, pm, pl, warp, Gq, lane);
+  __syncthreads();
+  attn_merge<Cta256>(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+}
+
+// ---------------------------------------------------------------- host side
+static int a128(int x) { return (x + 127) & ~127; }
+
+static int two_dstride(int64_t L, int k, int S) {
+  const int keff = (int)std::max<int64_t>(0, std::min<int64_t>(k, L - S));
+  return (keff + 16 + 31) & ~31;
+}
+
+static TwoArgs two_layout(int64_t L, int k, int S, int cap) {
+  TwoArgs a{};
+  const int W = (int)((L + 31) / 32);
+  a.capw = std::max(32, cap / DW);
+  int off = a128((512 + FD + 256 + 256) * 4 + (int)sizeof(Misc));
+  a.g_hist = off;
+  off += a128((NBIN + 64) * 4);
+  a.g_forced = off;
+  off += a128(W * 4);
+  a.g_cand = off;
+  off += a128(std::max(DW * a.capw * 8, 8 * FD * 4));
+  a.g_bytes = off;
+  a.dstride = two_dstride(L, k, S);
+  return a;
+}
+
+int two_select_smem_bytes(int64_t L, int k, int S, int cap) {
+  return TBL_BYTES + 2 * two_layout(L, k, S, cap).g_bytes;
+}
+int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
+  return std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4) + two_dstride(L, k, S) * 4 + (8 * FD + FD) * 4;
+}
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
+  const int64_t W = (L + 31) / 32;
+  return 256 + a256((size_t)U * 4) + a256((size_t)U * two_dstride(L, k, S) * 4) + (size_t)U * 2 * W * 4;
+}
+
+cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const float* cent32, const float* alpha32,
+                              const int32_t* sink_idx, int S, const uint32_t* ffrag, int fblocks, int R,
+                              const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
+                              int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
+                              int nsm, cudaStream_t st) {
+  TwoArgs a = two_layout(L, k, S, cap);
+  a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx;
+  a.ffrag = ffrag; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
+  char* ws = reinterpret_cast<char*>(workspace) + 256;
+  a.ndyn = reinterpret_cast<int32_t*>(ws);
+  ws += a256((size_t)U * 4);
+  a.dynl = reinterpret_cast<int32_t*>(ws);
+  ws += a256((size_t)U * a.dstride * 4);
+  a.gbits = reinterpret_cast<uint32_t*>(ws);
+  a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
+  const int smem_s = TBL_BYTES + 2 * a.g_bytes;
+  cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(nsm, (U + 1) / 2);
+  decode_select_kernel<<<grid, SEL_THREADS, smem_s, st>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int smem_a = two_attend_smem_bytes(L, k, S, Gq);
+  e = cudaFuncSetAttribute(decode_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
+  if (e != cudaSuccess) return e;
+  decode_attend_kernel<<<(unsigned)U, ATT_THREADS, smem_a, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sikv

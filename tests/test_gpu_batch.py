@@ -116,7 +116,7 @@ def _check_decode(units, cb, oc, q, k, **kw):
     return res
 
 
-KERNELS = [1, 2, 3]    # one CTA per unit / warp-specialised persistent / split across a cluster
+KERNELS = [1, 2, 3, 4]  # one CTA per unit / warp-specialised persistent / split across a cluster / two kernels
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -159,13 +159,18 @@ def test_decode_sampled_threshold_32k(c32k, kernel):
     assert ((d & 3) == 3).all() and not (d & 4).any()
 
 
-def test_kernels_agree_bitwise(c32k):
-    """Both kernels run the same arithmetic: outputs and selections are bit-identical."""
+@pytest.mark.parametrize("kernel", [2, 4])
+def test_kernels_agree_bitwise(c32k, kernel):
+    """The one-CTA, persistent and two-kernel paths run the same arithmetic in the same
+    order: outputs and selections are bit-identical."""
     units, cb, oc, q = c32k
     r1 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=1)
-    r2 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=2)
+    r2 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=kernel)
     assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.counts, r2.counts)
     assert torch.equal(r1.out, r2.out) and torch.equal(r1.lse, r2.lse)
+    # without the sorted selection the dynamic rows come straight from the candidate segments
+    r3 = B.decode_step(cb, q, 2048, with_lse=True, kernel=kernel)
+    assert torch.equal(r1.out, r3.out) and torch.equal(r1.lse, r3.lse)
 
 
 def test_split_kernel_matches_single_cta(c32k):
@@ -203,9 +208,12 @@ def test_persistent_kernel_many_units():
     cb = B.prefill_batch(K.repeat(reps, 1, 1), V.repeat(reps, 1, 1), sink_count=64)
     q = torch.tensor(np.stack([u.queries[:4] for u in units]), dtype=torch.float32, device="cuda").repeat(reps, 1, 1)
     r1 = B.decode_step(cb, q, 100, with_selection=True, kernel=1)
-    r2 = B.decode_step(cb, q, 100, with_selection=True, kernel=2)
-    assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.out, r2.out)
-    assert torch.equal(r2.out[0::2], r2.out[0:1].expand(reps, -1, -1))
+    for kern in (2, 4):
+        r2 = B.decode_step(cb, q, 100, with_selection=True, kernel=kern)
+        assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.out, r2.out)
+        assert torch.equal(r2.out[0::2], r2.out[0:1].expand(reps, -1, -1))
+    r0 = B.decode_step(cb, q, 100, with_selection=True)        # auto: two kernels at 800 units
+    assert torch.equal(r1.selection, r0.selection) and torch.equal(r1.out, r0.out)
 
 
 def test_decode_ties_lowest_index_first():
@@ -224,7 +232,7 @@ def test_decode_ties_lowest_index_first():
     c = O.prefill(reps, V, sink_count=64)
     q = torch.tensor(base.queries[None, :4], dtype=torch.float32, device="cuda")
     for k, cap, kern in ((500, 0, 1), (500, 200, 1), (333, 0, 1), (500, 0, 2), (500, 200, 2), (500, 0, 3),
-                         (500, 200, 3), (333, 0, 3)):
+                         (500, 200, 3), (333, 0, 3), (500, 0, 4), (500, 200, 4), (333, 0, 4)):
         res = B.decode_step(cb, q, k, cap=cap, with_selection=True, kernel=kern)
         idx = R.select32(c, base.queries[:4].astype(np.float32), k)[0]
         got = res.selection[0, : res.counts[0]].cpu().numpy()

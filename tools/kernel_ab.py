@@ -16,7 +16,7 @@ for name in cfgs:
     units = layers * batch * kvh
     cb, q = bench.build_cache(units, 0, L, gq, 1234, dev)
     out = torch.empty(units, gq, 128, device=dev)
-    for kern in ([1, 2, 3] if units < 1000 else [1, 2]):
+    for kern in ([1, 2, 3, 4] if units < 1000 else [1, 2, 4]):
         try:
             for _ in range(3):
                 B.decode_step(cb, q, k, out=out, kernel=kern)
