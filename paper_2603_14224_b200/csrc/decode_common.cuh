@@ -188,6 +188,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -231,6 +234,28 @@ struct Attn {
   float o[8][4];
   float mrun, lrun;
 };
+
+// q~ = q * alpha-hat straight from global memory (each warp on its own, no barrier)
+__device__ __forceinline__ void attn_init_g(Attn& A, const float* __restrict__ q_u, const float* __restrict__ alpha_u,
+                                            int Gq, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  const int gg = g < Gq ? g : 0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int d = 16 * s + 2 * t4 + 8 * e;
+      const float2 qv = __ldg(reinterpret_cast<const float2*>(q_u + gg * FD + d));
+      const float2 av = __ldg(reinterpret_cast<const float2*>(alpha_u + d));
+      const float a0 = av.x > 0.f ? av.x : 1.0f, a1 = av.y > 0.f ? av.y : 1.0f;
+      const float x0 = g < Gq ? qv.x * a0 : 0.f, x1 = g < Gq ? qv.y * a1 : 0.f;
+      A.qa[s][e] = h2u(__floats2half2_rn(x0, x1));
+    }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) A.o[m][0] = A.o[m][1] = A.o[m][2] = A.o[m][3] = 0.f;
+  A.mrun = -INFINITY;
+  A.lrun = 0.f;
+}
 
 __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float* ahat, int Gq, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
@@ -352,11 +377,18 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     dst[r] = (uint32_t)(j * FREC + 16 * (kk ^ stage_sw(j)));
   }
   const uint8_t* src0 = recs_u + 16 * kk;
-  auto stage_blk = [&](uint32_t buf, int base) {
-    const int32_t* dl = dyn + base + jb;
+  // the row indices of the block staged next are loaded one block ahead (registers), so the
+  // list read (shared or global memory) is off the staging path
+  int32_t tix[4];
+  auto load_ix = [&](int blk) {
+    const int32_t* dl = dyn + blk * 16 + jb;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) tix[r] = dl[4 * r];
+  };
+  auto stage_blk = [&](uint32_t buf) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const uint8_t* src = src0 + (size_t)((uint32_t)dl[4 * r] * (uint32_t)FREC);
+      const uint8_t* src = src0 + (size_t)((uint32_t)tix[r] * (uint32_t)FREC);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + buf + dst[r]), "l"(src));
     }
   };
@@ -371,13 +403,17 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   constexpr int P8 = 8 * FREC;
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (first + s * nw < nbd) stage_blk(s * STAGE_BYTES, (first + s * nw) * 16);
+    if (first + s * nw < nbd) { load_ix(first + s * nw); stage_blk(s * STAGE_BYTES); }
     cp_commit();
   }
+  if (first + (NSTAGE - 1) * nw < nbd) load_ix(first + (NSTAGE - 1) * nw);
   int buf = 0;
   for (int db = first; db < nbd; db += nw) {
     const int nx = db + (NSTAGE - 1) * nw;
-    if (nx < nbd) stage_blk(((buf + NSTAGE - 1) % NSTAGE) * STAGE_BYTES, nx * 16);
+    if (nx < nbd) {
+      stage_blk(((buf + NSTAGE - 1) % NSTAGE) * STAGE_BYTES);
+      if (nx + nw < nbd) load_ix(nx + nw);
+    }
     cp_commit();
     cp_wait<NSTAGE - 1>();
     __syncwarp();

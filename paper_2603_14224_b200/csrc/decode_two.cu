@@ -146,29 +146,18 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 // ---------------------------------------------------------------- attention
 constexpr int ATT_THREADS = 256;
 
+// Every warp starts on its own: q~ and the row indices come straight from global memory
+// (L2), so the only block-wide barriers are the two around the partial merge.
 __global__ void __launch_bounds__(ATT_THREADS, 2) decode_attend_kernel(TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
   const int64_t u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = a.S, R = a.R, Gq = a.Gq;
-  // layout: staging (also the merge partials) | dynamic list | qs | ahat
-  char* stage = sm;
-  const int att_region = std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4);
-  int32_t* dyn = reinterpret_cast<int32_t*>(sm + att_region);
-  float* qs = reinterpret_cast<float*>(sm + att_region + a.dstride * 4);
-  float* ahat = qs + 8 * FD;
-  const int ndyn = a.ndyn[u];
-  const int npad = (ndyn + 15) & ~15;
-  const int4* src = reinterpret_cast<const int4*>(a.dynl + u * a.dstride);
-  for (int i = tid; i < npad / 4; i += ATT_THREADS) reinterpret_cast<int4*>(dyn)[i] = src[i];
-  for (int i = tid; i < Gq * FD; i += ATT_THREADS) qs[i] = a.q[u * Gq * FD + i];
-  if (tid < FD) {
-    const float al = a.alpha32[u * FD + tid];
-    ahat[tid] = al > 0.f ? al : 1.0f;
-  }
-  __syncthreads();
+  char* stage = sm;                    // staging, then the merge partials
+  const int32_t* dyn = a.dynl + u * a.dstride;
+  const int ndyn = __ldg(a.ndyn + u);
   Attn A;
-  attn_init(A, qs, ahat, Gq, lane);
+  attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + u * FD, Gq, lane);
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
   attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
@@ -211,7 +200,7 @@ int two_select_smem_bytes(int64_t L, int k, int S, int cap) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap).g_bytes;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
-  return std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4) + two_dstride(L, k, S) * 4 + (8 * FD + FD) * 4;
+  return std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
