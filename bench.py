@@ -274,6 +274,9 @@ def run_ours(args, rank, world, cfg):
     res = B.decode_step(cb, q, k, with_diag=True)
     torch.cuda.synchronize()
     fallbacks = int(((res.diag & 4) != 0).sum().item())
+    from paper_2603_14224_b200 import _lib as L_
+    path = int(L_.lib().sikv_decode_last_kernel())
+    launches_per_step = 2 if path == 4 else 1
 
     if rank != 0:
         return None
@@ -308,7 +311,9 @@ def run_ours(args, rank, world, cfg):
                 "h2d_bytes_per_step": int(qh.numel() * qh.element_size()),
                 "d2h_bytes_per_step": int(oh[0].numel() * oh[0].element_size()),
                 "overlap": "H2D and D2H on two side streams, double-buffered device q / out"},
-        "gpu_launches": args.steps * (1 + 0),
+        "gpu_launches": args.steps * launches_per_step,
+        "decode_path": {1: "one CTA per unit", 2: "persistent warp-specialised", 3: "cluster split",
+                        4: "two kernels: decode_select_kernel + decode_attend_kernel"}.get(path),
         "clocks": clk.summary(),
         "selection_fallbacks_last_step": fallbacks,
     }

@@ -105,6 +105,10 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int32_t* sel_count, int32_t* diag, void* workspace, size_t workspace_bytes,
                      int kernel, void* stream);
 
+/* the decode path (1-4, as the kernel argument) the last sikv_decode_step of this host
+ * thread launched; the two-kernel path (4) starts two kernels per step, the others one */
+int sikv_decode_last_kernel(void);
+
 /* forced rows (sinks then recents; float32 centred K' and V) -> the decode kernel's fp16
  * mma-fragment blocks of 16 rows: forced_frag [U][frag_blocks][2][32][32] u32.  Re-packs the
  * blocks covering rows [row_begin, row_end); rows >= sinks + recent are zero.

@@ -36,6 +36,7 @@ _SIGS = {
     "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, I, P]),
     "sikv_decode_workspace_bytes": (SZ, [I64, I64]),
     "sikv_decode_workspace_bytes_k": (SZ, [I64, I64, I, I]),
+    "sikv_decode_last_kernel": (I, []),
     "sikv_forced_blocks": (I, [I, I64]),
     "sikv_pack_forced": (I, [P, P, I, P, P, I64, I, P, I64, P, I, I, I, P]),
     "sikv_score_fast": (I, [P, P, P, I, I64, I64, P, P]),

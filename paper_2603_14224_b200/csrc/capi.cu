@@ -205,6 +205,9 @@ size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int s
   return std::max(ws_workspace_bytes(units, tokens), two_workspace_bytes(units, tokens, k, sinks));
 }
 
+static thread_local int g_last_decode_kernel = 0;
+int sikv_decode_last_kernel() { return g_last_decode_kernel; }
+
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
                      int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq, int k,
@@ -237,6 +240,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                       two_attend_smem_bytes(tokens, k, sinks, gq) <= max_smem();
     const bool ws_ok = workspace && workspace_bytes >= two_workspace_bytes(units, tokens, k, sinks);
     if (fits && ws_ok) {
+      g_last_decode_kernel = 4;
       return cuda_ret(launch_decode_two(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                         frag_blocks, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
                                         sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
@@ -264,6 +268,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     }
     REQUIRE(pick || kernel != 3, SIKV_EUNSUPPORTED, "the split kernel does not fit this configuration");
     if (pick) {
+      g_last_decode_kernel = 3;
       return cuda_ret(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                           frag_blocks, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
                                           sel, sel_stride, sel_count, diag, (cudaStream_t)stream),
@@ -280,6 +285,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     // auto never picks the persistent kernel: the one-CTA-per-unit kernel (two co-resident
     // CTAs per SM) measured faster at C2 (32K tokens) and C4 (8K tokens); kernel = 2 forces it
     if (fits && kernel == 2) {
+      g_last_decode_kernel = 2;
       return cuda_ret(launch_decode_ws(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                        frag_blocks, recent, q, units, tokens, gq, k, wcap, out, lse, sel,
                                        sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
@@ -292,6 +298,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   REQUIRE(need <= max_smem(), SIKV_EUNSUPPORTED,
           "decode shared-memory footprint " + std::to_string(need) + " B exceeds the device limit");
   int smem = 0;
+  g_last_decode_kernel = 1;
   cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
                                 recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag,
                                 (cudaStream_t)stream, &smem);
