@@ -146,6 +146,14 @@ __device__ __forceinline__ void score_batch(const uint4 (&w)[N], const Key& key,
   for (int x = 0; x < N; x += 2) unpack2(acc[x / 2], s[x], s[x + 1]);
 }
 
+// streaming 16-byte load of the sign plane: read once, no L1 allocation
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ bool forced_bit(const uint32_t* fb, int64_t t) {
   return (fb[t >> 5] >> (t & 31)) & 1u;
 }
@@ -575,17 +583,20 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
 // th / tmin: 256 + 256 words of scratch for the threshold histogram (may alias cand: the
 // histogram is rebuilt from the register-resident sample keys for every attempt).
 //
-// The sampled threshold is the sample key of rank r = e + 4 sqrt(e) + 16 (e = expected
+// The sampled threshold is the sample key of rank r = e + 3 sqrt(e) + 8 (e = expected
 // sample items in the top-k).  When the scan then overflows a warp segment (tau too low) or
 // yields fewer than k candidates (tau too high), r is rescaled from the observed counts and
 // the scan is repeated (at most kRetries times) before falling back to the exact path.
 constexpr int kRetries = 2;
 
-template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB>
+// SKS: the sample keys live in shared memory (sks[x * DT + tid]) instead of 8 registers
+// across the B2 scan (they are only needed again for a retry).
+template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB, bool SKS = false>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
                                                    uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
-                                                   uint32_t& tau_out, const Xch& xch = Xch()) {
+                                                   uint32_t& tau_out, const Xch& xch = Xch(),
+                                                   uint32_t* sks = nullptr) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const Key lb(lane);
   const int capw = g.capw;
@@ -606,6 +617,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       uint32_t key = 0;
       if (x < g.nsc && t < g.L && !(t < g.flim && forced_bit(forced, t))) key = f32_key(sv[x]);
       sk[x] = key;
+      if constexpr (SKS) sks[x * DT + tid] = key;
       nv += key != 0;
       smax = max(smax, key);
       if (key) smin = min(smin, key);
@@ -625,7 +637,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     kmn = ms->tau;
     xch.sample(nsv, kmx, kmn);            // cluster: the whole unit's sample
     const double e = (double)g.keff * (double)nsv / (double)(g.ncand);
-    r = min((int)ceil(e + 4.0 * sqrt(e) + 16.0), nsv);
+    r = min((int)ceil(e + 3.0 * sqrt(e) + 8.0), nsv);
   }
   const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
   const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
@@ -636,11 +648,11 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     const uint4* p = pbase + (int64_t)c0 * 256;     // constant offsets 4 KiB apart: no per-load address math
     if ((c0 + NBT) * 256 <= Li) {
 #pragma unroll
-      for (int x = 0; x < NBT; ++x) w[x] = __ldg(p + 256 * x);
+      for (int x = 0; x < NBT; ++x) w[x] = ld_stream(p + 256 * x);
     } else {
       const int t0 = c0 * 256 + tid;
 #pragma unroll
-      for (int x = 0; x < NBT; ++x) w[x] = t0 + 256 * x < Li ? __ldg(p + 256 * x) : make_uint4(0, 0, 0, 0);
+      for (int x = 0; x < NBT; ++x) w[x] = t0 + 256 * x < Li ? ld_stream(p + 256 * x) : make_uint4(0, 0, 0, 0);
     }
   };
   for (int attempt = 0;; ++attempt) {
@@ -654,10 +666,11 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
         Grp::sync();
 #pragma unroll
         for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-          if (sk[x]) {
-            const int b = min(255, (int)((__uint_as_float(unkey_bits(sk[x])) - fmn) * scale));
+          const uint32_t kx = SKS ? sks[x * DT + tid] : sk[x];
+          if (kx) {
+            const int b = min(255, (int)((__uint_as_float(unkey_bits(kx)) - fmn) * scale));
             atomicAdd(&th[b], 1);
-            atomicMin(&tmin[b], sk[x]);
+            atomicMin(&tmin[b], kx);
           }
         }
         Grp::sync();
@@ -689,10 +702,12 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       Grp::sync();
       if (tid == 0) { ms->maxx = 0; ms->bad = 0; }
       Grp::sync();
-      uint32_t bits = 0;
+      uint32_t bits = 0, skx[MAX_SAMPLE_CHUNKS];
 #pragma unroll
-      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x)
-        if (x < g.nsc && sk[x] != 0 && sk[x] >= tau) bits |= 1u << x;
+      for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+        skx[x] = SKS ? sks[x * DT + tid] : sk[x];
+        if (x < g.nsc && skx[x] != 0 && skx[x] >= tau) bits |= 1u << x;
+      }
       const int cnt = __popc(bits);
       int inc = cnt;
 #pragma unroll
@@ -705,7 +720,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
 #pragma unroll
       for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
         if ((bits >> x) & 1u) {
-          const uint32_t xk = sk[x] - tau;
+          const uint32_t xk = skx[x] - tau;
           if (pos < capw) { seg[2 * pos] = xk; seg[2 * pos + 1] = (uint32_t)(x * g.sstride * 256 + tid); }
           mx = max(mx, xk);
           ++pos;

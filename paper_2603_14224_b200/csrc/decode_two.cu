@@ -24,6 +24,10 @@
 namespace sikv {
 
 constexpr int SEL_THREADS = 512;
+#ifndef SIKV_SEL_SKS
+#define SIKV_SEL_SKS 0
+#endif
+constexpr bool SEL_SKS = SIKV_SEL_SKS;    // sample keys in shared memory (A/B: slower at C2)
 using SG0 = NamedGroup<1, 0>;
 using SG1 = NamedGroup<2, 256>;
 
@@ -46,7 +50,7 @@ struct TwoArgs {
   int64_t L, U;
   int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
   // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
-  int g_bytes, g_hist, g_forced, g_cand;
+  int g_bytes, g_hist, g_forced, g_cand, g_sks;
 };
 
 // ---------------------------------------------------------------- selection
@@ -66,6 +70,7 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
   int* hist = reinterpret_cast<int*>(base + a.g_hist);
   uint32_t* forced = reinterpret_cast<uint32_t*>(base + a.g_forced);
   uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
+  uint32_t* sks = reinterpret_cast<uint32_t*>(base + a.g_sks);
   for (int it = 0;; ++it) {
     const int64_t u = (int64_t)blockIdx.x + (int64_t)(2 * it + G) * gridDim.x;
     if (u >= a.U) break;
@@ -118,7 +123,8 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
     uint32_t kstar = 0;
     if (mode >= 2) {
       uint32_t tau;
-      fb = produce_candidates<PG, NoX, ColKey, NB>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau) ? 1 : 0;
+      fb = produce_candidates<PG, NoX, ColKey, NB, SEL_SKS>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(),
+                                                             sks) ? 1 : 0;
       if (!fb) {
         ndyn = select_emit_candidates<PG>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
                                           a.R, sel_count_u, kstar);
@@ -191,6 +197,8 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap) {
   off += a128(W * 4);
   a.g_cand = off;
   off += a128(std::max(DW * a.capw * 8, 8 * FD * 4));
+  a.g_sks = off;
+  off += SEL_SKS ? MAX_SAMPLE_CHUNKS * DT * 4 : 0;
   a.g_bytes = off;
   a.dstride = two_dstride(L, k, S);
   return a;
