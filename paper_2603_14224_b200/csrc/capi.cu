@@ -33,6 +33,7 @@ cudaError_t set_decode_profile(long long*);
 cudaError_t set_decode_ws_profile(long long*);
 cudaError_t set_decode_ws_skip(int);
 cudaError_t set_k1_skip(int);
+cudaError_t set_decode_two_profile(long long*);
 int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap);
 int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
@@ -314,6 +315,7 @@ int sikv_debug_set_ws_skip(int v) {
 int sikv_debug_set_decode_profile(void* clocks) {
   cudaError_t e = set_decode_profile((long long*)clocks);
   if (e == cudaSuccess) e = set_decode_ws_profile((long long*)clocks);
+  if (e == cudaSuccess) e = set_decode_two_profile((long long*)clocks);
   return cuda_ret(e, "sikv_debug_set_decode_profile");
 }
 

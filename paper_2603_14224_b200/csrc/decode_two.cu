@@ -24,6 +24,7 @@
 namespace sikv {
 
 constexpr int SEL_THREADS = 512;
+__device__ long long* g_prof_two = nullptr;   // optional per-unit phase clocks (profiling)
 #ifndef SIKV_SEL_SKS
 #define SIKV_SEL_SKS 0
 #endif
@@ -74,6 +75,8 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
   for (int it = 0;; ++it) {
     const int64_t u = (int64_t)blockIdx.x + (int64_t)(2 * it + G) * gridDim.x;
     if (u >= a.U) break;
+    long long* prof = g_prof_two ? g_prof_two + u * 12 : nullptr;
+    if (prof && tid == 0) prof[0] = clock64();
     const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
     const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
     // every small per-unit input is in flight at once, before any shared-memory step
@@ -113,6 +116,7 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
     }
     PG::sync();
     build_pair_rows_col<PG>(lut, T);
+    if (prof && tid == 0) prof[1] = clock64();
     const int mode = g.mode;
     int32_t* dyn = a.dynl + u * a.dstride;
     int32_t* sel_u = a.sel ? a.sel + u * a.sel_stride : nullptr;
@@ -125,6 +129,7 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
       uint32_t tau;
       fb = produce_candidates<PG, NoX, ColKey, NB, SEL_SKS>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(),
                                                              sks) ? 1 : 0;
+      if (prof && tid == 0) prof[2] = clock64();
       if (!fb) {
         ndyn = select_emit_candidates<PG>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
                                           a.R, sel_count_u, kstar);
@@ -133,6 +138,7 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
       }
     }
     if (ndyn < 0) ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.R, sel_count_u, ms);
+    if (prof && tid == 0) prof[3] = clock64();
     if (tid == 0) {
       a.ndyn[u] = ndyn;
       if (a.diag) a.diag[u] = (mode & 3) | (fb ? 4 : 0);
@@ -180,6 +186,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 2) decode_attend_kernel(TwoArgs a
 
 // ---------------------------------------------------------------- host side
 static int a128(int x) { return (x + 127) & ~127; }
+cudaError_t set_decode_two_profile(long long* p) { return cudaMemcpyToSymbol(g_prof_two, &p, sizeof(p)); }
 
 static int two_dstride(int64_t L, int k, int S) {
   const int keff = (int)std::max<int64_t>(0, std::min<int64_t>(k, L - S));

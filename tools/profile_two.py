@@ -1,0 +1,34 @@
+"""Per-unit phase clocks of decode_select_kernel (two-kernel path): setup, scoring +
+candidates, selection + emission.   python tools/profile_two.py [--units 4096 --L 32768 --k 2048]"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2603_14224_b200 import _lib  # noqa: E402
+from paper_2603_14224_b200 import batch as B  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--units", type=int, default=4096)
+ap.add_argument("--L", type=int, default=32768)
+ap.add_argument("--k", type=int, default=2048)
+ap.add_argument("--gq", type=int, default=4)
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+cb, q = bench.build_cache(a.units, 0, a.L, a.gq, 1234, dev)
+out = torch.empty(a.units, a.gq, 128, device=dev)
+for _ in range(3):
+    B.decode_step(cb, q, a.k, out=out, kernel=4)
+clk = torch.zeros(a.units, 12, dtype=torch.int64, device=dev)
+_lib.call("sikv_debug_set_decode_profile", _lib.ptr(clk))
+B.decode_step(cb, q, a.k, out=out, kernel=4)
+torch.cuda.synchronize()
+_lib.call("sikv_debug_set_decode_profile", None)
+c = clk.cpu().numpy().astype(np.float64)
+for n, i, j in [("setup+table", 0, 1), ("score+cand", 1, 2), ("select+emit", 2, 3), ("unit total", 0, 3)]:
+    d = c[:, j] - c[:, i]
+    print(f"  {n:12s} mean {d.mean():9.0f}  p50 {np.median(d):9.0f}  max {d.max():9.0f}")
