@@ -283,7 +283,11 @@ __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float*
 }
 
 constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;   // log2(e) / sqrt(128)
-// 2^x on the SFU (x <= 0 here: logits minus the running max; -inf -> +0)
+#ifndef SIKV_LAZY
+#define SIKV_LAZY 8.0f
+#endif
+constexpr float kLazyRescale = SIKV_LAZY;
+// 2^x on the SFU (x <= 8 here: logits minus the reference max; -inf -> +0)
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -307,7 +311,9 @@ __device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][
   float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
   bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
   bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-  const float mnew = fmaxf(A.mrun, bm);
+  // lazy rescale: the reference max only moves when the block max exceeds it by more than
+  // 2^8 (exp2 domain), so P <= 256 (exact range in fp16) and most blocks skip the O rescale
+  const float mnew = bm > A.mrun + kLazyRescale ? bm : A.mrun;
   const float fac = ex2(A.mrun - mnew);
   A.mrun = mnew;
   const __half2 p01 = __floats2half2_rn(ex2(x[0] - mnew), ex2(x[1] - mnew));
