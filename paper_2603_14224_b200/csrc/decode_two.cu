@@ -48,10 +48,11 @@ struct TwoArgs {
   int32_t* ndyn;        // [U]
   int32_t* dynl;        // [U][dstride]
   uint32_t* gbits;      // [U][2W] fallback / sorted-selection bitmaps
+  uint32_t* gforced;    // [U][W] forced bitmaps when they do not fit shared memory (long units)
   int64_t L, U;
   int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
   // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
-  int g_bytes, g_hist, g_forced, g_cand, g_sks;
+  int g_bytes, g_hist, g_forced, g_cand, g_sks;   // g_forced < 0: forced bitmap in gforced
 };
 
 // ---------------------------------------------------------------- selection
@@ -69,7 +70,7 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
   uint32_t* tmin = reinterpret_cast<uint32_t*>(th + 256);
   Misc* ms = reinterpret_cast<Misc*>(tmin + 256);
   int* hist = reinterpret_cast<int*>(base + a.g_hist);
-  uint32_t* forced = reinterpret_cast<uint32_t*>(base + a.g_forced);
+  uint32_t* const forced_s = reinterpret_cast<uint32_t*>(base + (a.g_forced >= 0 ? a.g_forced : 0));
   uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
   uint32_t* sks = reinterpret_cast<uint32_t*>(base + a.g_sks);
   for (int it = 0;; ++it) {
@@ -88,6 +89,7 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
     const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
     uint4 wsamp[MAX_SAMPLE_CHUNKS];
     load_sample(g, signs, tid, wsamp);
+    uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
     // q-bar: the Gq heads summed left to right (qs staged in the candidate buffer)
     float* qs = reinterpret_cast<float*>(cand);
 #pragma unroll
@@ -193,15 +195,15 @@ static int two_dstride(int64_t L, int k, int S) {
   return (keff + 16 + 31) & ~31;
 }
 
-static TwoArgs two_layout(int64_t L, int k, int S, int cap) {
+static TwoArgs two_layout(int64_t L, int k, int S, int cap, bool forced_in_smem = true) {
   TwoArgs a{};
   const int W = (int)((L + 31) / 32);
   a.capw = std::max(32, cap / DW);
   int off = a128((512 + FD + 256 + 256) * 4 + (int)sizeof(Misc));
   a.g_hist = off;
   off += a128((NBIN + 64) * 4);
-  a.g_forced = off;
-  off += a128(W * 4);
+  a.g_forced = forced_in_smem ? off : -1;
+  if (forced_in_smem) off += a128(W * 4);
   a.g_cand = off;
   off += a128(std::max(DW * a.capw * 8, 8 * FD * 4));
   a.g_sks = off;
@@ -211,8 +213,13 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap) {
   return a;
 }
 
+// the forced bitmaps stay in shared memory unless that is what keeps the kernel from fitting
+static bool two_forced_smem(int64_t L, int k, int S, int cap) {
+  return TBL_BYTES + 2 * two_layout(L, k, S, cap, true).g_bytes <= 227 * 1024;
+}
+
 int two_select_smem_bytes(int64_t L, int k, int S, int cap) {
-  return TBL_BYTES + 2 * two_layout(L, k, S, cap).g_bytes;
+  return TBL_BYTES + 2 * two_layout(L, k, S, cap, two_forced_smem(L, k, S, cap)).g_bytes;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
   return std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4);
@@ -220,7 +227,8 @@ int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
   const int64_t W = (L + 31) / 32;
-  return 256 + a256((size_t)U * 4) + a256((size_t)U * two_dstride(L, k, S) * 4) + (size_t)U * 2 * W * 4;
+  return 256 + a256((size_t)U * 4) + a256((size_t)U * two_dstride(L, k, S) * 4) + a256((size_t)U * 2 * W * 4) +
+         (size_t)U * W * 4;
 }
 
 cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const float* cent32, const float* alpha32,
@@ -228,7 +236,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
                               const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
                               int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
                               int nsm, cudaStream_t st) {
-  TwoArgs a = two_layout(L, k, S, cap);
+  TwoArgs a = two_layout(L, k, S, cap, two_forced_smem(L, k, S, cap));
   a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx;
   a.ffrag = ffrag; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
   char* ws = reinterpret_cast<char*>(workspace) + 256;
@@ -237,6 +245,8 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   a.dynl = reinterpret_cast<int32_t*>(ws);
   ws += a256((size_t)U * a.dstride * 4);
   a.gbits = reinterpret_cast<uint32_t*>(ws);
+  ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
+  a.gforced = reinterpret_cast<uint32_t*>(ws);
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
   const int smem_s = TBL_BYTES + 2 * a.g_bytes;
   cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
