@@ -10,7 +10,7 @@
 
 using namespace sikv;
 
-template <int THREADS, int NBX, int CAND>
+template <int THREADS, int NBX, int CAND, int PF = 1>
 __global__ void __launch_bounds__(THREADS, 1)
 score_stream(const uint4* __restrict__ signs, int64_t L, int units, float tauf, float* sink, int* cnt) {
   extern __shared__ __align__(16) char T[];
@@ -19,22 +19,29 @@ score_stream(const uint4* __restrict__ signs, int64_t L, int units, float tauf, 
   for (int i = tid; i < 256 * 64; i += THREADS)
     reinterpret_cast<float*>(T)[i] = (float)((i * 2654435761u) >> 20) * 1e-3f;
   __syncthreads();
-  const uint32_t lb = (uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15));
+  const RepKey lb(lane);
   float acc = 0.f;
   int c = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const uint4* p = signs + (int64_t)u * L + tid;
     const int nch = (int)(L / THREADS);
-    uint4 wn[NBX];
+    uint4 wn[PF ? NBX : 1];
+    if (PF) {
 #pragma unroll
-    for (int x = 0; x < NBX; ++x) wn[x] = __ldg(p + THREADS * x);
+      for (int x = 0; x < NBX; ++x) wn[PF ? x : 0] = __ldg(p + THREADS * x);
+    }
     for (int c0 = 0; c0 < nch; c0 += NBX) {
       uint4 w[NBX];
+      if (PF) {
 #pragma unroll
-      for (int x = 0; x < NBX; ++x) w[x] = wn[x];
-      if (c0 + NBX < nch) {
+        for (int x = 0; x < NBX; ++x) w[x] = wn[PF ? x : 0];
+        if (c0 + NBX < nch) {
 #pragma unroll
-        for (int x = 0; x < NBX; ++x) wn[x] = __ldg(p + (int64_t)THREADS * (c0 + NBX + x));
+          for (int x = 0; x < NBX; ++x) wn[PF ? x : 0] = __ldg(p + (int64_t)THREADS * (c0 + NBX + x));
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < NBX; ++x) w[x] = __ldg(p + (int64_t)THREADS * (c0 + x));
       }
       float sv[NBX];
       score_batch(w, lb, T, sv);
@@ -74,9 +81,9 @@ score_stream(const uint4* __restrict__ signs, int64_t L, int units, float tauf, 
   atomicAdd(cnt, c);
 }
 
-template <int THREADS, int NBX, int CAND = 0>
+template <int THREADS, int NBX, int CAND = 0, int PF = 1>
 void run(const uint4* d, int64_t L, int units, float* sink, int* cnt, int nsm, float tauf = 1e9f) {
-  auto k = score_stream<THREADS, NBX, CAND>;
+  auto k = score_stream<THREADS, NBX, CAND, PF>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
   for (int i = 0; i < 3; ++i) k<<<nsm, THREADS, 65536>>>(d, L, units, tauf, sink, cnt);
   cudaEvent_t a, b;
@@ -91,8 +98,9 @@ void run(const uint4* d, int64_t L, int units, float* sink, int* cnt, int nsm, f
   cudaEventElapsedTime(&ms, a, b);
   ms /= it;
   const double bytes = (double)units * L * 16;
-  printf("cand %d threads %4d NB %2d: %.3f ms  %.0f GB/s  (%.0f cycles/unit/SM at 1.965 GHz)\n", CAND, THREADS, NBX, ms,
+  printf("pf %d cand %d threads %4d NB %2d: %.3f ms  %.0f GB/s  (%.0f cycles/unit/SM at 1.965 GHz)\n", PF, CAND, THREADS, NBX, ms,
          bytes / ms / 1e6, ms * 1e-3 * 1.965e9 / ((double)units / nsm));
+  (void)PF;
 }
 
 int main() {
@@ -125,6 +133,9 @@ int main() {
   }
   run<512, 8, 1>(d, L, units, sink, cnt, nsm, 38.0f);
   run<512, 4, 1>(d, L, units, sink, cnt, nsm, 38.0f);
+  run<512, 8, 1, 0>(d, L, units, sink, cnt, nsm, 38.0f);
+  run<512, 16, 1, 0>(d, L, units, sink, cnt, nsm, 38.0f);
+  run<512, 12, 1, 0>(d, L, units, sink, cnt, nsm, 38.0f);
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
   return 0;

@@ -10,26 +10,28 @@ import bench  # noqa: E402
 from paper_2603_14224_b200 import batch as B  # noqa: E402
 
 dev = torch.device("cuda", 0)
+CAP = int(os.environ.get("CAP", "0"))   # candidate buffer entries (0 = the library's choice)
+ONLY = [int(x) for x in os.environ["KERNELS"].split(",")] if "KERNELS" in os.environ else None
 cfgs = sys.argv[1:] or ["c2", "c3", "c4"]
 for name in cfgs:
     layers, batch, kvh, gq, L, k, _ = bench.CONFIGS[name]
     units = layers * batch * kvh
     cb, q = bench.build_cache(units, 0, L, gq, 1234, dev)
     out = torch.empty(units, gq, 128, device=dev)
-    for kern in ([1, 2, 3, 4] if units < 1000 else [1, 2, 4]):
+    for kern in ONLY or ([1, 2, 3, 4] if units < 1000 else [1, 2, 4]):
         try:
             for _ in range(3):
-                B.decode_step(cb, q, k, out=out, kernel=kern)
+                B.decode_step(cb, q, k, out=out, kernel=kern, cap=CAP)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(10):
-                B.decode_step(cb, q, k, out=out, kernel=kern)
+                B.decode_step(cb, q, k, out=out, kernel=kern, cap=CAP)
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 10
             gb = bench.algo_bytes_per_unit(L, k, gq) * units / 1e9
-            print(f"{name} kernel {kern}: {ms:.3f} ms  {gb / ms * 1e3:.0f} GB/s")
+            print(f"{name} kernel {kern} cap {CAP}: {ms:.3f} ms  {gb / ms * 1e3:.0f} GB/s")
         except Exception as ex:  # noqa: BLE001
             print(f"{name} kernel {kern}: {ex}")
     del cb, q, out
