@@ -236,6 +236,11 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
     const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
     int tcap = cap > 0 ? cap : (int)std::max<int64_t>(2 * ke + 1024, 1024);
+    // the selection kernel streams 64 KB of sign records per SM in flight through L1: keep
+    // its shared memory at or below the 164 KB carveout (L1 >= 92 KB) while the candidate
+    // buffer stays >= 1.5 k + 1024 (no segment overflow at the sampled threshold)
+    const int soft_cap = (int)std::max<int64_t>(ke + ke / 2 + 1024, floor_cap);
+    while (cap <= 0 && tcap > soft_cap && two_select_smem_bytes(tokens, k, sinks, tcap) > 164 * 1024) tcap -= 64;
     while (cap <= 0 && tcap > floor_cap && two_select_smem_bytes(tokens, k, sinks, tcap) > max_smem()) tcap -= 64;
     const bool fits = two_select_smem_bytes(tokens, k, sinks, tcap) <= max_smem() &&
                       two_attend_smem_bytes(tokens, k, sinks, gq) <= max_smem();

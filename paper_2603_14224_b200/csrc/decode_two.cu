@@ -218,8 +218,11 @@ static bool two_forced_smem(int64_t L, int k, int S, int cap) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, true).g_bytes <= 227 * 1024;
 }
 
+#ifndef SIKV_SEL_PAD
+#define SIKV_SEL_PAD 0
+#endif
 int two_select_smem_bytes(int64_t L, int k, int S, int cap) {
-  return TBL_BYTES + 2 * two_layout(L, k, S, cap, two_forced_smem(L, k, S, cap)).g_bytes;
+  return TBL_BYTES + 2 * two_layout(L, k, S, cap, two_forced_smem(L, k, S, cap)).g_bytes + SIKV_SEL_PAD;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
   return std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4);
@@ -248,7 +251,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
   a.gforced = reinterpret_cast<uint32_t*>(ws);
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
-  const int smem_s = TBL_BYTES + 2 * a.g_bytes;
+  const int smem_s = TBL_BYTES + 2 * a.g_bytes + SIKV_SEL_PAD;
   cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(nsm, (U + 1) / 2);
