@@ -72,18 +72,18 @@ class ClockSampler:
         self._t = None
 
     def __enter__(self):
-        def run_nvml(pynvml):
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        def run_nvml(pynvml, h):
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             bits = [0x8, 0x40, 0x20, 0x4]   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-            while not self._stop.is_set():
+            while True:
                 try:
                     sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                     r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                     self.samples.append([sm, mx] + ["active" if r & b else "" for b in bits])
                 except Exception:
                     pass
-                self._stop.wait(0.01)
+                if self._stop.wait(0.002):
+                    break
 
         def run_smi():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -100,10 +100,11 @@ class ClockSampler:
                     pass
                 self._stop.wait(0.05)
 
-        try:
+        try:   # NVML is initialised here, before the timed region starts
             import pynvml
             pynvml.nvmlInit()
-            target = lambda: run_nvml(pynvml)  # noqa: E731
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            target = lambda: run_nvml(pynvml, h)  # noqa: E731
         except Exception:
             target = run_smi
         self._t = threading.Thread(target=target, daemon=True)
@@ -448,15 +449,18 @@ def main():
             return
         cores = os.cpu_count() or 1
         sample = args.cpu_sample or max(cores, 8)
-        vals = []
-        for _ in range(max(1, min(args.steps, 2))):
-            vals.append(cpu_baseline(cfg, sample, cores))
-        v = vals[-1]
+        # every step is a bounded sample of the workload (cpu_baseline); at most 3 warm-up and
+        # 5 timed samples keep the whole run within a few minutes; the median is reported
+        nw, ns = min(args.warmup, 3), max(1, min(args.steps, 5))
+        for _ in range(nw):
+            cpu_baseline(cfg, sample, cores)
+        vals = sorted((cpu_baseline(cfg, sample, cores) for _ in range(ns)), key=lambda x: x["value"])
+        v = vals[len(vals) // 2]
         layers, batch, kvh, gq, L, k, label = cfg
         print(json.dumps({
             "metric": "decode steps/sec + HBM roofline fraction, Llama-3-8B geometry, 32K ctx",
-            "value": v["value"], "unit": "decode steps/s", "n_gpus": args.gpus, "steps": len(vals),
-            "warmup": 0, "ms_per_step": round(1000.0 / v["value"], 3) if v["value"] else None,
+            "value": v["value"], "unit": "decode steps/s", "n_gpus": args.gpus, "steps": ns,
+            "warmup": nw, "ms_per_step": round(1000.0 / v["value"], 3) if v["value"] else None,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_synthetic distribution)", "impl": "reference",
             "config": {"workload": args.config, "label": label, "context": L, "top_k": k},
