@@ -149,14 +149,36 @@ __global__ void __launch_bounds__(256) stats_partial_fast_kernel(const void* __r
   int low[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
   uint32_t emin[4] = {0x7F800000u, 0x7F800000u, 0x7F800000u, 0x7F800000u};
   if (active) {
-    constexpr int UN = 8;                        // rows in flight per warp
+    constexpr int UN = 8;                        // rows per warp per batch; two batches in flight
+    using Raw = typename std::conditional<DTY == IN_BF16, uint2, float4>::type;
+    auto ld = [&](int64_t t) -> Raw {
+      if (t >= t1) {                             // -0 leaves sum / sab / low unchanged
+        if constexpr (DTY == IN_BF16) return make_uint2(0x80008000u, 0x80008000u);
+        else return make_float4(-0.f, -0.f, -0.f, -0.f);
+      }
+      const int64_t idx = ((int64_t)u * L + t) * D + 4 * lane;
+      if constexpr (DTY == IN_BF16)
+        return __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(keys) + idx));
+      else
+        return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(keys) + idx));
+    };
+    Raw nx[UN];
+#pragma unroll
+    for (int r = 0; r < UN; ++r) nx[r] = ld(t0 + warp + 8 * r);
     for (int64_t tb = t0 + warp; tb < t1; tb += 8 * UN) {
       float x[UN][4];
 #pragma unroll
       for (int r = 0; r < UN; ++r) {
-        const int64_t t = tb + 8 * r;
-        if (t < t1) load4<DTY>(keys, ((int64_t)u * L + t) * D + 4 * lane, x[r]);
-        else x[r][0] = x[r][1] = x[r][2] = x[r][3] = -0.f;  // -0 leaves sum / sab / low unchanged
+        if constexpr (DTY == IN_BF16) {
+          x[r][0] = __uint_as_float(nx[r].x << 16); x[r][1] = __uint_as_float(nx[r].x & 0xFFFF0000u);
+          x[r][2] = __uint_as_float(nx[r].y << 16); x[r][3] = __uint_as_float(nx[r].y & 0xFFFF0000u);
+        } else {
+          x[r][0] = nx[r].x; x[r][1] = nx[r].y; x[r][2] = nx[r].z; x[r][3] = nx[r].w;
+        }
+      }
+      if (tb + 8 * UN < t1) {                    // the next batch's loads fly while this one sums
+#pragma unroll
+        for (int r = 0; r < UN; ++r) nx[r] = ld(tb + 8 * UN + 8 * r);
       }
 #pragma unroll
       for (int r = 0; r < UN; ++r) {
