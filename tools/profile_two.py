@@ -17,18 +17,21 @@ ap.add_argument("--units", type=int, default=4096)
 ap.add_argument("--L", type=int, default=32768)
 ap.add_argument("--k", type=int, default=2048)
 ap.add_argument("--gq", type=int, default=4)
+ap.add_argument("--cap", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 cb, q = bench.build_cache(a.units, 0, a.L, a.gq, 1234, dev)
 out = torch.empty(a.units, a.gq, 128, device=dev)
 for _ in range(3):
-    B.decode_step(cb, q, a.k, out=out, kernel=4)
+    B.decode_step(cb, q, a.k, out=out, kernel=4, cap=a.cap)
 clk = torch.zeros(a.units, 12, dtype=torch.int64, device=dev)
 _lib.call("sikv_debug_set_decode_profile", _lib.ptr(clk))
-B.decode_step(cb, q, a.k, out=out, kernel=4)
+B.decode_step(cb, q, a.k, out=out, kernel=4, cap=a.cap)
 torch.cuda.synchronize()
 _lib.call("sikv_debug_set_decode_profile", None)
 c = clk.cpu().numpy().astype(np.float64)
+d = c[:, 2] - c[:, 1]
+print("  score+cand deciles", np.percentile(d, [10, 50, 80, 90, 95, 99, 100]).astype(int).tolist())
 for n, i, j in [("setup+table", 0, 1), ("score+cand", 1, 2), ("select+emit", 2, 3), ("unit total", 0, 3)]:
     d = c[:, j] - c[:, i]
     print(f"  {n:12s} mean {d.mean():9.0f}  p50 {np.median(d):9.0f}  max {d.max():9.0f}")
