@@ -52,7 +52,7 @@ struct TwoArgs {
   int64_t L, U;
   int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
   // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
-  int g_bytes, g_hist, g_forced, g_cand, g_sks;   // g_forced < 0: forced bitmap in gforced
+  int g_bytes, g_hist, g_forced, g_cand, g_sks, g_pre;   // g_forced < 0: forced bitmap in gforced
 };
 
 // ---------------------------------------------------------------- selection
@@ -73,6 +73,21 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
   uint32_t* const forced_s = reinterpret_cast<uint32_t*>(base + (a.g_forced >= 0 ? a.g_forced : 0));
   uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
   uint32_t* sks = reinterpret_cast<uint32_t*>(base + a.g_sks);
+  // the next unit's queries and centroids are copied into the group's staging area by
+  // cp.async while this unit scores and selects
+  float* pre_q = reinterpret_cast<float*>(base + a.g_pre);       // [8][128]
+  const float4* pre_c = reinterpret_cast<const float4*>(pre_q + 8 * FD);   // [512]
+  const uint32_t pre_s = (uint32_t)__cvta_generic_to_shared(pre_q);
+  auto prefetch = [&](int64_t un) {
+    if (un < a.U) {
+      for (int i = tid; i < Gq * FD / 4; i += DT)
+        cp_async16_s(pre_s + 16u * (uint32_t)i, a.q + un * Gq * FD + 4 * i);
+      for (int i = tid; i < 512; i += DT)
+        cp_async16_s(pre_s + (uint32_t)(8 * FD * 4) + 16u * (uint32_t)i, a.cent32 + un * 2048 + 4 * i);
+    }
+    cp_commit();
+  };
+  prefetch((int64_t)blockIdx.x + (int64_t)G * gridDim.x);
   for (int it = 0;; ++it) {
     const int64_t u = (int64_t)blockIdx.x + (int64_t)(2 * it + G) * gridDim.x;
     if (u >= a.U) break;
@@ -80,21 +95,12 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
     if (prof && tid == 0) prof[0] = clock64();
     const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
     const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
-    // every small per-unit input is in flight at once, before any shared-memory step
-    float pq[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) pq[i] = tid + DT * i < Gq * FD ? a.q[u * Gq * FD + tid + DT * i] : 0.f;
-    const float4* c4 = reinterpret_cast<const float4*>(a.cent32 + u * 32 * 16 * 4);
-    const float4 pc0 = c4[tid], pc1 = c4[tid + DT];
     const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
     uint4 wsamp[MAX_SAMPLE_CHUNKS];
     load_sample(g, signs, tid, wsamp);
     uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
-    // q-bar: the Gq heads summed left to right (qs staged in the candidate buffer)
-    float* qs = reinterpret_cast<float*>(cand);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (tid + DT * i < Gq * FD) qs[tid + DT * i] = pq[i];
+    const float* qs = pre_q;
+    cp_wait<0>();                      // this unit's queries / centroids have landed
     for (int i = tid; i < W; i += DT) forced[i] = 0u;
     PG::sync();
     if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
@@ -111,12 +117,13 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int e = tid + DT * r, gg = e >> 4;
-      const float4 c = r ? pc1 : pc0;
+      const float4 c = pre_c[e];
       const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
       lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
                                           __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
     }
-    PG::sync();
+    PG::sync();                        // every read of the staged inputs is done
+    prefetch(u + 2 * gridDim.x);
     build_pair_rows_col<PG>(lut, T);
     if (prof && tid == 0) prof[1] = clock64();
     const int mode = g.mode;
@@ -208,6 +215,8 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap, bool forced_in_smem 
   off += a128(std::max(DW * a.capw * 8, 8 * FD * 4));
   a.g_sks = off;
   off += SEL_SKS ? MAX_SAMPLE_CHUNKS * DT * 4 : 0;
+  a.g_pre = off;
+  off += a128((8 * FD + 2048) * 4);
   a.g_bytes = off;
   a.dstride = two_dstride(L, k, S);
   return a;
