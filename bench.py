@@ -475,7 +475,7 @@ def main():
         dist.init_process_group("nccl")
     line = run_prefill(args, rank, world, cfg) if args.config == "c5" else run_ours(args, rank, world, cfg)
     if rank == 0 and line is not None:
-        if not args.no_cpu_baseline and args.config != "c5":
+        if world == 1 and not args.no_cpu_baseline and args.config != "c5":   # rank 0 at N = 1 only
             cores = os.cpu_count() or 1
             sample = args.cpu_sample or max(8, cores)
             try:
