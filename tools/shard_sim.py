@@ -11,6 +11,7 @@ from paper_2603_14224_b200 import _lib  # noqa: E402
 from paper_2603_14224_b200 import batch as B  # noqa: E402
 
 dev = torch.device("cuda", 0)
+KERNEL = int(os.environ.get("KERNEL", "0"))
 layers, batch, kvh, gq, L, k, _ = bench.CONFIGS["c2"]
 units = layers * batch * kvh
 base = None
@@ -19,12 +20,12 @@ for n in (1, 2, 4, 8):
     cb, q = bench.build_cache(ul, 0, L, gq, 1234, dev)
     out = torch.empty(ul, gq, 128, device=dev)
     for _ in range(5):
-        B.decode_step(cb, q, k, out=out)
+        B.decode_step(cb, q, k, out=out, kernel=KERNEL)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(50):
-        B.decode_step(cb, q, k, out=out)
+        B.decode_step(cb, q, k, out=out, kernel=KERNEL)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 50
