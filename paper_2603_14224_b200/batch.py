@@ -183,8 +183,11 @@ _WS: dict = {}
 
 
 def _workspace(units: int, tokens: int, k: int, sinks: int, device) -> torch.Tensor:
+    """Decode scratch (fallback bitmaps, dynamic lists), cached per (device, stream): steps on
+    one stream reuse it in order; steps on different streams never share one."""
     need = L_.lib().sikv_decode_workspace_bytes_k(units, tokens, k, sinks)
-    key = (device.index if device.index is not None else torch.cuda.current_device())
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=device)
