@@ -56,6 +56,10 @@ def test_full_scale(config, path):
         idx = R.select32(c, qu, k)[0]
         got = sel[u, : int(cnt[u])].cpu().numpy()
         np.testing.assert_array_equal(got, idx)
+        # and the float64 reference selection on the group-summed query (cache.py:290-309):
+        # the float32 order may only move boundary ties (>= k - 1 of k)
+        ref64 = O.select(c, qu.astype(np.float64).sum(axis=0), k)[0]
+        assert len(np.intersect1d(ref64, idx)) >= len(idx) - 1
         out = res.out[u].cpu().numpy()
         for h in range(gq):
             ref = O.sparse_attention(qu[h].astype(np.float64), idx, c)
