@@ -56,8 +56,23 @@ struct TwoArgs {
 };
 
 // ---------------------------------------------------------------- selection
+// the group's staging area for the next unit's queries and centroids (cp.async)
+__device__ __forceinline__ void prefetch_unit(const TwoArgs& a, char* base, int tid, int64_t un) {
+  const uint32_t pre_s = (uint32_t)__cvta_generic_to_shared(base + a.g_pre);
+  if (un >= 0 && un < a.U) {
+    for (int i = tid; i < a.Gq * FD / 4; i += DT)
+      cp_async16_s(pre_s + 16u * (uint32_t)i, a.q + un * a.Gq * FD + 4 * i);
+    for (int i = tid; i < 512; i += DT)
+      cp_async16_s(pre_s + (uint32_t)(8 * FD * 4) + 16u * (uint32_t)i, a.cent32 + un * 2048 + 4 * i);
+  }
+  cp_commit();
+}
+
+// one unit's selection by one 8-warp group: the unit's queries / centroids were prefetched
+// into the staging area; `next` (or -1) is prefetched once they have been consumed.
+// Returns the dynamic list length (the list is in a.dynl).
 template <class PG, int G>
-__device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
+__device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u, int64_t next) {
   const int64_t L = a.L;
   const int W = (int)((L + 31) >> 5);
   const int S = a.S, Gq = a.Gq;
@@ -73,86 +88,80 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
   uint32_t* const forced_s = reinterpret_cast<uint32_t*>(base + (a.g_forced >= 0 ? a.g_forced : 0));
   uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
   uint32_t* sks = reinterpret_cast<uint32_t*>(base + a.g_sks);
-  // the next unit's queries and centroids are copied into the group's staging area by
-  // cp.async while this unit scores and selects
-  float* pre_q = reinterpret_cast<float*>(base + a.g_pre);       // [8][128]
-  const float4* pre_c = reinterpret_cast<const float4*>(pre_q + 8 * FD);   // [512]
-  const uint32_t pre_s = (uint32_t)__cvta_generic_to_shared(pre_q);
-  auto prefetch = [&](int64_t un) {
-    if (un < a.U) {
-      for (int i = tid; i < Gq * FD / 4; i += DT)
-        cp_async16_s(pre_s + 16u * (uint32_t)i, a.q + un * Gq * FD + 4 * i);
-      for (int i = tid; i < 512; i += DT)
-        cp_async16_s(pre_s + (uint32_t)(8 * FD * 4) + 16u * (uint32_t)i, a.cent32 + un * 2048 + 4 * i);
+  const float* pre_q = reinterpret_cast<const float*>(base + a.g_pre);   // [8][128]
+  const float4* pre_c = reinterpret_cast<const float4*>(pre_q + 8 * FD);  // [512]
+  long long* prof = g_prof_two ? g_prof_two + u * 12 : nullptr;
+  if (prof && tid == 0) prof[0] = clock64();
+  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
+  const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
+  const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
+  uint4 wsamp[MAX_SAMPLE_CHUNKS];
+  load_sample(g, signs, tid, wsamp);
+  uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
+  const float* qs = pre_q;
+  cp_wait<0>();                      // this unit's queries / centroids have landed
+  for (int i = tid; i < W; i += DT) forced[i] = 0u;
+  PG::sync();
+  if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
+  for (int j = tid + DT; j < S; j += DT) {
+    const int t = a.sink_idx[u * S + j];
+    atomicOr(&forced[t >> 5], 1u << (t & 31));
+  }
+  if (tid < FD) {
+    float sq = qs[tid];
+    for (int h = 1; h < Gq; ++h) sq = __fadd_rn(sq, qs[h * FD + tid]);
+    qbar[tid] = sq;
+  }
+  PG::sync();
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int e = tid + DT * r, gg = e >> 4;
+    const float4 c = pre_c[e];
+    const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
+    lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
+                                        __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
+  }
+  PG::sync();                        // every read of the staged inputs is done
+  prefetch_unit(a, base, tid, next);
+  build_pair_rows_col<PG>(lut, T);
+  if (prof && tid == 0) prof[1] = clock64();
+  const int mode = g.mode;
+  int32_t* dyn = a.dynl + u * a.dstride;
+  int32_t* sel_u = a.sel ? a.sel + u * a.sel_stride : nullptr;
+  int32_t* sel_count_u = a.sel_count ? a.sel_count + u : nullptr;
+  uint32_t* gt = a.gbits + u * 2 * W;
+  uint32_t* eq = gt + W;
+  int ndyn = -1, fb = 0, need_eq = 0, eq_count = 0;
+  uint32_t kstar = 0;
+  if (mode >= 2) {
+    uint32_t tau;
+    fb = produce_candidates<PG, NoX, ColKey, NB, SEL_SKS>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(),
+                                                           sks) ? 1 : 0;
+    if (prof && tid == 0) prof[2] = clock64();
+    if (!fb) {
+      ndyn = select_emit_candidates<PG>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
+                                        a.R, sel_count_u, kstar);
+    } else {
+      produce_exact<PG, NoX, ColKey>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
     }
-    cp_commit();
-  };
-  prefetch((int64_t)blockIdx.x + (int64_t)G * gridDim.x);
+  }
+  if (ndyn < 0) ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.R, sel_count_u, ms);
+  if (prof && tid == 0) prof[3] = clock64();
+  if (tid == 0) {
+    a.ndyn[u] = ndyn;
+    if (a.diag) a.diag[u] = (mode & 3) | (fb ? 4 : 0);
+  }
+  PG::sync();                       // the group's shared memory is reused by its next unit
+  return ndyn;
+}
+
+template <class PG, int G>
+__device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
+  prefetch_unit(a, sm + TBL_BYTES + G * a.g_bytes, PG::tid(), (int64_t)blockIdx.x + (int64_t)G * gridDim.x);
   for (int it = 0;; ++it) {
     const int64_t u = (int64_t)blockIdx.x + (int64_t)(2 * it + G) * gridDim.x;
     if (u >= a.U) break;
-    long long* prof = g_prof_two ? g_prof_two + u * 12 : nullptr;
-    if (prof && tid == 0) prof[0] = clock64();
-    const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
-    const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
-    const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
-    uint4 wsamp[MAX_SAMPLE_CHUNKS];
-    load_sample(g, signs, tid, wsamp);
-    uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
-    const float* qs = pre_q;
-    cp_wait<0>();                      // this unit's queries / centroids have landed
-    for (int i = tid; i < W; i += DT) forced[i] = 0u;
-    PG::sync();
-    if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
-    for (int j = tid + DT; j < S; j += DT) {
-      const int t = a.sink_idx[u * S + j];
-      atomicOr(&forced[t >> 5], 1u << (t & 31));
-    }
-    if (tid < FD) {
-      float sq = qs[tid];
-      for (int h = 1; h < Gq; ++h) sq = __fadd_rn(sq, qs[h * FD + tid]);
-      qbar[tid] = sq;
-    }
-    PG::sync();
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int e = tid + DT * r, gg = e >> 4;
-      const float4 c = pre_c[e];
-      const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
-      lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
-                                          __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
-    }
-    PG::sync();                        // every read of the staged inputs is done
-    prefetch(u + 2 * gridDim.x);
-    build_pair_rows_col<PG>(lut, T);
-    if (prof && tid == 0) prof[1] = clock64();
-    const int mode = g.mode;
-    int32_t* dyn = a.dynl + u * a.dstride;
-    int32_t* sel_u = a.sel ? a.sel + u * a.sel_stride : nullptr;
-    int32_t* sel_count_u = a.sel_count ? a.sel_count + u : nullptr;
-    uint32_t* gt = a.gbits + u * 2 * W;
-    uint32_t* eq = gt + W;
-    int ndyn = -1, fb = 0, need_eq = 0, eq_count = 0;
-    uint32_t kstar = 0;
-    if (mode >= 2) {
-      uint32_t tau;
-      fb = produce_candidates<PG, NoX, ColKey, NB, SEL_SKS>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(),
-                                                             sks) ? 1 : 0;
-      if (prof && tid == 0) prof[2] = clock64();
-      if (!fb) {
-        ndyn = select_emit_candidates<PG>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
-                                          a.R, sel_count_u, kstar);
-      } else {
-        produce_exact<PG, NoX, ColKey>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
-      }
-    }
-    if (ndyn < 0) ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.R, sel_count_u, ms);
-    if (prof && tid == 0) prof[3] = clock64();
-    if (tid == 0) {
-      a.ndyn[u] = ndyn;
-      if (a.diag) a.diag[u] = (mode & 3) | (fb ? 4 : 0);
-    }
-    PG::sync();                       // the group's shared memory is reused by its next unit
+    select_unit<PG, G>(a, sm, u, u + 2 * gridDim.x);
   }
 }
 
@@ -167,30 +176,34 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 // ---------------------------------------------------------------- attention
 constexpr int ATT_THREADS = 256;
 
-// Every warp starts on its own: q~ and the row indices come straight from global memory
-// (L2), so the only block-wide barriers are the two around the partial merge.
-__global__ void __launch_bounds__(ATT_THREADS, 2) decode_attend_kernel(TwoArgs a) {
-  extern __shared__ __align__(128) char sm[];
-  const int64_t u = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// One unit's attention by one 8-warp group.  Every warp starts on its own: q~ and the row
+// indices come straight from global memory (L2), so the only group-wide barriers are the
+// two around the partial merge.
+template <class PG>
+__device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u) {
+  const int tid = PG::tid(), lane = tid & 31, warp = tid >> 5;
   const int S = a.S, R = a.R, Gq = a.Gq;
-  char* stage = sm;                    // staging, then the merge partials
   const int32_t* dyn = a.dynl + u * a.dstride;
-  const int ndyn = __ldg(a.ndyn + u);
   Attn A;
   attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + u * FD, Gq, lane);
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
   attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
+  const int ndyn = __ldg(a.ndyn + u);
   attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
                stage + warp * 2 * STAGE_BYTES, lane);
-  __syncthreads();
+  PG::sync();
   float* part = reinterpret_cast<float*>(stage);
   float* pm = part + DW * Gq * FD;
   float* pl = pm + DW * Gq;
   attn_write_partial(A, part, pm, pl, warp, Gq, lane);
-  __syncthreads();
-  attn_merge<Cta256>(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+  PG::sync();
+  attn_merge<PG>(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+}
+
+__global__ void __launch_bounds__(ATT_THREADS, 2) decode_attend_kernel(TwoArgs a) {
+  extern __shared__ __align__(128) char sm[];
+  attend_unit<Cta256>(a, sm, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- host side

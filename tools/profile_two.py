@@ -18,15 +18,16 @@ ap.add_argument("--L", type=int, default=32768)
 ap.add_argument("--k", type=int, default=2048)
 ap.add_argument("--gq", type=int, default=4)
 ap.add_argument("--cap", type=int, default=0)
+ap.add_argument("--kernel", type=int, default=4)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 cb, q = bench.build_cache(a.units, 0, a.L, a.gq, 1234, dev)
 out = torch.empty(a.units, a.gq, 128, device=dev)
 for _ in range(3):
-    B.decode_step(cb, q, a.k, out=out, kernel=4, cap=a.cap)
+    B.decode_step(cb, q, a.k, out=out, kernel=a.kernel, cap=a.cap)
 clk = torch.zeros(a.units, 12, dtype=torch.int64, device=dev)
 _lib.call("sikv_debug_set_decode_profile", _lib.ptr(clk))
-B.decode_step(cb, q, a.k, out=out, kernel=4, cap=a.cap)
+B.decode_step(cb, q, a.k, out=out, kernel=a.kernel, cap=a.cap)
 torch.cuda.synchronize()
 _lib.call("sikv_debug_set_decode_profile", None)
 c = clk.cpu().numpy().astype(np.float64)
