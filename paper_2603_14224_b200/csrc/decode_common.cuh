@@ -146,11 +146,25 @@ __device__ __forceinline__ void score_batch(const uint4 (&w)[N], const Key& key,
   for (int x = 0; x < N; x += 2) unpack2(acc[x / 2], s[x], s[x + 1]);
 }
 
-// streaming 16-byte load of the sign plane: read once, no L1 allocation
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+// streaming 16-byte load of the sign plane: read once, no L1 allocation, and first out of L2
+// (the dynamic lists and queries the attention reads next stay resident instead)
+#ifndef SIKV_SIGNS_EVICT_FIRST
+#define SIKV_SIGNS_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
   uint4 v;
+#if SIKV_SIGNS_EVICT_FIRST
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+#endif
   return v;
 }
 
@@ -376,9 +390,14 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
 // (pad_dyn), so staging needs no bounds.  Every lane's shared-memory offsets are fixed for
 // the whole unit (16-byte chunk k of token j lives at chunk k ^ (j & 7)), so they are
 // computed once; token g and g + 8 (and 2t4 + x and 2t4 + x + 8) differ by 1 KiB.
-template <int NSTAGE = 2>
+struct NoPrologue {
+  __device__ __forceinline__ void operator()() const {}
+};
+// `pro` runs once the first blocks' gathers are in flight (e.g. the q~ setup and the forced
+// rows, so their latencies overlap those of the list and the gathers)
+template <int NSTAGE = 2, class Pro = NoPrologue>
 __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, const int32_t* dyn, int ndyn,
-                                             int first, int nw, char* stage, int lane) {
+                                             int first, int nw, char* stage, int lane, Pro pro = Pro()) {
   const int g = lane >> 2, t4 = lane & 3;
   const int nbd = (ndyn + 15) >> 4;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
@@ -415,12 +434,22 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   const int off_vp0 = jv0 * FREC + 16 * (7 ^ stage_sw(jv0));
   const int off_vp1 = jv1 * FREC + 16 * (7 ^ stage_sw(jv1));
   constexpr int P8 = 8 * FREC;
+  // prologue: the next block's indices are requested before this block's wait on its own
+  if (first < nbd) load_ix(first);
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (first + s * nw < nbd) { load_ix(first + s * nw); stage_blk(s * STAGE_BYTES); }
+    const int bn = first + (s + 1) * nw;
+    int32_t tn[4] = {0, 0, 0, 0};
+    if (bn < nbd) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) tn[r] = dyn[bn * 16 + jb + 4 * r];
+    }
+    if (first + s * nw < nbd) stage_blk(s * STAGE_BYTES);
     cp_commit();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) tix[r] = tn[r];
   }
-  if (first + (NSTAGE - 1) * nw < nbd) load_ix(first + (NSTAGE - 1) * nw);
+  pro();
   int buf = 0;
   for (int db = first; db < nbd; db += nw) {
     const int nx = db + (NSTAGE - 1) * nw;
@@ -523,11 +552,17 @@ __device__ __forceinline__ void attn_merge(const float* part, float* pm, float* 
     if (lse_u) lse_u[h] = (M + log2f(den)) * 0.6931471805599453f;
   }
   Grp::sync();
-  for (int e = gtid; e < Gq * FD; e += gsize) {
-    const int h = e / FD, d = e % FD;
-    float num = 0.f;
-    for (int w = 0; w < nw; ++w) num += part[(w * Gq + h) * FD + d] * pm[w * Gq + h];
-    out_u[h * FD + d] = num / pl[h];
+  // four channels per thread (same per-element order: num += part * factor over w)
+  for (int e = gtid; e < Gq * FD / 4; e += gsize) {
+    const int h = e / (FD / 4), d4 = e % (FD / 4);
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int w = 0; w < nw; ++w) {
+      const float4 p = reinterpret_cast<const float4*>(part + (w * Gq + h) * FD)[d4];
+      const float f = pm[w * Gq + h];
+      num.x += p.x * f; num.y += p.y * f; num.z += p.z * f; num.w += p.w * f;
+    }
+    const float den = pl[h];
+    reinterpret_cast<float4*>(out_u + h * FD)[d4] = make_float4(num.x / den, num.y / den, num.z / den, num.w / den);
   }
 }
 
@@ -650,15 +685,16 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
   const int Li = (int)g.L;
   const int end_s = g.nsc * g.sstride;
   const uint4* pbase = signs + tid;
+  const uint64_t pol = l2_evict_first_policy();
   auto load_batch = [&](int c0, uint4 (&w)[NBT]) {
     const uint4* p = pbase + (int64_t)c0 * 256;     // constant offsets 4 KiB apart: no per-load address math
     if ((c0 + NBT) * 256 <= Li) {
 #pragma unroll
-      for (int x = 0; x < NBT; ++x) w[x] = ld_stream(p + 256 * x);
+      for (int x = 0; x < NBT; ++x) w[x] = ld_stream(p + 256 * x, pol);
     } else {
       const int t0 = c0 * 256 + tid;
 #pragma unroll
-      for (int x = 0; x < NBT; ++x) w[x] = t0 + 256 * x < Li ? ld_stream(p + 256 * x) : make_uint4(0, 0, 0, 0);
+      for (int x = 0; x < NBT; ++x) w[x] = t0 + 256 * x < Li ? ld_stream(p + 256 * x, pol) : make_uint4(0, 0, 0, 0);
     }
   };
   for (int attempt = 0;; ++attempt) {

@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 
 // ---------------------------------------------------------------- attention
 constexpr int ATT_THREADS = 256;
+#ifndef SIKV_ATT_PREFETCH
+#define SIKV_ATT_PREFETCH 1
+#endif
 
 // One unit's attention by one 8-warp group.  Every warp starts on its own: q~ and the row
 // indices come straight from global memory (L2), so the only group-wide barriers are the
@@ -184,11 +187,17 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   const int tid = PG::tid(), lane = tid & 31, warp = tid >> 5;
   const int S = a.S, R = a.R, Gq = a.Gq;
   const int32_t* dyn = a.dynl + u * a.dstride;
-  Attn A;
-  attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + u * FD, Gq, lane);
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
-  attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
+  const uint32_t* ffrag_u = a.ffrag + u * a.fblocks * 2 * 32 * 32;
+#if SIKV_ATT_PREFETCH
+  // start the forced fragments and the list on their way to L2 while q~ loads
+  if (tid < nbf * 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ffrag_u) + 128 * tid));
+  if (tid < a.dstride / 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dyn) + 128 * tid));
+#endif
+  Attn A;
+  attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + u * FD, Gq, lane);
+  attn_forced(A, ffrag_u, nf, warp, DW, lane);
   const int ndyn = __ldg(a.ndyn + u);
   attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
                stage + warp * 2 * STAGE_BYTES, lane);
