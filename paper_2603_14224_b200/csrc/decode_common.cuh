@@ -10,6 +10,13 @@ constexpr int TBL_BYTES = 256 * 64 * 4;   // pair table: 256 byte values x 64 co
 constexpr int NB = 8;                     // chunks (of 256 tokens) scored per thread per batch
 constexpr int STAGE_BYTES = 16 * FREC;    // one 16-token block of records
 constexpr int MAX_SAMPLE_CHUNKS = 8;
+// sample chunks are at least SSTRIDE_MIN chunks apart (>= NB: one per B2 batch at most), so
+// short units (< 32K tokens) still sample up to 8 chunks: a tighter threshold, fewer candidates
+#ifndef SIKV_SSTRIDE_MIN
+#define SIKV_SSTRIDE_MIN 8
+#endif
+constexpr int SSTRIDE_MIN = SIKV_SSTRIDE_MIN;
+static_assert(SSTRIDE_MIN >= NB, "at most one sample chunk per B2 batch");
 
 // ---------------------------------------------------------------- pair table
 // LUT[g][c] = q-bar_g . centroid[g][c] (float32, no FMA, the reference pairing) and the
@@ -606,7 +613,7 @@ __device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw,
   else if (g.keff == ncand) g.mode = 1;
   else if ((int64_t)g.nchunks * 32 <= (int64_t)capw) g.mode = 2;
   else g.mode = 3;
-  g.sstride = g.mode == 3 ? max(16, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
+  g.sstride = g.mode == 3 ? max(SSTRIDE_MIN, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
   g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
   g.flim = S > 0 ? (int64_t)sink_idx_u[S - 1] + 1 : 0;
   return g;

@@ -24,6 +24,9 @@
 namespace sikv {
 
 constexpr int SEL_THREADS = 512;
+#ifndef SIKV_PDL
+#define SIKV_PDL 1   // attention launched as a programmatic dependent of the selection grid
+#endif
 __device__ long long* g_prof_two = nullptr;   // optional per-unit phase clocks (profiling)
 #ifndef SIKV_SEL_SKS
 #define SIKV_SEL_SKS 0
@@ -167,6 +170,11 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
 
 __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
+#if SIKV_PDL
+  // the attention grid may be scheduled onto SMs as this grid's CTAs retire: it attends the
+  // forced rows, then waits for this grid to complete (griddepcontrol.wait) before the lists
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   // group from a value the compiler can prove warp-uniform (uniform-datapath table base)
   const int grp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 8), 0);
   if (grp == 0) select_group<SG0, 0>(a, sm);
@@ -174,17 +182,23 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 }
 
 // ---------------------------------------------------------------- attention
-constexpr int ATT_THREADS = 256;
+#ifndef SIKV_ATT_WARPS
+#define SIKV_ATT_WARPS 4
+#endif
+constexpr int ATT_WARPS = SIKV_ATT_WARPS;          // warps per attention CTA (one unit each)
+constexpr int ATT_THREADS = 32 * ATT_WARPS;
+constexpr int ATT_CTAS_PER_SM = 16 / ATT_WARPS;
 #ifndef SIKV_ATT_PREFETCH
 #define SIKV_ATT_PREFETCH 1
 #endif
 
-// One unit's attention by one 8-warp group.  Every warp starts on its own: q~ and the row
-// indices come straight from global memory (L2), so the only group-wide barriers are the
+// One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
+// indices come straight from global memory (L2), so the only CTA-wide barriers are the
 // two around the partial merge.
-template <class PG>
+template <int NW>
 __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u) {
-  const int tid = PG::tid(), lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = 32 * NW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = a.S, R = a.R, Gq = a.Gq;
   const int32_t* dyn = a.dynl + u * a.dstride;
   const int nf = S + R;
@@ -192,27 +206,32 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   const uint32_t* ffrag_u = a.ffrag + u * a.fblocks * 2 * 32 * 32;
 #if SIKV_ATT_PREFETCH
   // start the forced fragments and the list on their way to L2 while q~ loads
-  if (tid < nbf * 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ffrag_u) + 128 * tid));
-  if (tid < a.dstride / 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dyn) + 128 * tid));
+  for (int i = tid; i < nbf * 64; i += NT)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ffrag_u) + 128 * i));
+  for (int i = tid; i < a.dstride / 32; i += NT)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dyn) + 128 * i));
 #endif
   Attn A;
   attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + u * FD, Gq, lane);
-  attn_forced(A, ffrag_u, nf, warp, DW, lane);
+  attn_forced(A, ffrag_u, nf, warp, NW, lane);
+#if SIKV_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the selection grid is complete
+#endif
   const int ndyn = __ldg(a.ndyn + u);
-  attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
+  attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
                stage + warp * 2 * STAGE_BYTES, lane);
-  PG::sync();
+  __syncthreads();
   float* part = reinterpret_cast<float*>(stage);
-  float* pm = part + DW * Gq * FD;
-  float* pl = pm + DW * Gq;
+  float* pm = part + NW * Gq * FD;
+  float* pl = pm + NW * Gq;
   attn_write_partial(A, part, pm, pl, warp, Gq, lane);
-  PG::sync();
-  attn_merge<PG>(part, pm, pl, DW, Gq, tid, DT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+  __syncthreads();
+  attn_merge<Cta256>(part, pm, pl, NW, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
 }
 
-__global__ void __launch_bounds__(ATT_THREADS, 2) decode_attend_kernel(TwoArgs a) {
+__global__ void __launch_bounds__(ATT_THREADS, ATT_CTAS_PER_SM) decode_attend_kernel(TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
-  attend_unit<Cta256>(a, sm, blockIdx.x);
+  attend_unit<ATT_WARPS>(a, sm, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- host side
@@ -256,7 +275,7 @@ int two_select_smem_bytes(int64_t L, int k, int S, int cap) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, two_forced_smem(L, k, S, cap)).g_bytes + SIKV_SEL_PAD;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
-  return std::max(DW * 2 * STAGE_BYTES, DW * Gq * (FD + 2) * 4);
+  return std::max(ATT_WARPS * 2 * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
@@ -292,8 +311,22 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   const int smem_a = two_attend_smem_bytes(L, k, S, Gq);
   e = cudaFuncSetAttribute(decode_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
   if (e != cudaSuccess) return e;
+#if SIKV_PDL
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)U);
+  cfg.blockDim = dim3(ATT_THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem_a;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_attend_kernel, a);
+#else
   decode_attend_kernel<<<(unsigned)U, ATT_THREADS, smem_a, st>>>(a);
   return cudaGetLastError();
+#endif
 }
 
 }  // namespace sikv

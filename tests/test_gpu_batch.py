@@ -159,18 +159,32 @@ def test_decode_sampled_threshold_32k(c32k, kernel):
     assert ((d & 3) == 3).all() and not (d & 4).any()
 
 
+def _assert_order_close(a, b, lse_a=None, lse_b=None):
+    """Same selection, attention split over a different number of warps: the outputs agree to
+    the fp16 rounding of P against each warp's own running max."""
+    rel = (a - b).norm(dim=-1) / b.norm(dim=-1)
+    assert rel.max().item() <= 1e-3, rel.max().item()
+    if lse_a is not None:
+        torch.testing.assert_close(lse_a, lse_b, rtol=1e-5, atol=1e-4)
+
+
 @pytest.mark.parametrize("kernel", [2, 4])
 def test_kernels_agree_bitwise(c32k, kernel):
-    """The one-CTA, persistent and two-kernel paths run the same arithmetic in the same
-    order: outputs and selections are bit-identical."""
+    """The one-CTA and persistent paths run the same arithmetic in the same order: outputs and
+    selections are bit-identical.  The two-kernel path selects bit-identically; its attention
+    CTAs have 4 warps instead of 8, so its outputs agree to fp16 P rounding."""
     units, cb, oc, q = c32k
     r1 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=1)
     r2 = B.decode_step(cb, q, 2048, with_selection=True, with_lse=True, kernel=kernel)
     assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.counts, r2.counts)
-    assert torch.equal(r1.out, r2.out) and torch.equal(r1.lse, r2.lse)
-    # without the sorted selection the dynamic rows come straight from the candidate segments
+    if kernel == 2:
+        assert torch.equal(r1.out, r2.out) and torch.equal(r1.lse, r2.lse)
+    else:
+        _assert_order_close(r2.out, r1.out, r2.lse, r1.lse)
+    # without the sorted selection the dynamic rows come straight from the candidate segments,
+    # in the same order
     r3 = B.decode_step(cb, q, 2048, with_lse=True, kernel=kernel)
-    assert torch.equal(r1.out, r3.out) and torch.equal(r1.lse, r3.lse)
+    assert torch.equal(r2.out, r3.out) and torch.equal(r2.lse, r3.lse)
 
 
 def test_split_kernel_matches_single_cta(c32k):
@@ -210,10 +224,14 @@ def test_persistent_kernel_many_units():
     r1 = B.decode_step(cb, q, 100, with_selection=True, kernel=1)
     for kern in (2, 4):
         r2 = B.decode_step(cb, q, 100, with_selection=True, kernel=kern)
-        assert torch.equal(r1.selection, r2.selection) and torch.equal(r1.out, r2.out)
+        assert torch.equal(r1.selection, r2.selection)
+        if kern == 2:
+            assert torch.equal(r1.out, r2.out)
+        else:
+            _assert_order_close(r2.out, r1.out)
         assert torch.equal(r2.out[0::2], r2.out[0:1].expand(reps, -1, -1))
     r0 = B.decode_step(cb, q, 100, with_selection=True)        # auto: two kernels at 800 units
-    assert torch.equal(r1.selection, r0.selection) and torch.equal(r1.out, r0.out)
+    assert torch.equal(r2.selection, r0.selection) and torch.equal(r2.out, r0.out)
 
 
 def test_decode_ties_lowest_index_first():

@@ -41,9 +41,10 @@ for f, ln, src, s, ni, st in sorted(recs, key=lambda x: -x[k])[:n]:
 
 if "--ranges" in sys.argv:
     # decode_common.cuh regions (edit when the file moves)
-    regions = [("table build", "decode_common.cuh", 14, 45), ("score_batch", "decode_common.cuh", 79, 99),
-               ("attention", "decode_common.cuh", 133, 400), ("sample/tau", "decode_common.cuh", 427, 573),
-               ("B2 loop+append", "decode_common.cuh", 574, 642), ("select/emit", "decode_common.cuh", 643, 900)]
+    regions = [("table build", "decode_common.cuh", 14, 70), ("score_batch", "decode_common.cuh", 71, 200),
+               ("attention", "decode_common.cuh", 240, 570), ("geom/sample load", "decode_common.cuh", 571, 634),
+               ("B1 sample/tau", "decode_common.cuh", 635, 771), ("B2 loop+append", "decode_common.cuh", 772, 841),
+               ("exact fallback", "decode_common.cuh", 842, 876), ("select/emit", "decode_common.cuh", 877, 1100)]
     agg = defaultdict(lambda: [0.0, 0.0])
     for f, ln, src, s, ni, st in recs:
         name = f
