@@ -75,6 +75,9 @@ __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent,
 // 16 of its half-warp copy) sit in 4 registers and the PRMT that extracts the sign byte also
 // picks the column byte (sign-replicating selectors zero the high bytes: offsets < 128).
 // Both are bank-conflict free: the 32 lanes of a step hit 32 distinct columns mod 32.
+#ifndef SIKV_KEY_OPAQUE
+#define SIKV_KEY_OPAQUE 1
+#endif
 struct RepKey {
   uint32_t lb;
   __device__ __forceinline__ explicit RepKey(int lane) : lb((uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15))) {}
@@ -92,6 +95,11 @@ struct ColKey {
 #pragma unroll
       for (int m = 0; m < 4; ++m) v |= (uint32_t)(4 * (16 * h + ((j + 4 * k + m) & 15))) << (8 * m);
       c[k] = v;
+#if SIKV_KEY_OPAQUE
+      // opaque to the compiler: kept in registers instead of being rematerialised from the
+      // lane id inside every scoring batch (~25 integer instructions per batch)
+      asm volatile("" : "+r"(c[k]));
+#endif
     }
   }
   __device__ __forceinline__ uint32_t off(uint32_t w, int i) const {
