@@ -80,7 +80,11 @@ __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent,
 #endif
 struct RepKey {
   uint32_t lb;
-  __device__ __forceinline__ explicit RepKey(int lane) : lb((uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15))) {}
+  __device__ __forceinline__ explicit RepKey(int lane) : lb((uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15))) {
+#if SIKV_KEY_OPAQUE
+    asm volatile("" : "+r"(lb));
+#endif
+  }
   __device__ __forceinline__ uint32_t off(uint32_t w, int i) const {
     return prmt(w, lb, 0x5504u | ((uint32_t)(i & 3) << 4)) + 4 * i;
   }
