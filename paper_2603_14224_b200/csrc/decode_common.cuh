@@ -858,7 +858,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
 
 // Exact fallback: multi-pass radix select over rescored keys, then gt / eq bitmaps (zeroed
 // here; smem or global) of key > K* and key == K*.  hist needs NBIN + 33 ints.
-template <class Grp, class Xch = NoX, class Key = RepKey>
+template <class Grp, class Xch = NoX, class Key = RepKey, int NBINT = NBIN>
 __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* signs, const char* T,
                                               const uint32_t* forced, int* hist, Misc* ms, uint32_t* gt,
                                               uint32_t* eq, uint32_t& kstar, int& need_eq, int& eq_count,
@@ -867,7 +867,7 @@ __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* si
   const Key lb(lane);
   const int64_t L = g.L;
   const int nchunks = g.nchunks;
-  radix_kth<Grp, Xch>([&](auto f) {
+  radix_kth<Grp, Xch, NBINT>([&](auto f) {
     for (int c = 0; c < nchunks; ++c) {
       const int64_t t = (int64_t)c * 256 + tid;
       if (t < L && !forced_bit(forced, t)) f(f32_key(score_token(__ldg(signs + t), lb, T)));
@@ -893,7 +893,7 @@ __device__ __forceinline__ void produce_exact(const UnitGeom& g, const uint4* si
 
 // Exact k-th key among the candidate segments: xk (relative to tau) and how many of the
 // items equal to it belong to the top keff.
-template <class Grp, class Xch = NoX>
+template <class Grp, class Xch = NoX, int NBINT = NBIN>
 __device__ __forceinline__ void kth_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
                                                     uint32_t maxx, int* hist, Misc* ms, uint32_t& xk,
                                                     int& need_eq, const Xch& xch = Xch()) {
@@ -901,7 +901,7 @@ __device__ __forceinline__ void kth_from_candidates(const UnitGeom& g, const uin
   const uint32_t* seg = cand + 2 * warp * g.capw;
   const int n = wcnt[warp];
   maxx = xch.maxu(maxx);
-  radix_kth<Grp, Xch>([&](auto f) {
+  radix_kth<Grp, Xch, NBINT>([&](auto f) {
     for (int i = lane; i < n; i += 32) f(seg[2 * i]);
   }, maxx, g.keff, hist, ms, xk, need_eq, xch);
 }
@@ -1039,14 +1039,14 @@ __device__ __forceinline__ int emit_selection(const UnitGeom& g, int mode, const
 // fallback): the exact k-th key, then the dynamic list from the segments.  The sorted
 // selection (sel_u / sel_count_u, optional) and the rare index-cut ties go through the
 // bitmaps.  Returns the dynamic count; kstar = absolute k-th key.
-template <class Grp>
+template <class Grp, int NBINT = NBIN>
 __device__ __forceinline__ int select_emit_candidates(const UnitGeom& g, const uint32_t* forced, const uint32_t* cand,
                                                       const int* wcnt, uint32_t maxx, uint32_t tau, int* hist,
                                                       Misc* ms, uint32_t* gt, uint32_t* eq, int32_t* dyn,
                                                       int32_t* sel_u, int R, int32_t* sel_count_u, uint32_t& kstar) {
   uint32_t xk;
   int need_eq;
-  kth_from_candidates<Grp>(g, cand, wcnt, maxx, hist, ms, xk, need_eq);
+  kth_from_candidates<Grp, NoX, NBINT>(g, cand, wcnt, maxx, hist, ms, xk, need_eq);
   kstar = xk + tau;
   int ndyn = emit_from_segments<Grp>(g, cand, wcnt, xk, need_eq, dyn, ms);
   if (ndyn < 0 || sel_u || sel_count_u) {

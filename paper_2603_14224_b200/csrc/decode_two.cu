@@ -31,7 +31,13 @@ __device__ long long* g_prof_two = nullptr;   // optional per-unit phase clocks 
 #ifndef SIKV_SEL_SKS
 #define SIKV_SEL_SKS 0
 #endif
-constexpr bool SEL_SKS = SIKV_SEL_SKS;    // sample keys in shared memory (A/B: slower at C2)
+constexpr bool SEL_SKS = SIKV_SEL_SKS;
+// the selection groups' radix digit: 9 bits (512 bins) — at C4 (1.4 K candidates per unit)
+// 2.5% faster than 11 bits, neutral at C2; path 1 keeps 11 bits (C3: 6 K candidates)
+#ifndef SIKV_SEL_RB
+#define SIKV_SEL_RB 9
+#endif
+constexpr int SEL_NBIN = 1 << SIKV_SEL_RB;    // sample keys in shared memory (A/B: slower at C2)
 using SG0 = NamedGroup<1, 0>;
 using SG1 = NamedGroup<2, 256>;
 
@@ -142,10 +148,10 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
                                                            sks) ? 1 : 0;
     if (prof && tid == 0) prof[2] = clock64();
     if (!fb) {
-      ndyn = select_emit_candidates<PG>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
+      ndyn = select_emit_candidates<PG, SEL_NBIN>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
                                         a.R, sel_count_u, kstar);
     } else {
-      produce_exact<PG, NoX, ColKey>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
+      produce_exact<PG, NoX, ColKey, SEL_NBIN>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
     }
   }
   if (ndyn < 0) ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.R, sel_count_u, ms);
@@ -249,7 +255,7 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap, bool forced_in_smem 
   a.capw = std::max(32, cap / DW);
   int off = a128((512 + FD + 256 + 256) * 4 + (int)sizeof(Misc));
   a.g_hist = off;
-  off += a128((NBIN + 64) * 4);
+  off += a128((SEL_NBIN + 64) * 4);
   a.g_forced = forced_in_smem ? off : -1;
   if (forced_in_smem) off += a128(W * 4);
   a.g_cand = off;

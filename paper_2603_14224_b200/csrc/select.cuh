@@ -98,11 +98,12 @@ constexpr int RB = SIKV_RB;         // digit bits per pass
 constexpr int NBIN = 1 << RB;       // 2048 bins; thread t owns bins [NBIN-8(t+1), NBIN-8t)
 
 // Group-wide: choose the digit whose descending cumulative count reaches ms->rem_sel.
-template <class Grp = Cta256>
+template <class Grp = Cta256, int NBINT = NBIN>
 __device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
+  static_assert(NBINT >= DT && NBINT % DT == 0, "bins per thread");
   const int tid = Grp::tid();
-  constexpr int PER = NBIN / DT;
-  const int top = NBIN - 1 - PER * tid;          // this thread owns bins top, top-1, ..., top-PER+1
+  constexpr int PER = NBINT / DT;
+  const int top = NBINT - 1 - PER * tid;          // this thread owns bins top, top-1, ..., top-PER+1
   int s = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) s += hist[top - ((i + tid) & (PER - 1))];   // rotated: no bank conflicts
@@ -123,32 +124,34 @@ __device__ __forceinline__ void pick_digit_big(const int* hist, Misc* ms) {
 // Exact k-th largest of a multiset of 32-bit values x (all <= maxx).  `each(f)` must call
 // f(x) once per item on the calling thread (every thread of the group calls each()).
 // Returns the k-th value and how many items equal to it belong to the top `rank` (ties
-// are then resolved by index by the caller).  hist must hold NBIN + 33 ints.
-template <class Grp = Cta256, class Xch = NoX, typename Each>
+// are then resolved by index by the caller).  hist must hold NBINT + 33 ints (NBINT = 2^digit
+// bits: 2048 by default, 512 for the two-kernel path's selection groups).
+template <class Grp = Cta256, class Xch = NoX, int NBINT = NBIN, typename Each>
 __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, int* hist, Misc* ms,
                                           uint32_t& kth, int& need_eq, const Xch& xch = Xch()) {
   const int tid = Grp::tid();
   const int nbits = maxx ? 32 - __clz(maxx) : 0;
-  int* list = hist + NBIN;           // up to 32 items of a small boundary bin (+ counter)
+  constexpr int RBT = __builtin_ctz(NBINT);
+  int* list = hist + NBINT;          // up to 32 items of a small boundary bin (+ counter)
   if (tid == 0) ms->rem_sel = rank;
   uint32_t prefix = 0;
   int shift = nbits;
   Grp::sync();
   while (shift > 0) {
-    const int dbits = shift >= RB ? RB : shift;
+    const int dbits = shift >= RBT ? RBT : shift;
     const int hi = shift;            // bits >= hi are already fixed in prefix
     shift -= dbits;
-    for (int i = tid; i < NBIN; i += DT) hist[i] = 0;
+    for (int i = tid; i < NBINT; i += DT) hist[i] = 0;
     if (tid == 0) list[32] = 0;
     Grp::sync();
     const uint32_t want = hi >= 32 ? 0u : (prefix >> hi);
     const int sh = shift;
     each([&](uint32_t x) {
-      if ((hi >= 32 ? 0u : (x >> hi)) == want) atomicAdd(&hist[(x >> sh) & (NBIN - 1)], 1);
+      if ((hi >= 32 ? 0u : (x >> hi)) == want) atomicAdd(&hist[(x >> sh) & (NBINT - 1)], 1);
     });
     Grp::sync();
     const int* mh = xch.hist4k(hist);   // cluster: the sum of every CTA's histogram
-    pick_digit_big<Grp>(mh, ms);
+    pick_digit_big<Grp, NBINT>(mh, ms);
     const uint32_t d = (uint32_t)ms->digit;
     prefix |= d << shift;
     const int nb = mh[d];
