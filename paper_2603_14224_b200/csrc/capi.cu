@@ -41,7 +41,7 @@ cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, co
                                 const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, int, float*,
                                 float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t);
 size_t ws_workspace_bytes(int64_t U, int64_t L);
-int two_select_smem_bytes(int64_t L, int k, int S, int cap);
+int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq);
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq);
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
@@ -240,9 +240,9 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     // its shared memory at or below the 164 KB carveout (L1 >= 92 KB) while the candidate
     // buffer stays >= 1.5 k + 1024 (no segment overflow at the sampled threshold)
     const int soft_cap = (int)std::max<int64_t>(ke + ke / 2 + 1024, floor_cap);
-    while (cap <= 0 && tcap > soft_cap && two_select_smem_bytes(tokens, k, sinks, tcap) > 164 * 1024) tcap -= 64;
-    while (cap <= 0 && tcap > floor_cap && two_select_smem_bytes(tokens, k, sinks, tcap) > max_smem()) tcap -= 64;
-    const bool fits = two_select_smem_bytes(tokens, k, sinks, tcap) <= max_smem() &&
+    while (cap <= 0 && tcap > soft_cap && two_select_smem_bytes(tokens, k, sinks, tcap, gq) > 164 * 1024) tcap -= 64;
+    while (cap <= 0 && tcap > floor_cap && two_select_smem_bytes(tokens, k, sinks, tcap, gq) > max_smem()) tcap -= 64;
+    const bool fits = two_select_smem_bytes(tokens, k, sinks, tcap, gq) <= max_smem() &&
                       two_attend_smem_bytes(tokens, k, sinks, gq) <= max_smem();
     const bool ws_ok = workspace && workspace_bytes >= two_workspace_bytes(units, tokens, k, sinks);
     if (fits && ws_ok) {
