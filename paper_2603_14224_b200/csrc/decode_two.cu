@@ -270,7 +270,6 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap, int Gq, bool forced_
 }
 
 // the forced bitmaps stay in shared memory unless that is what keeps the kernel from fitting
-// the forced bitmaps stay in shared memory unless that is what keeps the kernel from fitting
 // (moving them to global memory to get C2 under the 164 KB carveout measured 1.5% slower)
 static bool two_forced_smem(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, true).g_bytes <= 227 * 1024;
