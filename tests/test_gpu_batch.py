@@ -255,3 +255,12 @@ def test_decode_ties_lowest_index_first():
         idx = R.select32(c, base.queries[:4].astype(np.float32), k)[0]
         got = res.selection[0, : res.counts[0]].cpu().numpy()
         np.testing.assert_array_equal(got, idx)
+
+
+@pytest.mark.parametrize("gq", [1, 8])
+@pytest.mark.parametrize("kernel", [1, 4])
+def test_decode_gqa_extremes(gq, kernel):
+    """GQA group sizes 1 and 8: the two-kernel path stages Gq x 128 queries per unit and the
+    attention packs Gq heads into the mma N dimension (8 = no padding)."""
+    units, cb, oc, q = make(4096, [300, 301], gq=gq)
+    _check_decode(units, cb, oc, q, 512, kernel=kernel)
