@@ -648,6 +648,12 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
 // yields fewer than k candidates (tau too high), r is rescaled from the observed counts and
 // the scan is repeated (at most kRetries times) before falling back to the exact path.
 constexpr int kRetries = 2;
+#ifndef SIKV_TAU_SIG
+#define SIKV_TAU_SIG 3.0   // sample-rank margin: r = e + SIG sqrt(e) + ADD
+#endif
+#ifndef SIKV_TAU_ADD
+#define SIKV_TAU_ADD 8.0
+#endif
 
 // SKS: the sample keys live in shared memory (sks[x * DT + tid]) instead of 8 registers
 // across the B2 scan (they are only needed again for a retry).
@@ -697,7 +703,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     kmn = ms->tau;
     xch.sample(nsv, kmx, kmn);            // cluster: the whole unit's sample
     const double e = (double)g.keff * (double)nsv / (double)(g.ncand);
-    r = min((int)ceil(e + 3.0 * sqrt(e) + 8.0), nsv);
+    r = min((int)ceil(e + SIKV_TAU_SIG * sqrt(e) + SIKV_TAU_ADD), nsv);
   }
   const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
   const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
