@@ -404,6 +404,65 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
   }
 }
 
+// fragment offsets of a lane inside a staged 16-token block (token g for K, tokens 2t4 /
+// 2t4 + 1 for V; the +8 tokens are P8 bytes further)
+struct BlkOffs {
+  int k4, kp, vw0, vw1, vp0, vp1;
+};
+constexpr int P8 = 8 * FREC;
+
+// QK^T, online softmax and PV of one staged 16-token block (rem = valid rows from its start)
+__device__ __forceinline__ void attn_block(Attn& A, const char* sb, const BlkOffs& o, int rem, int lane) {
+  float sacc[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const uint4 k4 = *reinterpret_cast<const uint4*>(sb + o.k4 + nt * P8);
+    const uint4 kp = *reinterpret_cast<const uint4*>(sb + o.kp + nt * P8);
+    const uint32_t kw[4] = {k4.x, k4.y, k4.z, k4.w};
+    const uint32_t par[4] = {kp.x, kp.y, kp.z, kp.w};
+    sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+    for (int grp = 0; grp < 4; ++grp) {
+      const __half2 qs2 = u2h(prmt(par[grp], par[grp], 0x1010u));
+      const uint32_t zp2 = prmt(par[grp], par[grp], 0x3232u);
+      // k-steps s = 2 grp (bytes 0, 1 of word grp) and 2 grp + 1 (bytes 2, 3)
+      mma16816(sacc[nt], A.qa[2 * grp][0], 0u, A.qa[2 * grp][1], 0u, k_dequant2<0>(kw[grp], qs2, zp2),
+               k_dequant2<1>(kw[grp], qs2, zp2));
+      mma16816(sacc[nt], A.qa[2 * grp + 1][0], 0u, A.qa[2 * grp + 1][1], 0u, k_dequant2<2>(kw[grp], qs2, zp2),
+               k_dequant2<3>(kw[grp], qs2, zp2));
+    }
+  }
+  // V words and params of tokens 2t4, 2t4+1, 2t4+8, 2t4+9
+  uint32_t vw[4];
+  uint4 vp[4];
+  vw[0] = *reinterpret_cast<const uint32_t*>(sb + o.vw0);
+  vw[1] = *reinterpret_cast<const uint32_t*>(sb + o.vw1);
+  vw[2] = *reinterpret_cast<const uint32_t*>(sb + o.vw0 + P8);
+  vw[3] = *reinterpret_cast<const uint32_t*>(sb + o.vw1 + P8);
+  vp[0] = *reinterpret_cast<const uint4*>(sb + o.vp0);
+  vp[1] = *reinterpret_cast<const uint4*>(sb + o.vp1);
+  vp[2] = *reinterpret_cast<const uint4*>(sb + o.vp0 + P8);
+  vp[3] = *reinterpret_cast<const uint4*>(sb + o.vp1 + P8);
+  attn_softmax_pv(A, sacc, rem, lane, [&](int jg, uint32_t (&v)[2][4]) {
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+      const uint32_t pa[4] = {vp[2 * pr].x, vp[2 * pr].y, vp[2 * pr].z, vp[2 * pr].w};
+      const uint32_t pb[4] = {vp[2 * pr + 1].x, vp[2 * pr + 1].y, vp[2 * pr + 1].z, vp[2 * pr + 1].w};
+      const uint32_t xj = prmt(vw[2 * pr], vw[2 * pr + 1],
+                               (uint32_t)(jg | (jg << 4) | ((4 + jg) << 8) | ((4 + jg) << 12)));
+      const __half2 qs2 = u2h(prmt(pa[jg], pb[jg], 0x5410u));
+      const __half2 zp2 = u2h(prmt(pa[jg], pb[jg], 0x7632u));
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const uint32_t xx = lop3_and_or(xj, 0x00030003u << (2 * ii), kMagic(ii));
+        const __half2 c = __hsub2(u2h(xx), u2h(kMagic(ii)));
+        // m = 2jg + (ii >> 1), e = ii & 1 -> a-register 2*pr + e of fragment m
+        v[ii >> 1][2 * pr + (ii & 1)] = h2u(__hfma2(c, qs2, zp2));
+      }
+    }
+  });
+}
+
 // dynamic rows: blocks first, first + nw, ... of [0, nbd), staged by cp.async (NSTAGE
 // buffers per warp: NSTAGE - 1 blocks in flight) and dequantised into mma fragments.  The list is padded to a multiple of 16
 // (pad_dyn), so staging needs no bounds.  Every lane's shared-memory offsets are fixed for
@@ -446,13 +505,13 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   };
   // fragment offsets (token g for K, tokens 2t4 / 2t4 + 1 for V; +1 KiB for the +8 tokens)
   const int jk = g, jv0 = 2 * t4, jv1 = 2 * t4 + 1;
-  const int off_k4 = jk * FREC + 16 * (t4 ^ stage_sw(jk));
-  const int off_kp = jk * FREC + 16 * (6 ^ stage_sw(jk));
-  const int off_vw0 = jv0 * FREC + 16 * ((4 + (g >> 2)) ^ stage_sw(jv0)) + 4 * (g & 3);
-  const int off_vw1 = jv1 * FREC + 16 * ((4 + (g >> 2)) ^ stage_sw(jv1)) + 4 * (g & 3);
-  const int off_vp0 = jv0 * FREC + 16 * (7 ^ stage_sw(jv0));
-  const int off_vp1 = jv1 * FREC + 16 * (7 ^ stage_sw(jv1));
-  constexpr int P8 = 8 * FREC;
+  BlkOffs o;
+  o.k4 = jk * FREC + 16 * (t4 ^ stage_sw(jk));
+  o.kp = jk * FREC + 16 * (6 ^ stage_sw(jk));
+  o.vw0 = jv0 * FREC + 16 * ((4 + (g >> 2)) ^ stage_sw(jv0)) + 4 * (g & 3);
+  o.vw1 = jv1 * FREC + 16 * ((4 + (g >> 2)) ^ stage_sw(jv1)) + 4 * (g & 3);
+  o.vp0 = jv0 * FREC + 16 * (7 ^ stage_sw(jv0));
+  o.vp1 = jv1 * FREC + 16 * (7 ^ stage_sw(jv1));
   // prologue: the next block's indices are requested before this block's wait on its own
   if (first < nbd) load_ix(first);
 #pragma unroll
@@ -479,56 +538,7 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     cp_commit();
     cp_wait<NSTAGE - 1>();
     __syncwarp();
-    const char* sb = stage + buf * STAGE_BYTES;
-    const int base = db * 16;
-    float sacc[2][4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      const uint4 k4 = *reinterpret_cast<const uint4*>(sb + off_k4 + nt * P8);
-      const uint4 kp = *reinterpret_cast<const uint4*>(sb + off_kp + nt * P8);
-      const uint32_t kw[4] = {k4.x, k4.y, k4.z, k4.w};
-      const uint32_t par[4] = {kp.x, kp.y, kp.z, kp.w};
-      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-      for (int grp = 0; grp < 4; ++grp) {
-        const __half2 qs2 = u2h(prmt(par[grp], par[grp], 0x1010u));
-        const uint32_t zp2 = prmt(par[grp], par[grp], 0x3232u);
-        // k-steps s = 2 grp (bytes 0, 1 of word grp) and 2 grp + 1 (bytes 2, 3)
-        mma16816(sacc[nt], A.qa[2 * grp][0], 0u, A.qa[2 * grp][1], 0u, k_dequant2<0>(kw[grp], qs2, zp2),
-                 k_dequant2<1>(kw[grp], qs2, zp2));
-        mma16816(sacc[nt], A.qa[2 * grp + 1][0], 0u, A.qa[2 * grp + 1][1], 0u, k_dequant2<2>(kw[grp], qs2, zp2),
-                 k_dequant2<3>(kw[grp], qs2, zp2));
-      }
-    }
-    // V words and params of tokens 2t4, 2t4+1, 2t4+8, 2t4+9
-    uint32_t vw[4];
-    uint4 vp[4];
-    vw[0] = *reinterpret_cast<const uint32_t*>(sb + off_vw0);
-    vw[1] = *reinterpret_cast<const uint32_t*>(sb + off_vw1);
-    vw[2] = *reinterpret_cast<const uint32_t*>(sb + off_vw0 + P8);
-    vw[3] = *reinterpret_cast<const uint32_t*>(sb + off_vw1 + P8);
-    vp[0] = *reinterpret_cast<const uint4*>(sb + off_vp0);
-    vp[1] = *reinterpret_cast<const uint4*>(sb + off_vp1);
-    vp[2] = *reinterpret_cast<const uint4*>(sb + off_vp0 + P8);
-    vp[3] = *reinterpret_cast<const uint4*>(sb + off_vp1 + P8);
-    attn_softmax_pv(A, sacc, ndyn - base, lane, [&](int jg, uint32_t (&v)[2][4]) {
-#pragma unroll
-      for (int pr = 0; pr < 2; ++pr) {
-        const uint32_t pa[4] = {vp[2 * pr].x, vp[2 * pr].y, vp[2 * pr].z, vp[2 * pr].w};
-        const uint32_t pb[4] = {vp[2 * pr + 1].x, vp[2 * pr + 1].y, vp[2 * pr + 1].z, vp[2 * pr + 1].w};
-        const uint32_t xj = prmt(vw[2 * pr], vw[2 * pr + 1],
-                                 (uint32_t)(jg | (jg << 4) | ((4 + jg) << 8) | ((4 + jg) << 12)));
-        const __half2 qs2 = u2h(prmt(pa[jg], pb[jg], 0x5410u));
-        const __half2 zp2 = u2h(prmt(pa[jg], pb[jg], 0x7632u));
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          const uint32_t xx = lop3_and_or(xj, 0x00030003u << (2 * ii), kMagic(ii));
-          const __half2 c = __hsub2(u2h(xx), u2h(kMagic(ii)));
-          // m = 2jg + (ii >> 1), e = ii & 1 -> a-register 2*pr + e of fragment m
-          v[ii >> 1][2 * pr + (ii & 1)] = h2u(__hfma2(c, qs2, zp2));
-        }
-      }
-    });
+    attn_block(A, stage + buf * STAGE_BYTES, o, ndyn - db * 16, lane);
     __syncwarp();
     buf = buf + 1 == NSTAGE ? 0 : buf + 1;
   }

@@ -19,6 +19,8 @@
 #include "select.cuh"
 #include "api_types.cuh"
 #include "decode_common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <algorithm>
 
 namespace sikv {
@@ -42,6 +44,7 @@ using SG0 = NamedGroup<1, 0>;
 using SG1 = NamedGroup<2, 256>;
 
 struct TwoArgs {
+  CUtensorMap recs_map;   // records as a [U*L][128 B] 2-D tensor: TMA gather4 of attention rows
   const uint8_t* signs;
   const uint8_t* recs;
   const float* cent32;
@@ -194,9 +197,101 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 constexpr int ATT_WARPS = SIKV_ATT_WARPS;          // warps per attention CTA (one unit each)
 constexpr int ATT_THREADS = 32 * ATT_WARPS;
 constexpr int ATT_CTAS_PER_SM = 16 / ATT_WARPS;
+#ifndef SIKV_TMA_GATHER
+#define SIKV_TMA_GATHER 0   // 1: attention rows staged by TMA tile::gather4 (measured 5% slower than cp.async)
+#endif
+#ifndef SIKV_TMA_STAGES
+#define SIKV_TMA_STAGES 2
+#endif
+constexpr int TMA_STAGES = SIKV_TMA_STAGES;
 #ifndef SIKV_ATT_PREFETCH
 #define SIKV_ATT_PREFETCH 1
 #endif
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT;\n}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+// four 128-B rows (tensor rows r0..r3) into 512 contiguous bytes at dst, 128-B swizzled
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int r0, int r1, int r2,
+                                            int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+
+// Dynamic rows staged by TMA: per 16-token block, lanes 0-3 each issue one gather4 (four
+// indexed rows, 512 B) onto the block's mbarrier; two 2 KiB buffers per warp (1 KiB aligned).
+// The hardware 128-B swizzle puts chunk k of smem row s at slot k ^ (s & 7); token j of the
+// block sits in smem row P(j) = j ^ ((j & 1) << 2) (an involution), so that the fragment reads
+// of attn_block stay conflict-free: tokens 2q / 2q + 1 differ in bit 2 of their row (K reads),
+// and tokens 0, 2, 4, 6 (and 1, 3, 5, 7) differ in bits 1-2 (V reads).
+__device__ __forceinline__ int tma_row(int j) { return j ^ ((j & 1) << 2); }
+
+__device__ __forceinline__ void attn_dynamic_tma(Attn& A, const CUtensorMap* map, int row0, const int32_t* dyn,
+                                                 int ndyn, int first, int nw, char* stage, uint32_t bars,
+                                                 int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nbd = (ndyn + 15) >> 4;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
+  const int jv0 = 2 * t4, jv1 = 2 * t4 + 1;
+  const int rk = tma_row(g), r0 = tma_row(jv0), r1 = tma_row(jv1);
+  BlkOffs o;
+  o.k4 = rk * FREC + 16 * (t4 ^ rk);
+  o.kp = rk * FREC + 16 * (6 ^ rk);
+  o.vw0 = r0 * FREC + 16 * ((4 + (g >> 2)) ^ r0) + 4 * (g & 3);
+  o.vw1 = r1 * FREC + 16 * ((4 + (g >> 2)) ^ r1) + 4 * (g & 3);
+  o.vp0 = r0 * FREC + 16 * (7 ^ r0);
+  o.vp1 = r1 * FREC + 16 * (7 ^ r1);
+  // lane l < 4 stages smem rows 4l .. 4l + 3: tokens tma_row(4l + i) (rows >= 8: + 8)
+  int ix[4];
+  auto load_ix = [&](int blk) {
+    if (lane < 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int srow = 4 * lane + i;
+        ix[i] = dyn[blk * 16 + (tma_row(srow & 7) | (srow & 8))];
+      }
+    }
+  };
+  auto stage_blk = [&](int buf) {
+    if (lane < 4) {
+      const uint32_t bar = bars + 8u * (uint32_t)buf;
+      if (lane == 0) mbar_expect_tx(bar, 16 * FREC);
+      tma_gather4(sbase + (uint32_t)(buf * STAGE_BYTES + 512 * lane), map, bar, row0 + ix[0], row0 + ix[1],
+                  row0 + ix[2], row0 + ix[3]);
+    }
+  };
+  uint32_t phase = 0;   // bit b: parity of buffer b's next completion
+#pragma unroll
+  for (int s = 0; s < TMA_STAGES - 1; ++s) {
+    if (first + s * nw < nbd) { load_ix(first + s * nw); stage_blk(s); }
+  }
+  if (first + (TMA_STAGES - 1) * nw < nbd) load_ix(first + (TMA_STAGES - 1) * nw);
+  int buf = 0;
+  for (int db = first; db < nbd; db += nw) {
+    const int nx = db + (TMA_STAGES - 1) * nw;
+    if (nx < nbd) {
+      stage_blk(buf == 0 ? TMA_STAGES - 1 : buf - 1);
+      if (nx + nw < nbd) load_ix(nx + nw);
+    }
+    mbar_wait(bars + 8u * (uint32_t)buf, (phase >> buf) & 1u);
+    phase ^= 1u << buf;
+    attn_block(A, stage + buf * STAGE_BYTES, o, ndyn - db * 16, lane);
+    __syncwarp();
+    buf = buf + 1 == TMA_STAGES ? 0 : buf + 1;
+  }
+}
 
 // One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
 // indices come straight from global memory (L2), so the only CTA-wide barriers are the
@@ -205,6 +300,18 @@ template <int NW>
 __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u) {
   constexpr int NT = 32 * NW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if SIKV_TMA_GATHER
+  // 1 KiB-aligned staging (128-B swizzle atoms), then the 2 mbarriers per warp
+  {
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage);
+    stage += (1024u - (s0 & 1023u)) & 1023u;
+  }
+  const int core = max(NW * TMA_STAGES * STAGE_BYTES, NW * a.Gq * (FD + 2) * 4);   // staging, then merge partials
+  const uint32_t bars = (uint32_t)__cvta_generic_to_shared(stage + ((core + 7) & ~7));
+  if (tid < TMA_STAGES * NW) mbar_init(bars + 8u * (uint32_t)tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+#endif
   const int S = a.S, R = a.R, Gq = a.Gq;
   const int32_t* dyn = a.dynl + u * a.dstride;
   const int nf = S + R;
@@ -224,8 +331,13 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   asm volatile("griddepcontrol.wait;" ::: "memory");   // the selection grid is complete
 #endif
   const int ndyn = __ldg(a.ndyn + u);
+#if SIKV_TMA_GATHER
+  attn_dynamic_tma(A, &a.recs_map, (int)(u * a.L), dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
+                   stage + warp * TMA_STAGES * STAGE_BYTES, bars + 8u * TMA_STAGES * (uint32_t)warp, lane);
+#else
   attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
                stage + warp * 2 * STAGE_BYTES, lane);
+#endif
   __syncthreads();
   float* part = reinterpret_cast<float*>(stage);
   float* pm = part + NW * Gq * FD;
@@ -235,7 +347,7 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   attn_merge<Cta256>(part, pm, pl, NW, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
 }
 
-__global__ void __launch_bounds__(ATT_THREADS, ATT_CTAS_PER_SM) decode_attend_kernel(TwoArgs a) {
+__global__ void __launch_bounds__(ATT_THREADS, ATT_CTAS_PER_SM) decode_attend_kernel(const __grid_constant__ TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
   attend_unit<ATT_WARPS>(a, sm, blockIdx.x);
 }
@@ -282,7 +394,9 @@ int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes + SIKV_SEL_PAD;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
-  return std::max(ATT_WARPS * 2 * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
+  const int st = SIKV_TMA_GATHER ? TMA_STAGES : 2;
+  const int core = std::max(ATT_WARPS * st * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
+  return SIKV_TMA_GATHER ? ((core + 7) & ~7) + 8 * TMA_STAGES * ATT_WARPS + 1024 : core;   // mbarriers, 1 KiB alignment slack
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
@@ -307,6 +421,27 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   a.gbits = reinterpret_cast<uint32_t*>(ws);
   ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
   a.gforced = reinterpret_cast<uint32_t*>(ws);
+#if SIKV_TMA_GATHER
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {(cuuint64_t)FREC, (cuuint64_t)(U * L)};
+    const cuuint64_t strides[1] = {(cuuint64_t)FREC};
+    const cuuint32_t box[2] = {(cuuint32_t)FREC, 1};
+    const cuuint32_t es[2] = {1, 1};
+    if (encode(&a.recs_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(recs), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+#endif
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
   const int smem_s = TBL_BYTES + 2 * a.g_bytes + SIKV_SEL_PAD;
   cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
