@@ -200,6 +200,10 @@ constexpr int ATT_CTAS_PER_SM = 16 / ATT_WARPS;
 #ifndef SIKV_TMA_GATHER
 #define SIKV_TMA_GATHER 0   // 1: attention rows staged by TMA tile::gather4 (measured 5% slower than cp.async)
 #endif
+#ifndef SIKV_ATT_STAGES
+#define SIKV_ATT_STAGES 2     // cp.async staging buffers per warp
+#endif
+constexpr int ATT_STAGES = SIKV_ATT_STAGES;
 #ifndef SIKV_TMA_STAGES
 #define SIKV_TMA_STAGES 2
 #endif
@@ -335,8 +339,8 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   attn_dynamic_tma(A, &a.recs_map, (int)(u * a.L), dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
                    stage + warp * TMA_STAGES * STAGE_BYTES, bars + 8u * TMA_STAGES * (uint32_t)warp, lane);
 #else
-  attn_dynamic(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
-               stage + warp * 2 * STAGE_BYTES, lane);
+  attn_dynamic<ATT_STAGES>(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
+                           stage + warp * ATT_STAGES * STAGE_BYTES, lane);
 #endif
   __syncthreads();
   float* part = reinterpret_cast<float*>(stage);
@@ -394,7 +398,7 @@ int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes + SIKV_SEL_PAD;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
-  const int st = SIKV_TMA_GATHER ? TMA_STAGES : 2;
+  const int st = SIKV_TMA_GATHER ? TMA_STAGES : ATT_STAGES;
   const int core = std::max(ATT_WARPS * st * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
   return SIKV_TMA_GATHER ? ((core + 7) & ~7) + 8 * TMA_STAGES * ATT_WARPS + 1024 : core;   // mbarriers, 1 KiB alignment slack
 }
