@@ -70,6 +70,7 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
 
     def __enter__(self):
         def run_nvml(pynvml, h):
@@ -100,18 +101,32 @@ class ClockSampler:
                     pass
                 self._stop.wait(0.05)
 
-        try:   # NVML is initialised here, before the timed region starts
+        try:   # NVML is initialised (and its first, slow queries made) before the timed region
             import pynvml
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self._nvml = (pynvml, h)
             target = lambda: run_nvml(pynvml, h)  # noqa: E731
         except Exception:
+            self._nvml = None
             target = run_smi
         self._t = threading.Thread(target=target, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *exc):
+        # one more sample taken here, as the timed region's final synchronize returns
+        if self._nvml is not None:
+            pynvml, h = self._nvml
+            try:
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([sm, mx] + ["active" if r & b else "" for b in (0x8, 0x40, 0x20, 0x4)])
+            except Exception:
+                pass
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
