@@ -157,25 +157,44 @@ def ncu_traffic(config: str):
     return best
 
 
+def decode_config(name: str, world: int) -> dict:
+    """The workload description both arms print (identical for the same config and N)."""
+    from paper_2603_14224_b200.shard import ShardPlan
+    layers, batch, kvh, gq, L, k, label = CONFIGS[name]
+    plan = ShardPlan(layers, batch, kvh, world)
+    planes = (16 + 128) * L * plan.units_per_rank / 1e9
+    return {"workload": name, "label": label, "layers": layers, "batch": batch, "kv_heads": kvh,
+            "q_heads_per_kv": gq, "context": L, "top_k": k, "sinks": SINKS, "units": layers * batch * kvh,
+            "units_per_gpu": plan.units_per_rank,
+            "parallelism": f"kv-head x batch shard {plan.head_parts}x{plan.batch_parts}",
+            "l2": (f"inputs > L2: {planes:.1f} GB of compressed planes per GPU, every step reads them afresh"
+                   if planes > 0.5 else f"inputs {planes * 1e3:.0f} MB, smaller than L2 (CPU-reference config)")}
+
+
 # ------------------------------------------------------------------------------- GPU arm
-def build_cache(units_local: int, unit_offset: int, L: int, gq: int, seed: int, device):
+def build_cache(gids, L: int, gq: int, seed: int, device):
+    """Compressed caches of the decode units with global ids `gids` (unit content depends
+    only on its id: synth.gen_units_by_id), plus their queries [n, gq, 128] float32."""
     import torch
 
+    from paper_2603_14224_b200 import _lib
     from paper_2603_14224_b200 import batch as B
-    from paper_2603_14224_b200.synth import gen_queries_torch, gen_units_torch
+    from paper_2603_14224_b200.synth import gen_queries_by_id, gen_units_by_id
 
-    cb = B.empty_batch(units_local, L, sink_count=SINKS, device=device)
-    q = torch.empty(units_local, gq, 128, device=device, dtype=torch.float32)
-    chunk = max(1, min(units_local, (1 << 31) // (L * 128 * 2)))   # <= 2 GiB of raw K per chunk
+    gids = [int(x) for x in gids]
+    n_units = len(gids)
+    cb = B.empty_batch(n_units, L, sink_count=SINKS, device=device)
+    q = torch.empty(n_units, gq, 128, device=device, dtype=torch.float32)
+    chunk = max(1, min(n_units, (1 << 31) // (L * 128 * 2)))   # <= 2 GiB of raw K per chunk
     ws = None
-    for u0 in range(0, units_local, chunk):
-        n = min(chunk, units_local - u0)
-        K, V = gen_units_torch(n, L, 128, seed + unit_offset + u0, device)
-        need = __import__("paper_2603_14224_b200._lib", fromlist=["lib"]).lib().sikv_encode_workspace_bytes(n, L, 128)
+    for u0 in range(0, n_units, chunk):
+        ids = gids[u0:u0 + chunk]
+        K, V = gen_units_by_id(ids, L, 128, seed, device)
+        need = _lib.lib().sikv_encode_workspace_bytes(len(ids), L, 128)
         if ws is None or ws.numel() < need:
             ws = torch.empty(need, dtype=torch.uint8, device=device)
         B.prefill_into(cb, u0, K, V, workspace=ws, check=False)
-        q[u0:u0 + n] = gen_queries_torch(K, gq, seed + 7919 + unit_offset + u0).float()
+        q[u0:u0 + len(ids)] = gen_queries_by_id(K, ids, gq, seed + 7919).float()
         del K, V
     torch.cuda.synchronize()
     return cb, q
@@ -186,25 +205,26 @@ def run_ours(args, rank, world, cfg):
     import torch.distributed as dist
 
     from paper_2603_14224_b200 import batch as B
+    from paper_2603_14224_b200.shard import ShardPlan, gather_outputs
 
     layers, batch, kvh, gq, L, k, label = cfg
     units = layers * batch * kvh
-    if units % world:
-        raise SystemExit(f"{units} units do not shard over {world} GPUs")
-    ul = units // world
+    plan = ShardPlan(layers, batch, kvh, world)
+    ul = plan.units_per_rank
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    cb, q = build_cache(ul, rank * ul, L, gq, 1234, dev)
-
-    from paper_2603_14224_b200.shard import gather_outputs
+    cb, q = build_cache(plan.local_units(rank).tolist(), L, gq, 1234, dev)
 
     out = torch.empty(ul, gq, 128, device=dev, dtype=torch.float32)
+    out16 = torch.empty(ul, gq, 128, device=dev, dtype=torch.bfloat16)
+    flat = torch.empty(world * ul, gq, 128, device=dev, dtype=torch.bfloat16) if world > 1 else None
     model_out = torch.empty(layers, batch, kvh * gq, 128, device=dev, dtype=torch.bfloat16) if world > 1 else None
 
-    def step(qq):
-        B.decode_step(cb, qq, k, out=out)
-        if world > 1:   # head-sharded outputs -> [layers, batch, H_q, D] on every rank (NCCL)
-            gather_outputs(out.to(torch.bfloat16), layers, batch, kvh, world, out=model_out)
+    def step(qq, o=out):
+        B.decode_step(cb, qq, k, out=o)
+        if world > 1:   # sharded outputs -> [layers, batch, H_q, D] on every rank (NCCL all-gather)
+            out16.copy_(o)
+            gather_outputs(out16, layers, batch, kvh, world, out=model_out, flat=flat)
 
     # correctness spot check on this rank (selection of unit 0 vs float32 restatement is in tests)
     for _ in range(args.warmup):
@@ -264,9 +284,7 @@ def run_ours(args, rank, world, cfg):
             st.wait_event(h2d[b])
             if i >= 2:
                 st.wait_event(d2h[b])                 # od[b] was copied out by step i-2
-            B.decode_step(cb, qd[b], k, out=od[b])
-            if world > 1:
-                gather_outputs(od[b].to(torch.bfloat16), layers, batch, kvh, world, out=model_out)
+            step(qd[b], od[b])
             comp[b].record(st)
             with torch.cuda.stream(cs_out):
                 cs_out.wait_event(comp[b])
@@ -318,10 +336,7 @@ def run_ours(args, rank, world, cfg):
         "vs_baseline": None,
         "dtype": "u2 K/V payload, f32 scores, f16 mma operands / f32 accumulate",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU), random-init caches",
-        "config": {"workload": args.config, "label": label, "layers": layers, "batch": batch,
-                   "kv_heads": kvh, "q_heads_per_kv": gq, "context": L, "top_k": k, "sinks": SINKS,
-                   "units": units, "parallelism": f"kv-head shard x{world}",
-                   "l2": "inputs > L2 (19 GB of compressed planes per GPU-step at C2)"},
+        "config": decode_config(args.config, world),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": traffic["bytes"] if traffic else None,
@@ -402,41 +417,85 @@ def run_prefill(args, rank, world, cfg):
 
 
 # ------------------------------------------------------------------------------- CPU arm
-def _cpu_unit(job):
-    """Reference-path decode of one unit on the CPU oracle: group-sum select + Gq attention."""
-    import numpy as np
-
+def _cpu_worker(conn, jobs):
+    """One host core: prefills its sample units once (untimed), then on every 'step' runs the
+    reference decode path of each of them (group-sum select_tokens + Gq x sparse_attention,
+    cache.py:290-309, attention.py:52-62) on the CPU oracle and reports the seconds taken."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle import sikv_oracle as O
     from paper_2603_14224_b200.synth import gen_unit
-    L, gq, k, seed = job
-    u = gen_unit(L, 128, gq, seed)
-    c = O.prefill(u.keys, u.values, sink_count=SINKS)
-    qs = u.queries[:gq]
-    t0 = time.perf_counter()
-    idx = O.select(c, qs.sum(axis=0), k=k)[0]
-    for h in range(gq):
-        O.sparse_attention(qs[h], idx, c)
-    return time.perf_counter() - t0
+    units = []
+    for (L, gq, k, seed) in jobs:
+        u = gen_unit(L, 128, gq, seed)
+        units.append((O.prefill(u.keys, u.values, sink_count=SINKS), u.queries[:gq], k))
+    conn.send("ready")
+    while conn.recv() == "step":
+        t0 = time.perf_counter()
+        for c, qs, k in units:
+            idx = O.select(c, qs.sum(axis=0), k=k)[0]
+            for h in range(qs.shape[0]):
+                O.sparse_attention(qs[h], idx, c)
+        conn.send(time.perf_counter() - t0)
+    conn.close()
 
 
-def cpu_baseline(cfg, sample_units: int, workers: int):
-    import concurrent.futures as cf
-    layers, batch, kvh, gq, L, k, label = cfg
-    units = layers * batch * kvh
-    jobs = [(L, gq, k, 9000 + i) for i in range(sample_units)]
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    t0 = time.perf_counter()
-    with cf.ProcessPoolExecutor(workers) as ex:
-        per_unit = list(ex.map(_cpu_unit, jobs))
-    wall = time.perf_counter() - t0
-    mean_unit_s = sum(per_unit) / len(per_unit)
-    steps_per_s = workers / (mean_unit_s * units)
-    return {"value": round(steps_per_s, 6), "unit": "decode steps/s", "cores": workers,
-            "kind": "port", "unit_ms_1core": round(mean_unit_s * 1e3, 2),
-            "sample": f"{sample_units} units of the {units}-unit step (decode only, prefill excluded), "
-                      f"extrapolated: steps/s = cores / (mean unit s x units)",
-            "cpu": _cpu_model(), "wall_s": round(wall, 1)}
+class CpuArm:
+    """The reference's CPU decode path on every host core, over a bounded sample of the
+    workload's units (prefilled once, outside the timing).  One step = every core decodes its
+    share of the sample; steps/s of the whole workload = (sample / units) / step seconds."""
+
+    def __init__(self, cfg, sample_units: int, cores: int):
+        import multiprocessing as mp
+        layers, batch, kvh, gq, L, k, _ = cfg
+        self.units = layers * batch * kvh
+        self.sample = sample_units
+        self.cores = min(cores, sample_units)
+        ctx = mp.get_context("fork")
+        self.procs, self.conns = [], []
+        for w in range(self.cores):
+            jobs = [(L, gq, k, 9000 + i) for i in range(w, sample_units, self.cores)]
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_cpu_worker, args=(b, jobs), daemon=True)
+            p.start()
+            self.procs.append(p)
+            self.conns.append(a)
+        for c in self.conns:
+            assert c.recv() == "ready"
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send("step")
+        busy = [c.recv() for c in self.conns]
+        self.last_busy = busy
+        return time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            c.send("stop")
+        for p in self.procs:
+            p.join(timeout=30)
+
+    def line(self, seconds: float) -> dict:
+        v = (self.sample / self.units) / seconds
+        return {"value": round(v, 6), "unit": "decode steps/s", "cores": self.cores, "kind": "port",
+                "unit_ms_1core": round(1e3 * sum(self.last_busy) / self.sample, 2),
+                "sample": f"{self.sample} of the {self.units} units of one decode step per timed step "
+                          f"(decode only: prefill once, untimed), steps/s = (sample / units) / step seconds",
+                "cpu": _cpu_model()}
+
+
+def cpu_baseline(cfg, sample_units: int, workers: int, steps: int = 3, warmup: int = 1):
+    arm = CpuArm(cfg, sample_units, workers)
+    try:
+        for _ in range(warmup):
+            arm.step()
+        t = sorted(arm.step() for _ in range(steps))
+        res = arm.line(t[len(t) // 2])
+    finally:
+        arm.close()
+    return res
 
 
 def _cpu_model():
@@ -461,6 +520,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # not launched by torchrun: become the launcher of N ranks (one process per GPU)
+        import socket
+        with socket.socket() as s_:
+            s_.bind(("127.0.0.1", 0))
+            port = s_.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
 
@@ -468,22 +537,27 @@ def main():
         if rank != 0:
             return
         cores = os.cpu_count() or 1
-        sample = args.cpu_sample or max(cores, 8)
-        # every step is a bounded sample of the workload (cpu_baseline); at most 3 warm-up and
-        # 5 timed samples keep the whole run within a few minutes; the median is reported
-        nw, ns = min(args.warmup, 3), max(1, min(args.steps, 5))
-        for _ in range(nw):
-            cpu_baseline(cfg, sample, cores)
-        vals = sorted((cpu_baseline(cfg, sample, cores) for _ in range(ns)), key=lambda x: x["value"])
-        v = vals[len(vals) // 2]
+        sample = args.cpu_sample or 2 * cores
+        # every step = the sample's decode on every host core; --warmup / --steps as given
+        arm = CpuArm(cfg, sample, cores)
+        try:
+            for _ in range(args.warmup):
+                arm.step()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                arm.step()
+            secs = (time.perf_counter() - t0) / args.steps
+            v = arm.line(secs)
+        finally:
+            arm.close()
         layers, batch, kvh, gq, L, k, label = cfg
         print(json.dumps({
             "metric": "decode steps/sec + HBM roofline fraction, Llama-3-8B geometry, 32K ctx",
-            "value": v["value"], "unit": "decode steps/s", "n_gpus": args.gpus, "steps": ns,
-            "warmup": nw, "ms_per_step": round(1000.0 / v["value"], 3) if v["value"] else None,
+            "value": v["value"], "unit": "decode steps/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1000.0 / v["value"], 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_synthetic distribution)", "impl": "reference",
-            "config": {"workload": args.config, "label": label, "context": L, "top_k": k},
+            "config": decode_config(args.config, world if world > 1 else args.gpus),
             "cpu_baseline": v,
             "e2e": {"value": v["value"], "unit": "decode steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}))
@@ -492,12 +566,18 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        dist.init_process_group("nccl")
+        # NCCL's init log (transport / NVLS choice) to a per-rank file, stdout stays one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(os.environ.get("SIKV_NCCL_LOG_DIR", "/tmp"),
+                                                              "sikv_nccl.%h.%p.log"))
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     line = run_prefill(args, rank, world, cfg) if args.config == "c5" else run_ours(args, rank, world, cfg)
     if rank == 0 and line is not None:
         if world == 1 and not args.no_cpu_baseline and args.config != "c5":   # rank 0 at N = 1 only
             cores = os.cpu_count() or 1
-            sample = args.cpu_sample or max(8, cores)
+            sample = args.cpu_sample or 2 * cores
             try:
                 line["cpu_baseline"] = cpu_baseline(cfg, sample, cores)
             except Exception as e:  # noqa: BLE001

@@ -94,6 +94,18 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
     return cb
 
 
+def subset(cb: CacheBatch, ids) -> CacheBatch:
+    """A new CacheBatch holding units `ids` of `cb` (copies; e.g. one rank's shard)."""
+    ix = torch.as_tensor(ids, dtype=torch.long, device=cb.signs.device)
+    take = lambda t: t.index_select(0, ix)  # noqa: E731
+    return CacheBatch(
+        units=int(ix.numel()), tokens=cb.tokens, mu64=take(cb.mu64), alpha64=take(cb.alpha64), mu32=take(cb.mu32),
+        alpha32=take(cb.alpha32), cent64=take(cb.cent64), cent32=take(cb.cent32), signs=take(cb.signs),
+        recs=take(cb.recs), sink_idx=take(cb.sink_idx), sink_k=take(cb.sink_k), sink_v=take(cb.sink_v),
+        recent_k=take(cb.recent_k), recent_v=take(cb.recent_v), ffrag=take(cb.ffrag), recent=cb.recent,
+        ref={k: take(v) for k, v in cb.ref.items()})
+
+
 def _sl(t: torch.Tensor | None, u0: int, n: int):
     return None if t is None else t[u0:u0 + n]
 

@@ -84,6 +84,29 @@ def gen_units_torch(units: int, tokens: int, dim: int, seed: int, device, *,
     return K.to(dtype), V.to(dtype)
 
 
+def gen_units_by_id(ids, tokens: int, dim: int, seed: int, device, *, offset: float = 0.5,
+                    spread: float = 0.5, dtype=None):
+    """(len(ids), tokens, dim) bf16 K and V: unit i drawn from its own Philox stream seeded
+    with ``seed + ids[i]``, so a unit's content depends only on its global id (a sharded
+    rank regenerates exactly the units of the single-GPU run)."""
+    import torch
+    dtype = dtype or torch.bfloat16
+    ids = [int(i) for i in ids]
+    K = torch.empty(len(ids), tokens, dim, device=device, dtype=dtype)
+    V = torch.empty_like(K)
+    for j, gid in enumerate(ids):
+        k, v = gen_units_torch(1, tokens, dim, seed + gid, device, offset=offset, spread=spread, dtype=dtype)
+        K[j].copy_(k[0])
+        V[j].copy_(v[0])
+    return K, V
+
+
+def gen_queries_by_id(keys, ids, heads: int, seed: int, **kw):
+    """(len(ids), heads, dim) queries, unit i from the stream ``seed + ids[i]``."""
+    import torch
+    return torch.cat([gen_queries_torch(keys[j:j + 1], heads, seed + int(gid), **kw) for j, gid in enumerate(ids)])
+
+
 def gen_queries_torch(keys, heads: int, seed: int, *, correlated: float = 0.5,
                       noise: float = 0.25):
     """(units, heads, dim) queries: per head, half are a rescaled key row + noise."""

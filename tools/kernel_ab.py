@@ -16,7 +16,7 @@ cfgs = sys.argv[1:] or ["c2", "c3", "c4"]
 for name in cfgs:
     layers, batch, kvh, gq, L, k, _ = bench.CONFIGS[name]
     units = layers * batch * kvh
-    cb, q = bench.build_cache(units, 0, L, gq, 1234, dev)
+    cb, q = bench.build_cache(range(units), L, gq, 1234, dev)
     out = torch.empty(units, gq, 128, device=dev)
     for kern in ONLY or ([1, 2, 3, 4] if units < 1000 else [1, 2, 4]):
         try:

@@ -18,7 +18,7 @@ ap.add_argument("--kernels", type=int, nargs="+", default=[4])
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 for units in a.units:
-    cb, q = bench.build_cache(units, 0, 32768, 4, 1234, dev)
+    cb, q = bench.build_cache(range(units), 32768, 4, 1234, dev)
     out = torch.empty(units, 4, 128, device=dev)
     for kern in a.kernels:
         for _ in range(5):

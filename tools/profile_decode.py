@@ -18,7 +18,7 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--kernel", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
-cb, q = bench.build_cache(a.units, 0, a.L, a.gq, 1234, dev)
+cb, q = bench.build_cache(range(a.units), a.L, a.gq, 1234, dev)
 out = torch.empty(a.units, a.gq, 128, device=dev)
 for _ in range(a.iters):
     B.decode_step(cb, q, a.k, out=out, kernel=a.kernel)

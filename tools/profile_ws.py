@@ -24,7 +24,7 @@ ap.add_argument("--skip", type=int, default=0, help="debug skip bits (1: no atte
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 _lib.call("sikv_debug_set_ws_skip", a.skip)
-cb, q = bench.build_cache(a.units, 0, a.L, a.gq, 1234, dev)
+cb, q = bench.build_cache(range(a.units), a.L, a.gq, 1234, dev)
 out = torch.empty(a.units, a.gq, 128, device=dev)
 for _ in range(3):
     B.decode_step(cb, q, a.k, out=out, kernel=a.kernel)

@@ -12,7 +12,7 @@ dev = torch.device("cuda", 0)
 units = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 kernels = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4]
-cb, q = bench.build_cache(units, 0, L, 4, 77, dev)
+cb, q = bench.build_cache(range(units), L, 4, 77, dev)
 for kern in kernels:
     for k, sel in ((256, True), (256, False), (L, False), (0, False)):
         r = B.decode_step(cb, q, k, with_selection=sel, with_lse=True, kernel=kern)

@@ -17,7 +17,7 @@ units = layers * batch * kvh
 base = None
 for n in (1, 2, 4, 8):
     ul = units // n
-    cb, q = bench.build_cache(ul, 0, L, gq, 1234, dev)
+    cb, q = bench.build_cache(range(ul), L, gq, 1234, dev)
     out = torch.empty(ul, gq, 128, device=dev)
     for _ in range(5):
         B.decode_step(cb, q, k, out=out, kernel=KERNEL)
