@@ -72,7 +72,8 @@ int sikv_gather_rows(const void* keys, const void* values, int in_dtype, int64_t
                      int64_t tokens, int64_t dim, const int32_t* idx, int64_t n,
                      const double* mu64, void* out_k, void* out_v, int out_f64, void* stream);
 
-/* decode-time append of one token per unit at ring position pos.
+/* decode-time append of one token per unit at ring position pos (float32/64 rows only; the
+ * batched fast path uses sikv_append_forced below).
  * replaces: append_token, cache.py:274-287 */
 int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64_t dim,
                 const double* mu64, void* recent_k, void* recent_v, int64_t rcap, int64_t pos,
@@ -96,36 +97,56 @@ size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int s
 /* kernel: 0 = auto (two kernels when units >= 2 x SMs, a workspace of
  * sikv_decode_workspace_bytes_k is given and the selection kernel fits shared memory; a
  * thread-block cluster per unit for few long units; else one CTA per unit),
- * 1 = one CTA per unit, 2 = the persistent warp-specialised kernel, 3 = split units across a
- * cluster, 4 = force the two-kernel path (selection, then attention). */
+ * 1 = one CTA per unit, 3 = split units across a cluster, 4 = force the two-kernel path
+ * (selection, then attention).
+ * Recent rows: recent_n (nullable) [U] int32 = recent rows of each unit (forced, scored
+ * -inf: cache.py:290-309; sel then ends with tokens + 0 .. recent_n[u] - 1); recent = their
+ * maximum (or the count of every unit when recent_n is NULL). */
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
-                     int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq,
-                     int k, int cap, float* out, float* lse, int32_t* sel, int sel_stride,
-                     int32_t* sel_count, int32_t* diag, void* workspace, size_t workspace_bytes,
-                     int kernel, void* stream);
+                     int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
+                     int64_t tokens, int gq, int k, int cap, float* out, float* lse, int32_t* sel,
+                     int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
+                     size_t workspace_bytes, int kernel, void* stream);
 
-/* the decode path (1-4, as the kernel argument) the last sikv_decode_step of this host
+/* the decode path (1, 3 or 4, as the kernel argument) the last sikv_decode_step of this host
  * thread launched; the two-kernel path (4) starts two kernels per step, the others one */
 int sikv_decode_last_kernel(void);
 
-/* forced rows (sinks then recents; float32 centred K' and V) -> the decode kernel's fp16
- * mma-fragment blocks of 16 rows: forced_frag [U][frag_blocks][2][32][32] u32.  Re-packs the
- * blocks covering rows [row_begin, row_end); rows >= sinks + recent are zero.
+/* forced rows (sinks then recents; float32 centred K' and V) -> the decode kernel's blocks of
+ * 16 rows: forced_frag [U][frag_blocks][sikv_forced_block_words()] u32 = fp16 K^ mma
+ * fragments [32][32], fp16 V fragments [32][32], 16 float32 row scales (K^ = K' /
+ * (alpha-hat * scale), scale a power of two, 1 unless |K'| of a recent row exceeds the
+ * prefill alpha).  Re-packs the blocks covering rows [row_begin, row_end); rows >= sinks +
+ * recent_n[u] (or + recent) are zero.  status_dev (nullable): bit2 non-finite, bit4 a V entry
+ * outside the fp16 range.
  * replaces: the full-precision sink / recent rows of cache.gather, cache.py:137-144 */
 int sikv_forced_blocks(int sinks, int64_t rcap);
+int sikv_forced_block_words(void);
 int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const float* recent_k,
-                     const float* recent_v, int64_t rcap, int recent, const float* alpha32,
-                     int64_t units, uint32_t* forced_frag, int frag_blocks, int row_begin,
-                     int row_end, void* stream);
+                     const float* recent_v, int64_t rcap, const int32_t* recent_n, int recent,
+                     const float* alpha32, int64_t units, uint32_t* forced_frag, int frag_blocks,
+                     int row_begin, int row_end, int* status_dev, void* stream);
+
+/* decode-time append into the forced-row ring of the batched fast path: row i of k / v
+ * [n][128] goes to unit unit_ids[i] (or i when unit_ids is NULL; ids distinct within a call)
+ * at ring position recent_n[unit], centred in float64 with the frozen prefill mu and stored
+ * as float32, the fragment block holding it is re-packed and recent_n[unit] is incremented,
+ * all on the device (no host sync).  The caller guarantees recent_n[unit] < rcap (status
+ * bit5 otherwise, row dropped); bit2 non-finite input, bit4 V outside the fp16 range.
+ * replaces: append_token, cache.py:274-287, for every listed unit at once */
+int sikv_append_forced(const void* k, const void* v, int in_dtype, int64_t n, const int32_t* unit_ids,
+                       const double* mu64, const float* alpha32, const float* sink_k, const float* sink_v,
+                       int sinks, float* recent_k, float* recent_v, int64_t rcap, int32_t* recent_n,
+                       uint32_t* forced_frag, int frag_blocks, int* status_dev, void* stream);
 
 /* debug: per-unit phase clocks [U][12] int64 (clock64 at phase boundaries) for every
  * subsequent sikv_decode_step; NULL disables. */
 int sikv_debug_set_decode_profile(void* clocks);
 
-/* debug: bit 0 makes the persistent decode kernel skip sparse attention (phase timing of
- * the scoring / selection half alone); 0 restores normal operation. */
-int sikv_debug_set_ws_skip(int bits);
+/* debug: bit 0 makes the one-CTA-per-unit decode kernel skip sparse attention (phase timing
+ * of the scoring / selection half alone); 0 restores normal operation. */
+int sikv_debug_set_attend_skip(int bits);
 
 /* fast-path float32 scores only (the decode kernel's scoring, for verification / API).
  * replaces: build_lut + score_tokens on the group-summed query, retrieval.py:46-77 */

@@ -40,10 +40,11 @@ class CacheBatch:
     sink_idx: torch.Tensor
     sink_k: torch.Tensor
     sink_v: torch.Tensor
-    recent_k: torch.Tensor
-    recent_v: torch.Tensor
-    ffrag: torch.Tensor                       # [U, blocks, 2, 32, 32] int32 forced-row fragments
-    recent: int = 0
+    recent_k: torch.Tensor                    # [U, capacity, 128] float32 centred K' rows
+    recent_v: torch.Tensor                    # [U, capacity, 128] float32 V rows
+    recent_n: torch.Tensor                    # [U] int32 recent rows per unit (device)
+    ffrag: torch.Tensor                       # [U, blocks, FBLK] int32 forced-row fragments + row scales
+    recent_host: torch.Tensor = None          # [U] int64 host mirror of recent_n (appends are host-issued)
     ref: dict = field(default_factory=dict)   # optional reference-layout planes
 
     @property
@@ -55,11 +56,20 @@ class CacheBatch:
         return int(self.recent_k.shape[1])
 
     @property
+    def recent(self) -> int:
+        """The largest recent-row count over the units."""
+        return int(self.recent_host.max()) if self.units else 0
+
+    @property
     def length(self) -> int:
         return self.tokens + self.recent
 
     def fast_bytes(self) -> int:
         return self.signs.numel() + self.recs.numel()
+
+
+def _frag_blocks(sinks: int, capacity: int) -> int:
+    return L_.lib().sikv_forced_blocks(sinks, capacity)
 
 
 def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacity: int = 0,
@@ -77,10 +87,12 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
         signs=torch.empty(units, tokens, 16, **u8), recs=torch.empty(units, tokens, 128, **u8),
         sink_idx=torch.arange(S, device=dev, dtype=torch.int32).repeat(units, 1),
         sink_k=torch.empty(units, S, FD, **f32), sink_v=torch.empty(units, S, FD, **f32),
-        recent_k=torch.empty(units, recent_capacity, FD, **f32),
-        recent_v=torch.empty(units, recent_capacity, FD, **f32),
-        ffrag=torch.zeros(units, L_.lib().sikv_forced_blocks(S, recent_capacity), 2, 32, 32,
+        recent_k=torch.zeros(units, recent_capacity, FD, **f32),
+        recent_v=torch.zeros(units, recent_capacity, FD, **f32),
+        recent_n=torch.zeros(units, device=dev, dtype=torch.int32),
+        ffrag=torch.zeros(units, _frag_blocks(S, recent_capacity), L_.lib().sikv_forced_block_words(),
                           device=dev, dtype=torch.int32),
+        recent_host=torch.zeros(units, dtype=torch.int64),
     )
     if keep_reference:
         cb.ref = dict(
@@ -102,8 +114,8 @@ def subset(cb: CacheBatch, ids) -> CacheBatch:
         units=int(ix.numel()), tokens=cb.tokens, mu64=take(cb.mu64), alpha64=take(cb.alpha64), mu32=take(cb.mu32),
         alpha32=take(cb.alpha32), cent64=take(cb.cent64), cent32=take(cb.cent32), signs=take(cb.signs),
         recs=take(cb.recs), sink_idx=take(cb.sink_idx), sink_k=take(cb.sink_k), sink_v=take(cb.sink_v),
-        recent_k=take(cb.recent_k), recent_v=take(cb.recent_v), ffrag=take(cb.ffrag), recent=cb.recent,
-        ref={k: take(v) for k, v in cb.ref.items()})
+        recent_k=take(cb.recent_k), recent_v=take(cb.recent_v), recent_n=take(cb.recent_n), ffrag=take(cb.ffrag),
+        recent_host=cb.recent_host.index_select(0, ix.cpu()), ref={k: take(v) for k, v in cb.ref.items()})
 
 
 def _sl(t: torch.Tensor | None, u0: int, n: int):
@@ -115,17 +127,19 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
     """Compress raw K/V [n, L, 128] (bf16/f32/f64, on device) into units u0..u0+n-1.
 
     Replaces prefill (cache.py:212-271) with bits=2, group_size=32, sign_in_quant=True
-    and first-S sinks, batched over units."""
+    and first-S sinks, batched over units.  Mixed K / V dtypes are promoted to the wider one
+    (the reference converts both to float64)."""
     n, L, D = keys.shape
     if values.shape != keys.shape:
         raise ValueError(f"keys and values must match, got {tuple(keys.shape)} and {tuple(values.shape)}")
     if D != FD or L != cb.tokens:
         raise ValueError(f"expected [n, {cb.tokens}, {FD}] keys, got {tuple(keys.shape)}")
+    if keys.dtype != values.dtype:
+        wide = torch.promote_types(keys.dtype, values.dtype)
+        keys, values = keys.to(wide), values.to(wide)
     keys = keys.contiguous()
     values = values.contiguous()
     dt = L_.dtype_code(keys)
-    if L_.dtype_code(values) != dt:
-        values = values.to(keys.dtype)
     need = L_.lib().sikv_encode_workspace_bytes(n, L, D)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=keys.device)
@@ -144,16 +158,16 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
         L_.call("sikv_gather_rows", L_.ptr(keys), L_.ptr(values), dt, n, L, D,
                 L_.ptr(cb.sink_idx[u0:u0 + n].contiguous()), S, L_.ptr(_sl(cb.mu64, u0, n)),
                 L_.ptr(_sl(cb.sink_k, u0, n)), L_.ptr(_sl(cb.sink_v, u0, n)), 0, L_.stream())
-    _pack_forced(cb, u0, n, 0, cb.ffrag.shape[1] * 16)
+    _pack_forced(cb, u0, n, 0, cb.ffrag.shape[1] * 16, status)
     if check:
         L_.raise_status(status, "keys")
 
 
-def _pack_forced(cb: CacheBatch, u0: int, n: int, row_begin: int, row_end: int) -> None:
+def _pack_forced(cb: CacheBatch, u0: int, n: int, row_begin: int, row_end: int, status=None) -> None:
     L_.call("sikv_pack_forced", L_.ptr(_sl(cb.sink_k, u0, n)), L_.ptr(_sl(cb.sink_v, u0, n)), cb.sinks,
-            L_.ptr(_sl(cb.recent_k, u0, n)), L_.ptr(_sl(cb.recent_v, u0, n)), cb.recent_capacity, cb.recent,
-            L_.ptr(_sl(cb.alpha32, u0, n)), n, L_.ptr(_sl(cb.ffrag, u0, n)), cb.ffrag.shape[1], row_begin,
-            row_end, L_.stream())
+            L_.ptr(_sl(cb.recent_k, u0, n)), L_.ptr(_sl(cb.recent_v, u0, n)), cb.recent_capacity,
+            L_.ptr(_sl(cb.recent_n, u0, n)), 0, L_.ptr(_sl(cb.alpha32, u0, n)), n,
+            L_.ptr(_sl(cb.ffrag, u0, n)), cb.ffrag.shape[1], row_begin, row_end, L_.ptr(status), L_.stream())
 
 
 def prefill_batch(keys: torch.Tensor, values: torch.Tensor, *, sink_count: int = 64,
@@ -165,21 +179,60 @@ def prefill_batch(keys: torch.Tensor, values: torch.Tensor, *, sink_count: int =
     return cb
 
 
-def append_batch(cb: CacheBatch, k: torch.Tensor, v: torch.Tensor) -> None:
-    """append_token for every unit (cache.py:274-287): row pos = cb.recent of the ring."""
-    if cb.recent >= cb.recent_capacity:
-        raise ValueError("recent buffer full")
-    if k.shape != (cb.units, FD) or v.shape != (cb.units, FD):
-        raise ValueError(f"k and v must have shape ({cb.units}, {FD})")
+def reserve_recent(cb: CacheBatch, capacity: int) -> None:
+    """Grow the recent-row ring to at least `capacity` rows per unit (amortised doubling by
+    the appends; call it up front to keep reallocation out of a timed decode loop).  The
+    stored rows and their packed fragment blocks are copied; the new blocks start empty."""
+    old = cb.recent_capacity
+    if capacity <= old:
+        return
+    cap = max(capacity, 2 * old, 16)
+    cap = (cap + 15) // 16 * 16
+    U, dev = cb.units, cb.recent_k.device
+    rk = torch.zeros(U, cap, FD, device=dev, dtype=torch.float32)
+    rv = torch.zeros(U, cap, FD, device=dev, dtype=torch.float32)
+    rk[:, :old] = cb.recent_k
+    rv[:, :old] = cb.recent_v
+    fr = torch.zeros(U, _frag_blocks(cb.sinks, cap), cb.ffrag.shape[2], device=dev, dtype=torch.int32)
+    fr[:, :cb.ffrag.shape[1]] = cb.ffrag
+    cb.recent_k, cb.recent_v, cb.ffrag = rk, rv, fr
+
+
+def append_batch(cb: CacheBatch, k: torch.Tensor, v: torch.Tensor, units=None, *, check: bool = True) -> None:
+    """append_token (cache.py:274-287) for every unit, or for the units `units` (distinct ids):
+    row i of k / v [n, 128] becomes the next recent row of its unit, centred with the frozen
+    prefill mu, force-included in every later decode step (scored -inf, cache.py:302).  The
+    ring grows by doubling when a unit fills it.  check=True reads the device status word
+    (one sync) and raises ValueError for non-finite rows like the reference; check=False
+    keeps the append fully asynchronous."""
+    ids = None if units is None else torch.as_tensor(units, dtype=torch.long)
+    n = cb.units if ids is None else int(ids.numel())
+    if k.shape != (n, FD) or v.shape != (n, FD):
+        raise ValueError(f"k and v must have shape ({n}, {FD})")
+    if ids is not None and (ids.numel() != torch.unique(ids).numel() or
+                            (ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= cb.units))):
+        raise ValueError("units must be distinct ids in range")
+    if k.dtype != v.dtype:
+        wide = torch.promote_types(k.dtype, v.dtype)
+        k, v = k.to(wide), v.to(wide)
     k = k.contiguous()
-    v = v.to(k.dtype).contiguous()
+    v = v.contiguous()
+    host = cb.recent_host if ids is None else cb.recent_host[ids]
+    need = int(host.max()) + 1 if n else 0
+    if need > cb.recent_capacity:
+        reserve_recent(cb, need)
+    dev_ids = None if ids is None else ids.to(device=k.device, dtype=torch.int32)
     status = torch.zeros(1, dtype=torch.int32, device=k.device)
-    L_.call("sikv_append", L_.ptr(k), L_.ptr(v), L_.dtype_code(k), cb.units, FD, L_.ptr(cb.mu64),
-            L_.ptr(cb.recent_k), L_.ptr(cb.recent_v), cb.recent_capacity, cb.recent, 0, L_.ptr(status),
-            L_.stream())
-    cb.recent += 1
-    row = cb.sinks + cb.recent - 1
-    _pack_forced(cb, 0, cb.units, row, row + 1)
+    L_.call("sikv_append_forced", L_.ptr(k), L_.ptr(v), L_.dtype_code(k), n, L_.ptr(dev_ids), L_.ptr(cb.mu64),
+            L_.ptr(cb.alpha32), L_.ptr(cb.sink_k), L_.ptr(cb.sink_v), cb.sinks, L_.ptr(cb.recent_k),
+            L_.ptr(cb.recent_v), cb.recent_capacity, L_.ptr(cb.recent_n), L_.ptr(cb.ffrag), cb.ffrag.shape[1],
+            L_.ptr(status), L_.stream())
+    if ids is None:
+        cb.recent_host += 1
+    else:
+        cb.recent_host[ids] += 1
+    if check:
+        L_.raise_status(status, "appended token")
 
 
 @dataclass
@@ -209,12 +262,15 @@ def _workspace(units: int, tokens: int, k: int, sinks: int, device) -> torch.Ten
 
 def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_selection: bool = False,
                 with_lse: bool = False, with_diag: bool = False, out: torch.Tensor | None = None,
-                sel_buf: torch.Tensor | None = None, kernel: int = 0) -> DecodeOutput:
+                sel_buf: torch.Tensor | None = None, kernel: int = 0, append=None) -> DecodeOutput:
     """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
 
-    kernel: 0 auto, 1 one CTA per unit, 2 warp-specialised persistent kernel, 3 each unit split
-    across a CTA cluster (long contexts, few units), 4 two kernels (selection with two unit
-    groups per SM, then attention)."""
+    append=(k, v) first appends one token per unit ([U, 128] rows, append_batch without the
+    status sync), so a generation step is one call.  kernel: 0 auto, 1 one CTA per unit,
+    3 each unit split across a CTA cluster (long contexts, few units), 4 two kernels
+    (selection with two unit groups per SM, then attention)."""
+    if append is not None:
+        append_batch(cb, append[0], append[1], check=False)
     U = cb.units
     if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
         raise ValueError(f"q must be [{U}, Gq, {FD}], got {tuple(q.shape)}")
@@ -225,19 +281,30 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
     dev = q.device
     if out is None:
         out = torch.empty(U, Gq, FD, device=dev, dtype=torch.float32)
+    elif (out.dtype != torch.float32 or tuple(out.shape) != (U, Gq, FD) or not out.is_contiguous()
+          or out.device != dev):
+        raise ValueError(f"out must be a contiguous float32 [{U}, {Gq}, {FD}] tensor on {dev}")
     lse = torch.empty(U, Gq, device=dev, dtype=torch.float32) if with_lse else None
+    R = cb.recent
     sel = cnt = None
     stride = 0
     if with_selection:
-        stride = cb.sinks + min(k, cb.tokens - cb.sinks) + cb.recent
-        sel = sel_buf if sel_buf is not None else torch.empty(U, max(stride, 1), device=dev, dtype=torch.int32)
+        need = cb.sinks + min(k, cb.tokens - cb.sinks) + R
+        if sel_buf is None:
+            sel = torch.empty(U, max(need, 1), device=dev, dtype=torch.int32)
+        elif (sel_buf.dtype != torch.int32 or sel_buf.dim() != 2 or sel_buf.shape[0] != U
+              or sel_buf.shape[1] < need or not sel_buf.is_contiguous() or sel_buf.device != dev):
+            raise ValueError(f"sel_buf must be a contiguous int32 [{U}, >= {need}] tensor on {dev}")
+        else:
+            sel = sel_buf
+        stride = int(sel.shape[1])
         cnt = torch.empty(U, device=dev, dtype=torch.int32)
     diag = torch.empty(U, device=dev, dtype=torch.int32) if with_diag else None
     ws = _workspace(U, cb.tokens, k, cb.sinks, dev)
     L_.call("sikv_decode_step", L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
-            L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], cb.recent, L_.ptr(qf), U,
-            cb.tokens, Gq, k, cap,
-            L_.ptr(out), L_.ptr(lse), L_.ptr(sel), max(stride, 1) if sel is not None else 0, L_.ptr(cnt),
+            L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], L_.ptr(cb.recent_n), R,
+            L_.ptr(qf), U, cb.tokens, Gq, k, cap,
+            L_.ptr(out), L_.ptr(lse), L_.ptr(sel), stride, L_.ptr(cnt),
             L_.ptr(diag), L_.ptr(ws), ws.numel(), kernel, L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)
 

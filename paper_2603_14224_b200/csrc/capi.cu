@@ -23,33 +23,29 @@ cudaError_t launch_append(const void*, const void*, int, int64_t, int, const dou
 // decode.cu
 DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap);
 cudaError_t launch_decode(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
-                          const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*,
+                          const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*,
                           float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t, int*);
-cudaError_t launch_pack_forced(const float*, const float*, int, const float*, const float*, int64_t, int,
-                               const float*, int64_t, int, int, int, uint32_t*, cudaStream_t);
+cudaError_t launch_pack_forced(const float*, const float*, int, const float*, const float*, int64_t, const int32_t*,
+                               int, const float*, int64_t, int, int, int, uint32_t*, int*, cudaStream_t);
+cudaError_t launch_append_forced(const void*, const void*, int, int64_t, const int32_t*, const double*, const float*,
+                                 const float*, const float*, int, float*, float*, int64_t, int32_t*, int, uint32_t*,
+                                 int*, cudaStream_t);
 cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
                               cudaStream_t);
 cudaError_t set_decode_profile(long long*);
-cudaError_t set_decode_ws_profile(long long*);
-cudaError_t set_decode_ws_skip(int);
 cudaError_t set_k1_skip(int);
 cudaError_t set_decode_two_profile(long long*);
-int ws_smem_bytes(int64_t L, int k, int S, int Gq, int cap);
 int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
 cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
-                                const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, int, float*,
+                                const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, int, float*,
                                 float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t);
-size_t ws_workspace_bytes(int64_t U, int64_t L);
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq);
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq);
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
-                              const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
+                              const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
                               int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
-cudaError_t launch_decode_ws(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
-                             const uint32_t*, int, int, const float*, int64_t, int64_t, int, int, int, float*,
-                             float*, int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
 // generic.cu
 cudaError_t launch_lut_f64(const double*, const double*, int64_t, int, int, double*, cudaStream_t);
 cudaError_t launch_score_f64(const double*, const uint8_t*, int64_t, int, int64_t, double*, cudaStream_t);
@@ -95,7 +91,7 @@ static int max_smem() {
 extern "C" {
 
 const char* sikv_last_error(void) { return g_err.c_str(); }
-int sikv_abi_version(void) { return 1; }
+int sikv_abi_version(void) { return 3; }
 
 size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
   return encode_workspace_bytes(units, tokens, (int)dim);
@@ -186,24 +182,44 @@ int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap) {
 
 int sikv_forced_blocks(int sinks, int64_t rcap) { return (int)std::max<int64_t>(1, (sinks + rcap + 15) / 16); }
 
+int sikv_forced_block_words(void) { return FBLK_WORDS; }
+
 int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const float* recent_k,
-                     const float* recent_v, int64_t rcap, int recent, const float* alpha32, int64_t units,
-                     uint32_t* forced_frag, int frag_blocks, int row_begin, int row_end, void* stream) {
+                     const float* recent_v, int64_t rcap, const int32_t* recent_n, int recent, const float* alpha32,
+                     int64_t units, uint32_t* forced_frag, int frag_blocks, int row_begin, int row_end,
+                     int* status_dev, void* stream) {
   REQUIRE(alpha32 && forced_frag, SIKV_EINVAL, "null pointer");
   REQUIRE(sinks == 0 || (sink_k && sink_v), SIKV_EINVAL, "sink rows missing");
-  REQUIRE(recent == 0 || (recent_k && recent_v), SIKV_EINVAL, "recent rows missing");
+  REQUIRE(rcap == 0 || (recent_k && recent_v), SIKV_EINVAL, "recent rows missing");
   REQUIRE(recent >= 0 && recent <= rcap, SIKV_EINVAL, "recent count out of range");
   REQUIRE(frag_blocks >= sikv_forced_blocks(sinks, rcap), SIKV_EINVAL, "frag_blocks too small");
   REQUIRE(row_begin >= 0 && row_end >= row_begin, SIKV_EINVAL, "bad row range");
   const int b0 = row_begin / 16, b1 = std::min(frag_blocks, (row_end + 15) / 16);
-  return cuda_ret(launch_pack_forced(sink_k, sink_v, sinks, recent_k, recent_v, rcap, recent, alpha32, units,
-                                     frag_blocks, b0, b1, forced_frag, (cudaStream_t)stream),
+  return cuda_ret(launch_pack_forced(sink_k, sink_v, sinks, recent_k, recent_v, rcap, recent_n, recent, alpha32,
+                                     units, frag_blocks, b0, b1, forced_frag, status_dev, (cudaStream_t)stream),
                   "sikv_pack_forced");
 }
 
-size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens) { return ws_workspace_bytes(units, tokens); }
+int sikv_append_forced(const void* k, const void* v, int in_dtype, int64_t n, const int32_t* unit_ids,
+                       const double* mu64, const float* alpha32, const float* sink_k, const float* sink_v, int sinks,
+                       float* recent_k, float* recent_v, int64_t rcap, int32_t* recent_n, uint32_t* forced_frag,
+                       int frag_blocks, int* status_dev, void* stream) {
+  REQUIRE(k && v && mu64 && alpha32 && recent_k && recent_v && recent_n && forced_frag, SIKV_EINVAL, "null pointer");
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
+  REQUIRE(n >= 0 && rcap >= 1, SIKV_EINVAL, "bad row count or capacity");
+  REQUIRE(sinks == 0 || (sink_k && sink_v), SIKV_EINVAL, "sink rows missing");
+  REQUIRE(frag_blocks >= sikv_forced_blocks(sinks, rcap), SIKV_EINVAL, "frag_blocks too small");
+  return cuda_ret(launch_append_forced(k, v, in_dtype, n, unit_ids, mu64, alpha32, sink_k, sink_v, sinks, recent_k,
+                                       recent_v, rcap, recent_n, frag_blocks, forced_frag, status_dev,
+                                       (cudaStream_t)stream),
+                  "sikv_append_forced");
+}
+
+size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens) {
+  return two_workspace_bytes(units, tokens, (int)std::min<int64_t>(tokens, 1 << 30), 0);
+}
 size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int sinks) {
-  return std::max(ws_workspace_bytes(units, tokens), two_workspace_bytes(units, tokens, k, sinks));
+  return two_workspace_bytes(units, tokens, k, sinks);
 }
 
 static thread_local int g_last_decode_kernel = 0;
@@ -211,7 +227,8 @@ int sikv_decode_last_kernel() { return g_last_decode_kernel; }
 
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
-                     int frag_blocks, int recent, const float* q, int64_t units, int64_t tokens, int gq, int k,
+                     int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
+                     int64_t tokens, int gq, int k,
                      int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
                      int32_t* diag, void* workspace, size_t workspace_bytes, int kernel, void* stream) {
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
@@ -226,12 +243,11 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   REQUIRE(sinks + recent == 0 || forced_frag, SIKV_EINVAL, "forced rows need forced_frag");
   REQUIRE(sinks + recent <= 16 * frag_blocks, SIKV_EINVAL, "forced rows exceed frag_blocks");
   const int64_t keff = std::min<int64_t>(k, tokens - sinks);
-  REQUIRE(sinks + keff + recent >= 1, SIKV_EINVAL, "selection is empty");
+  REQUIRE(sinks + keff + (recent_n ? 0 : recent) >= 1, SIKV_EINVAL, "selection is empty");
   REQUIRE(!sel || sel_stride >= sinks + keff + recent, SIKV_EINVAL, "sel_stride too small");
-  // kernel: 0 = auto, 1 = one CTA per unit, 2 = warp-specialised persistent, 3 = split units
-  // (a CTA cluster per unit), 4 = two kernels (selection with two unit groups per SM, then
-  // attention)
-  REQUIRE(kernel >= 0 && kernel <= 4, SIKV_EINVAL, "kernel must be 0, 1, 2, 3 or 4");
+  // kernel: 0 = auto, 1 = one CTA per unit, 3 = split units (a CTA cluster per unit),
+  // 4 = two kernels (selection with two unit groups per SM, then attention)
+  REQUIRE(kernel == 0 || kernel == 1 || kernel == 3 || kernel == 4, SIKV_EINVAL, "kernel must be 0, 1, 3 or 4");
   if (kernel == 4 || (kernel == 0 && units >= 2 * num_sms())) {
     const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
     const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
@@ -248,7 +264,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     if (fits && ws_ok) {
       g_last_decode_kernel = 4;
       return cuda_ret(launch_decode_two(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
-                                        frag_blocks, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
+                                        frag_blocks, recent_n, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
                                         sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
                       "sikv_decode_step");
     }
@@ -276,28 +292,10 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     if (pick) {
       g_last_decode_kernel = 3;
       return cuda_ret(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
-                                          frag_blocks, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
+                                          frag_blocks, recent_n, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
                                           sel, sel_stride, sel_count, diag, (cudaStream_t)stream),
                       "sikv_decode_step");
     }
-  }
-  if (kernel != 1 && workspace && workspace_bytes >= ws_workspace_bytes(units, tokens)) {
-    int wcap = cap > 0 ? cap : sikv_decode_default_cap(tokens, k, sinks);
-    // the persistent kernel keeps two hand-off slots; shrink the candidate buffer to fit
-    const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
-    const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
-    while (cap <= 0 && wcap > floor_cap && ws_smem_bytes(tokens, k, sinks, gq, wcap) > max_smem()) wcap -= 64;
-    const bool fits = ws_smem_bytes(tokens, k, sinks, gq, wcap) <= max_smem();
-    // auto never picks the persistent kernel: the one-CTA-per-unit kernel (two co-resident
-    // CTAs per SM) measured faster at C2 (32K tokens) and C4 (8K tokens); kernel = 2 forces it
-    if (fits && kernel == 2) {
-      g_last_decode_kernel = 2;
-      return cuda_ret(launch_decode_ws(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
-                                       frag_blocks, recent, q, units, tokens, gq, k, wcap, out, lse, sel,
-                                       sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
-                      "sikv_decode_step");
-    }
-    REQUIRE(kernel != 2, SIKV_EUNSUPPORTED, "the persistent kernel does not fit this configuration");
   }
   if (cap <= 0) cap = sikv_decode_default_cap(tokens, k, sinks);
   int need = decode_layout(tokens, k, sinks, gq, cap).total;
@@ -306,20 +304,18 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   int smem = 0;
   g_last_decode_kernel = 1;
   cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
-                                recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag,
+                                recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag,
                                 (cudaStream_t)stream, &smem);
   return cuda_ret(e, "sikv_decode_step");
 }
 
-int sikv_debug_set_ws_skip(int v) {
-  cudaError_t e = set_decode_ws_skip(v);
-  if (e == cudaSuccess) e = set_k1_skip(v);
-  return cuda_ret(e, "sikv_debug_set_ws_skip");
+int sikv_debug_set_attend_skip(int v) {
+  cudaError_t e = set_k1_skip(v);
+  return cuda_ret(e, "sikv_debug_set_attend_skip");
 }
 
 int sikv_debug_set_decode_profile(void* clocks) {
   cudaError_t e = set_decode_profile((long long*)clocks);
-  if (e == cudaSuccess) e = set_decode_ws_profile((long long*)clocks);
   if (e == cudaSuccess) e = set_decode_two_profile((long long*)clocks);
   return cuda_ret(e, "sikv_debug_set_decode_profile");
 }

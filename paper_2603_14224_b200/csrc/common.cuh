@@ -40,6 +40,11 @@ constexpr int R_K4 = 0;        // 64 B K as e2m1 nibbles (sign | 2-bit code), MM
 constexpr int R_VPAY = 64;     // 32 B V payload, MMA-permuted
 constexpr int R_KPAR = 96;     // 4 x (2 qs, zp) fp16
 constexpr int R_VPAR = 112;    // 4 x (qs, zp) fp16
+// one 16-row block of forced rows (sinks, then recents): K^ fragments [32 lanes][32 words],
+// V fragments [32 lanes][32 words], then 16 float32 row scales (a power of two per row:
+// K^ = K' / (alpha-hat * scale) stays within fp16 for recent rows whose |K'| exceeds the
+// prefill alpha; the logit is multiplied back by the scale)
+constexpr int FBLK_WORDS = 2 * 32 * 32 + 16;
 
 // ---- K nibble permutation (B operand of q~ K^T, m16n8k16, one token per n column).
 // A nibble is an e2m1 value: bit 3 = sign of K' (1 = negative), bits 0-1 = the 2-bit

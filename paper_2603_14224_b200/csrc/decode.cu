@@ -36,7 +36,8 @@ struct DecodeArgs {
   const float* cent32;      // [U][32][16][4]
   const float* alpha32;     // [U][128]
   const int32_t* sink_idx;  // [U][S] sorted, unique, < L
-  const uint32_t* ffrag;    // [U][fblocks][2][32 lanes][32 words] forced rows as fp16 fragments
+  const uint32_t* ffrag;    // [U][fblocks][FBLK_WORDS] forced rows: fp16 fragments + row scales
+  const int32_t* rn;        // [U] recent rows per unit, nullable (then R for every unit)
   const float* q;           // [U][Gq][128]
   float* out;               // [U][Gq][128]
   float* lse;               // [U][Gq] natural-log sum of exp(logits), nullable
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   float* inva = qbar + FD;                                        // [128] 1 / alpha-hat
   float* ahat = inva + FD;                                        // [128] alpha-hat
   const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
-  const int S = a.S, R = a.R, Gq = a.Gq;
+  const int S = a.S, R = a.rn ? a.rn[u] : a.R, Gq = a.Gq;
   const int W = (int)((L + 31) >> 5);
   long long* prof = g_prof ? g_prof + u * 12 : nullptr;
 #define PROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
   if (g_k1_skip & 1) return;
-  attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
+  attn_forced(A, a.ffrag + u * a.fblocks * FBLK_WORDS, nf, warp, DW, lane);
   PROF(6);
   attn_dynamic<K1_STAGES>(A, a.recs + u * L * FREC, reinterpret_cast<const int32_t*>(sm + a.off_dyn), ndyn,
                           (warp - nbf % DW + DW) % DW, DW, sm + warp * K1_STAGES * STAGE_BYTES, lane);
@@ -239,12 +240,12 @@ DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap) {
 
 cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float* cent32,
                           const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
-                          int fblocks, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
+                          int fblocks, const int32_t* rn, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
                           float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
                           int32_t* diag, cudaStream_t st, int* smem_out) {
   DecodeLayout d = decode_layout(L, k, S, Gq, cap);
   if (smem_out) *smem_out = d.total;
-  DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, ffrag, q, out, lse, sel,
+  DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, ffrag, rn, q, out, lse, sel,
                sel_count, diag, L, fblocks, S, R, Gq, k, d.capw, sel_stride,
                d.off_cand, d.off_forced, d.off_misc, d.off_bits, d.off_dyn, d.off_stage};
   cudaError_t e = cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, d.total);
@@ -254,15 +255,16 @@ cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float
 }
 
 // Forced rows (sinks then recents) -> fp16 mma fragments, one warp per (unit, 16-row block).
-// K^ = K' / alpha-hat (alpha folded into the query), V as is; rows >= S + R are zero.
-__global__ void pack_forced_kernel(const float* __restrict__ sink_k, const float* __restrict__ sink_v, int S,
-                                   const float* __restrict__ rec_k, const float* __restrict__ rec_v, int64_t rcap,
-                                   int R, const float* __restrict__ alpha32, int fblocks, int b0,
-                                   uint32_t* __restrict__ frag) {
-  const int64_t u = blockIdx.y;
-  const int blk = b0 + blockIdx.x, lane = threadIdx.x;
+// K^ = K' / (alpha-hat * scale) with alpha folded into the query and a power-of-two row scale
+// (1 unless the row's |K' / alpha-hat| exceeds 1: recent rows are not bounded by the prefill
+// alpha), V as is; rows >= S + R_u are zero.  status bit 2: non-finite entry, bit 4: a V entry
+// outside the fp16 range.
+__device__ __forceinline__ void pack_block(int64_t u, int blk, int lane, const float* __restrict__ sink_k,
+                                           const float* __restrict__ sink_v, int S, const float* rec_k,
+                                           const float* rec_v, int64_t rcap, int Ru, const float* __restrict__ alpha32,
+                                           int fblocks, uint32_t* __restrict__ frag, int* status) {
   const int g = lane >> 2, t4 = lane & 3;
-  const int nf = S + R;
+  const int nf = S + Ru;
   auto row = [&](int f, bool key) -> const float* {
     if (f >= nf) return nullptr;
     if (f < S) return (key ? sink_k : sink_v) + (u * S + f) * FD;
@@ -272,19 +274,37 @@ __global__ void pack_forced_kernel(const float* __restrict__ sink_k, const float
     const float al = alpha32[u * FD + d];
     return 1.0f / (al > 0.f ? al : 1.0f);
   };
-  uint32_t* out = frag + ((u * fblocks + blk) * 2 * 32 + lane) * 32;
+  uint32_t* fb = frag + (u * fblocks + blk) * FBLK_WORDS;
+  uint32_t* out = fb + lane * 32;
   const int base = blk * 16;
+  int bad = 0;
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const float* kr = row(base + g + 8 * nt, true);
+    float x[32];
+    float mx = 0.f;
 #pragma unroll
     for (int s = 0; s < 8; ++s)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int d = 16 * s + 2 * t4 + 8 * e;
-        const float x0 = kr ? kr[d] * inva(d) : 0.f, x1 = kr ? kr[d + 1] * inva(d + 1) : 0.f;
-        out[nt * 16 + 2 * s + e] = h2u(__floats2half2_rn(x0, x1));
+        x[4 * s + 2 * e] = kr ? kr[d] * inva(d) : 0.f;
+        x[4 * s + 2 * e + 1] = kr ? kr[d + 1] * inva(d + 1) : 0.f;
+        mx = fmaxf(mx, fmaxf(fabsf(x[4 * s + 2 * e]), fabsf(x[4 * s + 2 * e + 1])));
       }
+    // the row's four lanes (same g) hold all 128 channels
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    if (!(mx <= 3.0e38f)) { bad |= 4; mx = 1.f; }                 // inf / NaN
+    float scale = 1.f;
+    if (mx > 1.f) { int ex; frexpf(mx, &ex); scale = ldexpf(1.f, ex); }   // mx / scale <= 1
+    const float inv = 1.f / scale;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        out[nt * 16 + 2 * s + e] = h2u(__floats2half2_rn(x[4 * s + 2 * e] * inv, x[4 * s + 2 * e + 1] * inv));
+    if (t4 == 0) reinterpret_cast<float*>(fb + 2 * 32 * 32)[g + 8 * nt] = scale;
   }
   uint32_t* ov = out + 32 * 32;
 #pragma unroll
@@ -294,16 +314,73 @@ __global__ void pack_forced_kernel(const float* __restrict__ sink_k, const float
       const int d = 16 * m + g + 8 * (r & 1), pr = r >> 1;
       const float* va = row(base + 2 * t4 + 8 * pr, false);
       const float* vb = row(base + 2 * t4 + 8 * pr + 1, false);
-      ov[m * 4 + r] = h2u(__floats2half2_rn(va ? va[d] : 0.f, vb ? vb[d] : 0.f));
+      const float a0 = va ? va[d] : 0.f, a1 = vb ? vb[d] : 0.f;
+      if (!(fabsf(a0) <= 3.0e38f) || !(fabsf(a1) <= 3.0e38f)) bad |= 4;
+      else if (fabsf(a0) > 65504.f || fabsf(a1) > 65504.f) bad |= 16;
+      ov[m * 4 + r] = h2u(__floats2half2_rn(a0, a1));
     }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (bad && lane == 0 && status) atomicOr(status, bad);
+}
+
+__global__ void pack_forced_kernel(const float* __restrict__ sink_k, const float* __restrict__ sink_v, int S,
+                                   const float* __restrict__ rec_k, const float* __restrict__ rec_v, int64_t rcap,
+                                   const int32_t* __restrict__ rn, int R, const float* __restrict__ alpha32,
+                                   int fblocks, int b0, uint32_t* __restrict__ frag, int* status) {
+  const int64_t u = blockIdx.y;
+  pack_block(u, b0 + blockIdx.x, threadIdx.x, sink_k, sink_v, S, rec_k, rec_v, rcap, rn ? rn[u] : R, alpha32, fblocks,
+             frag, status);
 }
 
 cudaError_t launch_pack_forced(const float* sink_k, const float* sink_v, int S, const float* rec_k,
-                               const float* rec_v, int64_t rcap, int R, const float* alpha32, int64_t U,
-                               int fblocks, int b0, int b1, uint32_t* frag, cudaStream_t st) {
+                               const float* rec_v, int64_t rcap, const int32_t* rn, int R, const float* alpha32,
+                               int64_t U, int fblocks, int b0, int b1, uint32_t* frag, int* status, cudaStream_t st) {
   if (b1 <= b0 || U == 0) return cudaSuccess;
-  pack_forced_kernel<<<dim3(b1 - b0, (unsigned)U), 32, 0, st>>>(sink_k, sink_v, S, rec_k, rec_v, rcap, R,
-                                                               alpha32, fblocks, b0, frag);
+  pack_forced_kernel<<<dim3(b1 - b0, (unsigned)U), 32, 0, st>>>(sink_k, sink_v, S, rec_k, rec_v, rcap, rn, R,
+                                                               alpha32, fblocks, b0, frag, status);
+  return cudaGetLastError();
+}
+
+// Decode-time append into the forced-row ring (cache.py:274-287 for every listed unit): one
+// warp per appended row: recent row rn[u] <- (k - mu, v) as float32 (centred in float64 with
+// the frozen prefill mu), the 16-row fragment block holding it re-packed, rn[u] += 1.
+__global__ void append_forced_kernel(const void* __restrict__ k, const void* __restrict__ v, int dt, int64_t n,
+                                     const int32_t* __restrict__ ids, const double* __restrict__ mu64,
+                                     const float* __restrict__ alpha32, const float* __restrict__ sink_k,
+                                     const float* __restrict__ sink_v, int S, float* rec_k, float* rec_v,
+                                     int64_t rcap, int32_t* rn, int fblocks, uint32_t* __restrict__ frag,
+                                     int* status) {
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t u = ids ? ids[i] : i;
+  const int pos = rn[u];
+  if (pos >= rcap) {                                     // capacity is the caller's contract
+    if (lane == 0 && status) atomicOr(status, 32);
+    return;
+  }
+  int bad = 0;
+  for (int d = lane; d < FD; d += 32) {
+    const double kd = load_in(k, dt, i * FD + d), vd = load_in(v, dt, i * FD + d);
+    if (!isfinite(kd) || !isfinite(vd)) bad = 4;
+    rec_k[(u * rcap + pos) * FD + d] = (float)(kd - mu64[u * FD + d]);
+    rec_v[(u * rcap + pos) * FD + d] = (float)vd;
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (bad && lane == 0 && status) atomicOr(status, bad);
+  __syncwarp();                                          // the row is visible to the whole warp
+  pack_block(u, (S + pos) >> 4, lane, sink_k, sink_v, S, rec_k, rec_v, rcap, pos + 1, alpha32, fblocks, frag, status);
+  if (lane == 0) rn[u] = pos + 1;
+}
+
+cudaError_t launch_append_forced(const void* k, const void* v, int dt, int64_t n, const int32_t* ids,
+                                 const double* mu64, const float* alpha32, const float* sink_k, const float* sink_v,
+                                 int S, float* rec_k, float* rec_v, int64_t rcap, int32_t* rn, int fblocks,
+                                 uint32_t* frag, int* status, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((n + 3) / 4);
+  append_forced_kernel<<<blocks, 128, 0, st>>>(k, v, dt, n, ids, mu64, alpha32, sink_k, sink_v, S, rec_k, rec_v, rcap,
+                                                rn, fblocks, frag, status);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,5 @@
 // Device building blocks of the fused decode step, shared by the one-unit-per-CTA kernel
-// (decode.cu) and the warp-specialised persistent kernel (decode_ws.cu).
+// (decode.cu), the cluster-split kernel (decode_split.cu) and the two-kernel path (decode_two.cu).
 #pragma once
 #include "common.cuh"
 #include "select.cuh"
@@ -368,14 +368,18 @@ __device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][
   }
 }
 
-// forced rows (sinks then recents), pre-packed as fp16 fragments; this warp takes blocks
-// wi, wi + nw, ... of [0, nbf)
+// forced rows (sinks then recents), pre-packed as fp16 fragments with per-row scales
+// (FBLK_WORDS per 16-row block); this warp takes blocks wi, wi + nw, ... of [0, nbf)
 __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, int nf, int wi, int nw, int lane) {
   const int nbf = (nf + 15) >> 4;
+  const int t4 = lane & 3;
   for (int blk = wi; blk < nbf; blk += nw) {
     const int base = blk * 16;
-    const uint4* fk = reinterpret_cast<const uint4*>(ffrag_u + ((int64_t)blk * 2 * 32 + lane) * 32);
+    const uint32_t* fb = ffrag_u + (int64_t)blk * FBLK_WORDS;
+    const uint4* fk = reinterpret_cast<const uint4*>(fb + lane * 32);
     const uint4* fv = fk + 32 * 8;
+    const float2 sc0 = __ldg(reinterpret_cast<const float2*>(fb + 2 * 32 * 32) + t4);       // rows 2t4, 2t4 + 1
+    const float2 sc1 = __ldg(reinterpret_cast<const float2*>(fb + 2 * 32 * 32 + 8) + t4);   // rows 8 + 2t4, + 1
     uint32_t kwd[32], vwd[32];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -395,6 +399,8 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
       for (int s = 0; s < 8; ++s)
         mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, kwd[nt * 16 + 2 * s], kwd[nt * 16 + 2 * s + 1]);
     }
+    sacc[0][0] *= sc0.x; sacc[0][1] *= sc0.y; sacc[0][2] *= sc0.x; sacc[0][3] *= sc0.y;
+    sacc[1][0] *= sc1.x; sacc[1][1] *= sc1.y; sacc[1][2] *= sc1.x; sacc[1][3] *= sc1.y;
     attn_softmax_pv(A, sacc, nf - base, lane, [&](int mp, uint32_t (&v)[2][4]) {
 #pragma unroll
       for (int mm = 0; mm < 2; ++mm)

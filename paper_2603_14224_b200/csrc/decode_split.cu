@@ -104,7 +104,7 @@ struct ClusterX {
 
 struct SplitArgs {
   const uint8_t* signs; const uint8_t* recs; const float* cent32; const float* alpha32;
-  const int32_t* sink_idx; const uint32_t* ffrag; const float* q;
+  const int32_t* sink_idx; const uint32_t* ffrag; const int32_t* rn; const float* q;
   float* out; float* lse; int32_t* sel; int32_t* sel_count; int32_t* diag;
   int64_t L;
   int fblocks, S, R, Gq, k, capw, sel_stride, ns, wmax;
@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   const int64_t u = blockIdx.x / ns;
   const int64_t Lu = a.L;
   const int S = a.S, Gq = a.Gq;
+  const int Ru = a.rn ? a.rn[u] : a.R;   // recent rows of this unit
   // ---------------- this CTA's slice of the unit
   const int nch = (int)((Lu + 255) >> 8);
   const int c_lo = (int)((int64_t)rank * nch / ns), c_hi = (int)((int64_t)(rank + 1) * nch / ns);
@@ -267,8 +268,8 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     }
     if (rank == ns - 1) {
       if (sel_u)
-        for (int r = tid; r < a.R; r += DT) sel_u[sall + r] = (int32_t)(Lu + r);
-      if (tid == 0 && a.sel_count) a.sel_count[u] = sall + a.R;
+        for (int r = tid; r < Ru; r += DT) sel_u[sall + r] = (int32_t)(Lu + r);
+      if (tid == 0 && a.sel_count) a.sel_count[u] = sall + Ru;
     }
     if (tid == 0 && rank == 0 && a.diag) a.diag[u] = (mode & 3) | (ms->fb ? 4 : 0) | 8;
     __syncthreads();
@@ -278,9 +279,9 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   // ---------------- D: sparse attention over this slice's rows (+ forced rows on rank 0)
   Attn A;
   attn_init(A, qs, ahat, Gq, lane);
-  const int nf = rank == 0 ? S + a.R : 0;
+  const int nf = rank == 0 ? S + Ru : 0;
   const int nbf = (nf + 15) >> 4;
-  if (nf > 0) attn_forced(A, a.ffrag + u * a.fblocks * 2 * 32 * 32, nf, warp, DW, lane);
+  if (nf > 0) attn_forced(A, a.ffrag + u * a.fblocks * FBLK_WORDS, nf, warp, DW, lane);
   attn_dynamic(A, a.recs + u * Lu * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
                sm + a.off_stage + warp * 2 * STAGE_BYTES, lane);
   __syncthreads();
@@ -378,12 +379,12 @@ int split_default_cap(int64_t L, int k, int S, int ns) {
 
 cudaError_t launch_decode_split(const uint8_t* signs, const uint8_t* recs, const float* cent32,
                                 const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
-                                int fblocks, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
+                                int fblocks, const int32_t* rn, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
                                 int ns, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
                                 int32_t* diag, cudaStream_t st) {
   SplitLayout lay = split_layout(L, k, S, Gq, cap, ns);
   SplitArgs a = lay.a;
-  a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx; a.ffrag = ffrag;
+  a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx; a.ffrag = ffrag; a.rn = rn;
   a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
   a.L = L; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride; a.ns = ns;
   cudaError_t e = cudaFuncSetAttribute(decode_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total);

@@ -51,6 +51,7 @@ struct TwoArgs {
   const float* alpha32;
   const int32_t* sink_idx;
   const uint32_t* ffrag;
+  const int32_t* rn;    // [U] recent rows per unit, nullable (then R)
   const float* q;
   float* out;
   float* lse;
@@ -152,12 +153,14 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
     if (prof && tid == 0) prof[2] = clock64();
     if (!fb) {
       ndyn = select_emit_candidates<PG, SEL_NBIN>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
-                                        a.R, sel_count_u, kstar);
+                                        a.rn ? __ldg(a.rn + u) : a.R, sel_count_u, kstar);
     } else {
       produce_exact<PG, NoX, ColKey, SEL_NBIN>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
     }
   }
-  if (ndyn < 0) ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.R, sel_count_u, ms);
+  if (ndyn < 0)
+    ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.rn ? __ldg(a.rn + u) : a.R,
+                              sel_count_u, ms);
   if (prof && tid == 0) prof[3] = clock64();
   if (tid == 0) {
     a.ndyn[u] = ndyn;
@@ -316,14 +319,14 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 #endif
-  const int S = a.S, R = a.R, Gq = a.Gq;
+  const int S = a.S, R = a.rn ? __ldg(a.rn + u) : a.R, Gq = a.Gq;
   const int32_t* dyn = a.dynl + u * a.dstride;
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
-  const uint32_t* ffrag_u = a.ffrag + u * a.fblocks * 2 * 32 * 32;
+  const uint32_t* ffrag_u = a.ffrag + u * a.fblocks * FBLK_WORDS;
 #if SIKV_ATT_PREFETCH
   // start the forced fragments and the list on their way to L2 while q~ loads
-  for (int i = tid; i < nbf * 64; i += NT)
+  for (int i = tid; i < (nbf * FBLK_WORDS * 4 + 127) / 128; i += NT)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ffrag_u) + 128 * i));
   for (int i = tid; i < a.dstride / 32; i += NT)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dyn) + 128 * i));
@@ -410,13 +413,14 @@ size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
 }
 
 cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const float* cent32, const float* alpha32,
-                              const int32_t* sink_idx, int S, const uint32_t* ffrag, int fblocks, int R,
+                              const int32_t* sink_idx, int S, const uint32_t* ffrag, int fblocks,
+                              const int32_t* rn, int R,
                               const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
                               int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
                               int nsm, cudaStream_t st) {
   TwoArgs a = two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq));
   a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx;
-  a.ffrag = ffrag; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
+  a.ffrag = ffrag; a.rn = rn; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
   char* ws = reinterpret_cast<char*>(workspace) + 256;
   a.ndyn = reinterpret_cast<int32_t*>(ws);
   ws += a256((size_t)U * 4);
