@@ -72,6 +72,16 @@ int sikv_gather_rows(const void* keys, const void* values, int in_dtype, int64_t
                      int64_t tokens, int64_t dim, const int32_t* idx, int64_t n,
                      const double* mu64, void* out_k, void* out_v, int out_f64, void* stream);
 
+/* SnapKV-style sinks from a query window, float64 (K' = keys - mu; column softmax of
+ * K' W^T / sqrt(dim) over the tokens, votes = row sums, max-pool of width pool_width with
+ * edge replication, the count highest, ties -> lower index, sorted): sink_idx [U][count].
+ * window [U][window_n][dim] float64; needs 1 <= count < tokens.
+ * replaces: select_sink_tokens, cache.py:185-209 (prefill's query_window branch, 249-252) */
+size_t sikv_window_sinks_workspace_bytes(int64_t units, int64_t tokens, int window_n);
+int sikv_window_sinks(const void* keys, int in_dtype, int64_t units, int64_t tokens, int64_t dim,
+                      const double* mu64, const double* window, int window_n, int count, int pool_width,
+                      int32_t* sink_idx, void* workspace, size_t workspace_bytes, void* stream);
+
 /* decode-time append of one token per unit at ring position pos (float32/64 rows only; the
  * batched fast path uses sikv_append_forced below).
  * replaces: append_token, cache.py:274-287 */

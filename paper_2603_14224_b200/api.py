@@ -721,27 +721,23 @@ class SelfIndexingCache:
 
 
 def select_sink_tokens(keys_norm, query_window, count: int, pool_width: int = DEFAULT_POOL_WIDTH) -> torch.Tensor:
-    """cache.py:185-209: SnapKV-style sinks (cuBLAS float64 contraction, GPU softmax,
-    replicate-padded max-pool, stable top-count)."""
+    """cache.py:185-209: SnapKV-style sinks (snapkv.cu: float64 K' W^T, column softmax, votes,
+    edge-replicated max-pool, stable top-count, one C-ABI call)."""
     if count == 0:
         return torch.empty(0, dtype=torch.int64, device=_dev())
     K = _as_matrix(keys_norm, "keys_norm")
     W = _as_matrix(query_window, "query_window")
     if W.shape[1] != K.shape[1]:
         raise ValueError(f"window queries have {W.shape[1]} channels, keys have {K.shape[1]}")
-    L = K.shape[0]
+    L, D = K.shape
     if count >= L:
         return torch.arange(L, dtype=torch.int64, device=_dev())
-    logits = (K @ W.T) / math.sqrt(K.shape[1])
-    logits = logits - logits.max(dim=0, keepdim=True).values
-    w = torch.exp(logits)
-    w = w / w.sum(dim=0, keepdim=True)
-    votes = w.sum(dim=1)
-    half = pool_width // 2
-    padded = torch.cat([votes[:1].expand(half), votes, votes[-1:].expand(half)])
-    pooled = padded.unfold(0, pool_width, 1).max(dim=1).values
-    order = torch.sort(-pooled, stable=True).indices[:count]
-    return torch.sort(order).values.to(torch.int64)
+    mu0 = torch.zeros(D, dtype=torch.float64, device=K.device)
+    ws = torch.empty(L_.lib().sikv_window_sinks_workspace_bytes(1, L, W.shape[0]), dtype=torch.uint8, device=K.device)
+    out = torch.empty(count, dtype=torch.int32, device=K.device)
+    L_.call("sikv_window_sinks", L_.ptr(K.contiguous()), L_.IN_F64, 1, L, D, L_.ptr(mu0), L_.ptr(W.contiguous()),
+            W.shape[0], count, pool_width, L_.ptr(out), L_.ptr(ws), ws.numel(), L_.stream())
+    return out.to(torch.int64)
 
 
 def prefill(keys, values, query_window=None, config: CacheConfig = CacheConfig()) -> SelfIndexingCache:
@@ -755,8 +751,9 @@ def prefill(keys, values, query_window=None, config: CacheConfig = CacheConfig()
         raise ValueError(f"channel count {D} must be divisible by 4")
     if not config.lossless and D % config.group_size != 0:
         raise ValueError(f"channel count {D} not divisible by group_size {config.group_size}")
-    if V.dtype != K.dtype:
-        V = V.to(K.dtype)
+    if V.dtype != K.dtype:            # the reference converts both to float64: never round one down
+        wide = torch.promote_types(K.dtype, V.dtype)
+        K, V = K.to(wide), V.to(wide)
     bits = 0 if config.lossless else config.bits
     siq = int(config.sign_in_quant)
     r = _encode(K, V, bits=bits, group=config.group_size if bits else 4, siq=siq, what=3, want_codes=True,

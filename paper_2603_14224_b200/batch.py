@@ -123,12 +123,15 @@ def _sl(t: torch.Tensor | None, u0: int, n: int):
 
 
 def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tensor,
-                 workspace: torch.Tensor | None = None, check: bool = True) -> None:
+                 workspace: torch.Tensor | None = None, check: bool = True, window: torch.Tensor | None = None,
+                 pool_width: int = 7) -> None:
     """Compress raw K/V [n, L, 128] (bf16/f32/f64, on device) into units u0..u0+n-1.
 
-    Replaces prefill (cache.py:212-271) with bits=2, group_size=32, sign_in_quant=True
-    and first-S sinks, batched over units.  Mixed K / V dtypes are promoted to the wider one
-    (the reference converts both to float64)."""
+    Replaces prefill (cache.py:212-271) with bits=2, group_size=32, sign_in_quant=True,
+    batched over units.  Sinks: the first S positions, or with `window` [n, w, 128] the
+    SnapKV-style window sinks of each unit (select_sink_tokens, cache.py:185-209, on the GPU in
+    float64: snapkv.cu).  Mixed K / V dtypes are promoted to the wider one (the reference
+    converts both to float64)."""
     n, L, D = keys.shape
     if values.shape != keys.shape:
         raise ValueError(f"keys and values must match, got {tuple(keys.shape)} and {tuple(values.shape)}")
@@ -154,6 +157,17 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
             L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)), L_.ptr(_sl(cb.recs, u0, n)),
             L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
     S = cb.sinks
+    if window is not None and 0 < S < L:
+        if window.dim() != 3 or window.shape[0] != n or window.shape[2] != D:
+            raise ValueError(f"window must be [{n}, w, {D}], got {tuple(window.shape)}")
+        win = window.to(device=keys.device, dtype=torch.float64).contiguous()
+        wneed = L_.lib().sikv_window_sinks_workspace_bytes(n, L, win.shape[1])
+        wws = workspace if workspace is not None and workspace.numel() >= wneed else \
+            torch.empty(wneed, dtype=torch.uint8, device=keys.device)
+        sidx = torch.empty(n, S, dtype=torch.int32, device=keys.device)
+        L_.call("sikv_window_sinks", L_.ptr(keys), dt, n, L, D, L_.ptr(_sl(cb.mu64, u0, n)), L_.ptr(win),
+                win.shape[1], S, pool_width, L_.ptr(sidx), L_.ptr(wws), wws.numel(), L_.stream())
+        cb.sink_idx[u0:u0 + n] = sidx
     if S:
         L_.call("sikv_gather_rows", L_.ptr(keys), L_.ptr(values), dt, n, L, D,
                 L_.ptr(cb.sink_idx[u0:u0 + n].contiguous()), S, L_.ptr(_sl(cb.mu64, u0, n)),
@@ -171,11 +185,12 @@ def _pack_forced(cb: CacheBatch, u0: int, n: int, row_begin: int, row_end: int, 
 
 
 def prefill_batch(keys: torch.Tensor, values: torch.Tensor, *, sink_count: int = 64,
-                  recent_capacity: int = 0, keep_reference: bool = False) -> CacheBatch:
+                  recent_capacity: int = 0, keep_reference: bool = False, window: torch.Tensor | None = None,
+                  pool_width: int = 7) -> CacheBatch:
     U, L, D = keys.shape
     cb = empty_batch(U, L, sink_count=sink_count, recent_capacity=recent_capacity,
                      keep_reference=keep_reference, device=keys.device)
-    prefill_into(cb, 0, keys, values)
+    prefill_into(cb, 0, keys, values, window=window, pool_width=pool_width)
     return cb
 
 

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, os.environ.get("SIKV_LIB", "libsikv_b200.so"))
 BUILD = os.path.join(HERE, "_build" + os.environ.get("SIKV_BUILD_SUFFIX", ""))
-SOURCES = ["encode.cu", "decode.cu", "decode_split.cu", "decode_two.cu", "generic.cu", "capi.cu"]
+SOURCES = ["encode.cu", "decode.cu", "decode_split.cu", "decode_two.cu", "snapkv.cu", "generic.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"] + os.environ.get("SIKV_NVCC_EXTRA", "").split()

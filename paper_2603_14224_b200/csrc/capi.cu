@@ -46,6 +46,10 @@ size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                               const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
                               int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
+// snapkv.cu
+size_t snap_workspace_bytes(int64_t U, int64_t L, int w);
+cudaError_t launch_snap_pooled(const void*, int, int64_t, int64_t, int, const double*, const double*, int, int, void*,
+                               double**, cudaStream_t);
 // generic.cu
 cudaError_t launch_lut_f64(const double*, const double*, int64_t, int, int, double*, cudaStream_t);
 cudaError_t launch_score_f64(const double*, const uint8_t*, int64_t, int, int64_t, double*, cudaStream_t);
@@ -345,6 +349,38 @@ int sikv_score_f64(const double* lut, const uint8_t* codes_ref, int64_t units, i
 }
 
 size_t sikv_topk_workspace_bytes(int64_t units, int64_t tokens) { return topk_workspace_bytes(units, tokens); }
+
+static size_t a256h(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t sikv_window_sinks_workspace_bytes(int64_t units, int64_t tokens, int window) {
+  return a256h(snap_workspace_bytes(units, tokens, window)) + a256h(topk_workspace_bytes(units, tokens)) +
+         a256h((size_t)units * 2 * 4);
+}
+
+int sikv_window_sinks(const void* keys, int in_dtype, int64_t units, int64_t tokens, int64_t dim, const double* mu64,
+                      const double* window, int window_n, int count, int pool_width, int32_t* sink_idx,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  REQUIRE(keys && mu64 && window && sink_idx && workspace, SIKV_EINVAL, "null pointer");
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
+  REQUIRE(units >= 0 && tokens >= 1, SIKV_EINVAL, "keys must have at least one row");
+  REQUIRE(dim >= 4 && dim % 4 == 0 && dim <= 512, SIKV_EUNSUPPORTED, "window sinks support dim % 4 == 0, <= 512");
+  REQUIRE(window_n >= 1 && window_n <= 64, SIKV_EUNSUPPORTED, "window sinks support 1..64 window queries");
+  REQUIRE(count >= 1 && count < tokens, SIKV_EINVAL, "count must be in [1, tokens)");
+  REQUIRE(pool_width >= 1, SIKV_EINVAL, "pool_width must be positive");
+  REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
+  REQUIRE(workspace_bytes >= sikv_window_sinks_workspace_bytes(units, tokens, window_n), SIKV_EINVAL,
+          "workspace too small");
+  if (units == 0) return SIKV_OK;
+  double* pooled = nullptr;
+  cudaError_t e = launch_snap_pooled(keys, in_dtype, units, tokens, (int)dim, mu64, window, window_n, pool_width,
+                                     workspace, &pooled, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_ret(e, "sikv_window_sinks");
+  char* p = reinterpret_cast<char*>(workspace) + a256h(snap_workspace_bytes(units, tokens, window_n));
+  int32_t* counts = reinterpret_cast<int32_t*>(p + a256h(topk_workspace_bytes(units, tokens)));
+  return cuda_ret(launch_topk(pooled, 0, units, tokens, nullptr, 0, count, p, sink_idx, count, counts,
+                              (cudaStream_t)stream),
+                  "sikv_window_sinks");
+}
 
 int sikv_topk(const void* scores, int scores_f32, int64_t units, int64_t tokens, const int32_t* forced,
               int nforced, int k, void* workspace, int32_t* out, int out_stride, int32_t* counts, void* stream) {

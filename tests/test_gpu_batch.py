@@ -322,3 +322,48 @@ def test_append_rejects_non_finite_and_checks_buffers(c1):
         B.decode_step(cb, q, 16, with_selection=True, sel_buf=torch.empty(1, 8, dtype=torch.int32, device="cuda"))
     with pytest.raises(ValueError, match="out must"):
         B.decode_step(cb, q, 16, out=torch.empty(1, 4, 128, dtype=torch.float64, device="cuda"))
+
+
+# ---------------------------------------------------------------- SnapKV window sinks
+def make_window(L, seeds, gq=4, sinks=64, wn=32, pool=7):
+    units = [gen_unit(L, 128, gq, s, window=wn) for s in seeds]
+    K = torch.tensor(np.stack([u.keys for u in units]), dtype=torch.bfloat16, device="cuda")
+    V = torch.tensor(np.stack([u.values for u in units]), dtype=torch.bfloat16, device="cuda")
+    W = torch.tensor(np.stack([u.window for u in units]), device="cuda")
+    cb = B.prefill_batch(K, V, sink_count=sinks, window=W, pool_width=pool)
+    oc = []
+    for u in units:
+        c = O.prefill(u.keys, u.values, sink_count=sinks)
+        if sinks < L:
+            c.sinks = O.window_sinks(u.keys - c.mu, u.window, sinks, pool)
+            c.sink_k = (u.keys - c.mu)[c.sinks].copy()
+            c.sink_v = u.values[c.sinks].copy()
+        oc.append(c)
+    q = torch.tensor(np.stack([u.queries[:gq] for u in units]), dtype=torch.float32, device="cuda")
+    return units, cb, oc, q
+
+
+def test_window_sinks_golden_win_1k(golden):
+    """The batched GPU window sinks equal the real reference's select_sink_tokens (golden
+    win_1k: L = 1024, 32 window queries, 64 sinks, pool 7)."""
+    meta, _ = golden
+    rec = meta["win_1k"]
+    units, cb, oc, q = make_window(rec["L"], [rec["seed"]])
+    assert cb.sink_idx[0].cpu().tolist() == rec["sink_indices"]
+
+
+@pytest.mark.parametrize("L,sinks,wn,pool", [(4096, 64, 32, 7), (3001, 100, 8, 6), (20000, 64, 40, 1), (700, 650, 32, 7)])
+def test_window_sinks_match_oracle(L, sinks, wn, pool):
+    units, cb, oc, q = make_window(L, [300, 301, 302], sinks=sinks, wn=wn, pool=pool)
+    for i, c in enumerate(oc):
+        np.testing.assert_array_equal(cb.sink_idx[i].cpu().numpy(), c.sinks)
+        np.testing.assert_array_equal(cb.sink_k[i].cpu().numpy(), c.sink_k.astype(np.float32))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_decode_with_window_sinks(kernel):
+    """Non-prefix sinks (SnapKV) through every fused decode kernel: forced-bit exclusion
+    beyond the first block, forced fragments of scattered rows, sorted selection."""
+    units, cb, oc, q = make_window(32768 if kernel == 3 else 8192, [310, 311], sinks=64)
+    assert int(cb.sink_idx[:, -1].min()) > 64                   # scattered, not a prefix
+    _check_decode(units, cb, oc, q, 512, kernel=kernel)
