@@ -73,3 +73,61 @@ def select32(cache: O.OracleCache, qs: np.ndarray, k: int):
     s = scores32(lut32(qbar, cache.centroids), cache.packed_codes).astype(np.float64)
     s = np.concatenate([s, np.full(len(cache.recent_k), -np.inf)])
     return O.top_k(s, k, sink=cache.sinks, recent=cache.recents())
+
+
+# --------------------------------------------------------------------------- certified bound
+U32 = 2.0 ** -24
+U64 = 2.0 ** -53
+
+
+def _gamma(n: int, u: float) -> float:
+    return n * u / (1.0 - n * u)
+
+
+def score_error_bound(cache: O.OracleCache, qs: np.ndarray) -> float:
+    """A bound B with |scores32(t) - s64(t)| <= B for every prefill token t, where s64 is the
+    reference's float64 score of the group-sum query (select_tokens(cache, sum_h q_h),
+    cache.py:290-309) and scores32 the fast path's float32 order above.
+
+    Standard forward error analysis (Higham, ch. 3), per group g and code c:
+      qbar:   |fl32(sum_h q_h) - sum_h q_h| <= gamma_{Gq-1} sum_h |q_h|          (per channel)
+      LUT:    fl32 centroids (1 rounding), 4 products + 3 adds -> gamma_4 relative on
+              sum_i |qbar_i c_i|, plus the qbar error times |c|;
+      pairs:  one add (u |P|);  score: 15 sequential adds, gamma_15 on sum_p |P_p|;
+      and the reference's own float64 rounding (gamma_40 in double on the same sums).
+    The bound is uniform over tokens: every term is maximised over the 16 codes of a group."""
+    qs = np.asarray(qs, dtype=np.float64)
+    gq = qs.shape[0]
+    qbar = group_query(qs).astype(np.float64)
+    dq = _gamma(max(gq - 1, 0), U32) * np.abs(qs).sum(axis=0)           # per channel
+    c = np.abs(cache.centroids)                                          # (G, 16, 4)
+    G = c.shape[0]
+    qa = np.abs(qbar).reshape(G, 1, 4)
+    dqa = dq.reshape(G, 1, 4)
+    e_lut = ((dqa + (_gamma(4, U32) + U32) * qa) * c * (1 + U32)).sum(axis=2)   # (G, 16)
+    mag = (qa * c).sum(axis=2) * (1 + _gamma(5, U32))                   # |LUT| bound
+    e_lut_max = e_lut.max(axis=1)
+    mag_max = mag.max(axis=1)
+    pair_mag = mag_max[0::2] + mag_max[1::2]
+    B = e_lut_max.sum() + U32 * pair_mag.sum() + _gamma(15, U32) * pair_mag.sum() * (1 + U32)
+    B += _gamma(40, U64) * (np.abs(qs).sum(axis=0).reshape(G, 1, 4) * c).sum(axis=2).max(axis=1).sum()
+    return float(B * 1.01)
+
+
+def certified_selection_check(cache: O.OracleCache, qs: np.ndarray, k: int, got: np.ndarray):
+    """Compare a fast-path selection with the reference's float64 selection of the group-sum
+    query.  Returns (ok, n_diff, gap, bound): the sets must be equal, except that tokens whose
+    float64 score lies within 2B of the float64 k-th score (B = score_error_bound) may swap —
+    there the float32 order cannot certify which side of the boundary they fall on."""
+    q64 = np.asarray(qs, dtype=np.float64).sum(axis=0)
+    ref = O.select(cache, q64, k)[0]
+    got = np.asarray(got)
+    diff = np.setxor1d(ref, got)
+    B = score_error_bound(cache, qs)
+    if diff.size == 0:
+        return True, 0, np.inf, B
+    s64 = O.score(O.lut(q64, cache.centroids), cache.codes)
+    dyn = np.setdiff1d(ref, np.concatenate([cache.sinks, np.arange(cache.L, cache.L + len(cache.recent_k))]))
+    kth = s64[dyn].min()
+    gap = float(np.abs(s64[diff[diff < cache.L]] - kth).max()) if np.any(diff < cache.L) else np.inf
+    return bool(gap <= 2 * B), int(diff.size), gap, B

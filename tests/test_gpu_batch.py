@@ -5,8 +5,8 @@ vectors) and the float32 scoring restatement (oracle/restate32.py):
   * encoder planes, mu, alpha: bit-exact; float32 centroids == fl32(oracle float64);
   * fast-path scores: bit-exact vs restate32;
   * selections: exact index sets vs restate32 + the reference's top_k_select rule;
-  * attention: rel-L2 <= 3e-3 and cosine >= 0.99999 vs the float64 oracle on the same
-    selection (fp16 mma operands, fp32 accumulation).
+  * attention: rel-L2 and cosine vs the float64 oracle on the same selection within the bars
+    of tests/tolerances.py (set from the measured maxima; fp16 mma operands, fp32 accumulation).
 """
 
 import numpy as np
@@ -22,8 +22,7 @@ from .fastlayout import records_to_reference, unrotate_signs
 
 pytestmark = pytest.mark.gpu
 
-ATT_REL_L2 = 3e-3
-ATT_COS = 0.99999
+from .tolerances import ATT_COS, att_rel_l2
 
 
 def make(L, seeds, gq=4, sinks=64, appends=0, dtype=torch.bfloat16):
@@ -109,9 +108,10 @@ def _check_decode(units, cb, oc, q, k, **kw):
         idx, ns, nr, nd = R.select32(c, q[i].cpu().numpy(), k)
         assert cnt[i] == len(idx)
         np.testing.assert_array_equal(sel[i, :cnt[i]], idx)
+        tol = att_rel_l2(c.L)
         for h in range(qs.shape[0]):
             ref = O.sparse_attention(qs[h], idx, c)
-            assert O.rel_l2(out[i, h], ref) <= ATT_REL_L2, (i, h, O.rel_l2(out[i, h], ref))
+            assert O.rel_l2(out[i, h], ref) <= tol, (i, h, O.rel_l2(out[i, h], ref))
             assert O.cosine(out[i, h], ref) >= ATT_COS
     return res
 
@@ -133,7 +133,7 @@ def test_decode_matches_reference_selection(c1, golden):
     res = B.decode_step(cb, q, 256, with_selection=True)
     sel = res.selection[0, :res.counts[0]].cpu().numpy()
     ref = arr["c1_u0/sel"]
-    assert len(np.intersect1d(sel, ref)) >= len(ref) - 1
+    np.testing.assert_array_equal(sel, ref)          # measured: identical to the reference's set
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
