@@ -152,6 +152,43 @@ def _pack(codes: torch.Tensor, bits: int) -> torch.Tensor:
     return (buf.reshape(rows, width, per) << shifts).sum(-1).to(torch.uint8)
 
 
+def pack_rows(codes, bits: int) -> torch.Tensor:
+    """bitpack.py:27-48: rows of bits-bit codes -> uint8, lowest element in the low bits."""
+    if bits not in PACKABLE_BITS:
+        raise ValueError(f"bits must be one of {PACKABLE_BITS}, got {bits}")
+    if isinstance(codes, torch.Tensor):
+        c = codes.to(_dev())
+        integer = not (c.is_floating_point() or c.is_complex() or c.dtype == torch.bool)
+        lo_hi = (int(c.min()), int(c.max())) if c.numel() and integer else (0, 0)
+    else:
+        a = np.asarray(codes)
+        integer = np.issubdtype(a.dtype, np.integer)
+        lo_hi = (int(a.min()), int(a.max())) if a.size and integer else (0, 0)
+        c = torch.as_tensor(a.astype(np.int64) if integer else a, device=_dev())
+    if c.dim() != 2:
+        raise ValueError(f"expected a 2-D code array, got shape {tuple(c.shape)}")
+    if not integer:
+        raise ValueError(f"codes must be integers, got dtype {c.dtype}")
+    if lo_hi[0] < 0 or lo_hi[1] >= (1 << bits):
+        raise ValueError(f"codes out of range for {bits}-bit packing")
+    return _pack(c, bits)
+
+
+def unpack_rows(packed, bits: int, num_elements: int) -> torch.Tensor:
+    """bitpack.py:51-67: inverse of pack_rows, (rows, num_elements) uint8."""
+    if bits not in PACKABLE_BITS:
+        raise ValueError(f"bits must be one of {PACKABLE_BITS}, got {bits}")
+    p = packed.to(_dev()).to(torch.uint8) if isinstance(packed, torch.Tensor) else \
+        torch.as_tensor(np.asarray(packed, dtype=np.uint8), device=_dev())
+    if p.dim() != 2:
+        raise ValueError(f"expected a 2-D packed array, got shape {tuple(p.shape)}")
+    want = packed_row_bytes(num_elements, bits)
+    if p.shape[1] != want:
+        raise ValueError(f"packed row has {p.shape[1]} bytes, expected {want} for {num_elements} elements "
+                         f"at {bits} bits")
+    return _unpack(p, bits, num_elements)
+
+
 # ============================================================================ normalize
 @dataclass(frozen=True, eq=False)
 class NormalizationState:
