@@ -78,6 +78,24 @@ def _dev() -> torch.device:
     return L_.require_cuda()
 
 
+# Input validation follows the reference (ValueError at call time).  Host arrays are checked on
+# the host before they are uploaded (no device sync).  Device tensors need one device->host
+# read per check; set_device_input_checks(False) skips those (the caller vouches for its
+# tensors) so chained GPU calls stay asynchronous.
+_DEVICE_CHECKS = True
+
+
+def set_device_input_checks(on: bool) -> None:
+    global _DEVICE_CHECKS
+    _DEVICE_CHECKS = bool(on)
+
+
+def _finite(t: torch.Tensor, host) -> bool:
+    if host is not None:
+        return bool(np.isfinite(host).all())
+    return not _DEVICE_CHECKS or bool(torch.isfinite(t).all())
+
+
 def _tensor(x, dtype=torch.float64) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x.to(_dev())
@@ -87,26 +105,28 @@ def _tensor(x, dtype=torch.float64) -> torch.Tensor:
 
 def _as_matrix(x, name: str = "matrix", keep_dtype: bool = False) -> torch.Tensor:
     """normalize.py:16-24 validation; keep_dtype keeps bf16/f32 inputs for the encoder."""
-    t = x.to(_dev()) if isinstance(x, torch.Tensor) else _tensor(x)
+    host = None if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64)
+    t = x.to(_dev()) if host is None else torch.as_tensor(host, device=_dev())
     if not keep_dtype or t.dtype not in (torch.float32, torch.float64, torch.bfloat16):
         t = t.to(torch.float64)
     if t.dim() != 2:
         raise ValueError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
     if t.shape[0] < 1:
         raise ValueError(f"{name} must contain at least one row")
-    if not bool(torch.isfinite(t).all()):
+    if not _finite(t, host):
         raise ValueError(f"{name} contains non-finite entries")
     return t.contiguous()
 
 
 def _as_query(q, dim: int | None = None) -> torch.Tensor:
     """retrieval.py:20-28."""
-    t = _tensor(q)
+    host = None if isinstance(q, torch.Tensor) else np.asarray(q, dtype=np.float64)
+    t = _tensor(q if host is None else host)
     if t.dim() != 1:
         raise ValueError(f"query must be 1-D, got shape {tuple(t.shape)}")
     if dim is not None and t.shape[0] != dim:
         raise ValueError(f"query has {t.shape[0]} channels, expected {dim}")
-    if not bool(torch.isfinite(t).all()):
+    if not _finite(t, host):
         raise ValueError("query contains non-finite entries")
     return t.contiguous()
 
@@ -120,9 +140,14 @@ def _status() -> torch.Tensor:
 
 
 def _rows(rows, n: int) -> torch.Tensor:
-    r = torch.as_tensor(np.asarray(rows, dtype=np.int64) if not isinstance(rows, torch.Tensor) else rows,
-                        device=_dev()).to(torch.int64).reshape(-1).contiguous()
-    if r.numel() and (int(r.min()) < 0 or int(r.max()) >= n):
+    if isinstance(rows, torch.Tensor):
+        r = rows.to(_dev()).to(torch.int64).reshape(-1).contiguous()
+        bad = _DEVICE_CHECKS and r.numel() and (int(r.min()) < 0 or int(r.max()) >= n)
+    else:
+        h = np.asarray(rows, dtype=np.int64).reshape(-1)
+        bad = h.size and (h.min() < 0 or h.max() >= n)
+        r = torch.as_tensor(h, device=_dev())
+    if bad:
         raise ValueError(f"rows out of range [0, {n})")
     return r
 
@@ -573,6 +598,7 @@ class TokenSelection:
     sink_count: int
     recent_count: int
     dynamic_count: int
+    _valid: bool = field(default=False, repr=False)   # made by top_k_select: indices known in range
 
     def __post_init__(self) -> None:
         if self.indices.dim() != 1:
@@ -584,18 +610,18 @@ class TokenSelection:
         return int(self.indices.shape[0])
 
 
-def _as_index_set(indices, length: int, name: str) -> torch.Tensor:
-    """retrieval.py:116-124."""
+def _as_index_set(indices, length: int, name: str):
+    """retrieval.py:116-124: (device index set, host copy or None).  Host inputs are checked
+    and deduplicated on the host."""
     if isinstance(indices, torch.Tensor):
-        arr = indices.to(_dev()).to(torch.int64).reshape(-1)
-    elif isinstance(indices, np.ndarray):
-        arr = torch.as_tensor(indices.astype(np.int64), device=_dev()).reshape(-1)
-    else:
-        arr = torch.as_tensor(np.array(sorted(indices), dtype=np.int64), device=_dev())
-    idx = torch.unique(arr)
-    if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= length):
+        idx = torch.unique(indices.to(_dev()).to(torch.int64).reshape(-1))
+        if _DEVICE_CHECKS and idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= length):
+            raise ValueError(f"{name} indices out of range [0, {length})")
+        return idx, None
+    h = np.unique(np.asarray(indices if isinstance(indices, np.ndarray) else sorted(indices), dtype=np.int64))
+    if h.size and (h[0] < 0 or h[-1] >= length):
         raise ValueError(f"{name} indices out of range [0, {length})")
-    return idx
+    return torch.as_tensor(h, device=_dev()), h
 
 
 def top_k_select(scores, k: int, sink=(), recent=()) -> TokenSelection:
@@ -606,8 +632,8 @@ def top_k_select(scores, k: int, sink=(), recent=()) -> TokenSelection:
     if k < 0:
         raise ValueError(f"k must be non-negative, got {k}")
     L = int(s.shape[0])
-    sink_idx = _as_index_set(sink, L, "sink")
-    recent_idx = _as_index_set(recent, L, "recent")
+    sink_idx, sink_h = _as_index_set(sink, L, "sink")
+    recent_idx, recent_h = _as_index_set(recent, L, "recent")
     forced = torch.unique(torch.cat([sink_idx, recent_idx])).to(torch.int32).contiguous()
     F = int(forced.numel())
     keff = min(k, L - F)
@@ -618,9 +644,14 @@ def top_k_select(scores, k: int, sink=(), recent=()) -> TokenSelection:
         ws = _ws(L_.lib().sikv_topk_workspace_bytes(1, L))
         L_.call("sikv_topk", L_.ptr(s.contiguous()), 0, 1, L, L_.ptr(forced) if F else None, F, k, L_.ptr(ws),
                 L_.ptr(out), max(n, 1), L_.ptr(counts), L_.stream())
-    recent_only = int(torch.isin(recent_idx, sink_idx, invert=True).sum()) if recent_idx.numel() else 0
+    if not recent_idx.numel():
+        recent_only = 0
+    elif sink_h is not None and recent_h is not None:
+        recent_only = int(np.isin(recent_h, sink_h, invert=True).sum())
+    else:
+        recent_only = int(torch.isin(recent_idx, sink_idx, invert=True).sum())
     return TokenSelection(indices=out[:n].to(torch.int64), sink_count=int(sink_idx.numel()),
-                          recent_count=recent_only, dynamic_count=max(keff, 0))
+                          recent_count=recent_only, dynamic_count=max(keff, 0), _valid=True)
 
 
 def resolve_dynamic_k(length: int, forced_count: int, budget: int | None = None,
@@ -694,6 +725,14 @@ class SelfIndexingCache:
     @property
     def recent_count(self) -> int:
         return self._n_recent
+
+    def sink_host(self) -> np.ndarray:
+        """The sink indices as a host array (read once: they are fixed at prefill)."""
+        h = self.__dict__.get("_sink_h")
+        if h is None:
+            h = self.sink_indices.cpu().numpy().astype(np.int64)
+            self.__dict__["_sink_h"] = h
+        return h
 
     def recent_indices(self) -> torch.Tensor:
         return torch.arange(self.prefill_length, self.length, dtype=torch.int64, device=_dev())
@@ -862,18 +901,19 @@ def select_tokens(cache: SelfIndexingCache, q, k: int | None = None, budget: int
     lut = build_sign_lut(qq, cache.codes.num_groups) if sign_only else build_lut(qq, cache.codebook)
     pre = score_tokens(lut, cache.codes)
     scores = torch.cat([pre, torch.full((cache.recent_count,), -math.inf, dtype=torch.float64, device=_dev())])
-    forced = cache.forced_indices()
     if k is None:
-        k = resolve_dynamic_k(cache.length, int(forced.numel()), budget=budget, sparsity=sparsity)
+        nforced = int(np.union1d(cache.sink_host(), np.arange(cache.prefill_length, cache.length)).size)
+        k = resolve_dynamic_k(cache.length, nforced, budget=budget, sparsity=sparsity)
     elif budget is not None or sparsity is not None:
         raise ValueError("give exactly one of k, budget and sparsity")
-    return top_k_select(scores, k, sink=cache.sink_indices, recent=cache.recent_indices())
+    return top_k_select(scores, k, sink=cache.sink_host(), recent=np.arange(cache.prefill_length, cache.length))
 
 
 # ============================================================================ attention
 @dataclass(frozen=True, eq=False)
 class AttentionOutput:
-    """attention.py:23-26."""
+    """attention.py:23-26.  weights_checksum: a float, or a 0-d device tensor for outputs of
+    sparse_attention (no host sync; float(...) reads it)."""
     out: torch.Tensor
     weights_checksum: float
 
@@ -906,22 +946,28 @@ def sparse_attention(q, selection: TokenSelection, cache: SelfIndexingCache) -> 
     if len(selection) == 0:
         raise ValueError("selection is empty")
     qq = _as_query(q, dim=cache.dim)
-    idx = selection.indices.to(_dev()).to(torch.int32).contiguous()
+    si = selection.indices
+    idx = (si.to(_dev()) if isinstance(si, torch.Tensor) else
+           torch.as_tensor(np.asarray(si, dtype=np.int64), device=_dev())).to(torch.int32).contiguous()
     n = int(idx.numel())
-    if n and (int(idx.min()) < 0 or int(idx.max()) >= cache.length):
+    if not selection._valid and n and _DEVICE_CHECKS and (int(idx.min()) < 0 or int(idx.max()) >= cache.length):
         raise ValueError(f"indices out of range [0, {cache.length})")
     cnt = torch.tensor([n], dtype=torch.int32, device=_dev())
     ws = torch.empty(n, dtype=torch.float64, device=_dev())
     out = torch.empty(cache.dim, dtype=torch.float64, device=_dev())
-    chk = torch.empty(1, dtype=torch.float64, device=_dev())
+    chk = torch.empty((), dtype=torch.float64, device=_dev())
     S = int(cache.sink_indices.numel())
-    ndyn = int((~torch.isin(idx.to(torch.int64), cache.forced_indices())).sum())
+    # dequantised rows = the selection's dynamic (non-forced) rows (cache.py:118-158)
+    ndyn = selection.dynamic_count if selection._valid else \
+        int(np.isin(idx.cpu().numpy(), np.union1d(cache.sink_host(), np.arange(cache.prefill_length, cache.length)),
+                    invert=True).sum())
     tally("dequant_rows", 0 if cache.config.lossless else 2 * ndyn)
     L_.call("sikv_attend_f64", *cache._planes(), 1, cache.prefill_length, cache.dim, L_.ptr(qq), 1, L_.ptr(idx),
             L_.ptr(cnt), n, L_.ptr(cache.sink_indices.to(torch.int32).contiguous()) if S else None, S,
             L_.ptr(cache.sink_k), L_.ptr(cache.sink_v), L_.ptr(cache._recent_k), L_.ptr(cache._recent_v),
             cache._recent_k.shape[0], L_.ptr(ws), L_.ptr(out), L_.ptr(chk), L_.stream())
-    return AttentionOutput(out=out, weights_checksum=float(chk.item()))
+    # the checksum stays on the device (a 0-d tensor, read when used): no host sync here
+    return AttentionOutput(out=out, weights_checksum=chk)
 
 
 def output_error(a: AttentionOutput, b: AttentionOutput) -> ErrorReport:
