@@ -46,6 +46,16 @@ def lut32(qbar: np.ndarray, centroids64: np.ndarray) -> np.ndarray:
     return ((p[..., 0] + p[..., 2]) + (p[..., 1] + p[..., 3])).astype(np.float32)
 
 
+def sign_lut32(qbar: np.ndarray, groups: int) -> np.ndarray:
+    """Sign-only LUT (build_sign_lut, retrieval.py:54-62) in the same float32 pairing as
+    lut32, with the code's +-1 pattern (element i <-> bit 3 - i) in place of the centroid:
+    the products are exact, ``(s0 q0 + s2 q2) + (s1 q1 + s3 q3)``."""
+    pat = (((np.arange(16)[:, None] >> O._SH) & 1) * 2 - 1).astype(np.float32)   # (16, 4)
+    q = np.asarray(qbar, dtype=np.float32).reshape(groups, 1, 4)
+    p = (q * pat[None]).astype(np.float32)
+    return ((p[..., 0] + p[..., 2]) + (p[..., 1] + p[..., 3])).astype(np.float32)
+
+
 def pair_table(table: np.ndarray) -> np.ndarray:
     """(G/2, 256) float32 pair table."""
     G = table.shape[0]
@@ -67,10 +77,11 @@ def scores32(table: np.ndarray, packed_codes: np.ndarray) -> np.ndarray:
     return s
 
 
-def select32(cache: O.OracleCache, qs: np.ndarray, k: int):
+def select32(cache: O.OracleCache, qs: np.ndarray, k: int, sign_only: bool = False):
     """Group-sum fp32 selection on an oracle cache; returns (indices, counts...)."""
     qbar = group_query(qs)
-    s = scores32(lut32(qbar, cache.centroids), cache.packed_codes).astype(np.float64)
+    table = sign_lut32(qbar, cache.centroids.shape[0]) if sign_only else lut32(qbar, cache.centroids)
+    s = scores32(table, cache.packed_codes).astype(np.float64)
     s = np.concatenate([s, np.full(len(cache.recent_k), -np.inf)])
     return O.top_k(s, k, sink=cache.sinks, recent=cache.recents())
 
@@ -84,7 +95,7 @@ def _gamma(n: int, u: float) -> float:
     return n * u / (1.0 - n * u)
 
 
-def score_error_bound(cache: O.OracleCache, qs: np.ndarray) -> float:
+def score_error_bound(cache: O.OracleCache, qs: np.ndarray, sign_only: bool = False) -> float:
     """A bound B with |scores32(t) - s64(t)| <= B for every prefill token t, where s64 is the
     reference's float64 score of the group-sum query (select_tokens(cache, sum_h q_h),
     cache.py:290-309) and scores32 the fast path's float32 order above.
@@ -100,7 +111,7 @@ def score_error_bound(cache: O.OracleCache, qs: np.ndarray) -> float:
     gq = qs.shape[0]
     qbar = group_query(qs).astype(np.float64)
     dq = _gamma(max(gq - 1, 0), U32) * np.abs(qs).sum(axis=0)           # per channel
-    c = np.abs(cache.centroids)                                          # (G, 16, 4)
+    c = np.ones_like(cache.centroids) if sign_only else np.abs(cache.centroids)   # (G, 16, 4)
     G = c.shape[0]
     qa = np.abs(qbar).reshape(G, 1, 4)
     dqa = dq.reshape(G, 1, 4)
@@ -114,19 +125,21 @@ def score_error_bound(cache: O.OracleCache, qs: np.ndarray) -> float:
     return float(B * 1.01)
 
 
-def certified_selection_check(cache: O.OracleCache, qs: np.ndarray, k: int, got: np.ndarray):
+def certified_selection_check(cache: O.OracleCache, qs: np.ndarray, k: int, got: np.ndarray,
+                              sign_only: bool = False):
     """Compare a fast-path selection with the reference's float64 selection of the group-sum
     query.  Returns (ok, n_diff, gap, bound): the sets must be equal, except that tokens whose
     float64 score lies within 2B of the float64 k-th score (B = score_error_bound) may swap —
     there the float32 order cannot certify which side of the boundary they fall on."""
     q64 = np.asarray(qs, dtype=np.float64).sum(axis=0)
-    ref = O.select(cache, q64, k)[0]
+    ref = O.select(cache, q64, k, sign_only=sign_only)[0]
     got = np.asarray(got)
     diff = np.setxor1d(ref, got)
-    B = score_error_bound(cache, qs)
+    B = score_error_bound(cache, qs, sign_only)
     if diff.size == 0:
         return True, 0, np.inf, B
-    s64 = O.score(O.lut(q64, cache.centroids), cache.codes)
+    G = cache.centroids.shape[0]
+    s64 = O.score(O.sign_lut(q64, G) if sign_only else O.lut(q64, cache.centroids), cache.codes)
     dyn = np.setdiff1d(ref, np.concatenate([cache.sinks, np.arange(cache.L, cache.L + len(cache.recent_k))]))
     kth = s64[dyn].min()
     gap = float(np.abs(s64[diff[diff < cache.L]] - kth).max()) if np.any(diff < cache.L) else np.inf

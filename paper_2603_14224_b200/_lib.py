@@ -35,7 +35,7 @@ _SIGS = {
     "sikv_append": (I, [P, P, I, I64, I64, P, P, P, I64, I64, I, P, P]),
     "sikv_decode_smem_bytes": (I, [I64, I, I, I, I]),
     "sikv_decode_default_cap": (I, [I64, I, I]),
-    "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, P, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, I, P]),
+    "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, P, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, I, I, P]),
     "sikv_decode_workspace_bytes": (SZ, [I64, I64]),
     "sikv_decode_workspace_bytes_k": (SZ, [I64, I64, I, I]),
     "sikv_decode_last_kernel": (I, []),
@@ -43,7 +43,7 @@ _SIGS = {
     "sikv_forced_block_words": (I, []),
     "sikv_pack_forced": (I, [P, P, I, P, P, I64, P, I, P, I64, P, I, I, I, P, P]),
     "sikv_append_forced": (I, [P, P, I, I64, P, P, P, P, P, I, P, P, I64, P, P, I, P, P]),
-    "sikv_score_fast": (I, [P, P, P, I, I64, I64, P, P]),
+    "sikv_score_fast": (I, [P, P, P, I, I64, I64, I, P, P]),
     "sikv_debug_set_decode_profile": (I, [P]),
     "sikv_debug_set_attend_skip": (I, [I]),
     "sikv_build_lut_f64": (I, [P, P, I64, I, I, P, P]),

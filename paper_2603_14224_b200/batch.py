@@ -46,6 +46,8 @@ class CacheBatch:
     ffrag: torch.Tensor                       # [U, blocks, FBLK] int32 forced-row fragments + row scales
     recent_host: torch.Tensor = None          # [U] int64 host mirror of recent_n (appends are host-issued)
     ref: dict = field(default_factory=dict)   # optional reference-layout planes
+    bits: int = 2                             # payload bits: 2, or 1 (same record, codes in 2-bit fields)
+    sign_in_quant: bool = True                # False: keys quantised directly (cache.py:241-244)
 
     @property
     def sinks(self) -> int:
@@ -73,7 +75,12 @@ def _frag_blocks(sinks: int, capacity: int) -> int:
 
 
 def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacity: int = 0,
-                keep_reference: bool = False, device=None) -> CacheBatch:
+                keep_reference: bool = False, device=None, bits: int = 2, sign_in_quant: bool = True) -> CacheBatch:
+    """An empty batch of `units` caches of `tokens` prefill tokens.  Fast-path variants
+    (cache.py:52-75): bits 2 or 1 (the 1-bit codes use the same record, in its 2-bit fields),
+    sign_in_quant True (|K'| / alpha codes + sign plane) or False (direct signed K' codes)."""
+    if bits not in (1, 2):
+        raise NotImplementedError("the fast path supports bits 1 and 2 (the per-head API covers 4, 8, 16)")
     dev = device or L_.require_cuda()
     S = min(sink_count, tokens)
     f32 = dict(device=dev, dtype=torch.float32)
@@ -92,12 +99,12 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
         recent_n=torch.zeros(units, device=dev, dtype=torch.int32),
         ffrag=torch.zeros(units, _frag_blocks(S, recent_capacity), L_.lib().sikv_forced_block_words(),
                           device=dev, dtype=torch.int32),
-        recent_host=torch.zeros(units, dtype=torch.int64),
+        recent_host=torch.zeros(units, dtype=torch.int64), bits=bits, sign_in_quant=bool(sign_in_quant),
     )
     if keep_reference:
         cb.ref = dict(
             codes=torch.empty(units, tokens, 16, **u8),
-            kq=torch.empty(units, tokens, 32, **u8), vq=torch.empty(units, tokens, 32, **u8),
+            kq=torch.empty(units, tokens, 16 * bits, **u8), vq=torch.empty(units, tokens, 16 * bits, **u8),
             ks=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
             kz=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
             vs=torch.empty(units, tokens, 4, device=dev, dtype=torch.float16),
@@ -115,7 +122,8 @@ def subset(cb: CacheBatch, ids) -> CacheBatch:
         alpha32=take(cb.alpha32), cent64=take(cb.cent64), cent32=take(cb.cent32), signs=take(cb.signs),
         recs=take(cb.recs), sink_idx=take(cb.sink_idx), sink_k=take(cb.sink_k), sink_v=take(cb.sink_v),
         recent_k=take(cb.recent_k), recent_v=take(cb.recent_v), recent_n=take(cb.recent_n), ffrag=take(cb.ffrag),
-        recent_host=cb.recent_host.index_select(0, ix.cpu()), ref={k: take(v) for k, v in cb.ref.items()})
+        recent_host=cb.recent_host.index_select(0, ix.cpu()), ref={k: take(v) for k, v in cb.ref.items()},
+        bits=cb.bits, sign_in_quant=cb.sign_in_quant)
 
 
 def _sl(t: torch.Tensor | None, u0: int, n: int):
@@ -148,7 +156,7 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
         workspace = torch.empty(need, dtype=torch.uint8, device=keys.device)
     status = torch.zeros(1, dtype=torch.int32, device=keys.device)
     r = cb.ref
-    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, 2, 32, 1, 3, None,
+    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, cb.bits, 32, int(cb.sign_in_quant), 3, None,
             L_.ptr(_sl(cb.mu64, u0, n)), L_.ptr(_sl(cb.alpha64, u0, n)), L_.ptr(_sl(cb.mu32, u0, n)),
             L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.cent64, u0, n)), L_.ptr(_sl(cb.cent32, u0, n)),
             L_.ptr(_sl(r.get("codes"), u0, n)), L_.ptr(_sl(r.get("kq"), u0, n)),
@@ -156,6 +164,9 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
             L_.ptr(_sl(r.get("vq"), u0, n)), L_.ptr(_sl(r.get("vs"), u0, n)),
             L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)), L_.ptr(_sl(cb.recs, u0, n)),
             L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
+    if not cb.sign_in_quant:
+        # direct keys: the record dequantises to K' itself, so the attention's alpha-hat is 1
+        cb.alpha32[u0:u0 + n] = 1.0
     S = cb.sinks
     if window is not None and 0 < S < L:
         if window.dim() != 3 or window.shape[0] != n or window.shape[2] != D:
@@ -186,10 +197,10 @@ def _pack_forced(cb: CacheBatch, u0: int, n: int, row_begin: int, row_end: int, 
 
 def prefill_batch(keys: torch.Tensor, values: torch.Tensor, *, sink_count: int = 64,
                   recent_capacity: int = 0, keep_reference: bool = False, window: torch.Tensor | None = None,
-                  pool_width: int = 7) -> CacheBatch:
+                  pool_width: int = 7, bits: int = 2, sign_in_quant: bool = True) -> CacheBatch:
     U, L, D = keys.shape
     cb = empty_batch(U, L, sink_count=sink_count, recent_capacity=recent_capacity,
-                     keep_reference=keep_reference, device=keys.device)
+                     keep_reference=keep_reference, device=keys.device, bits=bits, sign_in_quant=sign_in_quant)
     prefill_into(cb, 0, keys, values, window=window, pool_width=pool_width)
     return cb
 
@@ -277,10 +288,12 @@ def _workspace(units: int, tokens: int, k: int, sinks: int, device) -> torch.Ten
 
 def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_selection: bool = False,
                 with_lse: bool = False, with_diag: bool = False, out: torch.Tensor | None = None,
-                sel_buf: torch.Tensor | None = None, kernel: int = 0, append=None) -> DecodeOutput:
+                sel_buf: torch.Tensor | None = None, kernel: int = 0, append=None,
+                sign_only: bool = False) -> DecodeOutput:
     """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
 
-    append=(k, v) first appends one token per unit ([U, 128] rows, append_batch without the
+    sign_only=True scores with the sign-only LUT (select_tokens(..., sign_only=True),
+    retrieval.py:54-62).  append=(k, v) first appends one token per unit ([U, 128] rows, append_batch without the
     status sync), so a generation step is one call.  kernel: 0 auto, 1 one CTA per unit,
     3 each unit split across a CTA cluster (long contexts, few units), 4 two kernels
     (selection with two unit groups per SM, then attention)."""
@@ -320,16 +333,16 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], L_.ptr(cb.recent_n), R,
             L_.ptr(qf), U, cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), stride, L_.ptr(cnt),
-            L_.ptr(diag), L_.ptr(ws), ws.numel(), kernel, L_.stream())
+            L_.ptr(diag), L_.ptr(ws), ws.numel(), int(sign_only), kernel, L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)
 
 
-def score_fast(cb: CacheBatch, q: torch.Tensor) -> torch.Tensor:
+def score_fast(cb: CacheBatch, q: torch.Tensor, sign_only: bool = False) -> torch.Tensor:
     """float32 fast-path scores of every prefill token (group-summed query) [U, L]."""
     qf = q.float().contiguous()
     out = torch.empty(cb.units, cb.tokens, device=q.device, dtype=torch.float32)
     L_.call("sikv_score_fast", L_.ptr(cb.signs), L_.ptr(cb.cent32), L_.ptr(qf), q.shape[1], cb.units,
-            cb.tokens, L_.ptr(out), L_.stream())
+            cb.tokens, int(sign_only), L_.ptr(out), L_.stream())
     return out
 
 

@@ -24,13 +24,13 @@ cudaError_t launch_append(const void*, const void*, int, int64_t, int, const dou
 DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap);
 cudaError_t launch_decode(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                           const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*,
-                          float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t, int*);
+                          float*, int32_t*, int, int32_t*, int32_t*, int, cudaStream_t, int*);
 cudaError_t launch_pack_forced(const float*, const float*, int, const float*, const float*, int64_t, const int32_t*,
                                int, const float*, int64_t, int, int, int, uint32_t*, int*, cudaStream_t);
 cudaError_t launch_append_forced(const void*, const void*, int, int64_t, const int32_t*, const double*, const float*,
                                  const float*, const float*, int, float*, float*, int64_t, int32_t*, int, uint32_t*,
                                  int*, cudaStream_t);
-cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, float*,
+cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, int64_t, int64_t, int, float*,
                               cudaStream_t);
 cudaError_t set_decode_profile(long long*);
 cudaError_t set_k1_skip(int);
@@ -39,13 +39,13 @@ int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
 cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                                 const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, int, float*,
-                                float*, int32_t*, int, int32_t*, int32_t*, cudaStream_t);
+                                float*, int32_t*, int, int32_t*, int32_t*, int, cudaStream_t);
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq);
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq);
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                               const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
-                              int32_t*, int, int32_t*, int32_t*, void*, int, cudaStream_t);
+                              int32_t*, int, int32_t*, int32_t*, void*, int, int, cudaStream_t);
 // snapkv.cu
 size_t snap_workspace_bytes(int64_t U, int64_t L, int w);
 cudaError_t launch_snap_pooled(const void*, int, int64_t, int64_t, int, const double*, const double*, int, int, void*,
@@ -95,7 +95,7 @@ static int max_smem() {
 extern "C" {
 
 const char* sikv_last_error(void) { return g_err.c_str(); }
-int sikv_abi_version(void) { return 3; }
+int sikv_abi_version(void) { return 4; }
 
 size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
   return encode_workspace_bytes(units, tokens, (int)dim);
@@ -130,8 +130,8 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
   }
   if (signs_fast || recs_fast) {
     REQUIRE(signs_fast && recs_fast, SIKV_EINVAL, "fast layout needs both signs_fast and recs_fast");
-    REQUIRE(dim == 128 && bits == 2 && group_size == 32 && sign_in_quant, SIKV_EUNSUPPORTED,
-            "fast layout requires dim=128, bits=2, group_size=32, sign_in_quant");
+    REQUIRE(dim == 128 && (bits == 1 || bits == 2) && group_size == 32, SIKV_EUNSUPPORTED,
+            "fast layout requires dim=128, bits 1 or 2, group_size=32");
   }
   if (kq_ref) REQUIRE(kq_scales && kq_zeros, SIKV_EINVAL, "kq_ref needs scales and zeros");
   if (vq_ref) REQUIRE(vq_scales && vq_zeros, SIKV_EINVAL, "vq_ref needs scales and zeros");
@@ -234,7 +234,8 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
                      int64_t tokens, int gq, int k,
                      int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                     int32_t* diag, void* workspace, size_t workspace_bytes, int kernel, void* stream) {
+                     int32_t* diag, void* workspace, size_t workspace_bytes, int lut_mode, int kernel,
+                     void* stream) {
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
@@ -252,6 +253,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   // kernel: 0 = auto, 1 = one CTA per unit, 3 = split units (a CTA cluster per unit),
   // 4 = two kernels (selection with two unit groups per SM, then attention)
   REQUIRE(kernel == 0 || kernel == 1 || kernel == 3 || kernel == 4, SIKV_EINVAL, "kernel must be 0, 1, 3 or 4");
+  REQUIRE(lut_mode == 0 || lut_mode == 1, SIKV_EINVAL, "lut_mode must be 0 (centroids) or 1 (sign-only)");
   if (kernel == 4 || (kernel == 0 && units >= 2 * num_sms())) {
     const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
     const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
@@ -269,7 +271,8 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
       g_last_decode_kernel = 4;
       return cuda_ret(launch_decode_two(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                         frag_blocks, recent_n, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
-                                        sel_stride, sel_count, diag, workspace, num_sms(), (cudaStream_t)stream),
+                                        sel_stride, sel_count, diag, workspace, num_sms(), lut_mode,
+                                        (cudaStream_t)stream),
                       "sikv_decode_step");
     }
     REQUIRE(kernel != 4, SIKV_EUNSUPPORTED,
@@ -297,7 +300,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
       g_last_decode_kernel = 3;
       return cuda_ret(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                           frag_blocks, recent_n, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
-                                          sel, sel_stride, sel_count, diag, (cudaStream_t)stream),
+                                          sel, sel_stride, sel_count, diag, lut_mode, (cudaStream_t)stream),
                       "sikv_decode_step");
     }
   }
@@ -308,7 +311,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   int smem = 0;
   g_last_decode_kernel = 1;
   cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
-                                recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag,
+                                recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag, lut_mode,
                                 (cudaStream_t)stream, &smem);
   return cuda_ret(e, "sikv_decode_step");
 }
@@ -325,10 +328,10 @@ int sikv_debug_set_decode_profile(void* clocks) {
 }
 
 int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq, int64_t units,
-                    int64_t tokens, float* out, void* stream) {
+                    int64_t tokens, int lut_mode, float* out, void* stream) {
   REQUIRE(signs_fast && cent32 && q && out, SIKV_EINVAL, "null pointer");
   REQUIRE(gq >= 1 && units >= 1 && tokens >= 1, SIKV_EINVAL, "bad shape");
-  return cuda_ret(launch_score_fast(signs_fast, cent32, q, gq, units, tokens, out, (cudaStream_t)stream),
+  return cuda_ret(launch_score_fast(signs_fast, cent32, q, gq, units, tokens, lut_mode, out, (cudaStream_t)stream),
                   "sikv_score_fast");
 }
 

@@ -47,6 +47,7 @@ struct DecodeArgs {
   int64_t L;
   int fblocks;
   int S, R, Gq, k, capw, sel_stride;
+  int lut_mode;             // 0: centroid LUT, 1: sign-only LUT
   // shared-memory layout (byte offsets)
   int off_cand, off_forced, off_misc, off_bits, off_dyn, off_stage;
 };
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int e = tid + DT * r, gg = e >> 4;
-    const float4 c = r ? pc1 : pc0;
+    const float4 c = lut_factors(r ? pc1 : pc0, e & 15, a.lut_mode);
     const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
     lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
                                         __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
@@ -175,7 +176,8 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
 
 // ---------------------------------------------------------------- scores only (tests / API)
 __global__ void score_fast_kernel(const uint8_t* __restrict__ signs_, const float* __restrict__ cent32,
-                                  const float* __restrict__ q, int Gq, int64_t L, float* __restrict__ out) {
+                                  const float* __restrict__ q, int Gq, int64_t L, int lut_mode,
+                                  float* __restrict__ out) {
   extern __shared__ __align__(16) char T[];                  // TBL_BYTES
   __shared__ float lut[512];
   __shared__ float qbar[FD];
@@ -190,7 +192,7 @@ __global__ void score_fast_kernel(const uint8_t* __restrict__ signs_, const floa
   const float* C = cent32 + u * 2048;
   for (int e = tid; e < 512; e += blockDim.x) {
     const int g = e >> 4;
-    const float4 c = reinterpret_cast<const float4*>(C)[e];
+    const float4 c = lut_factors(reinterpret_cast<const float4*>(C)[e], e & 15, lut_mode);
     lut[e] = __fadd_rn(__fadd_rn(__fmul_rn(qbar[4 * g], c.x), __fmul_rn(qbar[4 * g + 2], c.z)),
                        __fadd_rn(__fmul_rn(qbar[4 * g + 1], c.y), __fmul_rn(qbar[4 * g + 3], c.w)));
   }
@@ -242,11 +244,11 @@ cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float
                           const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
                           int fblocks, const int32_t* rn, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
                           float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                          int32_t* diag, cudaStream_t st, int* smem_out) {
+                          int32_t* diag, int lut_mode, cudaStream_t st, int* smem_out) {
   DecodeLayout d = decode_layout(L, k, S, Gq, cap);
   if (smem_out) *smem_out = d.total;
   DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, ffrag, rn, q, out, lse, sel,
-               sel_count, diag, L, fblocks, S, R, Gq, k, d.capw, sel_stride,
+               sel_count, diag, L, fblocks, S, R, Gq, k, d.capw, sel_stride, lut_mode,
                d.off_cand, d.off_forced, d.off_misc, d.off_bits, d.off_dyn, d.off_stage};
   cudaError_t e = cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, d.total);
   if (e != cudaSuccess) return e;
@@ -390,11 +392,11 @@ cudaError_t set_decode_profile(long long* p) {
 }
 
 cudaError_t launch_score_fast(const uint8_t* signs, const float* cent32, const float* q, int Gq,
-                              int64_t U, int64_t L, float* out, cudaStream_t st) {
+                              int64_t U, int64_t L, int lut_mode, float* out, cudaStream_t st) {
   const int bx = (int)std::min<int64_t>(64, (L + 255) / 256);
   cudaError_t e = cudaFuncSetAttribute(score_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TBL_BYTES);
   if (e != cudaSuccess) return e;
-  score_fast_kernel<<<dim3(bx, (unsigned)U), 256, TBL_BYTES, st>>>(signs, cent32, q, Gq, L, out);
+  score_fast_kernel<<<dim3(bx, (unsigned)U), 256, TBL_BYTES, st>>>(signs, cent32, q, Gq, L, lut_mode, out);
   return cudaGetLastError();
 }
 

@@ -51,13 +51,22 @@ __device__ __forceinline__ void build_pair_rows_col(const float* lutT, char* T) 
   Grp::sync();
 }
 
+// The four factors of LUT entry (group g, code c): its centroid, or for the sign-only ablation
+// (build_sign_lut, retrieval.py:54-62) the code's +-1 pattern (element i <-> bit 3 - i); the
+// products with q-bar are then exact and the stated pairing is unchanged.
+__device__ __forceinline__ float4 lut_factors(float4 c, int code, int sign_only) {
+  if (!sign_only) return c;
+  return make_float4((code & 8) ? 1.f : -1.f, (code & 4) ? 1.f : -1.f, (code & 2) ? 1.f : -1.f,
+                     (code & 1) ? 1.f : -1.f);
+}
+
 template <class Grp>
 __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent, const float* qbar, float* lut,
-                                                 char* T) {
+                                                 char* T, int sign_only = 0) {
   const int tid = Grp::tid();
   for (int e = tid; e < 512; e += DT) {
     const int g = e >> 4;
-    const float4 c = reinterpret_cast<const float4*>(cent)[e];
+    const float4 c = lut_factors(reinterpret_cast<const float4*>(cent)[e], e & 15, sign_only);
     const float q0 = qbar[4 * g], q1 = qbar[4 * g + 1], q2 = qbar[4 * g + 2], q3 = qbar[4 * g + 3];
     lut[(e & 15) * 32 + g] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
                                        __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));

@@ -108,6 +108,7 @@ struct SplitArgs {
   float* out; float* lse; int32_t* sel; int32_t* sel_count; int32_t* diag;
   int64_t L;
   int fblocks, S, R, Gq, k, capw, sel_stride, ns, wmax;
+  int lut_mode;                 // 0: centroid LUT, 1: sign-only LUT
   int off_cand, off_forced, off_misc, off_dyn, off_hist, off_bits, off_stage, off_x;
 };
 
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     inva[tid] = 1.0f / ahat[tid];
   }
   __syncthreads();
-  build_pair_table<Cta256>(a.cent32 + u * 32 * 16 * 4, qbar, lut, T);
+  build_pair_table<Cta256>(a.cent32 + u * 32 * 16 * 4, qbar, lut, T, a.lut_mode);
 
   // ---------------- B/C: candidates, the unit's k-th key, bitmaps of the slice
   const int mode = g.mode;
@@ -381,12 +382,13 @@ cudaError_t launch_decode_split(const uint8_t* signs, const uint8_t* recs, const
                                 const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
                                 int fblocks, const int32_t* rn, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
                                 int ns, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                                int32_t* diag, cudaStream_t st) {
+                                int32_t* diag, int lut_mode, cudaStream_t st) {
   SplitLayout lay = split_layout(L, k, S, Gq, cap, ns);
   SplitArgs a = lay.a;
   a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx; a.ffrag = ffrag; a.rn = rn;
   a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
   a.L = L; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride; a.ns = ns;
+  a.lut_mode = lut_mode;
   cudaError_t e = cudaFuncSetAttribute(decode_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};

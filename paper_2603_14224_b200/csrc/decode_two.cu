@@ -64,6 +64,7 @@ struct TwoArgs {
   uint32_t* gforced;    // [U][W] forced bitmaps when they do not fit shared memory (long units)
   int64_t L, U;
   int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
+  int lut_mode;         // 0: centroid LUT, 1: sign-only LUT
   // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
   int g_bytes, g_hist, g_forced, g_cand, g_sks, g_pre;   // g_forced < 0: forced bitmap in gforced
 };
@@ -129,7 +130,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int e = tid + DT * r, gg = e >> 4;
-    const float4 c = pre_c[e];
+    const float4 c = lut_factors(pre_c[e], e & 15, a.lut_mode);
     const float q0 = qbar[4 * gg], q1 = qbar[4 * gg + 1], q2 = qbar[4 * gg + 2], q3 = qbar[4 * gg + 3];
     lut[(e & 15) * 32 + gg] = __fadd_rn(__fadd_rn(__fmul_rn(q0, c.x), __fmul_rn(q2, c.z)),
                                         __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
@@ -417,7 +418,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
                               const int32_t* rn, int R,
                               const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
                               int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
-                              int nsm, cudaStream_t st) {
+                              int nsm, int lut_mode, cudaStream_t st) {
   TwoArgs a = two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq));
   a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx;
   a.ffrag = ffrag; a.rn = rn; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
@@ -451,6 +452,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   }
 #endif
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
+  a.lut_mode = lut_mode;
   const int smem_s = TBL_BYTES + 2 * a.g_bytes + SIKV_SEL_PAD;
   cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
   if (e != cudaSuccess) return e;

@@ -500,7 +500,8 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
         for (int i = 0; i < 4; ++i) {
           int wd, bt;
           k4_pos(c0 + i, wd, bt);
-          if (wd == w) ck |= (kc[i] | (kp[i] < 0.0 ? 8u : 0u)) << bt;
+          // sign-in-quant: bit 3 = sign of K'; direct keys: the (unsigned) code alone
+          if (wd == w) ck |= (kc[i] | (a.siq && kp[i] < 0.0 ? 8u : 0u)) << bt;
         }
         ck = __reduce_or_sync(0xffffffffu, ck);
         if (lane == w) out = ck;
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         };
         auto kemit = [&](int n, uint32_t c) {
           kref[n / PER] |= c << (BITS * (n % PER));
-          if constexpr (BITS == 2) {
+          if constexpr (BITS <= 2) {
             // channel 32j + n -> K4 word 4 t4(n) + j, nibble at bit 16(n>>4) + 8e(n) + 4hi(n)
             const int r = n & 15, e = r >> 3, rr = r & 7;
             kp4[rr >> 1] |= c << (16 * (n >> 4) + 8 * e + 4 * (rr & 1));
@@ -773,7 +774,7 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         for (int n = 0; n < 32; ++n) { vf[n] = vr[n]; vmin = fminf(vmin, vf[n]); vmax = fmaxf(vmax, vf[n]); }
         auto vemit = [&](int n, uint32_t c) {
           vref[n / PER] |= c << (BITS * (n % PER));
-          if constexpr (BITS == 2) vp8[n & 7] |= c << (4 * (n >> 4) + 2 * ((n >> 3) & 1));
+          if constexpr (BITS <= 2) vp8[n & 7] |= c << (4 * (n >> 4) + 2 * ((n >> 3) & 1));
         };
         double vmx;
         quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
@@ -804,8 +805,8 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
       if (a.ks_ref) { a.ks_ref[pi] = kqs; a.kz_ref[pi] = kzp; }
       if (a.vs_ref) { a.vs_ref[pi] = vqs; a.vz_ref[pi] = vzp; }
     }
-    // ---------------- fast layout (bits = 2, sign-in-quant)
-    if constexpr (BITS == 2) {
+    // ---------------- fast layout (bits 1 or 2: codes in 2-bit fields; sign-in-quant or direct)
+    if constexpr (BITS <= 2) {
       if (a.signs_fast) {
         // rotated sign row: byte i of token t = reference byte (t + i) mod 16
         const int rot = (int)(t & 15), base = lane & ~3;
@@ -813,11 +814,14 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         const uint32_t lo = __shfl_sync(0xffffffffu, cw, base + ((j + wsh) & 3));
         const uint32_t hi = __shfl_sync(0xffffffffu, cw, base + ((j + wsh + 1) & 3));
         const uint32_t rw = bsh ? ((lo >> bsh) | (hi << (32 - bsh))) : lo;
-        // K4 nibbles: bit 3 = sign of K' (1 = negative), bits 0-1 = magnitude code
+        // K4 nibbles: bit 3 = sign of K' (1 = negative), bits 0-1 = magnitude code; direct keys
+        // keep bit 3 clear (the nibble decodes to code / 2 and zp carries the sign)
+        if (siq) {
   #pragma unroll
-        for (int n = 0; n < 32; ++n) {
-          const int r = n & 15, e = r >> 3, rr = r & 7;
-          kp4[rr >> 1] |= ((negw >> n) & 1u) << (16 * (n >> 4) + 8 * e + 4 * (rr & 1) + 3);
+          for (int n = 0; n < 32; ++n) {
+            const int r = n & 15, e = r >> 3, rr = r & 7;
+            kp4[rr >> 1] |= ((negw >> n) & 1u) << (16 * (n >> 4) + 8 * e + 4 * (rr & 1) + 3);
+          }
         }
         // V payload words g: byte j of every word comes from group j
   #pragma unroll

@@ -367,3 +367,62 @@ def test_decode_with_window_sinks(kernel):
     units, cb, oc, q = make_window(32768 if kernel == 3 else 8192, [310, 311], sinks=64)
     assert int(cb.sink_idx[:, -1].min()) > 64                   # scattered, not a prefix
     _check_decode(units, cb, oc, q, 512, kernel=kernel)
+
+
+# ---------------------------------------------------------------- fast-path variants (§8f3)
+def make_variant(L, seeds, bits, siq, gq=4, sinks=64):
+    units = [gen_unit(L, 128, gq, s) for s in seeds]
+    K = torch.tensor(np.stack([u.keys for u in units]), dtype=torch.bfloat16, device="cuda")
+    V = torch.tensor(np.stack([u.values for u in units]), dtype=torch.bfloat16, device="cuda")
+    cb = B.prefill_batch(K, V, sink_count=sinks, keep_reference=True, bits=bits, sign_in_quant=siq)
+    oc = [O.prefill(u.keys, u.values, bits=bits, sink_count=sinks, sign_in_quant=siq) for u in units]
+    q = torch.tensor(np.stack([u.queries[:gq] for u in units]), dtype=torch.float32, device="cuda")
+    return units, cb, oc, q
+
+
+@pytest.mark.parametrize("bits,siq", [(2, False), (1, True), (1, False)])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fast_path_variants(bits, siq, kernel):
+    """bits 1 / 2 x sign-in-quant / direct keys (cache.py:236-244) on the fused path: reference
+    planes bit-exact, fast records decode to them, selections exact, attention in tolerance."""
+    L = 32768 if kernel == 3 else 4096
+    units, cb, oc, q = make_variant(L, [500, 501], bits, siq)
+    for i, c in enumerate(oc):
+        plane = c.kmag if siq else c.kdirect
+        np.testing.assert_array_equal(cb.ref["kq"][i].cpu().numpy(), plane.packed)
+        np.testing.assert_array_equal(cb.ref["ks"][i].cpu().numpy(), plane.scales)
+        np.testing.assert_array_equal(cb.ref["kz"][i].cpu().numpy(), plane.zeros)
+        np.testing.assert_array_equal(cb.ref["vq"][i].cpu().numpy(), c.vq.packed)
+        kc, vc, kpar, vpar, neg = records_to_reference(cb.recs[i].cpu().numpy())
+        np.testing.assert_array_equal(kc, plane.codes())
+        np.testing.assert_array_equal(vc, c.vq.codes())
+        np.testing.assert_array_equal(kpar[:, :, 1], plane.zeros.view(np.uint16))
+        np.testing.assert_array_equal(neg, (O.sign_plane(c.codes) < 0) if siq else np.zeros_like(neg))
+    _check_decode(units, cb, oc, q, 256, kernel=kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_sign_only_lut(kernel, golden):
+    """select_tokens(..., sign_only=True) (retrieval.py:54-62) on the fused path: exact vs the
+    float32 sign-LUT restatement, certified vs the float64 reference sets, and the golden
+    sparsity-0.05 sign-only selection of c1_u0 (k = 205 - 64 = 141)."""
+    L = 32768 if kernel == 3 else 4096
+    seeds = [100, 101] if L == 4096 else [610, 611]
+    units, cb, oc, q = make_variant(L, seeds, 2, True)
+    res = B.decode_step(cb, q, 141, with_selection=True, kernel=kernel, sign_only=True)
+    for i, c in enumerate(oc):
+        got = res.selection[i, : int(res.counts[i])].cpu().numpy()
+        np.testing.assert_array_equal(got, R.select32(c, q[i].cpu().numpy(), 141, sign_only=True)[0])
+        ok, nd, gap, bound = R.certified_selection_check(c, q[i].cpu().numpy(), 141, got, sign_only=True)
+        assert ok, (nd, gap, bound)
+        for h in range(4):
+            ref = O.sparse_attention(q[i, h].cpu().numpy().astype(np.float64), got, c)
+            assert O.rel_l2(res.out[i, h].cpu().numpy(), ref) <= att_rel_l2(L)
+    if L == 4096:
+        meta, _ = golden
+        np.testing.assert_array_equal(res.selection[0, : int(res.counts[0])].cpu().numpy(),
+                                      meta["c1_u0"]["sparsity_signonly_sel"])
+    s = B.score_fast(cb, q, sign_only=True).cpu().numpy()
+    for i, c in enumerate(oc):
+        qbar = R.group_query(q[i].cpu().numpy())
+        np.testing.assert_array_equal(s[i], R.scores32(R.sign_lut32(qbar, 32), c.packed_codes))
