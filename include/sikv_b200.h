@@ -45,7 +45,7 @@ extern "C" {
 #define SIKV_EUNSUPPORTED 3
 
 const char* sikv_last_error(void);
-int sikv_abi_version(void);   /* 4 */
+int sikv_abi_version(void);   /* 5 */
 
 /* ---------------------------------------------------------------- encoder (prefill)
  * replaces: compute_channel_stats   normalize.py:56-61
@@ -112,6 +112,9 @@ size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int s
  * Recent rows: recent_n (nullable) [U] int32 = recent rows of each unit (forced, scored
  * -inf: cache.py:290-309; sel then ends with tokens + 0 .. recent_n[u] - 1); recent = their
  * maximum (or the count of every unit when recent_n is NULL).
+ * unit_map (nullable) [units] int32: the cache unit each query unit reads (q, out, sel, diag are
+ * per query unit; the planes, sinks, recents per cache unit): the per-q-head policy runs one
+ * query unit of gq = 1 per query head over its KV head's cache (cache.py:290-309 per head).
  * lut_mode: 0 = centroid LUT (build_lut), 1 = sign-only LUT (build_sign_lut, retrieval.py:54-62:
  * the code's +-1 pattern instead of its centroid; select_tokens(..., sign_only=True)). */
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
@@ -119,7 +122,8 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
                      int64_t tokens, int gq, int k, int cap, float* out, float* lse, int32_t* sel,
                      int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
-                     size_t workspace_bytes, int lut_mode, int kernel, void* stream);
+                     size_t workspace_bytes, const int32_t* unit_map, int lut_mode, int kernel,
+                     void* stream);
 
 /* the decode path (1, 3 or 4, as the kernel argument) the last sikv_decode_step of this host
  * thread launched; the two-kernel path (4) starts two kernels per step, the others one */

@@ -35,7 +35,7 @@ _SIGS = {
     "sikv_append": (I, [P, P, I, I64, I64, P, P, P, I64, I64, I, P, P]),
     "sikv_decode_smem_bytes": (I, [I64, I, I, I, I]),
     "sikv_decode_default_cap": (I, [I64, I, I]),
-    "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, P, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, I, I, P]),
+    "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, P, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, P, I, I, P]),
     "sikv_decode_workspace_bytes": (SZ, [I64, I64]),
     "sikv_decode_workspace_bytes_k": (SZ, [I64, I64, I, I]),
     "sikv_decode_last_kernel": (I, []),

@@ -289,9 +289,11 @@ def _workspace(units: int, tokens: int, k: int, sinks: int, device) -> torch.Ten
 def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_selection: bool = False,
                 with_lse: bool = False, with_diag: bool = False, out: torch.Tensor | None = None,
                 sel_buf: torch.Tensor | None = None, kernel: int = 0, append=None,
-                sign_only: bool = False) -> DecodeOutput:
+                sign_only: bool = False, unit_map=None) -> DecodeOutput:
     """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
 
+    unit_map ([Uq] ints, each < cb.units): query unit i reads cache unit unit_map[i] (q, out and
+    the selection are per query unit); see decode_step_per_head.
     sign_only=True scores with the sign-only LUT (select_tokens(..., sign_only=True),
     retrieval.py:54-62).  append=(k, v) first appends one token per unit ([U, 128] rows, append_batch without the
     status sync), so a generation step is one call.  kernel: 0 auto, 1 one CTA per unit,
@@ -299,7 +301,14 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
     (selection with two unit groups per SM, then attention)."""
     if append is not None:
         append_batch(cb, append[0], append[1], check=False)
+    umap = None
     U = cb.units
+    if unit_map is not None:
+        um = torch.as_tensor(unit_map)
+        if um.dim() != 1 or (um.numel() and (int(um.min()) < 0 or int(um.max()) >= cb.units)):
+            raise ValueError(f"unit_map must be 1-D ids in [0, {cb.units})")
+        umap = um.to(device=cb.signs.device, dtype=torch.int32).contiguous()
+        U = int(umap.numel())
     if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
         raise ValueError(f"q must be [{U}, Gq, {FD}], got {tuple(q.shape)}")
     Gq = q.shape[1]
@@ -333,8 +342,21 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], L_.ptr(cb.recent_n), R,
             L_.ptr(qf), U, cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), stride, L_.ptr(cnt),
-            L_.ptr(diag), L_.ptr(ws), ws.numel(), int(sign_only), kernel, L_.stream())
+            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only), kernel, L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)
+
+
+def decode_step_per_head(cb: CacheBatch, q: torch.Tensor, k: int, **kw) -> DecodeOutput:
+    """The per-q-head selection policy (cache.py:290-309 with each query head's own query):
+    every query head selects its own top-k over its KV head's cache and attends to it.  q is
+    [U, Gq, 128]; out [U, Gq, 128]; selection / counts per (unit, head) as [U * Gq, ...]."""
+    U, Gq, D = q.shape
+    if U != cb.units or D != FD:
+        raise ValueError(f"q must be [{cb.units}, Gq, {FD}], got {tuple(q.shape)}")
+    umap = torch.arange(U, dtype=torch.int32).repeat_interleave(Gq)
+    res = decode_step(cb, q.reshape(U * Gq, 1, D), k, unit_map=umap, **kw)
+    lse = None if res.lse is None else res.lse.view(U, Gq)
+    return DecodeOutput(res.out.view(U, Gq, D), lse, res.selection, res.counts, res.diag)
 
 
 def score_fast(cb: CacheBatch, q: torch.Tensor, sign_only: bool = False) -> torch.Tensor:

@@ -24,7 +24,7 @@ cudaError_t launch_append(const void*, const void*, int, int64_t, int, const dou
 DecodeLayout decode_layout(int64_t L, int k, int S, int Gq, int cap);
 cudaError_t launch_decode(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                           const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*,
-                          float*, int32_t*, int, int32_t*, int32_t*, int, cudaStream_t, int*);
+                          float*, int32_t*, int, int32_t*, int32_t*, const int32_t*, int, cudaStream_t, int*);
 cudaError_t launch_pack_forced(const float*, const float*, int, const float*, const float*, int64_t, const int32_t*,
                                int, const float*, int64_t, int, int, int, uint32_t*, int*, cudaStream_t);
 cudaError_t launch_append_forced(const void*, const void*, int, int64_t, const int32_t*, const double*, const float*,
@@ -39,13 +39,13 @@ int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
 cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                                 const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, int, float*,
-                                float*, int32_t*, int, int32_t*, int32_t*, int, cudaStream_t);
+                                float*, int32_t*, int, int32_t*, int32_t*, const int32_t*, int, cudaStream_t);
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq);
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq);
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                               const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
-                              int32_t*, int, int32_t*, int32_t*, void*, int, int, cudaStream_t);
+                              int32_t*, int, int32_t*, int32_t*, void*, int, const int32_t*, int, cudaStream_t);
 // snapkv.cu
 size_t snap_workspace_bytes(int64_t U, int64_t L, int w);
 cudaError_t launch_snap_pooled(const void*, int, int64_t, int64_t, int, const double*, const double*, int, int, void*,
@@ -95,7 +95,7 @@ static int max_smem() {
 extern "C" {
 
 const char* sikv_last_error(void) { return g_err.c_str(); }
-int sikv_abi_version(void) { return 4; }
+int sikv_abi_version(void) { return 5; }
 
 size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
   return encode_workspace_bytes(units, tokens, (int)dim);
@@ -234,8 +234,8 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
                      int64_t tokens, int gq, int k,
                      int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                     int32_t* diag, void* workspace, size_t workspace_bytes, int lut_mode, int kernel,
-                     void* stream) {
+                     int32_t* diag, void* workspace, size_t workspace_bytes, const int32_t* unit_map,
+                     int lut_mode, int kernel, void* stream) {
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
@@ -271,7 +271,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
       g_last_decode_kernel = 4;
       return cuda_ret(launch_decode_two(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                         frag_blocks, recent_n, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
-                                        sel_stride, sel_count, diag, workspace, num_sms(), lut_mode,
+                                        sel_stride, sel_count, diag, workspace, num_sms(), unit_map, lut_mode,
                                         (cudaStream_t)stream),
                       "sikv_decode_step");
     }
@@ -300,7 +300,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
       g_last_decode_kernel = 3;
       return cuda_ret(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                           frag_blocks, recent_n, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
-                                          sel, sel_stride, sel_count, diag, lut_mode, (cudaStream_t)stream),
+                                          sel, sel_stride, sel_count, diag, unit_map, lut_mode, (cudaStream_t)stream),
                       "sikv_decode_step");
     }
   }
@@ -311,8 +311,8 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   int smem = 0;
   g_last_decode_kernel = 1;
   cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
-                                recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag, lut_mode,
-                                (cudaStream_t)stream, &smem);
+                                recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag, unit_map,
+                                lut_mode, (cudaStream_t)stream, &smem);
   return cuda_ret(e, "sikv_decode_step");
 }
 

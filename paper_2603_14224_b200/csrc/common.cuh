@@ -44,7 +44,7 @@ constexpr int R_VPAR = 112;    // 4 x (qs, zp) fp16
 // V fragments [32 lanes][32 words], then 16 float32 row scales (a power of two per row:
 // K^ = K' / (alpha-hat * scale) stays within fp16 for recent rows whose |K'| exceeds the
 // prefill alpha; the logit is multiplied back by the scale)
-constexpr int FBLK_WORDS = 2 * 32 * 32 + 16;
+constexpr int FBLK_WORDS = 2 * 32 * 32 + 32;   // scales padded to a 128-B line: blocks stay line-aligned
 
 // ---- K nibble permutation (B operand of q~ K^T, m16n8k16, one token per n column).
 // A nibble is an e2m1 value: bit 3 = sign of K' (1 = negative), bits 0-1 = the 2-bit

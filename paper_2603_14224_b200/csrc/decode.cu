@@ -23,10 +23,7 @@
 
 namespace sikv {
 
-#ifndef SIKV_K1_STAGES
-#define SIKV_K1_STAGES 2
-#endif
-constexpr int K1_STAGES = SIKV_K1_STAGES;             // cp.async stages per warp in the attention phase
+constexpr int K1_STAGES = 2;             // cp.async stages per warp in the attention phase
 __device__ long long* g_prof = nullptr;
 __device__ int g_k1_skip = 0;            // debug: bit 0 skips the attention phase   // optional per-unit phase clocks (debug / profiling)
 
@@ -38,6 +35,7 @@ struct DecodeArgs {
   const int32_t* sink_idx;  // [U][S] sorted, unique, < L
   const uint32_t* ffrag;    // [U][fblocks][FBLK_WORDS] forced rows: fp16 fragments + row scales
   const int32_t* rn;        // [U] recent rows per unit, nullable (then R for every unit)
+  const int32_t* umap;      // [U] cache unit of each query unit (per-q-head policy), nullable = identity
   const float* q;           // [U][Gq][128]
   float* out;               // [U][Gq][128]
   float* lse;               // [U][Gq] natural-log sum of exp(logits), nullable
@@ -67,21 +65,22 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   float* qbar = lut + 512;                                        // [128]
   float* inva = qbar + FD;                                        // [128] 1 / alpha-hat
   float* ahat = inva + FD;                                        // [128] alpha-hat
-  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
-  const int S = a.S, R = a.rn ? a.rn[u] : a.R, Gq = a.Gq;
+  const int64_t cu = a.umap ? (int64_t)a.umap[u] : u;              // the unit's cache
+  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + cu * L * FSIGN);
+  const int S = a.S, R = a.rn ? a.rn[cu] : a.R, Gq = a.Gq;
   const int W = (int)((L + 31) >> 5);
   long long* prof = g_prof ? g_prof + u * 12 : nullptr;
 #define PROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
   PROF(0);
-  const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
+  const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + cu * S);
   // every small per-unit input is in flight at once, before any shared-memory step
   float pq[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) pq[i] = tid + DT * i < Gq * FD ? a.q[u * Gq * FD + tid + DT * i] : 0.f;
-  const float pal = tid < FD ? a.alpha32[u * FD + tid] : 0.f;
-  const float4* c4 = reinterpret_cast<const float4*>(a.cent32 + u * 32 * 16 * 4);
+  const float pal = tid < FD ? a.alpha32[cu * FD + tid] : 0.f;
+  const float4* c4 = reinterpret_cast<const float4*>(a.cent32 + cu * 32 * 16 * 4);
   const float4 pc0 = c4[tid], pc1 = c4[tid + DT];
-  const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
+  const int psid = tid < S ? a.sink_idx[cu * S + tid] : -1;
   uint4 wsamp[MAX_SAMPLE_CHUNKS];      // the sample's loads overlap the setup below
   load_sample(g, signs, tid, wsamp);
 
@@ -94,7 +93,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   __syncthreads();
   if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
   for (int j = tid + DT; j < S; j += DT) {
-    const int t = a.sink_idx[u * S + j];
+    const int t = a.sink_idx[cu * S + j];
     atomicOr(&forced[t >> 5], 1u << (t & 31));
   }
   if (tid < FD) {
@@ -156,9 +155,9 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
   if (g_k1_skip & 1) return;
-  attn_forced(A, a.ffrag + u * a.fblocks * FBLK_WORDS, nf, warp, DW, lane);
+  attn_forced(A, a.ffrag + cu * a.fblocks * FBLK_WORDS, nf, warp, DW, lane);
   PROF(6);
-  attn_dynamic<K1_STAGES>(A, a.recs + u * L * FREC, reinterpret_cast<const int32_t*>(sm + a.off_dyn), ndyn,
+  attn_dynamic<K1_STAGES>(A, a.recs + cu * L * FREC, reinterpret_cast<const int32_t*>(sm + a.off_dyn), ndyn,
                           (warp - nbf % DW + DW) % DW, DW, sm + warp * K1_STAGES * STAGE_BYTES, lane);
   PROF(7);
   // ---------------- merge the 8 warp partials (fixed order)
@@ -244,10 +243,10 @@ cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float
                           const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
                           int fblocks, const int32_t* rn, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
                           float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                          int32_t* diag, int lut_mode, cudaStream_t st, int* smem_out) {
+                          int32_t* diag, const int32_t* umap, int lut_mode, cudaStream_t st, int* smem_out) {
   DecodeLayout d = decode_layout(L, k, S, Gq, cap);
   if (smem_out) *smem_out = d.total;
-  DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, ffrag, rn, q, out, lse, sel,
+  DecodeArgs a{signs, recs, cent32, alpha32, sink_idx, ffrag, rn, umap, q, out, lse, sel,
                sel_count, diag, L, fblocks, S, R, Gq, k, d.capw, sel_stride, lut_mode,
                d.off_cand, d.off_forced, d.off_misc, d.off_bits, d.off_dyn, d.off_stage};
   cudaError_t e = cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, d.total);

@@ -12,10 +12,7 @@ constexpr int STAGE_BYTES = 16 * FREC;    // one 16-token block of records
 constexpr int MAX_SAMPLE_CHUNKS = 8;
 // sample chunks are at least SSTRIDE_MIN chunks apart (>= NB: one per B2 batch at most), so
 // short units (< 32K tokens) still sample up to 8 chunks: a tighter threshold, fewer candidates
-#ifndef SIKV_SSTRIDE_MIN
-#define SIKV_SSTRIDE_MIN 8
-#endif
-constexpr int SSTRIDE_MIN = SIKV_SSTRIDE_MIN;
+constexpr int SSTRIDE_MIN = 8;
 static_assert(SSTRIDE_MIN >= NB, "at most one sample chunk per B2 batch");
 
 // ---------------------------------------------------------------- pair table
@@ -84,15 +81,10 @@ __device__ __forceinline__ void build_pair_table(const float* __restrict__ cent,
 // 16 of its half-warp copy) sit in 4 registers and the PRMT that extracts the sign byte also
 // picks the column byte (sign-replicating selectors zero the high bytes: offsets < 128).
 // Both are bank-conflict free: the 32 lanes of a step hit 32 distinct columns mod 32.
-#ifndef SIKV_KEY_OPAQUE
-#define SIKV_KEY_OPAQUE 1
-#endif
 struct RepKey {
   uint32_t lb;
   __device__ __forceinline__ explicit RepKey(int lane) : lb((uint32_t)(64 * ((lane >> 4) & 1) + 4 * (lane & 15))) {
-#if SIKV_KEY_OPAQUE
-    asm volatile("" : "+r"(lb));
-#endif
+    asm volatile("" : "+r"(lb));     // kept in a register (not rematerialised per batch)
   }
   __device__ __forceinline__ uint32_t off(uint32_t w, int i) const {
     return prmt(w, lb, 0x5504u | ((uint32_t)(i & 3) << 4)) + 4 * i;
@@ -108,11 +100,9 @@ struct ColKey {
 #pragma unroll
       for (int m = 0; m < 4; ++m) v |= (uint32_t)(4 * (16 * h + ((j + 4 * k + m) & 15))) << (8 * m);
       c[k] = v;
-#if SIKV_KEY_OPAQUE
       // opaque to the compiler: kept in registers instead of being rematerialised from the
       // lane id inside every scoring batch (~25 integer instructions per batch)
       asm volatile("" : "+r"(c[k]));
-#endif
     }
   }
   __device__ __forceinline__ uint32_t off(uint32_t w, int i) const {
@@ -176,9 +166,6 @@ __device__ __forceinline__ void score_batch(const uint4 (&w)[N], const Key& key,
 
 // streaming 16-byte load of the sign plane: read once, no L1 allocation, and first out of L2
 // (the dynamic lists and queries the attention reads next stay resident instead)
-#ifndef SIKV_SIGNS_EVICT_FIRST
-#define SIKV_SIGNS_EVICT_FIRST 1
-#endif
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -186,13 +173,8 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
   uint4 v;
-#if SIKV_SIGNS_EVICT_FIRST
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
-#else
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-#endif
   return v;
 }
 
@@ -325,10 +307,7 @@ __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float*
 }
 
 constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;   // log2(e) / sqrt(128)
-#ifndef SIKV_LAZY
-#define SIKV_LAZY 8.0f
-#endif
-constexpr float kLazyRescale = SIKV_LAZY;
+constexpr float kLazyRescale = 8.0f;
 // 2^x on the SFU (x <= 8 here: logits minus the reference max; -inf -> +0)
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -673,21 +652,13 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
 // yields fewer than k candidates (tau too high), r is rescaled from the observed counts and
 // the scan is repeated (at most kRetries times) before falling back to the exact path.
 constexpr int kRetries = 2;
-#ifndef SIKV_TAU_SIG
-#define SIKV_TAU_SIG 3.0   // sample-rank margin: r = e + SIG sqrt(e) + ADD
-#endif
-#ifndef SIKV_TAU_ADD
-#define SIKV_TAU_ADD 8.0
-#endif
+constexpr double kTauSig = 3.0, kTauAdd = 8.0;   // sample-rank margin: r = e + SIG sqrt(e) + ADD
 
-// SKS: the sample keys live in shared memory (sks[x * DT + tid]) instead of 8 registers
-// across the B2 scan (they are only needed again for a retry).
-template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB, bool SKS = false>
+template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
                                                    uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
-                                                   uint32_t& tau_out, const Xch& xch = Xch(),
-                                                   uint32_t* sks = nullptr) {
+                                                   uint32_t& tau_out, const Xch& xch = Xch()) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const Key lb(lane);
   const int capw = g.capw;
@@ -708,7 +679,6 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       uint32_t key = 0;
       if (x < g.nsc && t < g.L && !(t < g.flim && forced_bit(forced, t))) key = f32_key(sv[x]);
       sk[x] = key;
-      if constexpr (SKS) sks[x * DT + tid] = key;
       nv += key != 0;
       smax = max(smax, key);
       if (key) smin = min(smin, key);
@@ -728,7 +698,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     kmn = ms->tau;
     xch.sample(nsv, kmx, kmn);            // cluster: the whole unit's sample
     const double e = (double)g.keff * (double)nsv / (double)(g.ncand);
-    r = min((int)ceil(e + SIKV_TAU_SIG * sqrt(e) + SIKV_TAU_ADD), nsv);
+    r = min((int)ceil(e + kTauSig * sqrt(e) + kTauAdd), nsv);
   }
   const float fmn = __uint_as_float(unkey_bits(kmn)), fmx = __uint_as_float(unkey_bits(kmx));
   const float scale = fmx > fmn ? 256.0f / (fmx - fmn) : 0.f;
@@ -758,7 +728,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
         Grp::sync();
 #pragma unroll
         for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-          const uint32_t kx = SKS ? sks[x * DT + tid] : sk[x];
+          const uint32_t kx = sk[x];
           if (kx) {
             const int b = min(255, (int)((__uint_as_float(unkey_bits(kx)) - fmn) * scale));
             atomicAdd(&th[b], 1);
@@ -797,7 +767,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       uint32_t bits = 0, skx[MAX_SAMPLE_CHUNKS];
 #pragma unroll
       for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
-        skx[x] = SKS ? sks[x * DT + tid] : sk[x];
+        skx[x] = sk[x];
         if (x < g.nsc && skx[x] != 0 && skx[x] >= tau) bits |= 1u << x;
       }
       const int cnt = __popc(bits);

@@ -104,7 +104,7 @@ struct ClusterX {
 
 struct SplitArgs {
   const uint8_t* signs; const uint8_t* recs; const float* cent32; const float* alpha32;
-  const int32_t* sink_idx; const uint32_t* ffrag; const int32_t* rn; const float* q;
+  const int32_t* sink_idx; const uint32_t* ffrag; const int32_t* rn; const int32_t* umap; const float* q;
   float* out; float* lse; int32_t* sel; int32_t* sel_count; int32_t* diag;
   int64_t L;
   int fblocks, S, R, Gq, k, capw, sel_stride, ns, wmax;
@@ -118,9 +118,10 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   const int ns = a.ns;
   const int rank = (int)cg::this_cluster().block_rank();
   const int64_t u = blockIdx.x / ns;
+  const int64_t cu = a.umap ? (int64_t)a.umap[u] : u;            // the unit's cache
   const int64_t Lu = a.L;
   const int S = a.S, Gq = a.Gq;
-  const int Ru = a.rn ? a.rn[u] : a.R;   // recent rows of this unit
+  const int Ru = a.rn ? a.rn[cu] : a.R;   // recent rows of this unit
   // ---------------- this CTA's slice of the unit
   const int nch = (int)((Lu + 255) >> 8);
   const int c_lo = (int)((int64_t)rank * nch / ns), c_hi = (int)((int64_t)(rank + 1) * nch / ns);
@@ -138,8 +139,8 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   float* qbar = lut + 512;
   float* inva = qbar + FD;
   float* ahat = inva + FD;
-  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + (u * Lu + t_lo) * FSIGN);
-  const int32_t* sidx = a.sink_idx + u * S;
+  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + (cu * Lu + t_lo) * FSIGN);
+  const int32_t* sidx = a.sink_idx + cu * S;
   ClusterX xch{ns, slot};
 
   // geometry of the slice; the selection parameters are the unit's
@@ -174,12 +175,12 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     float s = qs[tid];
     for (int h = 1; h < Gq; ++h) s = __fadd_rn(s, qs[h * FD + tid]);
     qbar[tid] = s;
-    const float al = a.alpha32[u * FD + tid];
+    const float al = a.alpha32[cu * FD + tid];
     ahat[tid] = al > 0.f ? al : 1.0f;
     inva[tid] = 1.0f / ahat[tid];
   }
   __syncthreads();
-  build_pair_table<Cta256>(a.cent32 + u * 32 * 16 * 4, qbar, lut, T, a.lut_mode);
+  build_pair_table<Cta256>(a.cent32 + cu * 32 * 16 * 4, qbar, lut, T, a.lut_mode);
 
   // ---------------- B/C: candidates, the unit's k-th key, bitmaps of the slice
   const int mode = g.mode;
@@ -282,8 +283,8 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   attn_init(A, qs, ahat, Gq, lane);
   const int nf = rank == 0 ? S + Ru : 0;
   const int nbf = (nf + 15) >> 4;
-  if (nf > 0) attn_forced(A, a.ffrag + u * a.fblocks * FBLK_WORDS, nf, warp, DW, lane);
-  attn_dynamic(A, a.recs + u * Lu * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
+  if (nf > 0) attn_forced(A, a.ffrag + cu * a.fblocks * FBLK_WORDS, nf, warp, DW, lane);
+  attn_dynamic(A, a.recs + cu * Lu * FREC, dyn, ndyn, (warp - nbf % DW + DW) % DW, DW,
                sm + a.off_stage + warp * 2 * STAGE_BYTES, lane);
   __syncthreads();
   // this CTA's (max, denominator, unnormalised numerator) per head, warps combined in order
@@ -382,10 +383,10 @@ cudaError_t launch_decode_split(const uint8_t* signs, const uint8_t* recs, const
                                 const float* alpha32, const int32_t* sink_idx, int S, const uint32_t* ffrag,
                                 int fblocks, const int32_t* rn, int R, const float* q, int64_t U, int64_t L, int Gq, int k, int cap,
                                 int ns, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
-                                int32_t* diag, int lut_mode, cudaStream_t st) {
+                                int32_t* diag, const int32_t* umap, int lut_mode, cudaStream_t st) {
   SplitLayout lay = split_layout(L, k, S, Gq, cap, ns);
   SplitArgs a = lay.a;
-  a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx; a.ffrag = ffrag; a.rn = rn;
+  a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx; a.ffrag = ffrag; a.rn = rn; a.umap = umap;
   a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
   a.L = L; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride; a.ns = ns;
   a.lut_mode = lut_mode;

@@ -8,43 +8,33 @@
 //                          the workspace.  The groups' 32-column pair tables interleave in one
 //                          64 KiB region (ColKey), so 16 warps stream sign planes per SM while
 //                          either group sits in its latency-bound setup / selection steps.
-//   decode_attend_kernel   one 256-thread CTA per unit, two per SM: the unit's dynamic list,
-//                          forced rows and sparse flash-decode (decode_common.cuh), fixed-order
-//                          merge, output.
+//   decode_attend_kernel   one 128-thread CTA (4 warps) per unit, four per SM, launched as a
+//                          programmatic dependent of the selection grid: the unit's forced rows,
+//                          then (griddepcontrol.wait) its dynamic list, sparse flash-decode
+//                          (decode_common.cuh), fixed-order merge of the 4 warp partials.
 //
-// The arithmetic is that of decode.cu (shared device code): selections are identical, the
-// outputs equal within float32 accumulation order (the dynamic list is emitted in segment
-// order by 8-warp groups exactly as decode.cu does, so they are in fact bit-identical).
+// The arithmetic is that of decode.cu (shared device code): selections are identical; the
+// attention splits a unit over 4 warps instead of 8, so outputs agree with the one-CTA path to
+// the fp16 rounding of P against each warp's running max (not bit for bit).
+// Tried and removed: TMA tile::gather4 row staging (5% slower than cp.async),
+// sample keys in shared memory, padding the selection kernel's shared memory.
 #include "common.cuh"
 #include "select.cuh"
 #include "api_types.cuh"
 #include "decode_common.cuh"
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <algorithm>
 
 namespace sikv {
 
 constexpr int SEL_THREADS = 512;
-#ifndef SIKV_PDL
-#define SIKV_PDL 1   // attention launched as a programmatic dependent of the selection grid
-#endif
 __device__ long long* g_prof_two = nullptr;   // optional per-unit phase clocks (profiling)
-#ifndef SIKV_SEL_SKS
-#define SIKV_SEL_SKS 0
-#endif
-constexpr bool SEL_SKS = SIKV_SEL_SKS;
 // the selection groups' radix digit: 9 bits (512 bins) — at C4 (1.4 K candidates per unit)
 // 2.5% faster than 11 bits, neutral at C2; path 1 keeps 11 bits (C3: 6 K candidates)
-#ifndef SIKV_SEL_RB
-#define SIKV_SEL_RB 9
-#endif
-constexpr int SEL_NBIN = 1 << SIKV_SEL_RB;    // sample keys in shared memory (A/B: slower at C2)
+constexpr int SEL_NBIN = 512;
 using SG0 = NamedGroup<1, 0>;
 using SG1 = NamedGroup<2, 256>;
 
 struct TwoArgs {
-  CUtensorMap recs_map;   // records as a [U*L][128 B] 2-D tensor: TMA gather4 of attention rows
   const uint8_t* signs;
   const uint8_t* recs;
   const float* cent32;
@@ -52,6 +42,7 @@ struct TwoArgs {
   const int32_t* sink_idx;
   const uint32_t* ffrag;
   const int32_t* rn;    // [U] recent rows per unit, nullable (then R)
+  const int32_t* umap;  // [U] cache unit of each query unit (per-q-head policy), nullable = identity
   const float* q;
   float* out;
   float* lse;
@@ -66,7 +57,7 @@ struct TwoArgs {
   int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
   int lut_mode;         // 0: centroid LUT, 1: sign-only LUT
   // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
-  int g_bytes, g_hist, g_forced, g_cand, g_sks, g_pre;   // g_forced < 0: forced bitmap in gforced
+  int g_bytes, g_hist, g_forced, g_cand, g_pre;   // g_forced < 0: forced bitmap in gforced
 };
 
 // ---------------------------------------------------------------- selection
@@ -76,8 +67,9 @@ __device__ __forceinline__ void prefetch_unit(const TwoArgs& a, char* base, int 
   if (un >= 0 && un < a.U) {
     for (int i = tid; i < a.Gq * FD / 4; i += DT)
       cp_async16_s(pre_s + 16u * (uint32_t)i, a.q + un * a.Gq * FD + 4 * i);
+    const int64_t cn = a.umap ? (int64_t)__ldg(a.umap + un) : un;
     for (int i = tid; i < 512; i += DT)
-      cp_async16_s(pre_s + (uint32_t)(a.Gq * FD * 4) + 16u * (uint32_t)i, a.cent32 + un * 2048 + 4 * i);
+      cp_async16_s(pre_s + (uint32_t)(a.Gq * FD * 4) + 16u * (uint32_t)i, a.cent32 + cn * 2048 + 4 * i);
   }
   cp_commit();
 }
@@ -101,14 +93,14 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   int* hist = reinterpret_cast<int*>(base + a.g_hist);
   uint32_t* const forced_s = reinterpret_cast<uint32_t*>(base + (a.g_forced >= 0 ? a.g_forced : 0));
   uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
-  uint32_t* sks = reinterpret_cast<uint32_t*>(base + a.g_sks);
   const float* pre_q = reinterpret_cast<const float*>(base + a.g_pre);   // [8][128]
   const float4* pre_c = reinterpret_cast<const float4*>(pre_q + Gq * FD);  // [512]
   long long* prof = g_prof_two ? g_prof_two + u * 12 : nullptr;
   if (prof && tid == 0) prof[0] = clock64();
-  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + u * L * FSIGN);
-  const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + u * S);
-  const int psid = tid < S ? a.sink_idx[u * S + tid] : -1;
+  const int64_t cu = a.umap ? (int64_t)__ldg(a.umap + u) : u;    // the unit's cache
+  const uint4* signs = reinterpret_cast<const uint4*>(a.signs + cu * L * FSIGN);
+  const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + cu * S);
+  const int psid = tid < S ? a.sink_idx[cu * S + tid] : -1;
   uint4 wsamp[MAX_SAMPLE_CHUNKS];
   load_sample(g, signs, tid, wsamp);
   uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
@@ -118,7 +110,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   PG::sync();
   if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
   for (int j = tid + DT; j < S; j += DT) {
-    const int t = a.sink_idx[u * S + j];
+    const int t = a.sink_idx[cu * S + j];
     atomicOr(&forced[t >> 5], 1u << (t & 31));
   }
   if (tid < FD) {
@@ -149,18 +141,17 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   uint32_t kstar = 0;
   if (mode >= 2) {
     uint32_t tau;
-    fb = produce_candidates<PG, NoX, ColKey, NB, SEL_SKS>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(),
-                                                           sks) ? 1 : 0;
+    fb = produce_candidates<PG, NoX, ColKey, NB>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau) ? 1 : 0;
     if (prof && tid == 0) prof[2] = clock64();
     if (!fb) {
       ndyn = select_emit_candidates<PG, SEL_NBIN>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
-                                        a.rn ? __ldg(a.rn + u) : a.R, sel_count_u, kstar);
+                                        a.rn ? __ldg(a.rn + cu) : a.R, sel_count_u, kstar);
     } else {
       produce_exact<PG, NoX, ColKey, SEL_NBIN>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
     }
   }
   if (ndyn < 0)
-    ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.rn ? __ldg(a.rn + u) : a.R,
+    ndyn = emit_selection<PG>(g, mode, forced, gt, eq, need_eq, eq_count, dyn, sel_u, a.rn ? __ldg(a.rn + cu) : a.R,
                               sel_count_u, ms);
   if (prof && tid == 0) prof[3] = clock64();
   if (tid == 0) {
@@ -183,11 +174,9 @@ __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
 
 __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
-#if SIKV_PDL
   // the attention grid may be scheduled onto SMs as this grid's CTAs retire: it attends the
   // forced rows, then waits for this grid to complete (griddepcontrol.wait) before the lists
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
   // group from a value the compiler can prove warp-uniform (uniform-datapath table base)
   const int grp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 8), 0);
   if (grp == 0) select_group<SG0, 0>(a, sm);
@@ -195,111 +184,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 }
 
 // ---------------------------------------------------------------- attention
-#ifndef SIKV_ATT_WARPS
-#define SIKV_ATT_WARPS 4
-#endif
-constexpr int ATT_WARPS = SIKV_ATT_WARPS;          // warps per attention CTA (one unit each)
+constexpr int ATT_WARPS = 4;                        // warps per attention CTA (one unit each)
 constexpr int ATT_THREADS = 32 * ATT_WARPS;
 constexpr int ATT_CTAS_PER_SM = 16 / ATT_WARPS;
-#ifndef SIKV_TMA_GATHER
-#define SIKV_TMA_GATHER 0   // 1: attention rows staged by TMA tile::gather4 (measured 5% slower than cp.async)
-#endif
-#ifndef SIKV_ATT_STAGES
-#define SIKV_ATT_STAGES 2     // cp.async staging buffers per warp
-#endif
-constexpr int ATT_STAGES = SIKV_ATT_STAGES;
-#ifndef SIKV_TMA_STAGES
-#define SIKV_TMA_STAGES 2
-#endif
-constexpr int TMA_STAGES = SIKV_TMA_STAGES;
-#ifndef SIKV_ATT_PREFETCH
-#define SIKV_ATT_PREFETCH 1
-#endif
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT;\n}\n" ::"r"(bar),
-      "r"(phase)
-      : "memory");
-}
-// four 128-B rows (tensor rows r0..r3) into 512 contiguous bytes at dst, 128-B swizzled
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int r0, int r1, int r2,
-                                            int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-      : "memory");
-}
-
-// Dynamic rows staged by TMA: per 16-token block, lanes 0-3 each issue one gather4 (four
-// indexed rows, 512 B) onto the block's mbarrier; two 2 KiB buffers per warp (1 KiB aligned).
-// The hardware 128-B swizzle puts chunk k of smem row s at slot k ^ (s & 7); token j of the
-// block sits in smem row P(j) = j ^ ((j & 1) << 2) (an involution), so that the fragment reads
-// of attn_block stay conflict-free: tokens 2q / 2q + 1 differ in bit 2 of their row (K reads),
-// and tokens 0, 2, 4, 6 (and 1, 3, 5, 7) differ in bits 1-2 (V reads).
-__device__ __forceinline__ int tma_row(int j) { return j ^ ((j & 1) << 2); }
-
-__device__ __forceinline__ void attn_dynamic_tma(Attn& A, const CUtensorMap* map, int row0, const int32_t* dyn,
-                                                 int ndyn, int first, int nw, char* stage, uint32_t bars,
-                                                 int lane) {
-  const int g = lane >> 2, t4 = lane & 3;
-  const int nbd = (ndyn + 15) >> 4;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
-  const int jv0 = 2 * t4, jv1 = 2 * t4 + 1;
-  const int rk = tma_row(g), r0 = tma_row(jv0), r1 = tma_row(jv1);
-  BlkOffs o;
-  o.k4 = rk * FREC + 16 * (t4 ^ rk);
-  o.kp = rk * FREC + 16 * (6 ^ rk);
-  o.vw0 = r0 * FREC + 16 * ((4 + (g >> 2)) ^ r0) + 4 * (g & 3);
-  o.vw1 = r1 * FREC + 16 * ((4 + (g >> 2)) ^ r1) + 4 * (g & 3);
-  o.vp0 = r0 * FREC + 16 * (7 ^ r0);
-  o.vp1 = r1 * FREC + 16 * (7 ^ r1);
-  // lane l < 4 stages smem rows 4l .. 4l + 3: tokens tma_row(4l + i) (rows >= 8: + 8)
-  int ix[4];
-  auto load_ix = [&](int blk) {
-    if (lane < 4) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int srow = 4 * lane + i;
-        ix[i] = dyn[blk * 16 + (tma_row(srow & 7) | (srow & 8))];
-      }
-    }
-  };
-  auto stage_blk = [&](int buf) {
-    if (lane < 4) {
-      const uint32_t bar = bars + 8u * (uint32_t)buf;
-      if (lane == 0) mbar_expect_tx(bar, 16 * FREC);
-      tma_gather4(sbase + (uint32_t)(buf * STAGE_BYTES + 512 * lane), map, bar, row0 + ix[0], row0 + ix[1],
-                  row0 + ix[2], row0 + ix[3]);
-    }
-  };
-  uint32_t phase = 0;   // bit b: parity of buffer b's next completion
-#pragma unroll
-  for (int s = 0; s < TMA_STAGES - 1; ++s) {
-    if (first + s * nw < nbd) { load_ix(first + s * nw); stage_blk(s); }
-  }
-  if (first + (TMA_STAGES - 1) * nw < nbd) load_ix(first + (TMA_STAGES - 1) * nw);
-  int buf = 0;
-  for (int db = first; db < nbd; db += nw) {
-    const int nx = db + (TMA_STAGES - 1) * nw;
-    if (nx < nbd) {
-      stage_blk(buf == 0 ? TMA_STAGES - 1 : buf - 1);
-      if (nx + nw < nbd) load_ix(nx + nw);
-    }
-    mbar_wait(bars + 8u * (uint32_t)buf, (phase >> buf) & 1u);
-    phase ^= 1u << buf;
-    attn_block(A, stage + buf * STAGE_BYTES, o, ndyn - db * 16, lane);
-    __syncwarp();
-    buf = buf + 1 == TMA_STAGES ? 0 : buf + 1;
-  }
-}
+constexpr int ATT_STAGES = 2;                       // cp.async staging buffers per warp
 
 // One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
 // indices come straight from global memory (L2), so the only CTA-wide barriers are the
@@ -308,44 +196,24 @@ template <int NW>
 __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u) {
   constexpr int NT = 32 * NW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-#if SIKV_TMA_GATHER
-  // 1 KiB-aligned staging (128-B swizzle atoms), then the 2 mbarriers per warp
-  {
-    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(stage);
-    stage += (1024u - (s0 & 1023u)) & 1023u;
-  }
-  const int core = max(NW * TMA_STAGES * STAGE_BYTES, NW * a.Gq * (FD + 2) * 4);   // staging, then merge partials
-  const uint32_t bars = (uint32_t)__cvta_generic_to_shared(stage + ((core + 7) & ~7));
-  if (tid < TMA_STAGES * NW) mbar_init(bars + 8u * (uint32_t)tid, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-#endif
-  const int S = a.S, R = a.rn ? __ldg(a.rn + u) : a.R, Gq = a.Gq;
+  const int64_t cu = a.umap ? (int64_t)__ldg(a.umap + u) : u;    // the unit's cache
+  const int S = a.S, R = a.rn ? __ldg(a.rn + cu) : a.R, Gq = a.Gq;
   const int32_t* dyn = a.dynl + u * a.dstride;
   const int nf = S + R;
   const int nbf = (nf + 15) >> 4;
-  const uint32_t* ffrag_u = a.ffrag + u * a.fblocks * FBLK_WORDS;
-#if SIKV_ATT_PREFETCH
+  const uint32_t* ffrag_u = a.ffrag + cu * a.fblocks * FBLK_WORDS;
   // start the forced fragments and the list on their way to L2 while q~ loads
   for (int i = tid; i < (nbf * FBLK_WORDS * 4 + 127) / 128; i += NT)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ffrag_u) + 128 * i));
   for (int i = tid; i < a.dstride / 32; i += NT)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dyn) + 128 * i));
-#endif
   Attn A;
-  attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + u * FD, Gq, lane);
+  attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + cu * FD, Gq, lane);
   attn_forced(A, ffrag_u, nf, warp, NW, lane);
-#if SIKV_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");   // the selection grid is complete
-#endif
   const int ndyn = __ldg(a.ndyn + u);
-#if SIKV_TMA_GATHER
-  attn_dynamic_tma(A, &a.recs_map, (int)(u * a.L), dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
-                   stage + warp * TMA_STAGES * STAGE_BYTES, bars + 8u * TMA_STAGES * (uint32_t)warp, lane);
-#else
-  attn_dynamic<ATT_STAGES>(A, a.recs + u * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
+  attn_dynamic<ATT_STAGES>(A, a.recs + cu * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
                            stage + warp * ATT_STAGES * STAGE_BYTES, lane);
-#endif
   __syncthreads();
   float* part = reinterpret_cast<float*>(stage);
   float* pm = part + NW * Gq * FD;
@@ -380,8 +248,6 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap, int Gq, bool forced_
   if (forced_in_smem) off += a128(W * 4);
   a.g_cand = off;
   off += a128(std::max(DW * a.capw * 8, 8 * FD * 4));
-  a.g_sks = off;
-  off += SEL_SKS ? MAX_SAMPLE_CHUNKS * DT * 4 : 0;
   a.g_pre = off;
   off += a128((Gq * FD + 2048) * 4);      // next unit's queries and centroids
   a.g_bytes = off;
@@ -395,16 +261,12 @@ static bool two_forced_smem(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, true).g_bytes <= 227 * 1024;
 }
 
-#ifndef SIKV_SEL_PAD
-#define SIKV_SEL_PAD 0
-#endif
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq) {
-  return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes + SIKV_SEL_PAD;
+  return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
-  const int st = SIKV_TMA_GATHER ? TMA_STAGES : ATT_STAGES;
-  const int core = std::max(ATT_WARPS * st * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
-  return SIKV_TMA_GATHER ? ((core + 7) & ~7) + 8 * TMA_STAGES * ATT_WARPS + 1024 : core;   // mbarriers, 1 KiB alignment slack
+  (void)L; (void)k; (void)S;
+  return std::max(ATT_WARPS * ATT_STAGES * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
@@ -418,10 +280,10 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
                               const int32_t* rn, int R,
                               const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
                               int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
-                              int nsm, int lut_mode, cudaStream_t st) {
+                              int nsm, const int32_t* umap, int lut_mode, cudaStream_t st) {
   TwoArgs a = two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq));
   a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx;
-  a.ffrag = ffrag; a.rn = rn; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
+  a.ffrag = ffrag; a.rn = rn; a.umap = umap; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
   char* ws = reinterpret_cast<char*>(workspace) + 256;
   a.ndyn = reinterpret_cast<int32_t*>(ws);
   ws += a256((size_t)U * 4);
@@ -430,30 +292,9 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   a.gbits = reinterpret_cast<uint32_t*>(ws);
   ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
   a.gforced = reinterpret_cast<uint32_t*>(ws);
-#if SIKV_TMA_GATHER
-  {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-      void* fn = nullptr;
-      cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-          q != cudaDriverEntryPointSuccess)
-        fn = nullptr;
-      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }();
-    if (!encode) return cudaErrorNotSupported;
-    const cuuint64_t dims[2] = {(cuuint64_t)FREC, (cuuint64_t)(U * L)};
-    const cuuint64_t strides[1] = {(cuuint64_t)FREC};
-    const cuuint32_t box[2] = {(cuuint32_t)FREC, 1};
-    const cuuint32_t es[2] = {1, 1};
-    if (encode(&a.recs_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(recs), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
-  }
-#endif
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
   a.lut_mode = lut_mode;
-  const int smem_s = TBL_BYTES + 2 * a.g_bytes + SIKV_SEL_PAD;
+  const int smem_s = TBL_BYTES + 2 * a.g_bytes;
   cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(nsm, (U + 1) / 2);
@@ -463,7 +304,6 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   const int smem_a = two_attend_smem_bytes(L, k, S, Gq);
   e = cudaFuncSetAttribute(decode_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
   if (e != cudaSuccess) return e;
-#if SIKV_PDL
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)U);
   cfg.blockDim = dim3(ATT_THREADS);
@@ -475,10 +315,6 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, decode_attend_kernel, a);
-#else
-  decode_attend_kernel<<<(unsigned)U, ATT_THREADS, smem_a, st>>>(a);
-  return cudaGetLastError();
-#endif
 }
 
 }  // namespace sikv

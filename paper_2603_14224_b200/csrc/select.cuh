@@ -91,10 +91,7 @@ __device__ __forceinline__ void pick_digit(const int* hist, Misc* ms) {
 }
 
 // ---------------------------------------------------------------- 11-bit radix k-th selection
-#ifndef SIKV_RB
-#define SIKV_RB 11
-#endif
-constexpr int RB = SIKV_RB;         // digit bits per pass
+constexpr int RB = 11;              // digit bits per pass
 constexpr int NBIN = 1 << RB;       // 2048 bins; thread t owns bins [NBIN-8(t+1), NBIN-8t)
 
 // Group-wide: choose the digit whose descending cumulative count reaches ms->rem_sel.

@@ -426,3 +426,19 @@ def test_sign_only_lut(kernel, golden):
     for i, c in enumerate(oc):
         qbar = R.group_query(q[i].cpu().numpy())
         np.testing.assert_array_equal(s[i], R.scores32(R.sign_lut32(qbar, 32), c.packed_codes))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_per_q_head_policy(kernel):
+    """Per-q-head policy: each query head's own select_tokens(cache, q_h, k) (cache.py:290-309)
+    and attention, through unit_map (query unit -> cache unit) on every fused kernel."""
+    L = 32768 if kernel == 3 else 4096
+    units, cb, oc, q = make_variant(L, [700, 701], 2, True, gq=4)
+    res = B.decode_step_per_head(cb, q, 200, with_selection=True, kernel=kernel)
+    for i, c in enumerate(oc):
+        for h in range(4):
+            r = i * 4 + h
+            idx = R.select32(c, q[i, h:h + 1].cpu().numpy(), 200)[0]
+            np.testing.assert_array_equal(res.selection[r, : int(res.counts[r])].cpu().numpy(), idx)
+            ref = O.sparse_attention(q[i, h].cpu().numpy().astype(np.float64), idx, c)
+            assert O.rel_l2(res.out[i, h].cpu().numpy(), ref) <= att_rel_l2(L)

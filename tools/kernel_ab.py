@@ -1,4 +1,4 @@
-"""Time the decode kernels (1 = one CTA per unit, 2 = persistent warp-specialised, 3 = split)
+"""Time the decode kernels (1 = one CTA per unit, 3 = cluster split, 4 = two kernels)
 on the bench configurations; prints ms per launch and algorithmic GB/s."""
 import os
 import sys
@@ -18,7 +18,7 @@ for name in cfgs:
     units = layers * batch * kvh
     cb, q = bench.build_cache(range(units), L, gq, 1234, dev)
     out = torch.empty(units, gq, 128, device=dev)
-    for kern in ONLY or ([1, 2, 3, 4] if units < 1000 else [1, 2, 4]):
+    for kern in ONLY or ([1, 3, 4] if units < 1000 else [1, 4]):
         try:
             for _ in range(3):
                 B.decode_step(cb, q, k, out=out, kernel=kern, cap=CAP)
