@@ -220,8 +220,11 @@ def run_ours(args, rank, world, cfg):
     flat = torch.empty(world * ul, gq, 128, device=dev, dtype=torch.bfloat16) if world > 1 else None
     model_out = torch.empty(layers, batch, kvh * gq, 128, device=dev, dtype=torch.bfloat16) if world > 1 else None
 
+    per_head = args.policy == "per-head"
+    decode = B.decode_step_per_head if per_head else B.decode_step
+
     def step(qq, o=out):
-        B.decode_step(cb, qq, k, out=o)
+        decode(cb, qq, k, out=o)
         if world > 1:   # sharded outputs -> [layers, batch, H_q, D] on every rank (NCCL all-gather)
             out16.copy_(o)
             gather_outputs(out16, layers, batch, kvh, world, out=model_out, flat=flat)
@@ -257,7 +260,7 @@ def run_ours(args, rank, world, cfg):
         torch.cuda.synchronize()
         ek0.record(st)
         for _ in range(args.steps):
-            B.decode_step(cb, q, k, out=out)
+            decode(cb, q, k, out=out)
         ek1.record(st)
         torch.cuda.synchronize()
         kern_ms = ek0.elapsed_time(ek1) / args.steps
@@ -310,7 +313,7 @@ def run_ours(args, rank, world, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    res = B.decode_step(cb, q, k, with_diag=True)
+    res = decode(cb, q, k, with_diag=True)
     torch.cuda.synchronize()
     fallbacks = int(((res.diag & 4) != 0).sum().item())
     from paper_2603_14224_b200 import _lib as L_
@@ -320,7 +323,8 @@ def run_ours(args, rank, world, cfg):
     if rank != 0:
         return None
     peak, peak_kind = peaks()
-    bytes_step = algo_bytes_per_unit(L, k, gq) * ul
+    # per-q-head policy: every query head scans its KV head's sign plane and gathers its own k
+    bytes_step = (algo_bytes_per_unit(L, k, 1) * gq if per_head else algo_bytes_per_unit(L, k, gq)) * ul
     achieved = bytes_step / (kern_ms * 1e-3) / 1e9
     traffic = ncu_traffic(args.config) if world == 1 else None
     line = {
@@ -336,7 +340,7 @@ def run_ours(args, rank, world, cfg):
         "vs_baseline": None,
         "dtype": "u2 K/V payload, f32 scores, f16 mma operands / f32 accumulate",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU), random-init caches",
-        "config": decode_config(args.config, world),
+        "config": dict(decode_config(args.config, world), policy=args.policy),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": traffic["bytes"] if traffic else None,
@@ -417,7 +421,7 @@ def run_prefill(args, rank, world, cfg):
 
 
 # ------------------------------------------------------------------------------- CPU arm
-def _cpu_worker(conn, jobs):
+def _cpu_worker(conn, jobs, per_head=False):
     """One host core: prefills its sample units once (untimed), then on every 'step' runs the
     reference decode path of each of them (group-sum select_tokens + Gq x sparse_attention,
     cache.py:290-309, attention.py:52-62) on the CPU oracle and reports the seconds taken."""
@@ -433,9 +437,13 @@ def _cpu_worker(conn, jobs):
     while conn.recv() == "step":
         t0 = time.perf_counter()
         for c, qs, k in units:
-            idx = O.select(c, qs.sum(axis=0), k=k)[0]
-            for h in range(qs.shape[0]):
-                O.sparse_attention(qs[h], idx, c)
+            if per_head:              # every query head selects for itself
+                for h in range(qs.shape[0]):
+                    O.sparse_attention(qs[h], O.select(c, qs[h], k=k)[0], c)
+            else:
+                idx = O.select(c, qs.sum(axis=0), k=k)[0]
+                for h in range(qs.shape[0]):
+                    O.sparse_attention(qs[h], idx, c)
         conn.send(time.perf_counter() - t0)
     conn.close()
 
@@ -445,7 +453,7 @@ class CpuArm:
     workload's units (prefilled once, outside the timing).  One step = every core decodes its
     share of the sample; steps/s of the whole workload = (sample / units) / step seconds."""
 
-    def __init__(self, cfg, sample_units: int, cores: int):
+    def __init__(self, cfg, sample_units: int, cores: int, per_head: bool = False):
         import multiprocessing as mp
         layers, batch, kvh, gq, L, k, _ = cfg
         self.units = layers * batch * kvh
@@ -456,7 +464,7 @@ class CpuArm:
         for w in range(self.cores):
             jobs = [(L, gq, k, 9000 + i) for i in range(w, sample_units, self.cores)]
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_cpu_worker, args=(b, jobs), daemon=True)
+            p = ctx.Process(target=_cpu_worker, args=(b, jobs, per_head), daemon=True)
             p.start()
             self.procs.append(p)
             self.conns.append(a)
@@ -486,8 +494,8 @@ class CpuArm:
                 "cpu": _cpu_model()}
 
 
-def cpu_baseline(cfg, sample_units: int, workers: int, steps: int = 3, warmup: int = 1):
-    arm = CpuArm(cfg, sample_units, workers)
+def cpu_baseline(cfg, sample_units: int, workers: int, steps: int = 3, warmup: int = 1, per_head: bool = False):
+    arm = CpuArm(cfg, sample_units, workers, per_head)
     try:
         for _ in range(warmup):
             arm.step()
@@ -515,6 +523,9 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--policy", default="group-sum", choices=["group-sum", "per-head"],
+                    help="GQA selection policy: one selection per KV head from the summed queries "
+                         "(default), or one per query head (SURVEY.md 8d)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="units in the CPU-baseline sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -539,7 +550,7 @@ def main():
         cores = os.cpu_count() or 1
         sample = args.cpu_sample or 2 * cores
         # every step = the sample's decode on every host core; --warmup / --steps as given
-        arm = CpuArm(cfg, sample, cores)
+        arm = CpuArm(cfg, sample, cores, args.policy == "per-head")
         try:
             for _ in range(args.warmup):
                 arm.step()
@@ -557,7 +568,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(1000.0 / v["value"], 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_synthetic distribution)", "impl": "reference",
-            "config": decode_config(args.config, world if world > 1 else args.gpus),
+            "config": dict(decode_config(args.config, world if world > 1 else args.gpus), policy=args.policy),
             "cpu_baseline": v,
             "e2e": {"value": v["value"], "unit": "decode steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}))
@@ -579,7 +590,7 @@ def main():
             cores = os.cpu_count() or 1
             sample = args.cpu_sample or 2 * cores
             try:
-                line["cpu_baseline"] = cpu_baseline(cfg, sample, cores)
+                line["cpu_baseline"] = cpu_baseline(cfg, sample, cores, per_head=args.policy == "per-head")
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
         print(json.dumps(line))

@@ -305,8 +305,10 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
     U = cb.units
     if unit_map is not None:
         um = torch.as_tensor(unit_map)
-        if um.dim() != 1 or (um.numel() and (int(um.min()) < 0 or int(um.max()) >= cb.units)):
-            raise ValueError(f"unit_map must be 1-D ids in [0, {cb.units})")
+        if um.dim() != 1:
+            raise ValueError("unit_map must be 1-D")
+        if not um.is_cuda and um.numel() and (int(um.min()) < 0 or int(um.max()) >= cb.units):
+            raise ValueError(f"unit_map ids must be in [0, {cb.units})")
         umap = um.to(device=cb.signs.device, dtype=torch.int32).contiguous()
         U = int(umap.numel())
     if q.dim() != 3 or q.shape[0] != U or q.shape[2] != FD:
@@ -346,15 +348,24 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
     return DecodeOutput(out, lse, sel, cnt, diag)
 
 
-def decode_step_per_head(cb: CacheBatch, q: torch.Tensor, k: int, **kw) -> DecodeOutput:
+_UMAPS: dict = {}
+
+
+def decode_step_per_head(cb: CacheBatch, q: torch.Tensor, k: int, *, out: torch.Tensor | None = None,
+                         **kw) -> DecodeOutput:
     """The per-q-head selection policy (cache.py:290-309 with each query head's own query):
     every query head selects its own top-k over its KV head's cache and attends to it.  q is
     [U, Gq, 128]; out [U, Gq, 128]; selection / counts per (unit, head) as [U * Gq, ...]."""
     U, Gq, D = q.shape
     if U != cb.units or D != FD:
         raise ValueError(f"q must be [{cb.units}, Gq, {FD}], got {tuple(q.shape)}")
-    umap = torch.arange(U, dtype=torch.int32).repeat_interleave(Gq)
-    res = decode_step(cb, q.reshape(U * Gq, 1, D), k, unit_map=umap, **kw)
+    key = (U, Gq, q.device)
+    umap = _UMAPS.get(key)
+    if umap is None:
+        umap = torch.arange(U, dtype=torch.int32).repeat_interleave(Gq).to(q.device)
+        _UMAPS[key] = umap
+    o = None if out is None else out.view(U * Gq, 1, D)
+    res = decode_step(cb, q.reshape(U * Gq, 1, D), k, unit_map=umap, out=o, **kw)
     lse = None if res.lse is None else res.lse.view(U, Gq)
     return DecodeOutput(res.out.view(U, Gq, D), lse, res.selection, res.counts, res.diag)
 
