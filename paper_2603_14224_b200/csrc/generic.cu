@@ -131,9 +131,12 @@ __global__ void __launch_bounds__(DT) topk_kernel(const void* __restrict__ score
       __syncthreads();
       pick_digit(hist, ms);
       __syncthreads();
-      prefix |= (uint64_t)ms->digit << shift;
+      const uint64_t dg = (uint64_t)ms->digit;
+      const int rem = ms->rem_sel - ms->cnt_above;
+      __syncthreads();                  // every read of ms precedes the update (racecheck-clean)
+      prefix |= dg << shift;
       pmask |= (uint64_t)0xFF << shift;
-      if (tid == 0) ms->rem_sel -= ms->cnt_above;
+      if (tid == 0) ms->rem_sel = rem;
       __syncthreads();
     }
     const int need_eq = ms->rem_sel;

@@ -1,4 +1,9 @@
-"""Small decode workloads for compute-sanitizer (memcheck / racecheck) over every path."""
+"""Small workloads for compute-sanitizer (memcheck / racecheck / synccheck) over every decode
+path and feature: kernels 1 / 3 / 4, selection on / off, k = 0 / all, ring appends, window
+sinks, sign-only LUT, direct keys, per-q-head policy, the encoder and window-sink kernels.
+
+    compute-sanitizer --tool memcheck python tools/sanitize_decode.py [units L]
+"""
 import os
 import sys
 
@@ -7,14 +12,33 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2603_14224_b200 import batch as B  # noqa: E402
+from paper_2603_14224_b200.synth import gen_units_torch  # noqa: E402
 
 dev = torch.device("cuda", 0)
 units = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
-kernels = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4]
 cb, q = bench.build_cache(range(units), L, 4, 77, dev)
-for kern in kernels:
+for kern in (1, 3, 4):
     for k, sel in ((256, True), (256, False), (L, False), (0, False)):
-        r = B.decode_step(cb, q, k, with_selection=sel, with_lse=True, kernel=kern)
+        B.decode_step(cb, q, k, with_selection=sel, with_lse=True, kernel=kern)
         torch.cuda.synchronize()
-    print("kernel", kern, "ok")
+    B.decode_step(cb, q, 256, with_selection=True, kernel=kern, sign_only=True)
+    B.decode_step_per_head(cb, q, 128, with_selection=True, kernel=kern)
+    torch.cuda.synchronize()
+    print("kernel", kern, "ok", flush=True)
+# ring appends (growth) then decode
+for _ in range(20):
+    B.append_batch(cb, torch.randn(units, 128, device=dev), torch.randn(units, 128, device=dev), check=False)
+for kern in (1, 3, 4):
+    B.decode_step(cb, q, 256, with_selection=True, kernel=kern)
+torch.cuda.synchronize()
+print("appends ok", flush=True)
+# window sinks + direct keys through the encoder
+K, V = gen_units_torch(8, L, 128, 5, dev)
+W = torch.randn(8, 32, 128, device=dev)
+cbw = B.prefill_batch(K, V, sink_count=64, window=W, sign_in_quant=False, bits=1)
+qw = torch.randn(8, 4, 128, device=dev)
+for kern in (1, 3, 4):
+    B.decode_step(cbw, qw, 200, with_selection=True, kernel=kern)
+torch.cuda.synchronize()
+print("window sinks / direct / 1-bit ok", flush=True)
