@@ -658,7 +658,8 @@ template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
                                                    uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
-                                                   uint32_t& tau_out, const Xch& xch = Xch()) {
+                                                   uint32_t& tau_out, const Xch& xch = Xch(),
+                                                   long long* prof = nullptr) {
   const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const Key lb(lane);
   const int capw = g.capw;
@@ -697,6 +698,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     kmx = ms->maxx;
     kmn = ms->tau;
     xch.sample(nsv, kmx, kmn);            // cluster: the whole unit's sample
+    if (prof && tid == 0) prof[7] = clock64();            // sample scored
     const double e = (double)g.keff * (double)nsv / (double)(g.ncand);
     r = min((int)ceil(e + kTauSig * sqrt(e) + kTauAdd), nsv);
   }
@@ -760,6 +762,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
         }
         Grp::sync();
         tau = tminm[ms->digit];         // smallest sample key in the boundary bin
+        if (prof && tid == 0 && attempt == 0) prof[8] = clock64();   // threshold known
       }
       Grp::sync();
       if (tid == 0) { ms->maxx = 0; ms->bad = 0; }

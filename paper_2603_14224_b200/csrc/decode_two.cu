@@ -106,6 +106,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
   const float* qs = pre_q;
   cp_wait<0>();                      // this unit's queries / centroids have landed
+  if (prof && tid == 0) prof[4] = clock64();
   for (int i = tid; i < W; i += DT) forced[i] = 0u;
   PG::sync();
   if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
@@ -128,6 +129,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
                                         __fadd_rn(__fmul_rn(q1, c.y), __fmul_rn(q3, c.w)));
   }
   PG::sync();                        // every read of the staged inputs is done
+  if (prof && tid == 0) prof[5] = clock64();
   prefetch_unit(a, base, tid, next);
   build_pair_rows_col<PG>(lut, T);
   if (prof && tid == 0) prof[1] = clock64();
@@ -141,7 +143,8 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   uint32_t kstar = 0;
   if (mode >= 2) {
     uint32_t tau;
-    fb = produce_candidates<PG, NoX, ColKey, NB>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau) ? 1 : 0;
+    fb = produce_candidates<PG, NoX, ColKey, NB>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(), prof)
+             ? 1 : 0;
     if (prof && tid == 0) prof[2] = clock64();
     if (!fb) {
       ndyn = select_emit_candidates<PG, SEL_NBIN>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,

@@ -33,6 +33,8 @@ _lib.call("sikv_debug_set_decode_profile", None)
 c = clk.cpu().numpy().astype(np.float64)
 d = c[:, 2] - c[:, 1]
 print("  score+cand deciles", np.percentile(d, [10, 50, 80, 90, 95, 99, 100]).astype(int).tolist())
-for n, i, j in [("setup+table", 0, 1), ("score+cand", 1, 2), ("select+emit", 2, 3), ("unit total", 0, 3)]:
+for n, i, j in [("wait inputs", 0, 4), ("bitmap+qbar+LUT", 4, 5), ("pair table", 5, 1), ("sample score", 1, 7),
+                ("tau", 7, 8), ("scan (after tau)", 8, 2), ("setup+table", 0, 1), ("score+cand", 1, 2),
+                ("select+emit", 2, 3), ("unit total", 0, 3)]:
     d = c[:, j] - c[:, i]
     print(f"  {n:12s} mean {d.mean():9.0f}  p50 {np.median(d):9.0f}  max {d.max():9.0f}")
