@@ -45,11 +45,16 @@ CONFIGS = {
 SINKS = 64
 
 
-def algo_bytes_per_unit(L: int, k: int, gq: int, S: int = SINKS) -> int:
+# bytes of one selected token's K/V: 2-bit (payloads 2 x 32 B + fp16 params 2 x 16 B), 1-bit
+# (2 x 16 B + 2 x 16 B), 16-bit (2 x 256 B)
+SEL_BYTES = {2: 96, 1: 64, 16: 512}
+
+
+def algo_bytes_per_unit(L: int, k: int, gq: int, S: int = SINKS, bits: int = 2) -> int:
     """16 L (sign index) + 96 k (2-bit K/V payload + fp16 params of the
-    selected tokens) + 512 S (bf16 sink K, V) + 2 Gq 256 (q, out) + 8 KiB centroids +
-    512 B alpha."""
-    return 16 * L + 96 * min(k, L - S) + 512 * S + 2 * gq * 256 + 8192 + 512
+    selected tokens; 512 k at bits 16) + 512 S (bf16 sink K, V) + 2 Gq 256 (q, out) + 8 KiB
+    centroids + 512 B alpha."""
+    return 16 * L + SEL_BYTES[bits] * min(k, L - S) + 512 * S + 2 * gq * 256 + 8192 + 512
 
 
 def peaks():
@@ -172,7 +177,7 @@ def decode_config(name: str, world: int) -> dict:
 
 
 # ------------------------------------------------------------------------------- GPU arm
-def build_cache(gids, L: int, gq: int, seed: int, device):
+def build_cache(gids, L: int, gq: int, seed: int, device, bits: int = 2, sign_in_quant: bool = True):
     """Compressed caches of the decode units with global ids `gids` (unit content depends
     only on its id: synth.gen_units_by_id), plus their queries [n, gq, 128] float32."""
     import torch
@@ -183,7 +188,7 @@ def build_cache(gids, L: int, gq: int, seed: int, device):
 
     gids = [int(x) for x in gids]
     n_units = len(gids)
-    cb = B.empty_batch(n_units, L, sink_count=SINKS, device=device)
+    cb = B.empty_batch(n_units, L, sink_count=SINKS, device=device, bits=bits, sign_in_quant=sign_in_quant)
     q = torch.empty(n_units, gq, 128, device=device, dtype=torch.float32)
     chunk = max(1, min(n_units, (1 << 31) // (L * 128 * 2)))   # <= 2 GiB of raw K per chunk
     ws = None
@@ -213,7 +218,8 @@ def run_ours(args, rank, world, cfg):
     ul = plan.units_per_rank
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    cb, q = build_cache(plan.local_units(rank).tolist(), L, gq, 1234, dev)
+    cb, q = build_cache(plan.local_units(rank).tolist(), L, gq, 1234, dev, bits=args.bits,
+                        sign_in_quant=not args.direct_keys)
 
     out = torch.empty(ul, gq, 128, device=dev, dtype=torch.float32)
     out16 = torch.empty(ul, gq, 128, device=dev, dtype=torch.bfloat16)
@@ -324,7 +330,9 @@ def run_ours(args, rank, world, cfg):
         return None
     peak, peak_kind = peaks()
     # per-q-head policy: every query head scans its KV head's sign plane and gathers its own k
-    bytes_step = (algo_bytes_per_unit(L, k, 1) * gq if per_head else algo_bytes_per_unit(L, k, gq)) * ul
+    bpu = (algo_bytes_per_unit(L, k, 1, bits=args.bits) * gq if per_head
+           else algo_bytes_per_unit(L, k, gq, bits=args.bits))
+    bytes_step = bpu * ul
     achieved = bytes_step / (kern_ms * 1e-3) / 1e9
     traffic = ncu_traffic(args.config) if world == 1 else None
     line = {
@@ -340,7 +348,8 @@ def run_ours(args, rank, world, cfg):
         "vs_baseline": None,
         "dtype": "u2 K/V payload, f32 scores, f16 mma operands / f32 accumulate",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU), random-init caches",
-        "config": dict(decode_config(args.config, world), policy=args.policy),
+        "config": dict(decode_config(args.config, world), policy=args.policy, bits=args.bits,
+                       keys="direct" if args.direct_keys else "sign-in-quant"),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": traffic["bytes"] if traffic else None,
@@ -523,6 +532,8 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--bits", type=int, default=2, choices=[1, 2, 16], help="payload bits of the fast path")
+    ap.add_argument("--direct-keys", action="store_true", help="keys quantised directly (no sign-in-quant)")
     ap.add_argument("--policy", default="group-sum", choices=["group-sum", "per-head"],
                     help="GQA selection policy: one selection per KV head from the summed queries "
                          "(default), or one per query head (SURVEY.md 8d)")
@@ -568,7 +579,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(1000.0 / v["value"], 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_synthetic distribution)", "impl": "reference",
-            "config": dict(decode_config(args.config, world if world > 1 else args.gpus), policy=args.policy),
+            "config": dict(decode_config(args.config, world if world > 1 else args.gpus), policy=args.policy,
+                           bits=args.bits, keys="direct" if args.direct_keys else "sign-in-quant"),
             "cpu_baseline": v,
             "e2e": {"value": v["value"], "unit": "decode steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}))

@@ -45,7 +45,7 @@ extern "C" {
 #define SIKV_EUNSUPPORTED 3
 
 const char* sikv_last_error(void);
-int sikv_abi_version(void);   /* 5 */
+int sikv_abi_version(void);   /* 6 */
 
 /* ---------------------------------------------------------------- encoder (prefill)
  * replaces: compute_channel_stats   normalize.py:56-61
@@ -65,6 +65,12 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
                 uint16_t* kq_scales, uint16_t* kq_zeros, uint8_t* vq_ref, uint16_t* vq_scales,
                 uint16_t* vq_zeros, uint8_t* signs_fast, uint8_t* recs_fast, void* workspace,
                 size_t workspace_bytes, int* status_dev, void* stream);
+
+/* 16-bit fast-path records (bits = 16, "Ours (16 bits)"; cache.py:236-238 at model precision):
+ * recs16 [U][L][512] u8 = K^ = (K - mu) / alpha32 and V in fp16, in the mma fragment orders of
+ * DESIGN.md §3; decode with sikv_decode_step(mode bit 1).  status bit 4: V outside fp16. */
+int sikv_pack16(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
+                const double* mu64, const float* alpha32, uint8_t* recs16, int* status_dev, void* stream);
 
 /* full-precision rows: out_k = K[idx] - mu (centred), out_v = V[idx]; float32 or float64 out.
  * replaces: sink_k / sink_v construction, cache.py:247-270 */
@@ -115,8 +121,9 @@ size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int s
  * unit_map (nullable) [units] int32: the cache unit each query unit reads (q, out, sel, diag are
  * per query unit; the planes, sinks, recents per cache unit): the per-q-head policy runs one
  * query unit of gq = 1 per query head over its KV head's cache (cache.py:290-309 per head).
- * lut_mode: 0 = centroid LUT (build_lut), 1 = sign-only LUT (build_sign_lut, retrieval.py:54-62:
- * the code's +-1 pattern instead of its centroid; select_tokens(..., sign_only=True)). */
+ * lut_mode (mode bits): bit 0 = sign-only LUT (build_sign_lut, retrieval.py:54-62: the code's +-1
+ * pattern instead of its centroid; select_tokens(..., sign_only=True)); bit 1 = recs_fast holds
+ * 16-bit records (sikv_pack16; two-kernel path only). */
 int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
                      const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
                      int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,

@@ -31,6 +31,7 @@ _SIGS = {
                         P, P, P, SZ, P, P]),
     "sikv_window_sinks_workspace_bytes": (SZ, [I64, I64, I]),
     "sikv_window_sinks": (I, [P, I, I64, I64, I64, P, P, I, I, I, P, P, SZ, P]),
+    "sikv_pack16": (I, [P, P, I, I64, I64, P, P, P, P, P]),
     "sikv_gather_rows": (I, [P, P, I, I64, I64, I64, P, I64, P, P, P, I, P]),
     "sikv_append": (I, [P, P, I, I64, I64, P, P, P, I64, I64, I, P, P]),
     "sikv_decode_smem_bytes": (I, [I64, I, I, I, I]),

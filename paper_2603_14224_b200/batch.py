@@ -46,7 +46,8 @@ class CacheBatch:
     ffrag: torch.Tensor                       # [U, blocks, FBLK] int32 forced-row fragments + row scales
     recent_host: torch.Tensor = None          # [U] int64 host mirror of recent_n (appends are host-issued)
     ref: dict = field(default_factory=dict)   # optional reference-layout planes
-    bits: int = 2                             # payload bits: 2, or 1 (same record, codes in 2-bit fields)
+    bits: int = 2                             # payload bits: 2, 1 (same record, codes in 2-bit fields) or
+                                              # 16 (fp16 K^ / V records of 512 B, the "16 bits" variant)
     sign_in_quant: bool = True                # False: keys quantised directly (cache.py:241-244)
 
     @property
@@ -78,9 +79,10 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
                 keep_reference: bool = False, device=None, bits: int = 2, sign_in_quant: bool = True) -> CacheBatch:
     """An empty batch of `units` caches of `tokens` prefill tokens.  Fast-path variants
     (cache.py:52-75): bits 2 or 1 (the 1-bit codes use the same record, in its 2-bit fields),
-    sign_in_quant True (|K'| / alpha codes + sign plane) or False (direct signed K' codes)."""
-    if bits not in (1, 2):
-        raise NotImplementedError("the fast path supports bits 1 and 2 (the per-head API covers 4, 8, 16)")
+    sign_in_quant True (|K'| / alpha codes + sign plane) or False (direct signed K' codes), or
+    bits 16 (K' / alpha-hat and V stored in fp16: 512-B records, the two-kernel path)."""
+    if bits not in (1, 2, 16):
+        raise NotImplementedError("the fast path supports bits 1, 2 and 16 (the per-head API covers 4 and 8)")
     dev = device or L_.require_cuda()
     S = min(sink_count, tokens)
     f32 = dict(device=dev, dtype=torch.float32)
@@ -91,7 +93,8 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
         mu64=torch.empty(units, FD, **f64), alpha64=torch.empty(units, FD, **f64),
         mu32=torch.empty(units, FD, **f32), alpha32=torch.empty(units, FD, **f32),
         cent64=torch.empty(units, 32, 16, 4, **f64), cent32=torch.empty(units, 32, 16, 4, **f32),
-        signs=torch.empty(units, tokens, 16, **u8), recs=torch.empty(units, tokens, 128, **u8),
+        signs=torch.empty(units, tokens, 16, **u8),
+        recs=torch.empty(units, tokens, 512 if bits == 16 else 128, **u8),
         sink_idx=torch.arange(S, device=dev, dtype=torch.int32).repeat(units, 1),
         sink_k=torch.empty(units, S, FD, **f32), sink_v=torch.empty(units, S, FD, **f32),
         recent_k=torch.zeros(units, recent_capacity, FD, **f32),
@@ -101,7 +104,7 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
                           device=dev, dtype=torch.int32),
         recent_host=torch.zeros(units, dtype=torch.int64), bits=bits, sign_in_quant=bool(sign_in_quant),
     )
-    if keep_reference:
+    if keep_reference and bits != 16:
         cb.ref = dict(
             codes=torch.empty(units, tokens, 16, **u8),
             kq=torch.empty(units, tokens, 16 * bits, **u8), vq=torch.empty(units, tokens, 16 * bits, **u8),
@@ -156,14 +159,21 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
         workspace = torch.empty(need, dtype=torch.uint8, device=keys.device)
     status = torch.zeros(1, dtype=torch.int32, device=keys.device)
     r = cb.ref
-    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, cb.bits, 32, int(cb.sign_in_quant), 3, None,
+    r16 = cb.bits == 16
+    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, 0 if r16 else cb.bits, 32,
+            int(cb.sign_in_quant), 3, None,
             L_.ptr(_sl(cb.mu64, u0, n)), L_.ptr(_sl(cb.alpha64, u0, n)), L_.ptr(_sl(cb.mu32, u0, n)),
             L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.cent64, u0, n)), L_.ptr(_sl(cb.cent32, u0, n)),
             L_.ptr(_sl(r.get("codes"), u0, n)), L_.ptr(_sl(r.get("kq"), u0, n)),
             L_.ptr(_sl(r.get("ks"), u0, n)), L_.ptr(_sl(r.get("kz"), u0, n)),
             L_.ptr(_sl(r.get("vq"), u0, n)), L_.ptr(_sl(r.get("vs"), u0, n)),
-            L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)), L_.ptr(_sl(cb.recs, u0, n)),
+            L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)),
+            None if r16 else L_.ptr(_sl(cb.recs, u0, n)),
             L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
+    if r16:
+        # codes + codebook came from the encoder; the sign plane and the fp16 records here
+        L_.call("sikv_pack16", L_.ptr(keys), L_.ptr(values), dt, n, L, L_.ptr(_sl(cb.mu64, u0, n)),
+                L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.recs, u0, n)), L_.ptr(status), L_.stream())
     if not cb.sign_in_quant:
         # direct keys: the record dequantises to K' itself, so the attention's alpha-hat is 1
         cb.alpha32[u0:u0 + n] = 1.0
@@ -344,7 +354,8 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], L_.ptr(cb.recent_n), R,
             L_.ptr(qf), U, cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), stride, L_.ptr(cnt),
-            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only), kernel, L_.stream())
+            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only) | (2 if cb.bits == 16 else 0), kernel,
+            L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)
 
 

@@ -16,6 +16,8 @@ cudaError_t launch_encode(const void*, const void*, int, int64_t, int64_t, int, 
                           const uint8_t*, double*, double*, float*, float*, double*, float*, uint8_t*,
                           uint8_t*, __half*, __half*, uint8_t*, __half*, __half*, uint8_t*, uint8_t*, void*,
                           int*, cudaStream_t);
+cudaError_t launch_pack16(const void*, const void*, int, int64_t, int64_t, const double*, const float*, uint8_t*, int*,
+                          cudaStream_t);
 cudaError_t launch_gather_rows(const void*, const void*, int, int64_t, int64_t, int, const int32_t*, int,
                                const double*, void*, void*, int, cudaStream_t);
 cudaError_t launch_append(const void*, const void*, int, int64_t, int, const double*, void*, void*, int64_t,
@@ -41,7 +43,7 @@ cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, co
                                 const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, int, float*,
                                 float*, int32_t*, int, int32_t*, int32_t*, const int32_t*, int, cudaStream_t);
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq);
-int two_attend_smem_bytes(int64_t L, int k, int S, int Gq);
+int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16);
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                               const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
@@ -95,7 +97,7 @@ static int max_smem() {
 extern "C" {
 
 const char* sikv_last_error(void) { return g_err.c_str(); }
-int sikv_abi_version(void) { return 5; }
+int sikv_abi_version(void) { return 6; }
 
 size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
   return encode_workspace_bytes(units, tokens, (int)dim);
@@ -129,9 +131,10 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
             "workspace too small (sikv_encode_workspace_bytes)");
   }
   if (signs_fast || recs_fast) {
-    REQUIRE(signs_fast && recs_fast, SIKV_EINVAL, "fast layout needs both signs_fast and recs_fast");
-    REQUIRE(dim == 128 && (bits == 1 || bits == 2) && group_size == 32, SIKV_EUNSUPPORTED,
-            "fast layout requires dim=128, bits 1 or 2, group_size=32");
+    REQUIRE(signs_fast && (recs_fast || bits == 0), SIKV_EINVAL,
+            "fast layout needs both signs_fast and recs_fast (bits 0: signs_fast alone, for 16-bit records)");
+    REQUIRE(dim == 128 && (bits == 1 || bits == 2 || (bits == 0 && !recs_fast)) && group_size == 32,
+            SIKV_EUNSUPPORTED, "fast layout requires dim=128, bits 1 or 2 (0: sign plane only), group_size=32");
   }
   if (kq_ref) REQUIRE(kq_scales && kq_zeros, SIKV_EINVAL, "kq_ref needs scales and zeros");
   if (vq_ref) REQUIRE(vq_scales && vq_zeros, SIKV_EINVAL, "vq_ref needs scales and zeros");
@@ -182,6 +185,16 @@ int sikv_decode_default_cap(int64_t tokens, int k, int sinks) {
 int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap) {
   if (cap <= 0) cap = sikv_decode_default_cap(tokens, k, sinks);
   return decode_layout(tokens, k, sinks, gq, cap).total;
+}
+
+int sikv_pack16(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
+                const double* mu64, const float* alpha32, uint8_t* recs16, int* status_dev, void* stream) {
+  REQUIRE(keys && values && mu64 && alpha32 && recs16, SIKV_EINVAL, "null pointer");
+  REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
+  REQUIRE(units >= 0 && tokens >= 0, SIKV_EINVAL, "bad shape");
+  return cuda_ret(launch_pack16(keys, values, in_dtype, units, tokens, mu64, alpha32, recs16, status_dev,
+                                (cudaStream_t)stream),
+                  "sikv_pack16");
 }
 
 int sikv_forced_blocks(int sinks, int64_t rcap) { return (int)std::max<int64_t>(1, (sinks + rcap + 15) / 16); }
@@ -253,8 +266,10 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   // kernel: 0 = auto, 1 = one CTA per unit, 3 = split units (a CTA cluster per unit),
   // 4 = two kernels (selection with two unit groups per SM, then attention)
   REQUIRE(kernel == 0 || kernel == 1 || kernel == 3 || kernel == 4, SIKV_EINVAL, "kernel must be 0, 1, 3 or 4");
-  REQUIRE(lut_mode == 0 || lut_mode == 1, SIKV_EINVAL, "lut_mode must be 0 (centroids) or 1 (sign-only)");
-  if (kernel == 4 || (kernel == 0 && units >= 2 * num_sms())) {
+  REQUIRE(lut_mode >= 0 && lut_mode <= 3, SIKV_EINVAL, "mode bits: 1 = sign-only LUT, 2 = 16-bit records");
+  const bool rec16 = (lut_mode & 2) != 0;
+  REQUIRE(!rec16 || kernel == 0 || kernel == 4, SIKV_EUNSUPPORTED, "16-bit records run on the two-kernel path (kernel 0 or 4)");
+  if (kernel == 4 || (kernel == 0 && (units >= 2 * num_sms() || rec16))) {
     const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
     const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
     int tcap = cap > 0 ? cap : (int)std::max<int64_t>(2 * ke + 1024, 1024);
@@ -265,7 +280,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     while (cap <= 0 && tcap > soft_cap && two_select_smem_bytes(tokens, k, sinks, tcap, gq) > 164 * 1024) tcap -= 64;
     while (cap <= 0 && tcap > floor_cap && two_select_smem_bytes(tokens, k, sinks, tcap, gq) > max_smem()) tcap -= 64;
     const bool fits = two_select_smem_bytes(tokens, k, sinks, tcap, gq) <= max_smem() &&
-                      two_attend_smem_bytes(tokens, k, sinks, gq) <= max_smem();
+                      two_attend_smem_bytes(tokens, k, sinks, gq, rec16) <= max_smem();
     const bool ws_ok = workspace && workspace_bytes >= two_workspace_bytes(units, tokens, k, sinks);
     if (fits && ws_ok) {
       g_last_decode_kernel = 4;
@@ -275,7 +290,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                                         (cudaStream_t)stream),
                       "sikv_decode_step");
     }
-    REQUIRE(kernel != 4, SIKV_EUNSUPPORTED,
+    REQUIRE(kernel != 4 && !rec16, SIKV_EUNSUPPORTED,
             fits ? "the two-kernel path needs sikv_decode_workspace_bytes_k of workspace"
                  : "the two-kernel path does not fit this configuration");
   }

@@ -40,6 +40,26 @@ constexpr int R_K4 = 0;        // 64 B K as e2m1 nibbles (sign | 2-bit code), MM
 constexpr int R_VPAY = 64;     // 32 B V payload, MMA-permuted
 constexpr int R_KPAR = 96;     // 4 x (2 qs, zp) fp16
 constexpr int R_VPAR = 112;    // 4 x (qs, zp) fp16
+// 16-bit records (the bits = 16 "Ours (16 bits)" variant, cache.py:236-238 at model precision):
+// 512 B per token.  Bytes 0-255: K^ = K' / alpha-hat in fp16, B-operand order: 64-B chunk t4
+// holds, as word 2s + e, channels (16 s + 8 e + 2 t4, +1) (one quad lane's 8 k-steps).  Bytes
+// 256-511: V in fp16, 32-B chunk g holds, as word m, channels (16 m + g, 16 m + g + 8) (the
+// A-operand rows of lane group g for the 8 m-tiles).
+constexpr int FREC16 = 512;
+__host__ __device__ __forceinline__ int k16_off(int ch) {   // byte offset of K channel ch
+  const int s = ch >> 4, e = (ch >> 3) & 1, t4 = (ch & 7) >> 1;
+  return 64 * t4 + 4 * (2 * s + e) + 2 * (ch & 1);
+}
+__host__ __device__ __forceinline__ int v16_off(int ch) {   // byte offset of V channel ch
+  const int m = ch >> 4, r = ch & 15;
+  return 256 + 32 * (r & 7) + 4 * m + 2 * (r >> 3);
+}
+// staged 16-bit block: 16-B unit u of block token j at unit u ^ sw16(j, u) (conflict-free
+// K and V fragment reads; found by exhaustive search over XOR swizzles)
+__host__ __device__ __forceinline__ int sw16(int j, int u) {
+  return u ^ (((u >> 3) ^ ((j & 1) << 1) ^ ((j >> 1) & 1) ^ (((j >> 2) & 1) << 2)) & 7);
+}
+
 // one 16-row block of forced rows (sinks, then recents): K^ fragments [32 lanes][32 words],
 // V fragments [32 lanes][32 words], then 16 float32 row scales (a power of two per row:
 // K^ = K' / (alpha-hat * scale) stays within fp16 for recent rows whose |K'| exceeds the

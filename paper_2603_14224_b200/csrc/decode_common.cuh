@@ -539,6 +539,99 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   cp_wait<0>();
 }
 
+// ---- 16-bit records (FREC16): the fragments are stored, no dequantisation
+constexpr int STAGE16_BYTES = 16 * FREC16;     // one 16-token block
+
+// QK^T, online softmax and PV of one staged 16-bit block (rem = valid rows from its start)
+__device__ __forceinline__ void attn_block16(Attn& A, uint32_t sb, int rem, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  float sacc[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const int j = g + 8 * nt;
+    uint32_t kw[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 t;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
+                   : "r"(sb + (uint32_t)(j * FREC16 + 16 * sw16(j, 4 * t4 + i))));
+      kw[4 * i] = t.x; kw[4 * i + 1] = t.y; kw[4 * i + 2] = t.z; kw[4 * i + 3] = t.w;
+    }
+    sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, kw[2 * s], kw[2 * s + 1]);
+  }
+  // V words of tokens 2t4, 2t4 + 1, 2t4 + 8, 2t4 + 9: word m of chunk g = (ch 16m + g, 16m + g + 8)
+  uint32_t vw[4][8];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int j = 2 * t4 + (x & 1) + 8 * (x >> 1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint4 t;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
+                   : "r"(sb + (uint32_t)(j * FREC16 + 16 * sw16(j, 16 + 2 * g + h))));
+      vw[x][4 * h] = t.x; vw[x][4 * h + 1] = t.y; vw[x][4 * h + 2] = t.z; vw[x][4 * h + 3] = t.w;
+    }
+  }
+  attn_softmax_pv(A, sacc, rem, lane, [&](int mp, uint32_t (&v)[2][4]) {
+#pragma unroll
+    for (int mm = 0; mm < 2; ++mm) {
+      const int m = 2 * mp + mm;
+      v[mm][0] = prmt(vw[0][m], vw[1][m], 0x5410u);
+      v[mm][1] = prmt(vw[0][m], vw[1][m], 0x7632u);
+      v[mm][2] = prmt(vw[2][m], vw[3][m], 0x5410u);
+      v[mm][3] = prmt(vw[2][m], vw[3][m], 0x7632u);
+    }
+  });
+}
+
+// dynamic rows from 16-bit records: blocks first, first + nw, ... of [0, nbd), staged by
+// cp.async (NSTAGE buffers per warp); lane copies half (16 units) of block token lane >> 1
+template <int NSTAGE = 2>
+__device__ __forceinline__ void attn_dynamic16(Attn& A, const uint8_t* recs_u, const int32_t* dyn, int ndyn,
+                                               int first, int nw, char* stage, int lane) {
+  const int nbd = (ndyn + 15) >> 4;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
+  const int jt = lane >> 1, half = lane & 1;
+  int32_t tix = 0;
+  auto stage_blk = [&](uint32_t buf) {
+    const uint8_t* src = recs_u + (size_t)((uint32_t)tix * (uint32_t)FREC16) + 256 * half;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int u = 16 * half + i;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + buf + (uint32_t)(jt * FREC16 + 16 * sw16(jt, u))),
+                   "l"(src + 16 * i));
+    }
+  };
+  if (first < nbd) tix = dyn[first * 16 + jt];
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    const int bn = first + (s + 1) * nw;
+    const int32_t tn = bn < nbd ? dyn[bn * 16 + jt] : 0;
+    if (first + s * nw < nbd) stage_blk(s * STAGE16_BYTES);
+    cp_commit();
+    tix = tn;
+  }
+  int buf = 0;
+  for (int db = first; db < nbd; db += nw) {
+    const int nx = db + (NSTAGE - 1) * nw;
+    if (nx < nbd) {
+      stage_blk(((buf + NSTAGE - 1) % NSTAGE) * STAGE16_BYTES);
+      if (nx + nw < nbd) tix = dyn[(nx + nw) * 16 + jt];
+    }
+    cp_commit();
+    cp_wait<NSTAGE - 1>();
+    __syncwarp();
+    attn_block16(A, sbase + buf * STAGE16_BYTES, ndyn - db * 16, lane);
+    __syncwarp();
+    buf = buf + 1 == NSTAGE ? 0 : buf + 1;
+  }
+  cp_wait<0>();
+}
+
 // this warp's partial (O, m, l) -> shared memory [nw][Gq][128], [nw][Gq], [nw][Gq]
 __device__ __forceinline__ void attn_write_partial(const Attn& A, float* part, float* pm, float* pl, int wi,
                                                    int Gq, int lane) {

@@ -195,7 +195,7 @@ constexpr int ATT_STAGES = 2;                       // cp.async staging buffers 
 // One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
 // indices come straight from global memory (L2), so the only CTA-wide barriers are the
 // two around the partial merge.
-template <int NW>
+template <int NW, bool R16>
 __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u) {
   constexpr int NT = 32 * NW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -215,8 +215,12 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   attn_forced(A, ffrag_u, nf, warp, NW, lane);
   asm volatile("griddepcontrol.wait;" ::: "memory");   // the selection grid is complete
   const int ndyn = __ldg(a.ndyn + u);
-  attn_dynamic<ATT_STAGES>(A, a.recs + cu * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
-                           stage + warp * ATT_STAGES * STAGE_BYTES, lane);
+  if constexpr (R16)
+    attn_dynamic16<ATT_STAGES>(A, a.recs + cu * a.L * FREC16, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
+                               stage + warp * ATT_STAGES * STAGE16_BYTES, lane);
+  else
+    attn_dynamic<ATT_STAGES>(A, a.recs + cu * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
+                             stage + warp * ATT_STAGES * STAGE_BYTES, lane);
   __syncthreads();
   float* part = reinterpret_cast<float*>(stage);
   float* pm = part + NW * Gq * FD;
@@ -226,9 +230,11 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
   attn_merge<Cta256>(part, pm, pl, NW, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
 }
 
+// R16: 16-bit records (512 B per token, stored fp16 fragments; 64 KB of staging per CTA)
+template <bool R16>
 __global__ void __launch_bounds__(ATT_THREADS, ATT_CTAS_PER_SM) decode_attend_kernel(const __grid_constant__ TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
-  attend_unit<ATT_WARPS>(a, sm, blockIdx.x);
+  attend_unit<ATT_WARPS, R16>(a, sm, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- host side
@@ -267,9 +273,9 @@ static bool two_forced_smem(int64_t L, int k, int S, int cap, int Gq) {
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes;
 }
-int two_attend_smem_bytes(int64_t L, int k, int S, int Gq) {
+int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16) {
   (void)L; (void)k; (void)S;
-  return std::max(ATT_WARPS * ATT_STAGES * STAGE_BYTES, ATT_WARPS * Gq * (FD + 2) * 4);
+  return std::max(ATT_WARPS * ATT_STAGES * (rec16 ? STAGE16_BYTES : STAGE_BYTES), ATT_WARPS * Gq * (FD + 2) * 4);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
@@ -283,7 +289,9 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
                               const int32_t* rn, int R,
                               const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
                               int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
-                              int nsm, const int32_t* umap, int lut_mode, cudaStream_t st) {
+                              int nsm, const int32_t* umap, int mode, cudaStream_t st) {
+  const int lut_mode = mode & 1;
+  const bool rec16 = (mode & 2) != 0;
   TwoArgs a = two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq));
   a.signs = signs; a.recs = recs; a.cent32 = cent32; a.alpha32 = alpha32; a.sink_idx = sink_idx;
   a.ffrag = ffrag; a.rn = rn; a.umap = umap; a.q = q; a.out = out; a.lse = lse; a.sel = sel; a.sel_count = sel_count; a.diag = diag;
@@ -304,8 +312,9 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   decode_select_kernel<<<grid, SEL_THREADS, smem_s, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int smem_a = two_attend_smem_bytes(L, k, S, Gq);
-  e = cudaFuncSetAttribute(decode_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
+  const int smem_a = two_attend_smem_bytes(L, k, S, Gq, rec16);
+  auto attend = rec16 ? decode_attend_kernel<true> : decode_attend_kernel<false>;
+  e = cudaFuncSetAttribute(attend, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)U);
@@ -317,7 +326,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decode_attend_kernel, a);
+  return cudaLaunchKernelEx(&cfg, attend, a);
 }
 
 }  // namespace sikv

@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
         int pos = (p - (int)(t & 15)) & 15;
         a.signs_fast[((int64_t)u * a.L + t) * FSIGN + pos] = (uint8_t)(code | (partner << 4));
       }
+      if (a.recs_fast) {   // (bits = 0 with only the sign plane: the 16-bit records come from pack16)
       uint32_t out = 0;
       // K4 words 0-15: e2m1 nibbles (sign of K' at bit 3, magnitude code at bits 0-1)
 #pragma unroll
@@ -527,6 +528,7 @@ __global__ void __launch_bounds__(PACK_WARPS * 32) pack_kernel(PackArgs a) {
       if (lane >= 24 && lane < 28) out = kpj;
       if (lane >= 28) out = vpj;
       reinterpret_cast<uint32_t*>(a.recs_fast + ((int64_t)u * a.L + t) * FREC)[lane] = out;
+      }
     }
   }
   __syncthreads();
@@ -1055,6 +1057,54 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
                                                                                : launch(pack_kernel<IN_F64>);
   if (e != cudaSuccess) return e;
   codebook_final_kernel<<<dim3((unsigned)U, (G * 64 + 31) / 32), 256, 0, st>>>(G, ptiles, cbp, cbc, c64, c32);
+  return cudaGetLastError();
+}
+
+// 16-bit records (the bits = 16 fast path, cache.py:236-238 at model precision): one warp per
+// token writes its 128 words: K^ = (K - mu) / alpha-hat (float64, one rounding to fp16) in
+// the B-operand order of FREC16 and V in fp16 in the A-operand order.  status bit 4: a V entry
+// outside the fp16 range.
+__global__ void pack16_kernel(const void* __restrict__ keys, const void* __restrict__ values, int dt, int64_t L,
+                              const double* __restrict__ mu64, const float* __restrict__ alpha32,
+                              uint8_t* __restrict__ recs16, int* status) {
+  const int64_t u = blockIdx.y;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= L) return;
+  const int64_t row = (u * L + t) * FD;
+  uint32_t* out = reinterpret_cast<uint32_t*>(recs16 + (u * L + t) * FREC16);
+  int bad = 0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int w = lane + 32 * r;
+    {   // K word w: chunk t4 = w >> 4, word 2s + e = w & 15 -> channels 16s + 8e + 2t4 (+1)
+      const int t4 = w >> 4, s = (w & 15) >> 1, e = w & 1, c = 16 * s + 8 * e + 2 * t4;
+      uint32_t h2 = 0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float al = alpha32[u * FD + c + i];
+        const double x = (load_in(keys, dt, row + c + i) - mu64[u * FD + c + i]) / (double)(al > 0.f ? al : 1.0f);
+        h2 |= (uint32_t)__half_as_ushort(__double2half(x)) << (16 * i);
+      }
+      out[(k16_off(c) >> 2)] = h2;
+    }
+    {   // V word w: chunk g = w >> 3, word m = w & 7 -> channels 16m + g (low), 16m + g + 8
+      const int g = w >> 3, m = w & 7, c = 16 * m + g;
+      const double v0 = load_in(values, dt, row + c), v1 = load_in(values, dt, row + c + 8);
+      if (fabs(v0) > 65504.0 || fabs(v1) > 65504.0) bad = 16;
+      out[(v16_off(c) >> 2)] = (uint32_t)__half_as_ushort(__double2half(v0)) |
+                               ((uint32_t)__half_as_ushort(__double2half(v1)) << 16);
+    }
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (bad && lane == 0 && status) atomicOr(status, bad);
+}
+
+cudaError_t launch_pack16(const void* keys, const void* values, int dt, int64_t U, int64_t L, const double* mu64,
+                          const float* alpha32, uint8_t* recs16, int* status, cudaStream_t st) {
+  if (U == 0 || L == 0) return cudaSuccess;
+  pack16_kernel<<<dim3((unsigned)((L + 7) / 8), (unsigned)U), 256, 0, st>>>(keys, values, dt, L, mu64, alpha32,
+                                                                            recs16, status);
   return cudaGetLastError();
 }
 

@@ -54,3 +54,16 @@ def records_to_reference(recs: np.ndarray):
     assert (kpar[..., 0].view(np.float16) * np.float16(2) == qs2).all()
     vpar = recs[:, 112:128].copy().view(np.uint16).reshape(L, 4, 2)
     return kc, vc, kpar, vpar, neg
+
+
+def records16_to_arrays(recs: np.ndarray):
+    """[L, 512] u8 16-bit records -> (K^ [L, 128] fp16, V [L, 128] fp16) in channel order
+    (inverse of common.cuh k16_off / v16_off)."""
+    L = recs.shape[0]
+    h = recs.view(np.uint16)                    # [L, 256]
+    ch = np.arange(128)
+    s, e, t4 = ch >> 4, (ch >> 3) & 1, (ch & 7) >> 1
+    koff = 64 * t4 + 4 * (2 * s + e) + 2 * (ch & 1)
+    m, r = ch >> 4, ch & 15
+    voff = 256 + 32 * (r & 7) + 4 * m + 2 * (r >> 3)
+    return h[:, koff // 2].view(np.float16).reshape(L, 128), h[:, voff // 2].view(np.float16).reshape(L, 128)

@@ -442,3 +442,29 @@ def test_per_q_head_policy(kernel):
             np.testing.assert_array_equal(res.selection[r, : int(res.counts[r])].cpu().numpy(), idx)
             ref = O.sparse_attention(q[i, h].cpu().numpy().astype(np.float64), idx, c)
             assert O.rel_l2(res.out[i, h].cpu().numpy(), ref) <= att_rel_l2(L)
+
+
+def test_sixteen_bit_records():
+    """bits = 16 on the fast path ("Ours (16 bits)", cache.py:236-238 at model precision):
+    sign plane and codebook as the 2-bit path, records = fp16 K' / alpha-hat and V in fragment
+    order (bit-exact to the float64 values rounded once), selections exact vs restate32,
+    attention vs the float64 lossless oracle; the two-kernel path runs it (1 / 3 refuse)."""
+    from .fastlayout import records16_to_arrays
+    units = [gen_unit(L, 128, 4, s) for L, s in ((4096, 800), (4096, 801))]
+    K = torch.tensor(np.stack([u.keys for u in units]), dtype=torch.bfloat16, device="cuda")
+    V = torch.tensor(np.stack([u.values for u in units]), dtype=torch.bfloat16, device="cuda")
+    cb = B.prefill_batch(K, V, sink_count=64, bits=16)
+    oc = [O.prefill(u.keys, u.values, bits=16, sink_count=64) for u in units]
+    q = torch.tensor(np.stack([u.queries[:4] for u in units]), dtype=torch.float32, device="cuda")
+    for i, (u, c) in enumerate(zip(units, oc)):
+        np.testing.assert_array_equal(unrotate_signs(cb.signs[i].cpu().numpy()), c.packed_codes)
+        kh, vh = records16_to_arrays(cb.recs[i].cpu().numpy())
+        ahat = cb.alpha32[i].cpu().numpy().astype(np.float64)
+        ahat[ahat == 0] = 1.0
+        np.testing.assert_array_equal(kh, ((u.keys - c.mu) / ahat).astype(np.float16))
+        np.testing.assert_array_equal(vh, u.values.astype(np.float16))
+    for kern in (0, 4):
+        _check_decode(units, cb, oc, q, 256, kernel=kern)
+    for kern in (1, 3):
+        with pytest.raises(NotImplementedError):
+            B.decode_step(cb, q, 256, kernel=kern)
