@@ -49,6 +49,10 @@ CASES = [
     ("b1_d128", 512, 128, 9, 1, 32, 0, True, False, 64, 4, 0),
     ("lossless_d64", 256, 64, 10, 16, 32, 8, True, False, 32, 2, 0),
     ("c2_1unit", 32768, 128, 200, 2, 32, 64, True, False, 2048, 4, 0),
+    # the fast path's variants at its geometry (D = 128, group 32)
+    ("direct_d128", 2048, 128, 13, 2, 32, 64, False, False, 128, 4, 0),
+    ("b1_sinks_d128", 2048, 128, 14, 1, 32, 64, True, False, 128, 4, 0),
+    ("lossless_d128", 2048, 128, 15, 16, 32, 64, True, False, 128, 4, 0),
 ]
 
 

@@ -26,7 +26,7 @@ def sha(a):
 
 # ----------------------------------------------------------------- golden parity (reference outputs)
 GOLD = ["c1_u0", "c1_u1", "win_1k", "append_2k", "gq7_2k", "b4_d64", "direct_d32", "b8_d32",
-        "b1_d128", "lossless_d64", "c2_1unit"]
+        "b1_d128", "lossless_d64", "c2_1unit", "direct_d128", "b1_sinks_d128", "lossless_d128"]
 
 
 @pytest.mark.parametrize("name", GOLD)

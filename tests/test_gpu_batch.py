@@ -468,3 +468,25 @@ def test_sixteen_bit_records():
     for kern in (1, 3):
         with pytest.raises(NotImplementedError):
             B.decode_step(cb, q, 256, kernel=kern)
+
+
+@pytest.mark.parametrize("name,bits,siq", [("direct_d128", 2, False), ("b1_sinks_d128", 1, True),
+                                           ("lossless_d128", 16, True), ("c1_u0", 2, True)])
+def test_fast_variants_match_reference_golden(golden, name, bits, siq):
+    """Fast-path variants against the real reference's outputs (tests/golden, made by running
+    sikv.prefill / select_tokens / sparse_attention): the group-sum selection equals the
+    reference's set (certified float32 check, measured: identical) and the attention is within
+    the bars of the reference's float64 outputs on that selection."""
+    meta, arr = golden
+    rec = meta[name]
+    u = gen_unit(rec["L"], 128, rec["gq"], rec["seed"])
+    K = torch.tensor(u.keys[None], dtype=torch.bfloat16, device="cuda")
+    V = torch.tensor(u.values[None], dtype=torch.bfloat16, device="cuda")
+    cb = B.prefill_batch(K, V, sink_count=rec["sinks"], bits=bits, sign_in_quant=siq)
+    q = torch.tensor(u.queries[None, : rec["gq"]], dtype=torch.float32, device="cuda")
+    res = B.decode_step(cb, q, rec["k"], with_selection=True)
+    got = res.selection[0, : int(res.counts[0])].cpu().numpy()
+    np.testing.assert_array_equal(got, arr[f"{name}/sel"])
+    ref_out = arr[f"{name}/attn"]
+    for h in range(rec["gq"]):
+        assert O.rel_l2(res.out[0, h].cpu().numpy(), ref_out[h]) <= att_rel_l2(rec["L"]), h

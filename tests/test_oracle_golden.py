@@ -10,7 +10,7 @@ from oracle import sikv_oracle as O
 from paper_2603_14224_b200.synth import gen_unit
 
 FAST_CASES = ["c1_u0", "c1_u1", "win_1k", "append_2k", "gq7_2k", "b4_d64", "direct_d32",
-              "b8_d32", "b1_d128", "lossless_d64"]
+              "b8_d32", "b1_d128", "lossless_d64", "direct_d128", "b1_sinks_d128", "lossless_d128"]
 
 
 def sha(a):
