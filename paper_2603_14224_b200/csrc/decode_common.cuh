@@ -709,7 +709,9 @@ struct UnitGeom {
   int64_t flim;        // tokens below flim may be sinks
 };
 
-__device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw, const int32_t* sink_idx_u) {
+// sink_idx_u may be null when flim is filled in later (flim_known = 0)
+__device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw, const int32_t* sink_idx_u,
+                                              int flim_known = 1) {
   UnitGeom g;
   g.L = L;
   g.S = S;
@@ -724,7 +726,7 @@ __device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw,
   else g.mode = 3;
   g.sstride = g.mode == 3 ? max(SSTRIDE_MIN, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
   g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
-  g.flim = S > 0 ? (int64_t)sink_idx_u[S - 1] + 1 : 0;
+  g.flim = (S > 0 && flim_known) ? (int64_t)sink_idx_u[S - 1] + 1 : 0;
   return g;
 }
 

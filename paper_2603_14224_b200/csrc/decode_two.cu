@@ -61,7 +61,9 @@ struct TwoArgs {
 };
 
 // ---------------------------------------------------------------- selection
-// the group's staging area for the next unit's queries and centroids (cp.async)
+constexpr int SINK_STAGE = 256;   // sink indices staged with the next unit's inputs (more: read from L2)
+
+// the group's staging area for the next unit's queries, centroids and sink indices (cp.async)
 __device__ __forceinline__ void prefetch_unit(const TwoArgs& a, char* base, int tid, int64_t un) {
   const uint32_t pre_s = (uint32_t)__cvta_generic_to_shared(base + a.g_pre);
   if (un >= 0 && un < a.U) {
@@ -70,6 +72,9 @@ __device__ __forceinline__ void prefetch_unit(const TwoArgs& a, char* base, int 
     const int64_t cn = a.umap ? (int64_t)__ldg(a.umap + un) : un;
     for (int i = tid; i < 512; i += DT)
       cp_async16_s(pre_s + (uint32_t)(a.Gq * FD * 4) + 16u * (uint32_t)i, a.cent32 + cn * 2048 + 4 * i);
+    const uint32_t ps = pre_s + (uint32_t)((a.Gq * FD + 2048) * 4);
+    for (int i = tid; i < min(a.S, SINK_STAGE); i += DT)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ps + 4u * (uint32_t)i), "l"(a.sink_idx + cn * a.S + i));
   }
   cp_commit();
 }
@@ -99,19 +104,23 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   if (prof && tid == 0) prof[0] = clock64();
   const int64_t cu = a.umap ? (int64_t)__ldg(a.umap + u) : u;    // the unit's cache
   const uint4* signs = reinterpret_cast<const uint4*>(a.signs + cu * L * FSIGN);
-  const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + cu * S);
-  const int psid = tid < S ? a.sink_idx[cu * S + tid] : -1;
+  // the sample's loads first (its geometry does not depend on the sinks), the sink-dependent
+  // limit once the staged sink indices are visible
+  UnitGeom g = unit_geom(L, S, a.k, a.capw, nullptr, 0);
   uint4 wsamp[MAX_SAMPLE_CHUNKS];
   load_sample(g, signs, tid, wsamp);
   uint32_t* forced = a.g_forced >= 0 ? forced_s : a.gforced + u * W;
   const float* qs = pre_q;
-  cp_wait<0>();                      // this unit's queries / centroids have landed
+  const int* sidx = S <= SINK_STAGE ? reinterpret_cast<const int*>(pre_q + Gq * FD + 2048) : a.sink_idx + cu * S;
+  cp_wait<0>();                      // this unit's queries / centroids / sink indices have landed
   if (prof && tid == 0) prof[4] = clock64();
   for (int i = tid; i < W; i += DT) forced[i] = 0u;
-  PG::sync();
+  PG::sync();                        // (also makes every thread's staged data visible)
+  g.flim = S > 0 ? (int64_t)sidx[S - 1] + 1 : 0;
+  const int psid = tid < S ? sidx[tid] : -1;
   if (psid >= 0) atomicOr(&forced[psid >> 5], 1u << (psid & 31));
   for (int j = tid + DT; j < S; j += DT) {
-    const int t = a.sink_idx[cu * S + j];
+    const int t = sidx[j];
     atomicOr(&forced[t >> 5], 1u << (t & 31));
   }
   if (tid < FD) {
@@ -258,7 +267,7 @@ static TwoArgs two_layout(int64_t L, int k, int S, int cap, int Gq, bool forced_
   a.g_cand = off;
   off += a128(std::max(DW * a.capw * 8, 8 * FD * 4));
   a.g_pre = off;
-  off += a128((Gq * FD + 2048) * 4);      // next unit's queries and centroids
+  off += a128((Gq * FD + 2048 + SINK_STAGE) * 4);   // next unit's queries, centroids, sink indices
   a.g_bytes = off;
   a.dstride = two_dstride(L, k, S);
   return a;
