@@ -269,7 +269,18 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   REQUIRE(lut_mode >= 0 && lut_mode <= 3, SIKV_EINVAL, "mode bits: 1 = sign-only LUT, 2 = 16-bit records");
   const bool rec16 = (lut_mode & 2) != 0;
   REQUIRE(!rec16 || kernel == 0 || kernel == 4, SIKV_EUNSUPPORTED, "16-bit records run on the two-kernel path (kernel 0 or 4)");
-  if (kernel == 4 || (kernel == 0 && (units >= 2 * num_sms() || rec16))) {
+  // auto (measured, tools/dispatch_sweep.py): the one-CTA kernel while its units fill at most
+  // one wave (two when two CTAs fit an SM: wave quantisation then still beats the two-kernel
+  // path's per-unit cost), the split kernel for few long units, the two-kernel path otherwise
+  bool auto_two = false, auto_split = false;
+  if (kernel == 0) {
+    const int c1 = decode_layout(tokens, k, sinks, gq, sikv_decode_default_cap(tokens, k, sinks)).total <= 113 * 1024
+                       ? 2 : 1;
+    const double waves1 = (double)units / ((double)num_sms() * c1);
+    auto_split = units <= num_sms() / 2 && tokens >= 16384;
+    auto_two = rec16 || (!auto_split && !(waves1 <= 1.0 || (c1 >= 2 && waves1 <= 2.0)));
+  }
+  if (kernel == 4 || auto_two) {
     const int64_t ke = std::min<int64_t>(k, std::max<int64_t>(tokens - sinks, 0));
     const int floor_cap = (int)std::max<int64_t>(ke + ke * 2 / 5 + 512, 1024);
     int tcap = cap > 0 ? cap : (int)std::max<int64_t>(2 * ke + 1024, 1024);
@@ -295,7 +306,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                  : "the two-kernel path does not fit this configuration");
   }
   // few long units: split each across a cluster of 2 / 4 / 8 CTAs so every SM has work
-  if (kernel == 3 || (kernel == 0 && units < num_sms() && tokens >= 16384)) {
+  if (kernel == 3 || auto_split) {
     int pick = 0, pick_cap = 0;
     for (int ns : {2, 4, 8}) {
       if ((tokens + 255) / 256 < (kernel == 3 ? 1 : 4) * ns) break;   // chunks per CTA

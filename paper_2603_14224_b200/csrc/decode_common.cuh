@@ -682,6 +682,53 @@ __device__ __forceinline__ void attn_merge(const float* part, float* pm, float* 
   }
 }
 
+// merge of the nw warp partials into one CTA partial (caller synchronises before): per head
+// num[128] = sum_w part_w 2^(m_w - M), then M, den = sum_w l_w 2^(m_w - M) -> dst[h][FD + 2]
+__device__ __forceinline__ void attn_merge_partial(const float* part, float* pm, const float* pl, int nw, int Gq,
+                                                   int tid, int nt, float* dst) {
+  if (tid < Gq) {
+    const int h = tid;
+    float M = -INFINITY;
+    for (int w = 0; w < nw; ++w) M = fmaxf(M, pm[w * Gq + h]);
+    float den = 0.f;
+    for (int w = 0; w < nw; ++w) {
+      const float mw = pm[w * Gq + h];
+      const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      den += pl[w * Gq + h] * f;
+      pm[w * Gq + h] = f;
+    }
+    dst[h * (FD + 2) + FD] = M;
+    dst[h * (FD + 2) + FD + 1] = den;
+  }
+  __syncthreads();
+  for (int e = tid; e < Gq * FD; e += nt) {
+    const int h = e / FD, d = e % FD;
+    float num = 0.f;
+    for (int w = 0; w < nw; ++w) num += part[(w * Gq + h) * FD + d] * pm[w * Gq + h];
+    dst[h * (FD + 2) + d] = num;
+  }
+}
+
+// final merge of ns CTA partials [ns][Gq][FD + 2] (written by other CTAs: read through L2)
+__device__ __forceinline__ void attn_merge_splits(const float* sp, int ns, int Gq, int tid, int nt, float* out_u,
+                                                  float* lse_u) {
+  for (int e = tid; e < Gq * FD; e += nt) {
+    const int h = e / FD, d = e % FD;
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldcg(sp + (s * Gq + h) * (FD + 2) + FD));
+    float num = 0.f, den = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const float* p = sp + (s * Gq + h) * (FD + 2);
+      const float ms = __ldcg(p + FD);
+      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      num += __ldcg(p + d) * f;
+      den += __ldcg(p + FD + 1) * f;
+    }
+    out_u[h * FD + d] = num / den;
+    if (d == 0 && lse_u) lse_u[h] = (M + log2f(den)) * 0.6931471805599453f;
+  }
+}
+
 // pad the dynamic list [n, n rounded up to 16) with token 0 (masked in attention; it keeps
 // staging free of bounds checks).  Any thread may call it once n is known.
 __device__ __forceinline__ void pad_dyn(int32_t* dyn, int n, int tid) {
@@ -706,8 +753,17 @@ struct UnitGeom {
   int64_t L;           // tokens this group scans (a slice of the unit for split units)
   int64_t ncand;       // selectable tokens of the whole unit (L_unit - S)
   int S, keff, mode, nchunks, capw, sstride, nsc;
+  int npass;           // sample passes (long units: more sample chunks, a tighter threshold)
   int64_t flim;        // tokens below flim may be sinks
 };
+
+// Long units take up to 4 sample passes of MAX_SAMPLE_CHUNKS chunks (one per 32K tokens): the
+// sampled threshold's rank error shrinks as 1/sqrt(sample), so the candidate count stays well
+// inside the buffer (one pass at 128K tokens overflowed it in ~20% of units, each a rescan).
+// The extra passes' keys wait for the histogram in the candidate area, past the first 512
+// words (th / tmin may alias them).
+constexpr int kSampleScratchWords = 512;
+constexpr int kMaxSamplePasses = 4;
 
 // sink_idx_u may be null when flim is filled in later (flim_known = 0)
 __device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw, const int32_t* sink_idx_u,
@@ -726,6 +782,12 @@ __device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw,
   else g.mode = 3;
   g.sstride = g.mode == 3 ? max(SSTRIDE_MIN, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
   g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
+  g.npass = 1;
+  if (g.mode == 3 && g.nsc == MAX_SAMPLE_CHUNKS && g.sstride >= 2 * kMaxSamplePasses) {
+    const int by_len = min(kMaxSamplePasses, g.nchunks / 128);
+    const int by_room = 1 + (2 * capw * DW - kSampleScratchWords) / (MAX_SAMPLE_CHUNKS * DT);
+    g.npass = max(1, min(by_len, by_room));
+  }
   g.flim = (S > 0 && flim_known) ? (int64_t)sink_idx_u[S - 1] + 1 : 0;
   return g;
 }
@@ -739,6 +801,37 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
   }
 }
 
+// The extra sample passes of a long unit.  Keys -> xkeys[(p - 1) * 8 + x][DT]; returns the thread's count of valid keys and folds them
+// into smax / smin.
+template <class Key>
+__device__ __forceinline__ int sample_extra_passes(const UnitGeom& g, const uint4* signs, const char* T,
+                                                   const Key& lb, const uint32_t* forced, uint32_t* xkeys, int tid,
+                                                   uint32_t& smax, uint32_t& smin) {
+  const int off = g.sstride / g.npass;
+  int nvx = 0;
+  for (int p = 1; p < g.npass; ++p) {
+    uint4 w[MAX_SAMPLE_CHUNKS];
+#pragma unroll
+    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+      const int64_t t = ((int64_t)x * g.sstride + p * off) * 256 + tid;
+      w[x] = t < g.L ? __ldg(signs + t) : make_uint4(0, 0, 0, 0);
+    }
+    float svx[MAX_SAMPLE_CHUNKS];
+    score_batch(w, lb, T, svx);
+#pragma unroll
+    for (int x = 0; x < MAX_SAMPLE_CHUNKS; ++x) {
+      const int64_t t = ((int64_t)x * g.sstride + p * off) * 256 + tid;
+      uint32_t key = 0;
+      if (t < g.L && !(t < g.flim && forced_bit(forced, t))) key = f32_key(svx[x]);
+      xkeys[((p - 1) * MAX_SAMPLE_CHUNKS + x) * DT + tid] = key;
+      nvx += key != 0;
+      smax = max(smax, key);
+      if (key) smin = min(smin, key);
+    }
+  }
+  return nvx;
+}
+
 // th / tmin: 256 + 256 words of scratch for the threshold histogram (may alias cand: the
 // histogram is rebuilt from the register-resident sample keys for every attempt).
 //
@@ -749,7 +842,9 @@ __device__ __forceinline__ void load_sample(const UnitGeom& g, const uint4* sign
 constexpr int kRetries = 2;
 constexpr double kTauSig = 3.0, kTauAdd = 8.0;   // sample-rank margin: r = e + SIG sqrt(e) + ADD
 
-template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB>
+// XP: the unit may take extra sample passes (g.npass > 1; instantiated for long units only,
+// so the short-unit kernels keep their register allocation)
+template <class Grp, class Xch = NoX, class Key = RepKey, int NBT = NB, bool XP = false>
 __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint4* signs, const char* T,
                                                    const uint32_t* forced, const uint4 (&wsamp)[MAX_SAMPLE_CHUNKS],
                                                    uint32_t* cand, int* th, uint32_t* tmin, Misc* ms,
@@ -760,7 +855,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
   const int capw = g.capw;
   uint32_t* seg = cand + 2 * warp * capw;
   uint32_t sk[MAX_SAMPLE_CHUNKS];
-  int nsv = 0, r = 0;
+  int nsv = 0, nsv0 = 0, r = 0;     // sample keys (all passes / the first pass), sample rank
   uint32_t kmx = 0, kmn = 0;
   if (tid == 0) { ms->maxx = 0; ms->bad = 0; }
   if (g.mode == 3) {
@@ -780,16 +875,29 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
       if (key) smin = min(smin, key);
     }
     nv = warp_sum(nv);
+    // extra passes (long units): chunks offset by p * sstride / npass from the first pass's,
+    // rescored by the scan (not skipped); keys to the scratch words for the histogram
+    int nvx = 0;
+    if constexpr (XP)
+      if (g.npass > 1)
+        nvx = warp_sum(sample_extra_passes(g, signs, T, lb, forced, cand + kSampleScratchWords, tid, smax, smin));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
       smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
     }
-    if (tid == 0) { ms->nsv = 0; ms->tau = 0xFFFFFFFFu; }
+    if (tid == 0) { ms->nsv = 0; if (XP) ms->total = 0; ms->tau = 0xFFFFFFFFu; }
     Grp::sync();
-    if (lane == 0) { atomicAdd(&ms->nsv, nv); atomicMax(&ms->maxx, smax); atomicMin(&ms->tau, smin); }
+    if (lane == 0) {
+      atomicAdd(&ms->nsv, nv);
+      if (XP && nvx) atomicAdd(&ms->total, nvx);
+      atomicMax(&ms->maxx, smax);
+      atomicMin(&ms->tau, smin);
+    }
     Grp::sync();
     nsv = ms->nsv;
+    nsv0 = nsv;
+    if constexpr (XP) nsv += ms->total;
     kmx = ms->maxx;
     kmn = ms->tau;
     xch.sample(nsv, kmx, kmn);            // cluster: the whole unit's sample
@@ -830,6 +938,17 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
             const int b = min(255, (int)((__uint_as_float(unkey_bits(kx)) - fmn) * scale));
             atomicAdd(&th[b], 1);
             atomicMin(&tmin[b], kx);
+          }
+        }
+        if (XP && attempt == 0 && g.npass > 1) {   // the scan overwrites the scratch: first attempt only
+          const uint32_t* xkeys = cand + kSampleScratchWords;
+          for (int i = tid; i < (g.npass - 1) * MAX_SAMPLE_CHUNKS * DT; i += DT) {
+            const uint32_t kx = xkeys[i];
+            if (kx) {
+              const int b = max(0, min(255, (int)((__uint_as_float(unkey_bits(kx)) - fmn) * scale)));
+              atomicAdd(&th[b], 1);
+              atomicMin(&tmin[b], kx);
+            }
           }
         }
         Grp::sync();
@@ -944,12 +1063,17 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     tau_out = tau;
     bool bad = ms->bad != 0;
     xch.counts(total, maxwc, bad);        // cluster: unit totals, any CTA overflowing
+    if (prof && tid == 0) { prof[9] = attempt; prof[10] = total; prof[11] = maxwc; }
     if (!bad && total >= g.keff) return false;
     if (g.mode != 3 || attempt >= kRetries || r < 1) return true;
     // rescale the sample rank from the observed candidate counts and scan again
-    const int r2 = bad ? (int)((double)r * 0.85 * (double)capw / (double)maxwc)
-                       : min(nsv, (int)ceil((double)r * 1.25 * (double)g.keff / (double)max(total, 1)) + 8);
+    int r2 = bad ? (int)((double)r * 0.85 * (double)capw / (double)maxwc)
+                 : min(nsv, (int)ceil((double)r * 1.25 * (double)g.keff / (double)max(total, 1)) + 8);
     if (r2 < 1 || r2 == r) return true;
+    if (XP && attempt == 0 && nsv0 < nsv) {      // retries rank the first pass's keys only
+      r2 = max(1, min(nsv0, (int)((double)r2 * (double)nsv0 / (double)nsv + 0.5)));
+      nsv = nsv0;
+    }
     r = r2;
     Grp::sync();                          // every thread has read ms before it is reset
   }

@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   g.mode = g.keff == 0 ? 0 : (g.keff == g.ncand ? 1 : 3);
   g.sstride = g.mode == 3 ? max(16, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
   g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
+  g.npass = 1;                       // the cluster merges one register-resident sample pass
   {
     int64_t f = S > 0 ? (int64_t)sidx[S - 1] + 1 - t_lo : 0;
     f = f < 0 ? 0 : (f > Ls ? Ls : f);

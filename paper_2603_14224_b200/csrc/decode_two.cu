@@ -53,6 +53,9 @@ struct TwoArgs {
   int32_t* dynl;        // [U][dstride]
   uint32_t* gbits;      // [U][2W] fallback / sorted-selection bitmaps
   uint32_t* gforced;    // [U][W] forced bitmaps when they do not fit shared memory (long units)
+  float* spart;         // [U][nsplit][Gq][FD + 2] split-attention partials (num, M, den), nsplit > 1
+  int32_t* scnt;        // [U] split CTAs done (zeroed by the selection kernel)
+  int nsplit;           // attention CTAs per unit (few units: fill the SMs)
   int64_t L, U;
   int fblocks, S, R, Gq, k, capw, sel_stride, dstride;
   int lut_mode;         // 0: centroid LUT, 1: sign-only LUT
@@ -82,7 +85,7 @@ __device__ __forceinline__ void prefetch_unit(const TwoArgs& a, char* base, int 
 // one unit's selection by one 8-warp group: the unit's queries / centroids were prefetched
 // into the staging area; `next` (or -1) is prefetched once they have been consumed.
 // Returns the dynamic list length (the list is in a.dynl).
-template <class PG, int G>
+template <class PG, int G, bool XP>
 __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u, int64_t next) {
   const int64_t L = a.L;
   const int W = (int)((L + 31) >> 5);
@@ -152,7 +155,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   uint32_t kstar = 0;
   if (mode >= 2) {
     uint32_t tau;
-    fb = produce_candidates<PG, NoX, ColKey, NB>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(), prof)
+    fb = produce_candidates<PG, NoX, ColKey, NB, XP>(g, signs, T, forced, wsamp, cand, th, tmin, ms, tau, NoX(), prof)
              ? 1 : 0;
     if (prof && tid == 0) prof[2] = clock64();
     if (!fb) {
@@ -168,22 +171,25 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   if (prof && tid == 0) prof[3] = clock64();
   if (tid == 0) {
     a.ndyn[u] = ndyn;
+    if (a.nsplit > 1) a.scnt[u] = 0;
     if (a.diag) a.diag[u] = (mode & 3) | (fb ? 4 : 0);
   }
   PG::sync();                       // the group's shared memory is reused by its next unit
   return ndyn;
 }
 
-template <class PG, int G>
+template <class PG, int G, bool XP>
 __device__ __forceinline__ void select_group(const TwoArgs& a, char* sm) {
   prefetch_unit(a, sm + TBL_BYTES + G * a.g_bytes, PG::tid(), (int64_t)blockIdx.x + (int64_t)G * gridDim.x);
   for (int it = 0;; ++it) {
     const int64_t u = (int64_t)blockIdx.x + (int64_t)(2 * it + G) * gridDim.x;
     if (u >= a.U) break;
-    select_unit<PG, G>(a, sm, u, u + 2 * gridDim.x);
+    select_unit<PG, G, XP>(a, sm, u, u + 2 * gridDim.x);
   }
 }
 
+// XP: long units (>= 64K tokens) with extra sample passes
+template <bool XP>
 __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
   // the attention grid may be scheduled onto SMs as this grid's CTAs retire: it attends the
@@ -191,8 +197,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // group from a value the compiler can prove warp-uniform (uniform-datapath table base)
   const int grp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 8), 0);
-  if (grp == 0) select_group<SG0, 0>(a, sm);
-  else select_group<SG1, 1>(a, sm);
+  if (grp == 0) select_group<SG0, 0, XP>(a, sm);
+  else select_group<SG1, 1, XP>(a, sm);
 }
 
 // ---------------------------------------------------------------- attention
@@ -204,10 +210,16 @@ constexpr int ATT_STAGES = 2;                       // cp.async staging buffers 
 // One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
 // indices come straight from global memory (L2), so the only CTA-wide barriers are the
 // two around the partial merge.
-template <int NW, bool R16>
-__device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u) {
+// The unit's rows are dealt to the nsplit x NW warps of its CTAs (CTA part `sp`): with few
+// units (C3) one CTA per unit would leave most warp slots idle.  Each CTA merges its warps;
+// the last CTA of the unit to finish (counter) merges the CTA partials in split order, so
+// the result does not depend on which CTA finishes last.
+template <int NW, bool R16, bool SPLIT>
+__device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u, int sp) {
   constexpr int NT = 32 * NW;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nwa = SPLIT ? NW * a.nsplit : NW;      // warps attending the unit
+  const int warp = sp * NW + (tid >> 5);           // this warp among them
   const int64_t cu = a.umap ? (int64_t)__ldg(a.umap + u) : u;    // the unit's cache
   const int S = a.S, R = a.rn ? __ldg(a.rn + cu) : a.R, Gq = a.Gq;
   const int32_t* dyn = a.dynl + u * a.dstride;
@@ -219,31 +231,48 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ffrag_u) + 128 * i));
   for (int i = tid; i < a.dstride / 32; i += NT)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(dyn) + 128 * i));
+  const int lw = tid >> 5;
   Attn A;
   attn_init_g(A, a.q + u * Gq * FD, a.alpha32 + cu * FD, Gq, lane);
-  attn_forced(A, ffrag_u, nf, warp, NW, lane);
+  attn_forced(A, ffrag_u, nf, warp, nwa, lane);
   asm volatile("griddepcontrol.wait;" ::: "memory");   // the selection grid is complete
   const int ndyn = __ldg(a.ndyn + u);
   if constexpr (R16)
-    attn_dynamic16<ATT_STAGES>(A, a.recs + cu * a.L * FREC16, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
-                               stage + warp * ATT_STAGES * STAGE16_BYTES, lane);
+    attn_dynamic16<ATT_STAGES>(A, a.recs + cu * a.L * FREC16, dyn, ndyn, (warp - nbf % nwa + nwa) % nwa, nwa,
+                               stage + lw * ATT_STAGES * STAGE16_BYTES, lane);
   else
-    attn_dynamic<ATT_STAGES>(A, a.recs + cu * a.L * FREC, dyn, ndyn, (warp - nbf % NW + NW) % NW, NW,
-                             stage + warp * ATT_STAGES * STAGE_BYTES, lane);
+    attn_dynamic<ATT_STAGES>(A, a.recs + cu * a.L * FREC, dyn, ndyn, (warp - nbf % nwa + nwa) % nwa, nwa,
+                             stage + lw * ATT_STAGES * STAGE_BYTES, lane);
   __syncthreads();
   float* part = reinterpret_cast<float*>(stage);
   float* pm = part + NW * Gq * FD;
   float* pl = pm + NW * Gq;
-  attn_write_partial(A, part, pm, pl, warp, Gq, lane);
+  attn_write_partial(A, part, pm, pl, lw, Gq, lane);
   __syncthreads();
-  attn_merge<Cta256>(part, pm, pl, NW, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+  if constexpr (!SPLIT) {
+    attn_merge<Cta256>(part, pm, pl, NW, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+  } else {
+    // this CTA's partial (num, M, den per head) -> global; the last CTA merges
+    float* sp_u = a.spart + u * a.nsplit * Gq * (FD + 2);
+    attn_merge_partial(part, pm, pl, NW, Gq, tid, NT, sp_u + sp * Gq * (FD + 2));
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (tid == 0) last = atomicAdd(a.scnt + u, 1) == a.nsplit - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    attn_merge_splits(sp_u, a.nsplit, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+  }
 }
 
-// R16: 16-bit records (512 B per token, stored fp16 fragments; 64 KB of staging per CTA)
-template <bool R16>
+// R16: 16-bit records (512 B per token, stored fp16 fragments; 64 KB of staging per CTA);
+// SPLIT: nsplit CTAs per unit
+template <bool R16, bool SPLIT>
 __global__ void __launch_bounds__(ATT_THREADS, ATT_CTAS_PER_SM) decode_attend_kernel(const __grid_constant__ TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
-  attend_unit<ATT_WARPS, R16>(a, sm, blockIdx.x);
+  if constexpr (SPLIT) attend_unit<ATT_WARPS, R16, true>(a, sm, blockIdx.x / a.nsplit, (int)(blockIdx.x % a.nsplit));
+  else attend_unit<ATT_WARPS, R16, false>(a, sm, blockIdx.x, 0);
 }
 
 // ---------------------------------------------------------------- host side
@@ -287,10 +316,20 @@ int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16) {
   return std::max(ATT_WARPS * ATT_STAGES * (rec16 ? STAGE16_BYTES : STAGE_BYTES), ATT_WARPS * Gq * (FD + 2) * 4);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+// attention CTAs per unit: enough CTAs for four per SM when the units alone are too few
+constexpr int kMaxSplit = 8;
+constexpr int64_t kSplitUnits = 1024;   // workspace for split partials up to this many units
+static int two_nsplit(int64_t U, int nsm) {
+  if (U >= (int64_t)ATT_CTAS_PER_SM * nsm || U > kSplitUnits) return 1;
+  return (int)std::min<int64_t>(kMaxSplit, ((int64_t)ATT_CTAS_PER_SM * nsm + U - 1) / U);
+}
+static size_t split_bytes(int64_t U) {
+  return U > kSplitUnits ? 0 : a256((size_t)U * kMaxSplit * 8 * (FD + 2) * 4) + a256((size_t)U * 4);
+}
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S) {
   const int64_t W = (L + 31) / 32;
   return 256 + a256((size_t)U * 4) + a256((size_t)U * two_dstride(L, k, S) * 4) + a256((size_t)U * 2 * W * 4) +
-         (size_t)U * W * 4;
+         a256((size_t)U * W * 4) + split_bytes(U);
 }
 
 cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const float* cent32, const float* alpha32,
@@ -312,21 +351,29 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   a.gbits = reinterpret_cast<uint32_t*>(ws);
   ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
   a.gforced = reinterpret_cast<uint32_t*>(ws);
+  ws += a256((size_t)U * ((L + 31) / 32) * 4);
+  a.nsplit = two_nsplit(U, nsm);
+  if (a.nsplit > 1) {
+    a.spart = reinterpret_cast<float*>(ws);
+    a.scnt = reinterpret_cast<int32_t*>(ws + a256((size_t)U * kMaxSplit * 8 * (FD + 2) * 4));
+  }
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
   a.lut_mode = lut_mode;
   const int smem_s = TBL_BYTES + 2 * a.g_bytes;
-  cudaError_t e = cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
+  auto select = (L + 255) / 256 >= 256 ? decode_select_kernel<true> : decode_select_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(select, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(nsm, (U + 1) / 2);
-  decode_select_kernel<<<grid, SEL_THREADS, smem_s, st>>>(a);
+  select<<<grid, SEL_THREADS, smem_s, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int smem_a = two_attend_smem_bytes(L, k, S, Gq, rec16);
-  auto attend = rec16 ? decode_attend_kernel<true> : decode_attend_kernel<false>;
+  auto attend = a.nsplit > 1 ? (rec16 ? decode_attend_kernel<true, true> : decode_attend_kernel<false, true>)
+                             : (rec16 ? decode_attend_kernel<true, false> : decode_attend_kernel<false, false>);
   e = cudaFuncSetAttribute(attend, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)U);
+  cfg.gridDim = dim3((unsigned)(U * a.nsplit));
   cfg.blockDim = dim3(ATT_THREADS);
   cfg.dynamicSmemBytes = (size_t)smem_a;
   cfg.stream = st;

@@ -1,7 +1,7 @@
 """Full-size checks of the benchmarked workloads on the decode path bench.py times:
 C2 (BASELINE.json configs[1], the headline: 4096 units x 32K tokens, top-k 2048, auto ->
 the two-kernel path), C4 (Qwen2.5-7B: 7168 units x 8K, top-k 1024, GQA 7, two kernels) and
-C3 (Llama-3.1-8B: 256 units x 128K, top-k 4096, one CTA per unit).
+C3 (Llama-3.1-8B: 256 units x 128K, top-k 4096, two kernels with split attention).
 
   * every unit: size-independent properties of the selection (exactly 64 + k sorted,
     unique indices, the 64 sinks first, no exact-fallback) and finite outputs;
@@ -43,7 +43,7 @@ def full_run(config):
     return _FULL[config]
 
 
-@pytest.mark.parametrize("config,path", [("c2", 4), ("c4", 4), ("c3", 1)])
+@pytest.mark.parametrize("config,path", [("c2", 4), ("c4", 4), ("c3", 4)])
 def test_full_scale(config, path):
     layers, batch, kvh, gq, L, k, _ = bench.CONFIGS[config]
     units = layers * batch * kvh
@@ -81,8 +81,8 @@ def test_full_scale(config, path):
 
 
 # the auto path each rank's shard runs at N GPUs (units per rank decide it, capi.cu)
-SHARD_PATHS = {("c2", 2): 4, ("c2", 4): 4, ("c2", 8): 4, ("c4", 2): 4, ("c4", 4): 4, ("c4", 8): 4,
-               ("c3", 2): 3, ("c3", 4): 3, ("c3", 8): 3}
+SHARD_PATHS = {("c2", 2): 4, ("c2", 4): 4, ("c2", 8): 1, ("c4", 2): 4, ("c4", 4): 4, ("c4", 8): 4,
+               ("c3", 2): 1, ("c3", 4): 3, ("c3", 8): 3}
 
 
 @pytest.mark.parametrize("config", ["c2", "c4", "c3"])

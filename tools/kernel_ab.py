@@ -10,6 +10,7 @@ import bench  # noqa: E402
 from paper_2603_14224_b200 import batch as B  # noqa: E402
 
 dev = torch.device("cuda", 0)
+NIT = int(os.environ.get("NIT", "30"))
 CAP = int(os.environ.get("CAP", "0"))   # candidate buffer entries (0 = the library's choice)
 ONLY = [int(x) for x in os.environ["KERNELS"].split(",")] if "KERNELS" in os.environ else None
 cfgs = sys.argv[1:] or ["c2", "c3", "c4"]
@@ -25,11 +26,11 @@ for name in cfgs:
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(10):
+            for _ in range(NIT):
                 B.decode_step(cb, q, k, out=out, kernel=kern, cap=CAP)
             e1.record()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 10
+            ms = e0.elapsed_time(e1) / NIT
             gb = bench.algo_bytes_per_unit(L, k, gq) * units / 1e9
             print(f"{name} kernel {kern} cap {CAP}: {ms:.3f} ms  {gb / ms * 1e3:.0f} GB/s")
         except Exception as ex:  # noqa: BLE001

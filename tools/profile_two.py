@@ -33,8 +33,16 @@ _lib.call("sikv_debug_set_decode_profile", None)
 c = clk.cpu().numpy().astype(np.float64)
 d = c[:, 2] - c[:, 1]
 print("  score+cand deciles", np.percentile(d, [10, 50, 80, 90, 95, 99, 100]).astype(int).tolist())
-for n, i, j in [("wait inputs", 0, 4), ("bitmap+qbar+LUT", 4, 5), ("pair table", 5, 1), ("sample score", 1, 7),
+grid = min(148, (a.units + 1) // 2)
+grp = (np.arange(a.units) // grid) % 2
+rows = [("wait inputs", 0, 4), ("bitmap+qbar+LUT", 4, 5), ("pair table", 5, 1), ("sample score", 1, 7),
                 ("tau", 7, 8), ("scan (after tau)", 8, 2), ("setup+table", 0, 1), ("score+cand", 1, 2),
-                ("select+emit", 2, 3), ("unit total", 0, 3)]:
+                ("select+emit", 2, 3), ("unit total", 0, 3)]
+for n, i, j in rows:
     d = c[:, j] - c[:, i]
-    print(f"  {n:12s} mean {d.mean():9.0f}  p50 {np.median(d):9.0f}  max {d.max():9.0f}")
+    g0, g1 = d[grp == 0].mean(), d[grp == 1].mean()
+    print(f"  {n:16s} mean {d.mean():9.0f}  p50 {np.median(d):9.0f}  max {d.max():9.0f}   group0 {g0:9.0f} group1 {g1:9.0f}")
+att = clk.cpu().numpy()[:, 9]
+print("  scan attempts (0 = first scan sufficed):", {int(v): int((att == v).sum()) for v in np.unique(att)})
+tot, mw = clk.cpu().numpy()[:, 10], clk.cpu().numpy()[:, 11]
+print(f"  candidates per unit: mean {tot.mean():.0f} min {tot.min()} max {tot.max()}; max per-warp segment {mw.max()}")
