@@ -259,12 +259,16 @@ __device__ __forceinline__ uint32_t k_dequant2(uint32_t w, __half2 qs2, uint32_t
 }
 
 // ---------------------------------------------------------------- sparse attention
-// One warp's flash-decode state for the unit's GQA group: q~ fragments (rows = heads),
-// O^T accumulators (M = 128 channels as 8 m-tiles, N = 8 heads), running max / sum of head g.
+// One warp's flash-decode state for the unit's GQA group.  QK^T runs as S^T = K^ q~^T (M = 16
+// tokens of a block, N = 8 heads, K = channels): q~ is the B operand (qa[s] = b0, b1 of k-step
+// s: head g, channels 16 s + 2 t4 (+ 8)) and a thread's scores are (tokens g, g + 8) x (heads
+// 2 t4, 2 t4 + 1).  PV runs as O^T = V^T P (M = 128 channels as 8 m-tiles, N = 8 heads), so a
+// thread's O accumulators belong to the same two heads: mrun / lrun per head h0 = 2 t4,
+// h1 = 2 t4 + 1 (lrun: this thread's tokens only, summed over the g lanes at the end).
 struct Attn {
   uint32_t qa[8][2];
   float o[8][4];
-  float mrun, lrun;
+  float mrun[2], lrun[2];
 };
 
 // q~ = q * alpha-hat straight from global memory (each warp on its own, no barrier)
@@ -285,8 +289,8 @@ __device__ __forceinline__ void attn_init_g(Attn& A, const float* __restrict__ q
     }
 #pragma unroll
   for (int m = 0; m < 8; ++m) A.o[m][0] = A.o[m][1] = A.o[m][2] = A.o[m][3] = 0.f;
-  A.mrun = -INFINITY;
-  A.lrun = 0.f;
+  A.mrun[0] = A.mrun[1] = -INFINITY;
+  A.lrun[0] = A.lrun[1] = 0.f;
 }
 
 __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float* ahat, int Gq, int lane) {
@@ -302,8 +306,8 @@ __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float*
     }
 #pragma unroll
   for (int m = 0; m < 8; ++m) A.o[m][0] = A.o[m][1] = A.o[m][2] = A.o[m][3] = 0.f;
-  A.mrun = -INFINITY;
-  A.lrun = 0.f;
+  A.mrun[0] = A.mrun[1] = -INFINITY;
+  A.lrun[0] = A.lrun[1] = 0.f;
 }
 
 constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;   // log2(e) / sqrt(128)
@@ -318,41 +322,47 @@ __device__ __forceinline__ float ex2(float x) {
 // (w & mask_i) | magic_i is the half 2^(10-2i) + code exactly
 __host__ __device__ constexpr uint32_t kMagic(int i) { return ((25u - 2u * (uint32_t)i) << 10) * 0x00010001u; }
 
-// online softmax update + P V for one 16-token block (scores for head g in sacc); rows at
-// block offsets >= rem are padding
+// online softmax update + P V for one 16-token block: sacc = S^T fragment (tokens g, g + 8 x
+// heads 2 t4, 2 t4 + 1); rows at block offsets >= rem are padding
 template <typename VFrag>
-__device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][4], int rem, int lane,
+__device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[4], int rem, int lane,
                                                 VFrag&& vfrag) {
-  const int t4 = lane & 3;
+  const int g = lane >> 2;
   float x[4];
-  x[0] = 2 * t4 < rem ? sacc[0][0] * kSoftmaxScale : -INFINITY;
-  x[1] = 2 * t4 + 1 < rem ? sacc[0][1] * kSoftmaxScale : -INFINITY;
-  x[2] = 2 * t4 + 8 < rem ? sacc[1][0] * kSoftmaxScale : -INFINITY;
-  x[3] = 2 * t4 + 9 < rem ? sacc[1][1] * kSoftmaxScale : -INFINITY;
-  float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
-  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+  x[0] = g < rem ? sacc[0] * kSoftmaxScale : -INFINITY;       // token g, head h0
+  x[1] = g < rem ? sacc[1] * kSoftmaxScale : -INFINITY;       // token g, head h1
+  x[2] = g + 8 < rem ? sacc[2] * kSoftmaxScale : -INFINITY;   // token g + 8, head h0
+  x[3] = g + 8 < rem ? sacc[3] * kSoftmaxScale : -INFINITY;   // token g + 8, head h1
+  float bm0 = fmaxf(x[0], x[2]), bm1 = fmaxf(x[1], x[3]);
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+  }
   // lazy rescale: the reference max only moves when the block max exceeds it by more than
   // 2^8 (exp2 domain), so P <= 256 (exact range in fp16) and most blocks skip the O rescale
-  const float mnew = bm > A.mrun + kLazyRescale ? bm : A.mrun;
-  const float fac = ex2(A.mrun - mnew);
-  A.mrun = mnew;
-  const __half2 p01 = __floats2half2_rn(ex2(x[0] - mnew), ex2(x[1] - mnew));
-  const __half2 p23 = __floats2half2_rn(ex2(x[2] - mnew), ex2(x[3] - mnew));
-  const float2 f01 = __half22float2(p01), f23 = __half22float2(p23);
-  A.lrun = A.lrun * fac + ((f01.x + f01.y) + (f23.x + f23.y));
-  if (!__all_sync(0xffffffffu, fac == 1.0f)) {   // the running max moved for some head
-    const float fa = __shfl_sync(0xffffffffu, fac, 8 * t4);
-    const float fb = __shfl_sync(0xffffffffu, fac, 8 * t4 + 4);
+  const float mn0 = bm0 > A.mrun[0] + kLazyRescale ? bm0 : A.mrun[0];
+  const float mn1 = bm1 > A.mrun[1] + kLazyRescale ? bm1 : A.mrun[1];
+  const float fa = ex2(A.mrun[0] - mn0), fb = ex2(A.mrun[1] - mn1);
+  A.mrun[0] = mn0;
+  A.mrun[1] = mn1;
+  const __half2 p0 = __floats2half2_rn(ex2(x[0] - mn0), ex2(x[1] - mn1));   // token g: heads h0, h1
+  const __half2 p1 = __floats2half2_rn(ex2(x[2] - mn0), ex2(x[3] - mn1));   // token g + 8
+  const float2 f0 = __half22float2(p0), f1 = __half22float2(p1);
+  A.lrun[0] = A.lrun[0] * fa + (f0.x + f1.x);
+  A.lrun[1] = A.lrun[1] * fb + (f0.y + f1.y);
+  if (!__all_sync(0xffffffffu, fa == 1.0f && fb == 1.0f)) {   // the running max moved for some head
 #pragma unroll
     for (int m = 0; m < 8; ++m) { A.o[m][0] *= fa; A.o[m][1] *= fb; A.o[m][2] *= fa; A.o[m][3] *= fb; }
   }
+  // P as the PV B operand (tokens 2 t4, 2 t4 + 1 (+ 8) x head g): one transpose per 8 tokens
+  const uint32_t pb0 = movmatrix_trans(h2u(p0)), pb1 = movmatrix_trans(h2u(p1));
 #pragma unroll
   for (int mp = 0; mp < 4; ++mp) {
     uint32_t v[2][4];      // [m - 2mp][a0..a3]
     vfrag(mp, v);
-    mma16816(A.o[2 * mp], v[0][0], v[0][1], v[0][2], v[0][3], h2u(p01), h2u(p23));
-    mma16816(A.o[2 * mp + 1], v[1][0], v[1][1], v[1][2], v[1][3], h2u(p01), h2u(p23));
+    mma16816(A.o[2 * mp], v[0][0], v[0][1], v[0][2], v[0][3], pb0, pb1);
+    mma16816(A.o[2 * mp + 1], v[1][0], v[1][1], v[1][2], v[1][3], pb0, pb1);
   }
 }
 
@@ -360,14 +370,14 @@ __device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[2][
 // (FBLK_WORDS per 16-row block); this warp takes blocks wi, wi + nw, ... of [0, nbf)
 __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, int nf, int wi, int nw, int lane) {
   const int nbf = (nf + 15) >> 4;
-  const int t4 = lane & 3;
+  const int g = lane >> 2;
   for (int blk = wi; blk < nbf; blk += nw) {
     const int base = blk * 16;
     const uint32_t* fb = ffrag_u + (int64_t)blk * FBLK_WORDS;
     const uint4* fk = reinterpret_cast<const uint4*>(fb + lane * 32);
     const uint4* fv = fk + 32 * 8;
-    const float2 sc0 = __ldg(reinterpret_cast<const float2*>(fb + 2 * 32 * 32) + t4);       // rows 2t4, 2t4 + 1
-    const float2 sc1 = __ldg(reinterpret_cast<const float2*>(fb + 2 * 32 * 32 + 8) + t4);   // rows 8 + 2t4, + 1
+    const float sc0 = __ldg(reinterpret_cast<const float*>(fb + 2 * 32 * 32) + g);       // row g
+    const float sc1 = __ldg(reinterpret_cast<const float*>(fb + 2 * 32 * 32) + 8 + g);   // row g + 8
     uint32_t kwd[32], vwd[32];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -379,16 +389,11 @@ __device__ __forceinline__ void attn_forced(Attn& A, const uint32_t* ffrag_u, in
       const uint4 t = __ldg(fv + i);
       vwd[4 * i] = t.x; vwd[4 * i + 1] = t.y; vwd[4 * i + 2] = t.z; vwd[4 * i + 3] = t.w;
     }
-    float sacc[2][4];
+    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-      for (int s = 0; s < 8; ++s)
-        mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, kwd[nt * 16 + 2 * s], kwd[nt * 16 + 2 * s + 1]);
-    }
-    sacc[0][0] *= sc0.x; sacc[0][1] *= sc0.y; sacc[0][2] *= sc0.x; sacc[0][3] *= sc0.y;
-    sacc[1][0] *= sc1.x; sacc[1][1] *= sc1.y; sacc[1][2] *= sc1.x; sacc[1][3] *= sc1.y;
+    for (int s = 0; s < 8; ++s)
+      mma16816(sacc, kwd[2 * s], kwd[16 + 2 * s], kwd[2 * s + 1], kwd[16 + 2 * s + 1], A.qa[s][0], A.qa[s][1]);
+    sacc[0] *= sc0; sacc[1] *= sc0; sacc[2] *= sc1; sacc[3] *= sc1;
     attn_softmax_pv(A, sacc, nf - base, lane, [&](int mp, uint32_t (&v)[2][4]) {
 #pragma unroll
       for (int mm = 0; mm < 2; ++mm)
@@ -407,24 +412,26 @@ constexpr int P8 = 8 * FREC;
 
 // QK^T, online softmax and PV of one staged 16-token block (rem = valid rows from its start)
 __device__ __forceinline__ void attn_block(Attn& A, const char* sb, const BlkOffs& o, int rem, int lane) {
-  float sacc[2][4];
+  float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+  uint32_t kw[2][4], par[2][4];     // tokens g, g + 8
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const uint4 k4 = *reinterpret_cast<const uint4*>(sb + o.k4 + nt * P8);
     const uint4 kp = *reinterpret_cast<const uint4*>(sb + o.kp + nt * P8);
-    const uint32_t kw[4] = {k4.x, k4.y, k4.z, k4.w};
-    const uint32_t par[4] = {kp.x, kp.y, kp.z, kp.w};
-    sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+    kw[nt][0] = k4.x; kw[nt][1] = k4.y; kw[nt][2] = k4.z; kw[nt][3] = k4.w;
+    par[nt][0] = kp.x; par[nt][1] = kp.y; par[nt][2] = kp.z; par[nt][3] = kp.w;
+  }
 #pragma unroll
-    for (int grp = 0; grp < 4; ++grp) {
-      const __half2 qs2 = u2h(prmt(par[grp], par[grp], 0x1010u));
-      const uint32_t zp2 = prmt(par[grp], par[grp], 0x3232u);
-      // k-steps s = 2 grp (bytes 0, 1 of word grp) and 2 grp + 1 (bytes 2, 3)
-      mma16816(sacc[nt], A.qa[2 * grp][0], 0u, A.qa[2 * grp][1], 0u, k_dequant2<0>(kw[grp], qs2, zp2),
-               k_dequant2<1>(kw[grp], qs2, zp2));
-      mma16816(sacc[nt], A.qa[2 * grp + 1][0], 0u, A.qa[2 * grp + 1][1], 0u, k_dequant2<2>(kw[grp], qs2, zp2),
-               k_dequant2<3>(kw[grp], qs2, zp2));
-    }
+  for (int grp = 0; grp < 4; ++grp) {
+    const __half2 qa2 = u2h(prmt(par[0][grp], par[0][grp], 0x1010u)), qb2 = u2h(prmt(par[1][grp], par[1][grp], 0x1010u));
+    const uint32_t za2 = prmt(par[0][grp], par[0][grp], 0x3232u), zb2 = prmt(par[1][grp], par[1][grp], 0x3232u);
+    // k-steps s = 2 grp (bytes 0, 1 of word grp) and 2 grp + 1 (bytes 2, 3); A rows g / g + 8
+    mma16816(sacc, k_dequant2<0>(kw[0][grp], qa2, za2), k_dequant2<0>(kw[1][grp], qb2, zb2),
+             k_dequant2<1>(kw[0][grp], qa2, za2), k_dequant2<1>(kw[1][grp], qb2, zb2), A.qa[2 * grp][0],
+             A.qa[2 * grp][1]);
+    mma16816(sacc, k_dequant2<2>(kw[0][grp], qa2, za2), k_dequant2<2>(kw[1][grp], qb2, zb2),
+             k_dequant2<3>(kw[0][grp], qa2, za2), k_dequant2<3>(kw[1][grp], qb2, zb2), A.qa[2 * grp + 1][0],
+             A.qa[2 * grp + 1][1]);
   }
   // V words and params of tokens 2t4, 2t4+1, 2t4+8, 2t4+9
   uint32_t vw[4];
@@ -545,22 +552,21 @@ constexpr int STAGE16_BYTES = 16 * FREC16;     // one 16-token block
 // QK^T, online softmax and PV of one staged 16-bit block (rem = valid rows from its start)
 __device__ __forceinline__ void attn_block16(Attn& A, uint32_t sb, int rem, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
-  float sacc[2][4];
+  float sacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int nt = 0; nt < 2; ++nt) {
-    const int j = g + 8 * nt;
-    uint32_t kw[16];
+  for (int i = 0; i < 4; ++i) {      // k-steps 2i, 2i + 1
+    uint32_t kw[2][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int nt = 0; nt < 2; ++nt) {
+      const int j = g + 8 * nt;
       uint4 t;
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
                    : "r"(sb + (uint32_t)(j * FREC16 + 16 * sw16(j, 4 * t4 + i))));
-      kw[4 * i] = t.x; kw[4 * i + 1] = t.y; kw[4 * i + 2] = t.z; kw[4 * i + 3] = t.w;
+      kw[nt][0] = t.x; kw[nt][1] = t.y; kw[nt][2] = t.z; kw[nt][3] = t.w;
     }
-    sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) mma16816(sacc[nt], A.qa[s][0], 0u, A.qa[s][1], 0u, kw[2 * s], kw[2 * s + 1]);
+    mma16816(sacc, kw[0][0], kw[1][0], kw[0][1], kw[1][1], A.qa[2 * i][0], A.qa[2 * i][1]);
+    mma16816(sacc, kw[0][2], kw[1][2], kw[0][3], kw[1][3], A.qa[2 * i + 1][0], A.qa[2 * i + 1][1]);
   }
   // V words of tokens 2t4, 2t4 + 1, 2t4 + 8, 2t4 + 9: word m of chunk g = (ch 16m + g, 16m + g + 8)
   uint32_t vw[4][8];
@@ -636,10 +642,16 @@ __device__ __forceinline__ void attn_dynamic16(Attn& A, const uint8_t* recs_u, c
 __device__ __forceinline__ void attn_write_partial(const Attn& A, float* part, float* pm, float* pl, int wi,
                                                    int Gq, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
-  float l = A.lrun;
-  l += __shfl_xor_sync(0xffffffffu, l, 1);
-  l += __shfl_xor_sync(0xffffffffu, l, 2);
-  if (t4 == 0 && g < Gq) { pm[wi * Gq + g] = A.mrun; pl[wi * Gq + g] = l; }
+  float l0 = A.lrun[0], l1 = A.lrun[1];
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  if (g == 0) {
+    if (2 * t4 < Gq) { pm[wi * Gq + 2 * t4] = A.mrun[0]; pl[wi * Gq + 2 * t4] = l0; }
+    if (2 * t4 + 1 < Gq) { pm[wi * Gq + 2 * t4 + 1] = A.mrun[1]; pl[wi * Gq + 2 * t4 + 1] = l1; }
+  }
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     const int h0 = 2 * t4, h1 = 2 * t4 + 1, d0 = 16 * m + g, d1 = d0 + 8;
