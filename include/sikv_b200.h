@@ -110,11 +110,15 @@ int sikv_decode_default_cap(int64_t tokens, int k, int sinks);
 size_t sikv_decode_workspace_bytes(int64_t units, int64_t tokens);
 /* workspace for every decode kernel at top-k k (the two-kernel path stores the dynamic lists) */
 size_t sikv_decode_workspace_bytes_k(int64_t units, int64_t tokens, int k, int sinks);
-/* kernel: 0 = auto (two kernels when units >= 2 x SMs, a workspace of
- * sikv_decode_workspace_bytes_k is given and the selection kernel fits shared memory; a
- * thread-block cluster per unit for few long units; else one CTA per unit),
+/* kernel: 0 = auto (a thread-block cluster per unit for few long units: units <= SMs / 2 and
+ * tokens >= 16K; one CTA per unit while the units fill at most one wave of the SMs, or two
+ * waves when two CTAs fit an SM; else the two-kernel path, given a workspace of
+ * sikv_decode_workspace_bytes_k and a selection kernel that fits shared memory; its attention
+ * kernel splits each unit over several CTAs when the units are fewer than four per SM),
  * 1 = one CTA per unit, 3 = split units across a cluster, 4 = force the two-kernel path
  * (selection, then attention).
+ * sink_idx [U][sinks] int32: each unit's sink token indices in ascending order (as
+ * select_sink_tokens / sikv_window_sinks return them); the kernels rely on the order.
  * Recent rows: recent_n (nullable) [U] int32 = recent rows of each unit (forced, scored
  * -inf: cache.py:290-309; sel then ends with tokens + 0 .. recent_n[u] - 1); recent = their
  * maximum (or the count of every unit when recent_n is NULL).

@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:decode -c 12 
     > gpurun_out/bench_under_ncu_${CFG}.log 2>&1
 # 2) full capture of one decode step at the bench workload (after the warm-up steps; the
 #    two-kernel path launches decode_select_kernel + decode_attend_kernel per step)
-NK=$(python -c "import sys; sys.path.insert(0, '.'); import bench; c = bench.CONFIGS['${CFG}']; print(2 if c[0] * c[1] * c[2] >= 296 else 1)")
+NK=$(python -c "import sys; sys.path.insert(0, '.'); import bench; c = bench.CONFIGS['${CFG}']; print(1 if c[0] * c[1] * c[2] < 64 else 2)")   # two-kernel path: select + attend per step
 ncu --set full --import-source on --clock-control none -k regex:decode -s $((3 * NK)) -c ${NK} \
     -o gpurun_out/decode_${CFG} python bench.py --config ${CFG} --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_full_${CFG}.log 2>&1

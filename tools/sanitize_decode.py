@@ -42,3 +42,13 @@ for kern in (1, 3, 4):
     B.decode_step(cbw, qw, 200, with_selection=True, kernel=kern)
 torch.cuda.synchronize()
 print("window sinks / direct / 1-bit ok", flush=True)
+# 16-bit records (two-kernel path, split attention at 8 units)
+cb16 = B.prefill_batch(K, V, sink_count=64, bits=16)
+B.decode_step(cb16, qw, 200, with_selection=True, kernel=4)
+torch.cuda.synchronize()
+print("16-bit records ok", flush=True)
+# a long unit: extra sample passes (>= 64K tokens) on the two-kernel path, split attention
+cbl, ql = bench.build_cache(range(8), 65536, 4, 78, dev)
+B.decode_step(cbl, ql, 2048, with_selection=True, kernel=4)
+torch.cuda.synchronize()
+print("long units ok", flush=True)
