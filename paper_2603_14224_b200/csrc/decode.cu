@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(DT, 2) decode_step_kernel(DecodeArgs a) {
   const uint4* signs = reinterpret_cast<const uint4*>(a.signs + cu * L * FSIGN);
   const int S = a.S, R = a.rn ? a.rn[cu] : a.R, Gq = a.Gq;
   const int W = (int)((L + 31) >> 5);
-  long long* prof = g_prof ? g_prof + u * 12 : nullptr;
+  long long* prof = g_prof ? g_prof + u * 16 : nullptr;
 #define PROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
   PROF(0);
   const UnitGeom g = unit_geom(L, S, a.k, a.capw, a.sink_idx + cu * S);

@@ -1278,12 +1278,15 @@ template <class Grp, int NBINT = NBIN>
 __device__ __forceinline__ int select_emit_candidates(const UnitGeom& g, const uint32_t* forced, const uint32_t* cand,
                                                       const int* wcnt, uint32_t maxx, uint32_t tau, int* hist,
                                                       Misc* ms, uint32_t* gt, uint32_t* eq, int32_t* dyn,
-                                                      int32_t* sel_u, int R, int32_t* sel_count_u, uint32_t& kstar) {
+                                                      int32_t* sel_u, int R, int32_t* sel_count_u, uint32_t& kstar,
+                                                      long long* prof = nullptr) {
   uint32_t xk;
   int need_eq;
   kth_from_candidates<Grp, NoX, NBINT>(g, cand, wcnt, maxx, hist, ms, xk, need_eq);
+  if (prof && Grp::tid() == 0) prof[12] = clock64();
   kstar = xk + tau;
   int ndyn = emit_from_segments<Grp>(g, cand, wcnt, xk, need_eq, dyn, ms);
+  if (prof && Grp::tid() == 0) prof[13] = clock64();
   if (ndyn < 0 || sel_u || sel_count_u) {
     int eq_count;
     bitmaps_from_candidates<Grp>(g, cand, wcnt, xk, ms, gt, eq, eq_count);

@@ -103,7 +103,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
   uint32_t* cand = reinterpret_cast<uint32_t*>(base + a.g_cand);
   const float* pre_q = reinterpret_cast<const float*>(base + a.g_pre);   // [8][128]
   const float4* pre_c = reinterpret_cast<const float4*>(pre_q + Gq * FD);  // [512]
-  long long* prof = g_prof_two ? g_prof_two + u * 12 : nullptr;
+  long long* prof = g_prof_two ? g_prof_two + u * 16 : nullptr;
   if (prof && tid == 0) prof[0] = clock64();
   const int64_t cu = a.umap ? (int64_t)__ldg(a.umap + u) : u;    // the unit's cache
   const uint4* signs = reinterpret_cast<const uint4*>(a.signs + cu * L * FSIGN);
@@ -160,7 +160,7 @@ __device__ __forceinline__ int select_unit(const TwoArgs& a, char* sm, int64_t u
     if (prof && tid == 0) prof[2] = clock64();
     if (!fb) {
       ndyn = select_emit_candidates<PG, SEL_NBIN>(g, forced, cand, ms->wcnt, ms->maxx, tau, hist, ms, gt, eq, dyn, sel_u,
-                                        a.rn ? __ldg(a.rn + cu) : a.R, sel_count_u, kstar);
+                                        a.rn ? __ldg(a.rn + cu) : a.R, sel_count_u, kstar, prof);
     } else {
       produce_exact<PG, NoX, ColKey, SEL_NBIN>(g, signs, T, forced, hist, ms, gt, eq, kstar, need_eq, eq_count);
     }

@@ -1,0 +1,80 @@
+"""Code-generation guards for the hot loops (CPU: cuobjdump on the built library).
+
+ptxas' register allocation of the selection kernel is fragile: small changes elsewhere in the
+kernel have moved the pair-table base out of a uniform register (an R2UR or IMAD per table
+lookup) or made the register double buffer of the sign stream a copy (32 moves per batch),
+each worth 2-15% of the decode step.  These tests pin the scoring loop's instruction budget
+(per 8-token batch) and the attention kernels' freedom from local-memory spills.
+"""
+import collections
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2603_14224_b200", "libsikv_b200.so")
+
+pytestmark = pytest.mark.skipif(not (os.path.exists(LIB) and shutil.which("cuobjdump")),
+                                reason="library not built or cuobjdump missing")
+
+
+def _functions():
+    out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True, check=True).stdout
+    funcs, cur = {}, None
+    for line in out.splitlines():
+        m = re.match(r"\s+Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+            continue
+        m = re.match(r"\s+/\*([0-9a-f]{4,6})\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)(.*?);", line)
+        if m and cur:
+            funcs[cur].append((int(m.group(1), 16), m.group(3), m.group(4)))
+    return funcs
+
+
+def _loops(body):
+    """(ops Counter) of every backward-branch loop body."""
+    addr = {a: i for i, (a, _, _) in enumerate(body)}
+    loops = []
+    for i, (a, op, rest) in enumerate(body):
+        m = re.search(r"BRA\s+(?:`\()?(?:0x)?([0-9a-f]+)", op + rest) if op.startswith("BRA") else None
+        if m:
+            tgt = int(m.group(1), 16)
+            if tgt in addr and addr[tgt] < i:
+                seg = body[addr[tgt]:i + 1]
+                c = collections.Counter(o.split(".")[0] for _, o, _ in seg)
+                c["moves"] = sum(1 for _, o, _ in seg if o == "MOV" or o.startswith("IMAD.MOV"))
+                loops.append(c)
+    return loops
+
+
+@pytest.fixture(scope="module")
+def funcs():
+    return _functions()
+
+
+def _one(funcs, pat):
+    names = [n for n in funcs if re.search(pat, n)]
+    assert names, pat
+    return names
+
+
+def test_scoring_loop_budget(funcs):
+    for name in _one(funcs, r"decode_select_kernel"):
+        scans = [c for c in _loops(funcs[name]) if c["FADD2"] >= 60 and c["PRMT"] >= 128]
+        assert scans, name
+        main = min(scans, key=lambda c: sum(c.values()) - c["moves"])   # the 8-token batch loop
+        n = sum(main.values()) - main["moves"]
+        assert n <= 600, f"{name}: scoring loop grew to {n} instructions per batch ({main.most_common(8)})"
+        assert main["R2UR"] == 0 and main["LDL"] == 0 and main["STL"] == 0, main.most_common(12)
+        assert main["moves"] <= 12, main.most_common(12)   # no copies between the load buffers
+
+
+def test_attention_kernels_do_not_spill(funcs):
+    for name in _one(funcs, r"decode_attend_kernel"):
+        ops = collections.Counter(op.split(".")[0] for _, op, _ in funcs[name])
+        assert ops["LDL"] == 0 and ops["STL"] == 0, (name, ops["LDL"], ops["STL"])

@@ -25,7 +25,7 @@ cb, q = bench.build_cache(range(a.units), a.L, a.gq, 1234, dev)
 out = torch.empty(a.units, a.gq, 128, device=dev)
 for _ in range(3):
     B.decode_step(cb, q, a.k, out=out, kernel=a.kernel, cap=a.cap)
-clk = torch.zeros(a.units, 12, dtype=torch.int64, device=dev)
+clk = torch.zeros(a.units, 16, dtype=torch.int64, device=dev)
 _lib.call("sikv_debug_set_decode_profile", _lib.ptr(clk))
 B.decode_step(cb, q, a.k, out=out, kernel=a.kernel, cap=a.cap)
 torch.cuda.synchronize()
@@ -37,7 +37,8 @@ grid = min(148, (a.units + 1) // 2)
 grp = (np.arange(a.units) // grid) % 2
 rows = [("wait inputs", 0, 4), ("bitmap+qbar+LUT", 4, 5), ("pair table", 5, 1), ("sample score", 1, 7),
                 ("tau", 7, 8), ("scan (after tau)", 8, 2), ("setup+table", 0, 1), ("score+cand", 1, 2),
-                ("select+emit", 2, 3), ("unit total", 0, 3)]
+                ("select+emit", 2, 3), ("  k-th", 2, 12), ("  emit", 12, 13), ("  bitmaps/sel", 13, 3),
+                ("unit total", 0, 3)]
 for n, i, j in rows:
     d = c[:, j] - c[:, i]
     g0, g1 = d[grp == 0].mean(), d[grp == 1].mean()
