@@ -333,28 +333,34 @@ __device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[4],
   x[1] = g < rem ? sacc[1] * kSoftmaxScale : -INFINITY;       // token g, head h1
   x[2] = g + 8 < rem ? sacc[2] * kSoftmaxScale : -INFINITY;   // token g + 8, head h0
   x[3] = g + 8 < rem ? sacc[3] * kSoftmaxScale : -INFINITY;   // token g + 8, head h1
-  float bm0 = fmaxf(x[0], x[2]), bm1 = fmaxf(x[1], x[3]);
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
-    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
-    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
-  }
   // lazy rescale: the reference max only moves when the block max exceeds it by more than
-  // 2^8 (exp2 domain), so P <= 256 (exact range in fp16) and most blocks skip the O rescale
-  const float mn0 = bm0 > A.mrun[0] + kLazyRescale ? bm0 : A.mrun[0];
-  const float mn1 = bm1 > A.mrun[1] + kLazyRescale ? bm1 : A.mrun[1];
-  const float fa = ex2(A.mrun[0] - mn0), fb = ex2(A.mrun[1] - mn1);
-  A.mrun[0] = mn0;
-  A.mrun[1] = mn1;
-  const __half2 p0 = __floats2half2_rn(ex2(x[0] - mn0), ex2(x[1] - mn1));   // token g: heads h0, h1
-  const __half2 p1 = __floats2half2_rn(ex2(x[2] - mn0), ex2(x[3] - mn1));   // token g + 8
-  const float2 f0 = __half22float2(p0), f1 = __half22float2(p1);
-  A.lrun[0] = A.lrun[0] * fa + (f0.x + f1.x);
-  A.lrun[1] = A.lrun[1] * fb + (f0.y + f1.y);
-  if (!__all_sync(0xffffffffu, fa == 1.0f && fb == 1.0f)) {   // the running max moved for some head
+  // 2^8 (exp2 domain), so P <= 256 (exact range in fp16) and most blocks skip the O rescale.
+  // The block max is only reduced when some score exceeds the bound (the same decision as
+  // comparing the reduced block max, without its shuffles in the common case).
+  const float lim0 = A.mrun[0] + kLazyRescale, lim1 = A.mrun[1] + kLazyRescale;
+  if (__any_sync(0xffffffffu, x[0] > lim0 || x[2] > lim0 || x[1] > lim1 || x[3] > lim1)) {
+    float bm0 = fmaxf(x[0], x[2]), bm1 = fmaxf(x[1], x[3]);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+      bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+    }
+    const float mn0 = bm0 > lim0 ? bm0 : A.mrun[0];
+    const float mn1 = bm1 > lim1 ? bm1 : A.mrun[1];
+    const float fa = ex2(A.mrun[0] - mn0), fb = ex2(A.mrun[1] - mn1);
+    A.mrun[0] = mn0;
+    A.mrun[1] = mn1;
+    A.lrun[0] *= fa;
+    A.lrun[1] *= fb;
 #pragma unroll
     for (int m = 0; m < 8; ++m) { A.o[m][0] *= fa; A.o[m][1] *= fb; A.o[m][2] *= fa; A.o[m][3] *= fb; }
   }
+  const float mn0 = A.mrun[0], mn1 = A.mrun[1];
+  const __half2 p0 = __floats2half2_rn(ex2(x[0] - mn0), ex2(x[1] - mn1));   // token g: heads h0, h1
+  const __half2 p1 = __floats2half2_rn(ex2(x[2] - mn0), ex2(x[3] - mn1));   // token g + 8
+  const float2 f0 = __half22float2(p0), f1 = __half22float2(p1);
+  A.lrun[0] += f0.x + f1.x;
+  A.lrun[1] += f0.y + f1.y;
   // P as the PV B operand (tokens 2 t4, 2 t4 + 1 (+ 8) x head g): one transpose per 8 tokens
   const uint32_t pb0 = movmatrix_trans(h2u(p0)), pb1 = movmatrix_trans(h2u(p1));
 #pragma unroll
