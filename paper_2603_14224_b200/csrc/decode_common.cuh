@@ -486,12 +486,13 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   const int g = lane >> 2, t4 = lane & 3;
   const int nbd = (ndyn + 15) >> 4;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
-  // staging: lane copies chunk kk = lane & 7 of tokens j = (lane >> 3) + 4r, r = 0..3
+  // staging: lane copies chunk kk = lane & 7 of tokens j = 4 (lane >> 3) + r, r = 0..3 (its
+  // four row indices are one 16-byte load of the list)
   const int jb = lane >> 3, kk = lane & 7;
   uint32_t dst[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const int j = jb + 4 * r;
+    const int j = 4 * jb + r;
     dst[r] = (uint32_t)(j * FREC + 16 * (kk ^ stage_sw(j)));
   }
   const uint8_t* src0 = recs_u + 16 * kk;
@@ -499,9 +500,8 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
   // list read (shared or global memory) is off the staging path
   int32_t tix[4];
   auto load_ix = [&](int blk) {
-    const int32_t* dl = dyn + blk * 16 + jb;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) tix[r] = dl[4 * r];
+    const int4 v = *reinterpret_cast<const int4*>(dyn + blk * 16 + 4 * jb);
+    tix[0] = v.x; tix[1] = v.y; tix[2] = v.z; tix[3] = v.w;
   };
   auto stage_blk = [&](uint32_t buf) {
 #pragma unroll
@@ -526,8 +526,8 @@ __device__ __forceinline__ void attn_dynamic(Attn& A, const uint8_t* recs_u, con
     const int bn = first + (s + 1) * nw;
     int32_t tn[4] = {0, 0, 0, 0};
     if (bn < nbd) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) tn[r] = dyn[bn * 16 + jb + 4 * r];
+      const int4 v = *reinterpret_cast<const int4*>(dyn + bn * 16 + 4 * jb);
+      tn[0] = v.x; tn[1] = v.y; tn[2] = v.z; tn[3] = v.w;
     }
     if (first + s * nw < nbd) stage_blk(s * STAGE_BYTES);
     cp_commit();
