@@ -752,7 +752,8 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
       {
         const float E = __fmaf_ru(fmaxf(fabsf(kmin), fabsf(kmax)), 7.5e-7f, s_e0max[j]);
         auto kexact = [&](int n) -> double {
-          const double kd = (double)load1<DTY>(a.keys, row + n) - s_mu[j][n];
+          // the K value staged for the codebook walk (the same float; no global reload)
+          const double kd = (double)s_x[tl][32 * j + ((n + 8 * j) & 31)] - s_mu[j][n];
           if (!siq) return kd;
           const double al = s_al[j][n];
           return al == 0.0 ? 0.0 : fabs(kd) / al;
