@@ -37,6 +37,7 @@ cudaError_t launch_score_fast(const uint8_t*, const float*, const float*, int, i
 cudaError_t set_decode_profile(long long*);
 cudaError_t set_k1_skip(int);
 cudaError_t set_decode_two_profile(long long*);
+cudaError_t set_decode_split_profile(long long*);
 int split_smem_bytes(int64_t L, int k, int S, int Gq, int cap, int ns);
 int split_default_cap(int64_t L, int k, int S, int ns);
 cudaError_t launch_decode_split(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
@@ -350,6 +351,7 @@ int sikv_debug_set_attend_skip(int v) {
 int sikv_debug_set_decode_profile(void* clocks) {
   cudaError_t e = set_decode_profile((long long*)clocks);
   if (e == cudaSuccess) e = set_decode_two_profile((long long*)clocks);
+  if (e == cudaSuccess) e = set_decode_split_profile((long long*)clocks);
   return cuda_ret(e, "sikv_debug_set_decode_profile");
 }
 

@@ -1169,13 +1169,13 @@ __device__ __forceinline__ void bitmaps_from_candidates(const UnitGeom& g, const
 }
 
 // Exact k-th key among the candidate segments, then the gt / eq bitmaps (zeroed here).
-template <class Grp, class Xch = NoX>
+template <class Grp, class Xch = NoX, int NBINT = NBIN>
 __device__ __forceinline__ void select_from_candidates(const UnitGeom& g, const uint32_t* cand, const int* wcnt,
                                                        uint32_t maxx, uint32_t tau, int* hist, Misc* ms,
                                                        uint32_t* gt, uint32_t* eq, uint32_t& kstar,
                                                        int& need_eq, int& eq_count, const Xch& xch = Xch()) {
   uint32_t xk;
-  kth_from_candidates<Grp, Xch>(g, cand, wcnt, maxx, hist, ms, xk, need_eq, xch);
+  kth_from_candidates<Grp, Xch, NBINT>(g, cand, wcnt, maxx, hist, ms, xk, need_eq, xch);
   kstar = xk + tau;
   bitmaps_from_candidates<Grp>(g, cand, wcnt, xk, ms, gt, eq, eq_count);
 }

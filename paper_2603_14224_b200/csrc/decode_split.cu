@@ -74,9 +74,10 @@ struct ClusterX {
     }
     csync();
   }
+  template <int NBINT = NBIN>
   __device__ __forceinline__ const int* hist4k(const int* hc) const {
     int* h = const_cast<int*>(hc);
-    constexpr int PER = NBIN / DT;
+    constexpr int PER = NBINT / DT;
     int v[PER];
     csync();
 #pragma unroll
@@ -101,6 +102,12 @@ struct ClusterX {
     return m;
   }
 };
+
+__device__ long long* g_prof_split = nullptr;   // optional per-unit phase clocks of cluster rank 0
+cudaError_t set_decode_split_profile(long long* p) { return cudaMemcpyToSymbol(g_prof_split, &p, sizeof(p)); }
+#define SPROF(i) do { if (prof && tid == 0) prof[i] = clock64(); } while (0)
+
+constexpr int SPLIT_NBIN = 512;
 
 struct SplitArgs {
   const uint8_t* signs; const uint8_t* recs; const float* cent32; const float* alpha32;
@@ -129,6 +136,8 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   const int64_t Ls = t_hi > t_lo ? t_hi - t_lo : 0;
   const int W = (int)((Ls + 31) >> 5);
 
+  long long* prof = g_prof_split && rank == 0 ? g_prof_split + u * 16 : nullptr;
+  SPROF(0);
   char* T = sm;                                                    // pair table while scoring
   uint32_t* cand = reinterpret_cast<uint32_t*>(sm + a.off_cand);
   uint32_t* forced = reinterpret_cast<uint32_t*>(sm + a.off_forced);
@@ -182,6 +191,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   }
   __syncthreads();
   build_pair_table<Cta256>(a.cent32 + cu * 32 * 16 * 4, qbar, lut, T, a.lut_mode);
+  SPROF(1);
 
   // ---------------- B/C: candidates, the unit's k-th key, bitmaps of the slice
   const int mode = g.mode;
@@ -193,8 +203,11 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     uint32_t tau;
     const bool fb = produce_candidates<Cta256, ClusterX>(g, signs, T, forced, wsamp, cand,
                                                          reinterpret_cast<int*>(cand), cand + 256, ms, tau, xch);
+    SPROF(2);
     if (!fb) {
-      select_from_candidates<Cta256, ClusterX>(g, cand, ms->wcnt, ms->maxx, tau,
+      // 512-bin radix passes: each pass sums ns x 2 KB of histograms over the cluster (with
+      // 2048 bins the distributed-shared-memory merge was a third of the kernel at 8 CTAs)
+      select_from_candidates<Cta256, ClusterX, SPLIT_NBIN>(g, cand, ms->wcnt, ms->maxx, tau,
                                                reinterpret_cast<int*>(sm + a.off_hist), ms, gt, eq, kstar,
                                                need_eq, eq_count, xch);
     } else {
@@ -205,6 +218,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
                                       need_eq, eq_count, xch);
     }
   }
+  SPROF(3);
   // ties: the lower ranks (lower token indices) take theirs first
   if (tid == 0) slot->eqc = eq_count;
   ClusterX::csync();
@@ -279,6 +293,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     ndyn = dtot;
   }
 
+  SPROF(4);
   // ---------------- D: sparse attention over this slice's rows (+ forced rows on rank 0)
   Attn A;
   attn_init(A, qs, ahat, Gq, lane);
@@ -295,6 +310,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   float* xnum = reinterpret_cast<float*>(sm + a.off_x);           // [Gq][128]
   float* xm = xnum + Gq * FD;                                      // [Gq]
   float* xden = xm + 8;                                            // [Gq]
+  SPROF(5);
   attn_write_partial(A, part, pm, pl, warp, Gq, lane);
   __syncthreads();
   for (int e = tid; e < Gq * FD; e += DT) {
@@ -328,6 +344,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
     if (a.lse && d == 0) a.lse[u * Gq + h] = (M + log2f(den)) * 0.6931471805599453f;
   }
   ClusterX::csync();                 // remote reads of this CTA's shared memory are done
+  SPROF(6);
 }
 
 // ---------------------------------------------------------------- host side

@@ -27,6 +27,7 @@ struct NoX {
   __device__ __forceinline__ void sample(int&, uint32_t&, uint32_t&) const {}
   __device__ __forceinline__ void hist256(const int*&, const uint32_t*&) const {}
   __device__ __forceinline__ void counts(int&, int&, bool&) const {}
+  template <int NBINT = 2048>
   __device__ __forceinline__ const int* hist4k(const int* h) const { return h; }
   __device__ __forceinline__ uint32_t maxu(uint32_t v) const { return v; }
 };
@@ -147,7 +148,7 @@ __device__ __forceinline__ void radix_kth(Each each, uint32_t maxx, int rank, in
       if ((hi >= 32 ? 0u : (x >> hi)) == want) atomicAdd(&hist[(x >> sh) & (NBINT - 1)], 1);
     });
     Grp::sync();
-    const int* mh = xch.hist4k(hist);   // cluster: the sum of every CTA's histogram
+    const int* mh = xch.template hist4k<NBINT>(hist);   // cluster: the sum of every CTA's histogram
     pick_digit_big<Grp, NBINT>(mh, ms);
     const uint32_t d = (uint32_t)ms->digit;
     prefix |= d << shift;
