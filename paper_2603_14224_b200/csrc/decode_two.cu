@@ -23,6 +23,7 @@
 #include "api_types.cuh"
 #include "decode_common.cuh"
 #include <algorithm>
+#include <type_traits>
 
 namespace sikv {
 
@@ -202,9 +203,17 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 }
 
 // ---------------------------------------------------------------- attention
-constexpr int ATT_WARPS = 4;                        // warps per attention CTA (one unit each)
-constexpr int ATT_THREADS = 32 * ATT_WARPS;
-constexpr int ATT_CTAS_PER_SM = 16 / ATT_WARPS;
+// attention CTAs: NW warps each, 16 / NW per SM (16 warps per SM either way).  Units of at
+// most ATT_SMALL_ROWS dynamic + forced rows take 2-warp CTAs (C4: 0.743 -> 0.723 ms: the
+// per-CTA prologue and partial merge are amortised over more rows per warp), longer units
+// 4-warp CTAs (C3 0.205 vs 0.215 ms with 2)
+constexpr int ATT_WARPS_MAX = 4;
+constexpr int ATT_SMALL_ROWS = 1536;
+__host__ __device__ constexpr int att_ctas_per_sm(int nw) { return 16 / nw; }
+static int att_warps(int64_t L, int k, int S) {
+  const int64_t keff = std::max<int64_t>(0, std::min<int64_t>(k, L - S));
+  return keff + S <= ATT_SMALL_ROWS ? 2 : 4;
+}
 constexpr int ATT_STAGES = 2;                       // cp.async staging buffers per warp
 
 // One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
@@ -267,12 +276,12 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
 }
 
 // R16: 16-bit records (512 B per token, stored fp16 fragments; 64 KB of staging per CTA);
-// SPLIT: nsplit CTAs per unit
-template <bool R16, bool SPLIT>
-__global__ void __launch_bounds__(ATT_THREADS, ATT_CTAS_PER_SM) decode_attend_kernel(const __grid_constant__ TwoArgs a) {
+// SPLIT: nsplit CTAs per unit; NW warps per CTA
+template <bool R16, bool SPLIT, int NW>
+__global__ void __launch_bounds__(32 * NW, 16 / NW) decode_attend_kernel(const __grid_constant__ TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
-  if constexpr (SPLIT) attend_unit<ATT_WARPS, R16, true>(a, sm, blockIdx.x / a.nsplit, (int)(blockIdx.x % a.nsplit));
-  else attend_unit<ATT_WARPS, R16, false>(a, sm, blockIdx.x, 0);
+  if constexpr (SPLIT) attend_unit<NW, R16, true>(a, sm, blockIdx.x / a.nsplit, (int)(blockIdx.x % a.nsplit));
+  else attend_unit<NW, R16, false>(a, sm, blockIdx.x, 0);
 }
 
 // ---------------------------------------------------------------- host side
@@ -312,16 +321,17 @@ int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes;
 }
 int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16) {
-  (void)L; (void)k; (void)S;
-  return std::max(ATT_WARPS * ATT_STAGES * (rec16 ? STAGE16_BYTES : STAGE_BYTES), ATT_WARPS * Gq * (FD + 2) * 4);
+  const int nw = att_warps(L, k, S);
+  return std::max(nw * ATT_STAGES * (rec16 ? STAGE16_BYTES : STAGE_BYTES), nw * Gq * (FD + 2) * 4);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 // attention CTAs per unit: enough CTAs for four per SM when the units alone are too few
 constexpr int kMaxSplit = 8;
 constexpr int64_t kSplitUnits = 1024;   // workspace for split partials up to this many units
-static int two_nsplit(int64_t U, int nsm) {
-  if (U >= (int64_t)ATT_CTAS_PER_SM * nsm || U > kSplitUnits) return 1;
-  return (int)std::min<int64_t>(kMaxSplit, ((int64_t)ATT_CTAS_PER_SM * nsm + U - 1) / U);
+static int two_nsplit(int64_t U, int nsm, int nw) {
+  const int64_t slots = (int64_t)att_ctas_per_sm(nw) * nsm;
+  if (U >= slots || U > kSplitUnits) return 1;
+  return (int)std::min<int64_t>(kMaxSplit, (slots + U - 1) / U);
 }
 static size_t split_bytes(int64_t U) {
   return U > kSplitUnits ? 0 : a256((size_t)U * kMaxSplit * 8 * (FD + 2) * 4) + a256((size_t)U * 4);
@@ -352,7 +362,8 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
   a.gforced = reinterpret_cast<uint32_t*>(ws);
   ws += a256((size_t)U * ((L + 31) / 32) * 4);
-  a.nsplit = two_nsplit(U, nsm);
+  const int nw = att_warps(L, k, S);
+  a.nsplit = two_nsplit(U, nsm, nw);
   if (a.nsplit > 1) {
     a.spart = reinterpret_cast<float*>(ws);
     a.scnt = reinterpret_cast<int32_t*>(ws + a256((size_t)U * kMaxSplit * 8 * (FD + 2) * 4));
@@ -368,13 +379,17 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int smem_a = two_attend_smem_bytes(L, k, S, Gq, rec16);
-  auto attend = a.nsplit > 1 ? (rec16 ? decode_attend_kernel<true, true> : decode_attend_kernel<false, true>)
-                             : (rec16 ? decode_attend_kernel<true, false> : decode_attend_kernel<false, false>);
+  auto pick = [&](auto w) {
+    constexpr int W = decltype(w)::value;
+    return a.nsplit > 1 ? (rec16 ? decode_attend_kernel<true, true, W> : decode_attend_kernel<false, true, W>)
+                        : (rec16 ? decode_attend_kernel<true, false, W> : decode_attend_kernel<false, false, W>);
+  };
+  auto attend = nw == 2 ? pick(std::integral_constant<int, 2>()) : pick(std::integral_constant<int, ATT_WARPS_MAX>());
   e = cudaFuncSetAttribute(attend, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(U * a.nsplit));
-  cfg.blockDim = dim3(ATT_THREADS);
+  cfg.blockDim = dim3(32 * nw);
   cfg.dynamicSmemBytes = (size_t)smem_a;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
