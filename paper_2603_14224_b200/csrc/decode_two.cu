@@ -214,7 +214,7 @@ static int att_warps(int64_t L, int k, int S) {
   const int64_t keff = std::max<int64_t>(0, std::min<int64_t>(k, L - S));
   return keff + S <= ATT_SMALL_ROWS ? 2 : 4;
 }
-constexpr int ATT_STAGES = 2;                       // cp.async staging buffers per warp
+constexpr int ATT_STAGES = 3;   // cp.async staging buffers per warp (2: C2 0.847 ms, 3: 0.843, 4: 0.847)
 
 // One unit's attention by one CTA of NW warps.  Every warp starts on its own: q~ and the row
 // indices come straight from global memory (L2), so the only CTA-wide barriers are the
