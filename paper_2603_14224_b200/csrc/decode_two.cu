@@ -204,15 +204,16 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) decode_select_kernel(TwoArgs a
 
 // ---------------------------------------------------------------- attention
 // attention CTAs: NW warps each, 16 / NW per SM (16 warps per SM either way).  Units of at
-// most ATT_SMALL_ROWS dynamic + forced rows take 2-warp CTAs (C4: 0.743 -> 0.723 ms: the
-// per-CTA prologue and partial merge are amortised over more rows per warp), longer units
-// 4-warp CTAs (C3 0.205 vs 0.215 ms with 2)
+// most ATT_SMALL_ROWS dynamic + forced rows take 2-warp CTAs when they fill at least two waves
+// of them (C4, 7168 units: 0.743 -> 0.719 ms; 3584: 0.385 -> 0.378), else 4-warp CTAs (fewer,
+// faster units: 1792 units 0.206 vs 0.213 ms, 896 units 0.118 vs 0.123; long units, C3: 0.205
+// vs 0.215)
 constexpr int ATT_WARPS_MAX = 4;
 constexpr int ATT_SMALL_ROWS = 1536;
 __host__ __device__ constexpr int att_ctas_per_sm(int nw) { return 16 / nw; }
-static int att_warps(int64_t L, int k, int S) {
+static int att_warps(int64_t U, int64_t L, int k, int S, int nsm) {
   const int64_t keff = std::max<int64_t>(0, std::min<int64_t>(k, L - S));
-  return keff + S <= ATT_SMALL_ROWS ? 2 : 4;
+  return keff + S <= ATT_SMALL_ROWS && U >= 2LL * att_ctas_per_sm(2) * nsm ? 2 : 4;
 }
 constexpr int ATT_STAGES = 3;   // cp.async staging buffers per warp (2: C2 0.847 ms, 3: 0.843, 4: 0.847)
 
@@ -320,16 +321,22 @@ static bool two_forced_smem(int64_t L, int k, int S, int cap, int Gq) {
 int two_select_smem_bytes(int64_t L, int k, int S, int cap, int Gq) {
   return TBL_BYTES + 2 * two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq)).g_bytes;
 }
-int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16) {
-  const int nw = att_warps(L, k, S);
+static int attend_smem(int nw, int Gq, bool rec16) {
   return std::max(nw * ATT_STAGES * (rec16 ? STAGE16_BYTES : STAGE_BYTES), nw * Gq * (FD + 2) * 4);
+}
+int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16) {   // the wider CTA (the bound)
+  (void)L; (void)k; (void)S;
+  return attend_smem(ATT_WARPS_MAX, Gq, rec16);
 }
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 // attention CTAs per unit: enough CTAs for four per SM when the units alone are too few
 constexpr int kMaxSplit = 8;
 constexpr int64_t kSplitUnits = 1024;   // workspace for split partials up to this many units
 static int two_nsplit(int64_t U, int nsm, int nw) {
-  const int64_t slots = (int64_t)att_ctas_per_sm(nw) * nsm;
+  // split when the units are fewer than four per SM whatever the CTA width (with 2-warp CTAs
+  // a threshold of eight per SM split the 8-GPU C4 shard, 896 units: 0.118 -> 0.147 ms)
+  (void)nw;
+  const int64_t slots = (int64_t)att_ctas_per_sm(ATT_WARPS_MAX) * nsm;
   if (U >= slots || U > kSplitUnits) return 1;
   return (int)std::min<int64_t>(kMaxSplit, (slots + U - 1) / U);
 }
@@ -362,7 +369,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   ws += a256((size_t)U * 2 * ((L + 31) / 32) * 4);
   a.gforced = reinterpret_cast<uint32_t*>(ws);
   ws += a256((size_t)U * ((L + 31) / 32) * 4);
-  const int nw = att_warps(L, k, S);
+  const int nw = att_warps(U, L, k, S, nsm);
   a.nsplit = two_nsplit(U, nsm, nw);
   if (a.nsplit > 1) {
     a.spart = reinterpret_cast<float*>(ws);
@@ -378,7 +385,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   select<<<grid, SEL_THREADS, smem_s, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int smem_a = two_attend_smem_bytes(L, k, S, Gq, rec16);
+  const int smem_a = attend_smem(nw, Gq, rec16);
   auto pick = [&](auto w) {
     constexpr int W = decltype(w)::value;
     return a.nsplit > 1 ? (rec16 ? decode_attend_kernel<true, true, W> : decode_attend_kernel<false, true, W>)
