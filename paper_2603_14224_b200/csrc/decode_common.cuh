@@ -13,7 +13,7 @@ constexpr int MAX_SAMPLE_CHUNKS = 8;
 // sample chunks are at least SSTRIDE_MIN chunks apart (>= NB: one per B2 batch at most), so
 // short units (< 32K tokens) still sample up to 8 chunks: a tighter threshold, fewer candidates
 constexpr int SSTRIDE_MIN = 8;
-static_assert(SSTRIDE_MIN >= NB, "at most one sample chunk per B2 batch");
+static_assert(SSTRIDE_MIN >= NB, "at most one sample chunk per B2 batch (the stride is rounded to a multiple of NB)");
 
 // ---------------------------------------------------------------- pair table
 // LUT[g][c] = q-bar_g . centroid[g][c] (float32, no FMA, the reference pairing) and the
@@ -798,7 +798,9 @@ __device__ __forceinline__ UnitGeom unit_geom(int64_t L, int S, int k, int capw,
   else if (g.keff == ncand) g.mode = 1;
   else if ((int64_t)g.nchunks * 32 <= (int64_t)capw) g.mode = 2;
   else g.mode = 3;
-  g.sstride = g.mode == 3 ? max(SSTRIDE_MIN, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
+  // a multiple of NB: every sample chunk is the first chunk of a scan batch
+  g.sstride = g.mode == 3 ? (max(SSTRIDE_MIN, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) + NB - 1) / NB * NB
+                          : 1;
   g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
   g.npass = 1;
   if (g.mode == 3 && g.nsc == MAX_SAMPLE_CHUNKS && g.sstride >= 2 * kMaxSamplePasses) {
@@ -928,6 +930,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
   const int Li = (int)g.L;
   const int end_s = g.nsc * g.sstride;
   const uint4* pbase = signs + tid;
+  asm volatile("" : "+l"(pbase));   // kept in registers, not rematerialised from the arguments per batch
   const uint64_t pol = l2_evict_first_policy();
   auto load_batch = [&](int c0, uint4 (&w)[NBT]) {
     const uint4* p = pbase + (int64_t)c0 * 256;     // constant offsets 4 KiB apart: no per-load address math
@@ -1032,8 +1035,9 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
     uint4 wn[NBT];
     load_batch(0, wn);
     for (int c0 = 0; c0 < g.nchunks; c0 += NBT) {
-      int xs = -1;
-      if (next_s < c0 + NBT && next_s < end_s) { xs = next_s - c0; next_s += g.sstride; }
+      // sample chunks (scored in B1) open their batch (g.sstride is a multiple of NBT)
+      const uint32_t xsm = c0 == next_s && c0 < end_s ? 1u : 0u;
+      if (xsm) next_s += g.sstride;
       const int t0 = c0 * 256 + tid;
       const bool full = (c0 + NBT) * 256 <= Li;
       uint4 w[NBT];
@@ -1046,7 +1050,7 @@ __device__ __forceinline__ bool produce_candidates(const UnitGeom& g, const uint
 #pragma unroll
       for (int x = 0; x < NBT; ++x)
         if (sv[x] >= tauf) bits |= 1u << x;
-      if (xs >= 0) bits &= ~(1u << xs);
+      bits &= ~xsm;
       if (!full) bits &= (Li - t0 > 0) ? ((Li - t0 + 255) / 256 >= NBT ? 0xFFu : ((1u << ((Li - t0 + 255) / 256)) - 1u)) : 0u;
       if (c0 * 256 < g.flim) {
 #pragma unroll

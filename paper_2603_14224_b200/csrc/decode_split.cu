@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(DT, 2) decode_split_kernel(SplitArgs a) {
   g.nchunks = c_hi - c_lo;
   g.capw = a.capw;
   g.mode = g.keff == 0 ? 0 : (g.keff == g.ncand ? 1 : 3);
-  g.sstride = g.mode == 3 ? max(16, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) : 1;
+  g.sstride = g.mode == 3 ? (max(16, (g.nchunks + MAX_SAMPLE_CHUNKS - 1) / MAX_SAMPLE_CHUNKS) + NB - 1) / NB * NB : 1;
   g.nsc = g.mode == 3 ? (g.nchunks + g.sstride - 1) / g.sstride : 0;
   g.npass = 1;                       // the cluster merges one register-resident sample pass
   {

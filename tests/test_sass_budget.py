@@ -69,7 +69,7 @@ def test_scoring_loop_budget(funcs):
         assert scans, name
         main = min(scans, key=lambda c: sum(c.values()) - c["moves"])   # the 8-token batch loop
         n = sum(main.values()) - main["moves"]
-        assert n <= 600, f"{name}: scoring loop grew to {n} instructions per batch ({main.most_common(8)})"
+        assert n <= 590, f"{name}: scoring loop grew to {n} instructions per batch ({main.most_common(8)})"
         assert main["R2UR"] == 0 and main["LDL"] == 0 and main["STL"] == 0, main.most_common(12)
         assert main["moves"] <= 12, main.most_common(12)   # no copies between the load buffers
 
