@@ -429,7 +429,7 @@ __device__ __forceinline__ void attn_block(Attn& A, const char* sb, const BlkOff
   }
 #pragma unroll
   for (int grp = 0; grp < 4; ++grp) {
-    const __half2 qa2 = u2h(prmt(par[0][grp], par[0][grp], 0x1010u)), qb2 = u2h(prmt(par[1][grp], par[1][grp], 0x1010u));
+    const __half2 qa2 = __low2half2(u2h(par[0][grp])), qb2 = __low2half2(u2h(par[1][grp]));   // HFMA2 .H0_H0 operands
     const uint32_t za2 = prmt(par[0][grp], par[0][grp], 0x3232u), zb2 = prmt(par[1][grp], par[1][grp], 0x3232u);
     // k-steps s = 2 grp (bytes 0, 1 of word grp) and 2 grp + 1 (bytes 2, 3); A rows g / g + 8
     mma16816(sacc, k_dequant2<0>(kw[0][grp], qa2, za2), k_dequant2<0>(kw[1][grp], qb2, zb2),

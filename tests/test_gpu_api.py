@@ -321,6 +321,23 @@ class TestRetrieval:   # test_retrieval.py
                 got = sk.top_k_select(s, k, sink=sink)
                 assert N(got.indices).tolist() == O.top_k(s, k, sink=sink)[0].tolist()
 
+    def test_dense_scores(self):
+        """retrieval.py:80-89: the exact q . K'^T oracle (float64) and its validation / tallies."""
+        rng = np.random.default_rng(7)
+        for L, D in ((1, 4), (33, 16), (4096, 128)):
+            K = rng.standard_normal((L, D))
+            q = rng.standard_normal(D)
+            got = N(sk.dense_scores(q, K))
+            assert got.dtype == np.float64 and got.shape == (L,)
+            np.testing.assert_allclose(got, K @ q, rtol=1e-13, atol=1e-13)
+        with sk.collect() as ops:
+            sk.dense_scores(np.ones(8), np.ones((5, 8)))
+        assert (ops.dense_muls, ops.dense_adds) == (40, 35)
+        with pytest.raises(ValueError, match="2-D"):
+            sk.dense_scores(np.ones(4), np.ones(4))
+        with pytest.raises(ValueError, match="channels"):
+            sk.dense_scores(np.ones(3), np.ones((2, 4)))
+
     def test_resolve(self):
         assert sk.resolve_dynamic_k(4096, 64, budget=160) == 96
         assert sk.resolve_dynamic_k(4096, 0, sparsity=0.075) == 307
