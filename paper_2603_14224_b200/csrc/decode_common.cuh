@@ -271,7 +271,10 @@ struct Attn {
   float mrun[2], lrun[2];
 };
 
-// q~ = q * alpha-hat straight from global memory (each warp on its own, no barrier)
+// log2(e) / sqrt(128): folded into q~, so the MMA yields the exp2-domain logits directly
+constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;
+
+// q~ = q * alpha-hat * kSoftmaxScale straight from global memory (each warp on its own)
 __device__ __forceinline__ void attn_init_g(Attn& A, const float* __restrict__ q_u, const float* __restrict__ alpha_u,
                                             int Gq, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
@@ -284,7 +287,7 @@ __device__ __forceinline__ void attn_init_g(Attn& A, const float* __restrict__ q
       const float2 qv = __ldg(reinterpret_cast<const float2*>(q_u + gg * FD + d));
       const float2 av = __ldg(reinterpret_cast<const float2*>(alpha_u + d));
       const float a0 = av.x > 0.f ? av.x : 1.0f, a1 = av.y > 0.f ? av.y : 1.0f;
-      const float x0 = g < Gq ? qv.x * a0 : 0.f, x1 = g < Gq ? qv.y * a1 : 0.f;
+      const float x0 = g < Gq ? qv.x * a0 * kSoftmaxScale : 0.f, x1 = g < Gq ? qv.y * a1 * kSoftmaxScale : 0.f;
       A.qa[s][e] = h2u(__floats2half2_rn(x0, x1));
     }
 #pragma unroll
@@ -301,7 +304,10 @@ __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float*
     for (int e = 0; e < 2; ++e) {
       const int d = 16 * s + 2 * t4 + 8 * e;
       float x0 = 0.f, x1 = 0.f;
-      if (g < Gq) { x0 = qs[g * FD + d] * ahat[d]; x1 = qs[g * FD + d + 1] * ahat[d + 1]; }
+      if (g < Gq) {
+        x0 = qs[g * FD + d] * ahat[d] * kSoftmaxScale;
+        x1 = qs[g * FD + d + 1] * ahat[d + 1] * kSoftmaxScale;
+      }
       A.qa[s][e] = h2u(__floats2half2_rn(x0, x1));
     }
 #pragma unroll
@@ -310,7 +316,6 @@ __device__ __forceinline__ void attn_init(Attn& A, const float* qs, const float*
   A.lrun[0] = A.lrun[1] = 0.f;
 }
 
-constexpr float kSoftmaxScale = 1.4426950408889634f * 0.08838834764831845f;   // log2(e) / sqrt(128)
 constexpr float kLazyRescale = 8.0f;
 // 2^x on the SFU (x <= 8 here: logits minus the reference max; -inf -> +0)
 __device__ __forceinline__ float ex2(float x) {
@@ -329,10 +334,10 @@ __device__ __forceinline__ void attn_softmax_pv(Attn& A, const float (&sacc)[4],
                                                 VFrag&& vfrag) {
   const int g = lane >> 2;
   float x[4];
-  x[0] = g < rem ? sacc[0] * kSoftmaxScale : -INFINITY;       // token g, head h0
-  x[1] = g < rem ? sacc[1] * kSoftmaxScale : -INFINITY;       // token g, head h1
-  x[2] = g + 8 < rem ? sacc[2] * kSoftmaxScale : -INFINITY;   // token g + 8, head h0
-  x[3] = g + 8 < rem ? sacc[3] * kSoftmaxScale : -INFINITY;   // token g + 8, head h1
+  x[0] = g < rem ? sacc[0] : -INFINITY;       // token g, head h0 (exp2-domain logits: q~ is prescaled)
+  x[1] = g < rem ? sacc[1] : -INFINITY;       // token g, head h1
+  x[2] = g + 8 < rem ? sacc[2] : -INFINITY;   // token g + 8, head h0
+  x[3] = g + 8 < rem ? sacc[3] : -INFINITY;   // token g + 8, head h1
   // lazy rescale: the reference max only moves when the block max exceeds it by more than
   // 2^8 (exp2 domain), so P <= 256 (exact range in fp16) and most blocks skip the O rescale.
   // The block max is only reduced when some score exceeds the bound (the same decision as
