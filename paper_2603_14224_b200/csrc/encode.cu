@@ -598,13 +598,24 @@ __device__ __forceinline__ float load1(const void* p, int64_t idx) {
   return reinterpret_cast<const float*>(p)[idx];
 }
 
+// packed float32 pairs (sm_100a FFMA2 / FADD2: per lane the same correctly rounded ops)
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
 // Quantise one 32-element group (quantizer.py:119-130).  m: float32 estimates, E: group error
 // bound (0 = the estimates are exact), [mmin, mmax]: range of m, exact(n): float64 value.
 // emit(n, code) ORs a code into the caller's packed words (n is always a compile-time constant);
-// fix[32] is this thread's shared-memory scratch for the exact codes.
-template <int BITS, typename Exact, typename Emit>
+// reset() clears them; fix[32] is this thread's shared-memory scratch for the exact codes.
+template <int BITS, typename Exact, typename Emit, typename Reset>
 __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, float mmin, float mmax, Exact&& exact,
-                                              Emit&& emit, uint8_t* fix, __half& qs16, __half& zp16, double& mxo) {
+                                              Emit&& emit, Reset&& reset, uint8_t* fix, __half& qs16, __half& zp16,
+                                              double& mxo) {
   constexpr int levels = (1 << BITS) - 1;
   double mn, mx;
   if (E == 0.f) {
@@ -644,6 +655,33 @@ __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, flo
   const float B = (E * 1.0001f + mabs * 2.5e-7f) * iqs + fabsf(zq) * 3e-7f + 2e-6f;
   const float omB = 1.f - B;
   constexpr float kRnd = 12582912.f;               // 1.5 * 2^23: x + kRnd (round down) = floor(x)
+  // common case, in float32 pairs: every code from its estimate, and one test for the whole
+  // group — the largest |frac(x) - 1/2| against 1/2 - B (fr - 1/2 is exact for fr >= 1/4 and
+  // off by <= 2^-26 below, hence the 1e-7 margin: anything near a boundary takes the exact path)
+  {
+    const unsigned long long iq2 = f2pack(iqs, iqs), c02 = f2pack(c0, c0);
+    const unsigned long long rnd2 = f2pack(kRnd, kRnd), nrnd2 = f2pack(-kRnd, -kRnd), nh2 = f2pack(-0.5f, -0.5f);
+    float amax = 0.f;
+#pragma unroll
+    for (int n = 0; n < 32; n += 2) {
+      unsigned long long x2, y2, t2, r2, d2;
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(x2) : "l"(f2pack(m[n], m[n + 1])), "l"(iq2), "l"(c02));
+      asm("add.rm.f32x2 %0, %1, %2;" : "=l"(y2) : "l"(x2), "l"(rnd2));
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(y2), "l"(nrnd2));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r2) : "l"(x2), "l"(t2));
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d2) : "l"(r2), "l"(nh2));
+      float y0, y1, d0, d1;
+      f2unpack(y2, y0, y1);
+      f2unpack(d2, d0, d1);
+      amax = fmaxf(amax, fmaxf(fabsf(d0), fabsf(d1)));
+      const int c0i = min(max((int)(__float_as_uint(y0) - 0x4B400000u), 0), levels);
+      const int c1i = min(max((int)(__float_as_uint(y1) - 0x4B400000u), 0), levels);
+      emit(n, (uint32_t)c0i);
+      emit(n + 1, (uint32_t)c1i);
+    }
+    if (!(amax > 0.5f - B - 1e-7f)) return;
+    reset();                                       // rare: redo with per-element decisions
+  }
   uint32_t amb = 0;
 #pragma unroll
   for (int n = 0; n < 32; ++n) {
@@ -766,8 +804,14 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
             kp4[rr >> 1] |= c << (16 * (n >> 4) + 8 * e + 4 * (rr & 1));
           }
         };
+        auto kreset = [&]() {
+#pragma unroll
+          for (int q = 0; q < BITS; ++q) kref[q] = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) kp4[q] = 0;
+        };
         double kmx;
-        quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, s_fix[tid], kqs, kzp, kmx);
+        quant_group32<BITS>(km, E, kmin, kmax, kexact, kemit, kreset, s_fix[tid], kqs, kzp, kmx);
         if (valid && siq && kmx > 1.0 + 1e-9) atomicOr(a.status, 2);
       }
       {
@@ -779,9 +823,15 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
           vref[n / PER] |= c << (BITS * (n % PER));
           if constexpr (BITS <= 2) vp8[n & 7] |= c << (4 * (n >> 4) + 2 * ((n >> 3) & 1));
         };
+        auto vreset = [&]() {
+#pragma unroll
+          for (int q = 0; q < BITS; ++q) vref[q] = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) vp8[q] = 0;
+        };
         double vmx;
         quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
-                            vemit, s_fix[tid], vqs, vzp, vmx);
+                            vemit, vreset, s_fix[tid], vqs, vzp, vmx);
       }
       if (valid) {
         const bool kbad = !isfinite(__half2float(kqs)) || !isfinite(__half2float(kzp));
