@@ -263,7 +263,9 @@ cudaError_t launch_decode(const uint8_t* signs, const uint8_t* recs, const float
 __device__ __forceinline__ void pack_block(int64_t u, int blk, int lane, const float* __restrict__ sink_k,
                                            const float* __restrict__ sink_v, int S, const float* rec_k,
                                            const float* rec_v, int64_t rcap, int Ru, const float* __restrict__ alpha32,
-                                           int fblocks, uint32_t* __restrict__ frag, int* status) {
+                                           int fblocks, uint32_t* __restrict__ frag, int* status, int part = -1) {
+  // part: -1 = the whole block; 0 / 1 = the K rows g / g + 8; 2 / 3 = V m-tiles 0-3 / 4-7 (one
+  // warp each when a block is packed by four warps)
   const int g = lane >> 2, t4 = lane & 3;
   const int nf = S + Ru;
   auto row = [&](int f, bool key) -> const float* {
@@ -281,6 +283,7 @@ __device__ __forceinline__ void pack_block(int64_t u, int blk, int lane, const f
   int bad = 0;
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
+    if (part >= 0 && part != nt) continue;
     const float* kr = row(base + g + 8 * nt, true);
     float x[32];
     float mx = 0.f;
@@ -309,7 +312,8 @@ __device__ __forceinline__ void pack_block(int64_t u, int blk, int lane, const f
   }
   uint32_t* ov = out + 32 * 32;
 #pragma unroll
-  for (int m = 0; m < 8; ++m)
+  for (int m = 0; m < 8; ++m) {
+    if (part >= 0 && part != 2 + (m >> 2)) continue;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int d = 16 * m + g + 8 * (r & 1), pr = r >> 1;
@@ -320,6 +324,7 @@ __device__ __forceinline__ void pack_block(int64_t u, int blk, int lane, const f
       else if (fabsf(a0) > 65504.f || fabsf(a1) > 65504.f) bad |= 16;
       ov[m * 4 + r] = h2u(__floats2half2_rn(a0, a1));
     }
+  }
   bad = __reduce_or_sync(0xffffffffu, bad);
   if (bad && lane == 0 && status) atomicOr(status, bad);
 }
@@ -329,15 +334,15 @@ __global__ void pack_forced_kernel(const float* __restrict__ sink_k, const float
                                    const int32_t* __restrict__ rn, int R, const float* __restrict__ alpha32,
                                    int fblocks, int b0, uint32_t* __restrict__ frag, int* status) {
   const int64_t u = blockIdx.y;
-  pack_block(u, b0 + blockIdx.x, threadIdx.x, sink_k, sink_v, S, rec_k, rec_v, rcap, rn ? rn[u] : R, alpha32, fblocks,
-             frag, status);
+  pack_block(u, b0 + blockIdx.x, threadIdx.x & 31, sink_k, sink_v, S, rec_k, rec_v, rcap, rn ? rn[u] : R, alpha32,
+             fblocks, frag, status, (int)(threadIdx.x >> 5));
 }
 
 cudaError_t launch_pack_forced(const float* sink_k, const float* sink_v, int S, const float* rec_k,
                                const float* rec_v, int64_t rcap, const int32_t* rn, int R, const float* alpha32,
                                int64_t U, int fblocks, int b0, int b1, uint32_t* frag, int* status, cudaStream_t st) {
   if (b1 <= b0 || U == 0) return cudaSuccess;
-  pack_forced_kernel<<<dim3(b1 - b0, (unsigned)U), 32, 0, st>>>(sink_k, sink_v, S, rec_k, rec_v, rcap, rn, R,
+  pack_forced_kernel<<<dim3(b1 - b0, (unsigned)U), 128, 0, st>>>(sink_k, sink_v, S, rec_k, rec_v, rcap, rn, R,
                                                                alpha32, fblocks, b0, frag, status);
   return cudaGetLastError();
 }
