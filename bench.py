@@ -384,7 +384,7 @@ def run_prefill(args, rank, world, cfg):
     ul = units // world
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    chunk = 8
+    chunk = min(64, ul)           # heads per prefill call (8: 1.57 G token-heads/s, 32: 1.75 G, 64: 1.78 G)
     cb = B.empty_batch(chunk, L, sink_count=SINKS, device=dev)
     ws = torch.empty(_lib.lib().sikv_encode_workspace_bytes(chunk, L, 128), dtype=torch.uint8, device=dev)
     K, V = gen_units_torch(chunk, L, 128, 77 + rank, dev)
@@ -399,7 +399,7 @@ def run_prefill(args, rank, world, cfg):
     with ClockSampler(dev.index) as clk:
         e0.record(st)
         for _ in range(args.steps):
-            for _r in range(reps):       # every step encodes this rank's ul units (8 at a time)
+            for _r in range(reps):       # every step encodes this rank's ul units (chunk at a time)
                 B.prefill_into(cb, 0, K, V, workspace=ws, check=False)
         e1.record(st)
         torch.cuda.synchronize()
