@@ -490,3 +490,33 @@ def test_fast_variants_match_reference_golden(golden, name, bits, siq):
     ref_out = arr[f"{name}/attn"]
     for h in range(rec["gq"]):
         assert O.rel_l2(res.out[0, h].cpu().numpy(), ref_out[h]) <= att_rel_l2(rec["L"]), h
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 3, 4])
+def test_decode_step_in_cuda_graph(c1, kernel):
+    """The hot path is stream-ordered and allocation-free once its output and workspace exist
+    (no host syncs, PDL launches capture as programmatic edges): one decode step captured in a
+    CUDA graph and replayed with new queries gives the eager step's outputs bit for bit."""
+    units, cb, oc, q = c1
+    k = 256
+    q_static = q.clone()
+    out_static = torch.empty(q.shape[0], q.shape[1], 128, device="cuda")
+    B.decode_step(cb, q_static, k, out=out_static, kernel=kernel)          # warm-up: workspace, attributes
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        B.decode_step(cb, q_static, k, out=out_static, kernel=kernel)      # the capture stream's workspace
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        B.decode_step(cb, q_static, k, out=out_static, kernel=kernel)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        qn = torch.tensor(rng.standard_normal(tuple(q.shape)), dtype=torch.float32, device="cuda")
+        q_static.copy_(qn)
+        g.replay()
+        torch.cuda.synchronize()
+        ref = B.decode_step(cb, qn, k, kernel=kernel).out
+        torch.cuda.synchronize()
+        assert torch.equal(out_static, ref)
