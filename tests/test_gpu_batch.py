@@ -520,3 +520,22 @@ def test_decode_step_in_cuda_graph(c1, kernel):
         ref = B.decode_step(cb, qn, k, kernel=kernel).out
         torch.cuda.synchronize()
         assert torch.equal(out_static, ref)
+
+
+def test_long_units_extra_sample_passes_and_retries():
+    """Units of >= 64K tokens take extra sample passes (decode_select_kernel<true>); a candidate
+    buffer too small for the sampled threshold forces the rescan path, whose sample rank is
+    converted to the first pass's keys.  The selections stay exact (restate32) either way."""
+    from paper_2603_14224_b200 import _lib
+    units, cb, oc, q = make(65536, [300, 301], gq=4)
+    k = 2048
+    _check_decode(units, cb, oc, q, k, kernel=4)                  # default buffer: no rescan
+    clk = torch.zeros(len(units), 16, dtype=torch.int64, device="cuda")
+    _lib.call("sikv_debug_set_decode_profile", _lib.ptr(clk))
+    try:
+        res = _check_decode(units, cb, oc, q, k, kernel=4, cap=2400)
+    finally:
+        _lib.call("sikv_debug_set_decode_profile", None)
+    attempts = clk[:, 9].cpu().numpy()
+    fallback = (res.diag.cpu().numpy() & 4) != 0
+    assert ((attempts >= 1) | fallback).all(), (attempts, fallback)
