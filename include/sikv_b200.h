@@ -45,7 +45,7 @@ extern "C" {
 #define SIKV_EUNSUPPORTED 3
 
 const char* sikv_last_error(void);
-int sikv_abi_version(void);   /* 6 */
+int sikv_abi_version(void);   /* 7 */
 
 /* ---------------------------------------------------------------- encoder (prefill)
  * replaces: compute_channel_stats   normalize.py:56-61
@@ -202,7 +202,10 @@ int sikv_dequant_rows(const uint8_t* codes_ref, const uint8_t* kq_ref, const uin
                       int64_t units, int64_t tokens, int64_t dim, const int64_t* rows, int64_t n,
                       int which, double* out, void* stream);
 /* replaces: sparse_attention attention.py:52-62 with cache.gather cache.py:118-158, float64.
- * ws = [U][heads][sel_stride] doubles; out [U][heads][dim]; chk (nullable) [U][heads]. */
+ * ws: sikv_attend_f64_workspace_bytes(units, heads, sel_stride) bytes (the weights, then the
+ * split CTAs' partials and counters); out [U][heads][dim] (dim <= 128); chk (nullable)
+ * [U][heads] = the weights' sum. */
+size_t sikv_attend_f64_workspace_bytes(int64_t units, int heads, int sel_stride);
 int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
                     const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
                     const uint16_t* vq_zeros, const double* kfull, const double* vfull,

@@ -52,6 +52,7 @@ _SIGS = {
     "sikv_topk_workspace_bytes": (SZ, [I64, I64]),
     "sikv_topk": (I, [P, I, I64, I64, P, I, I, P, P, I, P, P]),
     "sikv_dequant_rows": (I, [P, P, P, P, P, P, P, P, P, P, I, I, I, I64, I64, I64, P, I64, I, P, P]),
+    "sikv_attend_f64_workspace_bytes": (SZ, [I64, I, I]),
     "sikv_attend_f64": (I, [P, P, P, P, P, P, P, P, P, P, I, I, I, I64, I64, I64, P, I, P, P, I, P, I, P,
                             P, P, P, I64, P, P, P, P]),
     "sikv_center": (I, [P, I, I64, I64, I64, P, P, P]),

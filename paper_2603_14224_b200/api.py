@@ -953,7 +953,8 @@ def sparse_attention(q, selection: TokenSelection, cache: SelfIndexingCache) -> 
     if not selection._valid and n and _DEVICE_CHECKS and (int(idx.min()) < 0 or int(idx.max()) >= cache.length):
         raise ValueError(f"indices out of range [0, {cache.length})")
     cnt = torch.tensor([n], dtype=torch.int32, device=_dev())
-    ws = torch.empty(n, dtype=torch.float64, device=_dev())
+    ws = torch.empty((L_.lib().sikv_attend_f64_workspace_bytes(1, 1, n) + 7) // 8, dtype=torch.float64,
+                     device=_dev())
     out = torch.empty(cache.dim, dtype=torch.float64, device=_dev())
     chk = torch.empty((), dtype=torch.float64, device=_dev())
     S = int(cache.sink_indices.numel())

@@ -15,7 +15,12 @@ struct RefPlanes {
   const double* alpha;      // [U][D]
   int bits, gs, siq, D;
   int64_t L;
+  // derived (make_planes): bits and group_size are powers of two, so the per-element payload
+  // byte / field / group indices are shifts (generic.cu deq_elem)
+  int lbits, lper, lgs, payb, ngroups;
 };
+
+constexpr int ATT_SPLIT = 16;     // CTAs per (unit, head) of the float64 sparse attention
 
 struct AttendArgs {
   RefPlanes p;
@@ -30,6 +35,8 @@ struct AttendArgs {
   const double* rec_k; const double* rec_v;     // [U][rcap][D]
   int64_t rcap;
   double* ws;               // [U][H][sel_stride]
+  double* part;             // [U][H][ATT_SPLIT][130] per-CTA (max, sum, P V) partials
+  uint32_t* cnt;            // [U][H] CTAs done
   double* out;              // [U][H][D]
   double* chk;              // [U][H]
 };

@@ -98,7 +98,7 @@ static int max_smem() {
 extern "C" {
 
 const char* sikv_last_error(void) { return g_err.c_str(); }
-int sikv_abi_version(void) { return 6; }
+int sikv_abi_version(void) { return 7; }
 
 size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
   return encode_workspace_bytes(units, tokens, (int)dim);
@@ -433,7 +433,15 @@ static RefPlanes make_planes(const uint8_t* codes_ref, const uint8_t* kq_ref, co
                              const double* alpha64, int bits, int gs, int siq, int64_t L, int64_t D) {
   RefPlanes p{codes_ref, kq_ref, (const __half*)kq_scales, (const __half*)kq_zeros, vq_ref,
               (const __half*)vq_scales, (const __half*)vq_zeros, kfull, vfull, alpha64, bits, gs, siq,
-              (int)D, L};
+              (int)D, L, 0, 0, 0, 0, 0};
+  auto lg2 = [](int v) { int r = 0; while (v > 1) { v >>= 1; ++r; } return r; };
+  if (bits >= 1 && bits <= 8 && gs > 0) {
+    p.lbits = lg2(bits);
+    p.lper = 3 - p.lbits;               // 8 / bits elements per byte
+    p.lgs = lg2(gs);
+    p.payb = (int)((D * bits + 7) / 8);
+    p.ngroups = (int)(D / gs);
+  }
   return p;
 }
 
@@ -465,6 +473,11 @@ int sikv_dequant_rows(const uint8_t* codes_ref, const uint8_t* kq_ref, const uin
   return cuda_ret(launch_dequant_rows(p, units, rows, n, which, out, (cudaStream_t)stream), "sikv_dequant_rows");
 }
 
+size_t sikv_attend_f64_workspace_bytes(int64_t units, int heads, int sel_stride) {
+  const int64_t uh = units * heads;
+  return (size_t)(uh * sel_stride + uh * ATT_SPLIT * 130) * sizeof(double) + (size_t)uh * sizeof(uint32_t);
+}
+
 int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint16_t* kq_scales,
                     const uint16_t* kq_zeros, const uint8_t* vq_ref, const uint16_t* vq_scales,
                     const uint16_t* vq_zeros, const double* kfull, const double* vfull, const double* alpha64,
@@ -479,8 +492,13 @@ int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint1
   if (rc) return rc;
   REQUIRE(q && sel && nsel && ws && out && heads >= 1, SIKV_EINVAL, "null pointer");
   REQUIRE(sinks == 0 || (sink_idx && sink_k && sink_v), SIKV_EINVAL, "sink rows missing");
+  REQUIRE(dim <= 128, SIKV_EUNSUPPORTED, "sparse attention supports dim <= 128");
+  // ws: [U][H][sel_stride] weights | [U][H][ATT_SPLIT][130] partials | [U][H] counters
+  const int64_t uh = units * heads;
+  double* part = ws + uh * sel_stride;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(part + uh * ATT_SPLIT * 130);
   AttendArgs a{p, q, heads, sel, nsel, sel_stride, sink_idx, sinks, sink_k, sink_v, recent_k, recent_v,
-               rcap, ws, out, chk};
+               rcap, ws, part, cnt, out, chk};
   return cuda_ret(launch_attend_f64(a, units, (cudaStream_t)stream), "sikv_attend_f64");
 }
 

@@ -119,14 +119,20 @@ __global__ void __launch_bounds__(DT) topk_kernel(const void* __restrict__ score
     for (int shift = 56; shift >= 0; shift -= 8) {
       hist[tid] = 0;
       __syncthreads();
-      for (int64_t i0 = 0; i0 < L; i0 += DT) {
-        const int64_t i = i0 + tid;
-        int bin = -1;
-        if (i < L && !((forced[i >> 5] >> (i & 31)) & 1u)) {
-          const uint64_t key = score_key(s, is_f32, i);
-          if ((key & pmask) == prefix) bin = (int)((key >> shift) & 255);
+      // eight keys per thread in flight per step (the passes were load-latency bound)
+      constexpr int UNR = 8;
+      for (int64_t i0 = 0; i0 < L; i0 += (int64_t)DT * UNR) {
+        uint64_t key[UNR];
+        bool ok[UNR];
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) {
+          const int64_t i = i0 + (int64_t)j * DT + tid;
+          ok[j] = i < L && !((forced[i >> 5] >> (i & 31)) & 1u);
+          key[j] = ok[j] ? score_key(s, is_f32, i) : 0;
         }
-        hist_add(hist, bin);
+#pragma unroll
+        for (int j = 0; j < UNR; ++j)
+          hist_add(hist, ok[j] && (key[j] & pmask) == prefix ? (int)((key[j] >> shift) & 255) : -1);
       }
       __syncthreads();
       pick_digit(hist, ms);
@@ -179,11 +185,9 @@ __global__ void __launch_bounds__(DT) topk_kernel(const void* __restrict__ score
 
 // ---------------------------------------------------------------- row dequantisation
 __device__ __forceinline__ double deq_elem(const uint8_t* pay, const __half* sc, const __half* zp,
-                                           int64_t row, int d, int bits, int gs, int D) {
-  const int payb = (D * bits + 7) / 8;
-  const int per = 8 / bits;
-  const int c = (pay[row * payb + d / per] >> ((d % per) * bits)) & ((1 << bits) - 1);
-  const int64_t pi = row * (D / gs) + d / gs;
+                                           int64_t row, int d, const RefPlanes& p) {
+  const int c = (pay[row * p.payb + (d >> p.lper)] >> ((d & ((1 << p.lper) - 1)) << p.lbits)) & ((1 << p.bits) - 1);
+  const int64_t pi = row * p.ngroups + (d >> p.lgs);
   return __dadd_rn(__dmul_rn((double)c, (double)__half2float(sc[pi])), (double)__half2float(zp[pi]));
 }
 
@@ -191,18 +195,18 @@ __device__ __forceinline__ double deq_elem(const uint8_t* pay, const __half* sc,
 __device__ __forceinline__ double key_elem(const RefPlanes& p, int64_t u, int64_t t, int d) {
   const int64_t row = u * p.L + t;
   if (p.bits == 16) return p.kfull[row * p.D + d];
-  if (!p.siq) return deq_elem(p.kq, p.ks, p.kz, row, d, p.bits, p.gs, p.D);
+  if (!p.siq) return deq_elem(p.kq, p.ks, p.kz, row, d, p);
   const int G = p.D / 4, rowb = (G + 1) / 2;
   const int g = d >> 2, i = d & 3;
   const int code = (p.codes[row * rowb + (g >> 1)] >> (4 * (g & 1))) & 15;
   const double sg = ((code >> (3 - i)) & 1) ? 1.0 : -1.0;
-  const double m = deq_elem(p.kq, p.ks, p.kz, row, d, p.bits, p.gs, p.D);
+  const double m = deq_elem(p.kq, p.ks, p.kz, row, d, p);
   return __dmul_rn(__dmul_rn(sg, p.alpha[u * p.D + d]), m);
 }
 __device__ __forceinline__ double value_elem(const RefPlanes& p, int64_t u, int64_t t, int d) {
   const int64_t row = u * p.L + t;
   if (p.bits == 16) return p.vfull[row * p.D + d];
-  return deq_elem(p.vq, p.vs, p.vz, row, d, p.bits, p.gs, p.D);
+  return deq_elem(p.vq, p.vs, p.vz, row, d, p);
 }
 
 // which = 0 values, 1 keys (cache.gather semantics for dynamic rows)
@@ -230,66 +234,139 @@ __device__ __forceinline__ const double* forced_row(const AttendArgs& a, int64_t
   return nullptr;
 }
 
-__global__ void __launch_bounds__(DT) attend_f64_kernel(AttendArgs a) {
-  __shared__ double red[DT];
+// ATT_SPLIT CTAs per (unit, head), CTA z taking the selected rows [z n / S, (z + 1) n / S):
+// a warp per row (32 warps, two rows in flight each; the rows are scattered over HBM), the
+// row's source resolved once (cache.gather), each lane owning channels lane + 32 j; logits by a
+// lane sum + warp tree (float64); the CTA's (max, sum, P V) written as a partial, and the last
+// CTA of the (unit, head) (a counter the launcher zeroes) merges the partials in CTA order.
+// Every order is fixed (deterministic); it differs from numpy's only by float64 rounding.
+constexpr int ATT_NT = 1024;
+constexpr int ATT_MAXD = 128;                 // channels: ATT_MAXD / 32 per lane
+__global__ void __launch_bounds__(ATT_NT) attend_f64_kernel(AttendArgs a) {
+  constexpr int NW = ATT_NT / 32, PER = ATT_MAXD / 32;
+  __shared__ double red[NW];
+  __shared__ double part[NW][ATT_MAXD];
+  __shared__ int last;
   const int64_t u = blockIdx.x;
-  const int h = blockIdx.y, tid = threadIdx.x, D = a.p.D;
+  const int h = blockIdx.y, z = blockIdx.z, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, D = a.p.D;
+  const int64_t uh = u * a.H + h;
   const int n = a.nsel[u];
+  const int i_lo = (int)((int64_t)z * n / ATT_SPLIT), i_hi = (int)((int64_t)(z + 1) * n / ATT_SPLIT);
   const int32_t* sel = a.sel + u * a.sel_stride;
-  const double* q = a.q + (u * a.H + h) * D;
-  double* lg = a.ws + (u * a.H + h) * (int64_t)a.sel_stride;
+  const double* q = a.q + uh * D;
+  double* lg = a.ws + uh * (int64_t)a.sel_stride;
   const double scale = sqrt((double)D);
+  double qv[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) qv[j] = 32 * j + lane < D ? q[32 * j + lane] : 0.0;
   double mx = -INFINITY;
-  for (int i = tid; i < n; i += DT) {
-    const int64_t t = sel[i];
-    const double* fr = forced_row(a, u, t, true);
-    double s = 0.0;
-    for (int d = 0; d < D; ++d) {
-      const double kd = fr ? fr[d] : key_elem(a.p, u, t, d);
-      s = __dadd_rn(s, __dmul_rn(kd, q[d]));
+  for (int i0 = i_lo + warp; i0 < i_hi; i0 += 2 * NW) {
+    double s[2] = {0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = i0 + r * NW;
+      if (i >= i_hi) continue;
+      const int64_t t = sel[i];
+      const double* fr = forced_row(a, u, t, true);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int d = 32 * j + lane;
+        if (d < D) s[r] = __fma_rn(fr ? fr[d] : key_elem(a.p, u, t, d), qv[j], s[r]);
+      }
     }
-    s = s / scale;
-    lg[i] = s;
-    mx = fmax(mx, s);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
+      const int i = i0 + r * NW;
+      if (i < i_hi) {
+        const double v = s[r] / scale;
+        if (lane == 0) lg[i] = v;
+        mx = fmax(mx, v);
+      }
+    }
   }
-  red[tid] = mx;
+  if (lane == 0) red[warp] = mx;
   __syncthreads();
-  for (int o = DT / 2; o > 0; o >>= 1) {
-    if (tid < o) red[tid] = fmax(red[tid], red[tid + o]);
-    __syncthreads();
-  }
   mx = red[0];
+  for (int w = 1; w < NW; ++w) mx = fmax(mx, red[w]);
   __syncthreads();
   double sum = 0.0;
-  for (int i = tid; i < n; i += DT) {
+  for (int i = i_lo + tid; i < i_hi; i += ATT_NT) {
     const double w = exp(lg[i] - mx);
     lg[i] = w;
     sum += w;
   }
-  red[tid] = sum;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) red[warp] = sum;
   __syncthreads();
-  for (int o = DT / 2; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
-  }
-  const double tot = red[0];
-  __syncthreads();
-  for (int d = tid; d < D; d += DT) {
-    double acc = 0.0;
-    for (int i = 0; i < n; ++i) {
+  double csum = 0.0;
+  for (int w = 0; w < NW; ++w) csum += red[w];
+  double acc[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) acc[j] = 0.0;
+  for (int i0 = i_lo + warp; i0 < i_hi; i0 += 2 * NW) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = i0 + r * NW;
+      if (i >= i_hi) continue;
       const int64_t t = sel[i];
       const double* fr = forced_row(a, u, t, false);
-      const double vd = fr ? fr[d] : value_elem(a.p, u, t, d);
-      acc += (lg[i] / tot) * vd;
+      const double w = lg[i];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int d = 32 * j + lane;
+        if (d < D) acc[j] = __fma_rn(w, fr ? fr[d] : value_elem(a.p, u, t, d), acc[j]);
+      }
     }
-    a.out[(u * a.H + h) * D + d] = acc;
   }
-  if (tid == 0 && a.chk) {
+#pragma unroll
+  for (int j = 0; j < PER; ++j)
+    if (32 * j + lane < D) part[warp][32 * j + lane] = acc[j];
+  __syncthreads();
+  // this CTA's partial: [max, sum, P V [D]]
+  double* pz = a.part + (uh * ATT_SPLIT + z) * (ATT_MAXD + 2);
+  for (int d = tid; d < D; d += ATT_NT) {
+    double o = part[0][d];
+    for (int w = 1; w < NW; ++w) o += part[w][d];
+    pz[2 + d] = o;
+  }
+  if (tid == 0) { pz[0] = mx; pz[1] = csum; }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(a.cnt + uh, 1u) == ATT_SPLIT - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double* p0 = a.part + uh * ATT_SPLIT * (ATT_MAXD + 2);
+  double M = -INFINITY;
+  for (int zz = 0; zz < ATT_SPLIT; ++zz) M = fmax(M, __ldcg(p0 + zz * (ATT_MAXD + 2)));
+  double tot = 0.0;
+  for (int zz = 0; zz < ATT_SPLIT; ++zz) {
+    const double mz = __ldcg(p0 + zz * (ATT_MAXD + 2));
+    if (mz != -INFINITY) tot += __ldcg(p0 + zz * (ATT_MAXD + 2) + 1) * exp(mz - M);
+  }
+  for (int d = tid; d < D; d += ATT_NT) {
+    double o = 0.0;
+    for (int zz = 0; zz < ATT_SPLIT; ++zz) {
+      const double mz = __ldcg(p0 + zz * (ATT_MAXD + 2));
+      if (mz != -INFINITY) o += __ldcg(p0 + zz * (ATT_MAXD + 2) + 2 + d) * exp(mz - M);
+    }
+    a.out[uh * D + d] = o / tot;
+  }
+  if (tid == 0 && a.chk) {            // the weights' sum: sum_z sum_z e^(m_z - M) / tot
     double c = 0.0;
-    for (int i = 0; i < n; ++i) c += lg[i] / tot;
-    a.chk[u * a.H + h] = c;
+    for (int zz = 0; zz < ATT_SPLIT; ++zz) {
+      const double mz = __ldcg(p0 + zz * (ATT_MAXD + 2));
+      if (mz != -INFINITY) c += __ldcg(p0 + zz * (ATT_MAXD + 2) + 1) * exp(mz - M) / tot;
+    }
+    a.chk[uh] = c;
   }
 }
+
+
+
 
 // ---------------------------------------------------------------- elementwise helpers
 // out[u][t][d] = x[u][t][d] - mu[u][d]  (apply_normalization, normalize.py:64-69)
@@ -331,7 +408,9 @@ cudaError_t launch_dequant_rows(const RefPlanes& p, int64_t U, const int64_t* ro
 }
 
 cudaError_t launch_attend_f64(const AttendArgs& a, int64_t U, cudaStream_t st) {
-  attend_f64_kernel<<<dim3((unsigned)U, a.H), DT, 0, st>>>(a);
+  cudaError_t e = cudaMemsetAsync(a.cnt, 0, (size_t)U * a.H * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  attend_f64_kernel<<<dim3((unsigned)U, a.H, ATT_SPLIT), ATT_NT, 0, st>>>(a);
   return cudaGetLastError();
 }
 
