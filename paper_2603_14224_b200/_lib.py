@@ -106,9 +106,15 @@ def call(name: str, *args) -> int:
     return rc
 
 
+_CUDA_SEEN = False
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2603_14224_b200 needs a CUDA device (B200, sm_100a); none is visible")
+    global _CUDA_SEEN
+    if not _CUDA_SEEN:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2603_14224_b200 needs a CUDA device (B200, sm_100a); none is visible")
+        _CUDA_SEEN = True
     return torch.device("cuda", torch.cuda.current_device())
 
 

@@ -611,8 +611,8 @@ class TokenSelection:
 
 
 def _as_index_set(indices, length: int, name: str):
-    """retrieval.py:116-124: (device index set, host copy or None).  Host inputs are checked
-    and deduplicated on the host."""
+    """retrieval.py:116-124: (device index set or None, host copy or None).  Host inputs are
+    checked and deduplicated on the host and not uploaded (the caller uploads what it needs)."""
     if isinstance(indices, torch.Tensor):
         idx = torch.unique(indices.to(_dev()).to(torch.int64).reshape(-1))
         if _DEVICE_CHECKS and idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= length):
@@ -621,7 +621,7 @@ def _as_index_set(indices, length: int, name: str):
     h = np.unique(np.asarray(indices if isinstance(indices, np.ndarray) else sorted(indices), dtype=np.int64))
     if h.size and (h[0] < 0 or h[-1] >= length):
         raise ValueError(f"{name} indices out of range [0, {length})")
-    return torch.as_tensor(h, device=_dev()), h
+    return None, h
 
 
 def top_k_select(scores, k: int, sink=(), recent=()) -> TokenSelection:
@@ -634,7 +634,15 @@ def top_k_select(scores, k: int, sink=(), recent=()) -> TokenSelection:
     L = int(s.shape[0])
     sink_idx, sink_h = _as_index_set(sink, L, "sink")
     recent_idx, recent_h = _as_index_set(recent, L, "recent")
-    forced = torch.unique(torch.cat([sink_idx, recent_idx])).to(torch.int32).contiguous()
+    if sink_h is not None and recent_h is not None:
+        # host sets: union on the host, one upload
+        forced = torch.as_tensor(np.union1d(sink_h, recent_h).astype(np.int32), device=_dev())
+    else:
+        if sink_idx is None:
+            sink_idx = torch.as_tensor(sink_h, device=_dev())
+        if recent_idx is None:
+            recent_idx = torch.as_tensor(recent_h, device=_dev())
+        forced = torch.unique(torch.cat([sink_idx, recent_idx])).to(torch.int32).contiguous()
     F = int(forced.numel())
     keff = min(k, L - F)
     n = F + max(keff, 0)
@@ -644,13 +652,14 @@ def top_k_select(scores, k: int, sink=(), recent=()) -> TokenSelection:
         ws = _ws(L_.lib().sikv_topk_workspace_bytes(1, L))
         L_.call("sikv_topk", L_.ptr(s.contiguous()), 0, 1, L, L_.ptr(forced) if F else None, F, k, L_.ptr(ws),
                 L_.ptr(out), max(n, 1), L_.ptr(counts), L_.stream())
-    if not recent_idx.numel():
+    n_sink = int(sink_h.size) if sink_h is not None else int(sink_idx.numel())
+    if sink_h is not None and recent_h is not None:
+        recent_only = int(np.isin(recent_h, sink_h, invert=True).sum()) if recent_h.size else 0
+    elif not recent_idx.numel():
         recent_only = 0
-    elif sink_h is not None and recent_h is not None:
-        recent_only = int(np.isin(recent_h, sink_h, invert=True).sum())
     else:
         recent_only = int(torch.isin(recent_idx, sink_idx, invert=True).sum())
-    return TokenSelection(indices=out[:n].to(torch.int64), sink_count=int(sink_idx.numel()),
+    return TokenSelection(indices=out[:n].to(torch.int64), sink_count=n_sink,
                           recent_count=recent_only, dynamic_count=max(keff, 0), _valid=True)
 
 
@@ -952,7 +961,7 @@ def sparse_attention(q, selection: TokenSelection, cache: SelfIndexingCache) -> 
     n = int(idx.numel())
     if not selection._valid and n and _DEVICE_CHECKS and (int(idx.min()) < 0 or int(idx.max()) >= cache.length):
         raise ValueError(f"indices out of range [0, {cache.length})")
-    cnt = torch.tensor([n], dtype=torch.int32, device=_dev())
+    cnt = torch.full((1,), n, dtype=torch.int32, device=_dev())
     ws = torch.empty((L_.lib().sikv_attend_f64_workspace_bytes(1, 1, n) + 7) // 8, dtype=torch.float64,
                      device=_dev())
     out = torch.empty(cache.dim, dtype=torch.float64, device=_dev())

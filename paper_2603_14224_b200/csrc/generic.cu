@@ -91,7 +91,6 @@ __global__ void __launch_bounds__(DT) topk_kernel(const void* __restrict__ score
                                                   uint32_t* __restrict__ ws, int32_t* __restrict__ out,
                                                   int out_stride, int32_t* __restrict__ counts) {
   __shared__ Misc ms_;
-  __shared__ int hist[256];
   Misc* ms = &ms_;
   const int tid = threadIdx.x;
   const int64_t u = blockIdx.x;
@@ -114,13 +113,23 @@ __global__ void __launch_bounds__(DT) topk_kernel(const void* __restrict__ score
   const int64_t ncand = L - nft;
   const int keff = (int)std::min<int64_t>(k, ncand);
   if (keff > 0) {
+    // 11-bit radix digits over the 64-bit keys (at most 6 passes), finished inside one warp as
+    // soon as the boundary digit holds <= 32 keys
+    constexpr int NB11 = 2048, UNR = 8;
+    __shared__ int hist11[NB11];
+    __shared__ uint64_t list64[32];
+    __shared__ uint64_t kth_s;
+    __shared__ int nlist;
     if (tid == 0) ms->rem_sel = keff;
-    uint64_t prefix = 0, pmask = 0;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      hist[tid] = 0;
+    uint64_t prefix = 0;
+    int hi = 64, need_eq = -1;
+    while (hi > 0) {
+      const int dbits = hi >= 11 ? 11 : hi;
+      const int sh = hi - dbits;
+      for (int i = tid; i < NB11; i += DT) hist11[i] = 0;
+      if (tid == 0) nlist = 0;
       __syncthreads();
-      // eight keys per thread in flight per step (the passes were load-latency bound)
-      constexpr int UNR = 8;
+      const uint64_t want = hi >= 64 ? 0ull : (prefix >> hi);
       for (int64_t i0 = 0; i0 < L; i0 += (int64_t)DT * UNR) {
         uint64_t key[UNR];
         bool ok[UNR];
@@ -132,20 +141,41 @@ __global__ void __launch_bounds__(DT) topk_kernel(const void* __restrict__ score
         }
 #pragma unroll
         for (int j = 0; j < UNR; ++j)
-          hist_add(hist, ok[j] && (key[j] & pmask) == prefix ? (int)((key[j] >> shift) & 255) : -1);
+          if (ok[j] && (hi >= 64 ? 0ull : (key[j] >> hi)) == want) atomicAdd(&hist11[(key[j] >> sh) & (NB11 - 1)], 1);
       }
       __syncthreads();
-      pick_digit(hist, ms);
-      __syncthreads();
-      const uint64_t dg = (uint64_t)ms->digit;
+      pick_digit_big<Cta256, NB11>(hist11, ms);
+      const int d = ms->digit, nb = hist11[d];
       const int rem = ms->rem_sel - ms->cnt_above;
       __syncthreads();                  // every read of ms precedes the update (racecheck-clean)
-      prefix |= dg << shift;
-      pmask |= (uint64_t)0xFF << shift;
+      prefix |= (uint64_t)d << sh;
+      hi = sh;
       if (tid == 0) ms->rem_sel = rem;
       __syncthreads();
+      if (hi > 0 && nb <= 32) {
+        // exact rank among the boundary digit's few keys
+        const uint64_t w2 = prefix >> hi;
+        for (int64_t i = tid; i < L; i += DT) {
+          if ((forced[i >> 5] >> (i & 31)) & 1u) continue;
+          const uint64_t key = score_key(s, is_f32, i);
+          if ((key >> hi) == w2) list64[atomicAdd(&nlist, 1)] = key;
+        }
+        __syncthreads();
+        if (tid < 32) {
+          const uint64_t v = tid < nb ? list64[tid] : 0ull;
+          int gtc = 0, eqc = 0;
+          for (int j = 0; j < nb; ++j) { gtc += list64[j] > v; eqc += list64[j] == v; }
+          __syncwarp();
+          if (tid < nb && gtc < rem && rem <= gtc + eqc) { kth_s = v; ms->digit = rem - gtc; }
+        }
+        __syncthreads();
+        prefix = kth_s;
+        need_eq = ms->digit;
+        __syncthreads();
+        break;
+      }
     }
-    const int need_eq = ms->rem_sel;
+    if (need_eq < 0) need_eq = ms->rem_sel;
     for (int64_t i = tid; i < L; i += DT) {
       if ((forced[i >> 5] >> (i & 31)) & 1u) continue;
       const uint64_t key = score_key(s, is_f32, i);
