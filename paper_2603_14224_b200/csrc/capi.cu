@@ -88,6 +88,18 @@ static int num_sms() {
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
   return v;
 }
+// The first runtime call of this library binds the calling thread's current context.  When
+// that first call is a kernel launch the runtime probes an invalid kernel handle once (a
+// reported API error under compute-sanitizer), so every launching entry point binds first.
+static void rt_bind() {
+  static thread_local bool bound = false;
+  if (bound) return;
+  cudaStreamCaptureMode m = cudaStreamCaptureModeRelaxed;   // legal while a capture is active
+  cudaThreadExchangeStreamCaptureMode(&m);
+  cudaFree(nullptr);
+  cudaThreadExchangeStreamCaptureMode(&m);
+  bound = true;
+}
 static int max_smem() {
   int dev = 0, v = 0;
   cudaGetDevice(&dev);
@@ -111,6 +123,7 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
                 uint16_t* kq_scales, uint16_t* kq_zeros, uint8_t* vq_ref, uint16_t* vq_scales,
                 uint16_t* vq_zeros, uint8_t* signs_fast, uint8_t* recs_fast, void* workspace,
                 size_t workspace_bytes, int* status_dev, void* stream) {
+  rt_bind();
   REQUIRE(keys && values && mu64 && alpha64 && status_dev, SIKV_EINVAL, "null required pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "keys must contain at least one row");
@@ -150,6 +163,7 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
 int sikv_gather_rows(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
                      int64_t dim, const int32_t* idx, int64_t n, const double* mu64, void* out_k, void* out_v,
                      int out_f64, void* stream) {
+  rt_bind();
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "bad in_dtype");
   REQUIRE(n >= 0 && units >= 1 && tokens >= 1 && dim >= 1, SIKV_EINVAL, "bad shape");
   if (n == 0) return SIKV_OK;
@@ -162,6 +176,7 @@ int sikv_gather_rows(const void* keys, const void* values, int in_dtype, int64_t
 int sikv_append(const void* k, const void* v, int in_dtype, int64_t units, int64_t dim, const double* mu64,
                 void* recent_k, void* recent_v, int64_t rcap, int64_t pos, int out_f64, int* status_dev,
                 void* stream) {
+  rt_bind();
   REQUIRE(k && v && mu64 && recent_k && recent_v && status_dev, SIKV_EINVAL, "null pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "bad in_dtype");
   REQUIRE(pos >= 0 && pos < rcap, SIKV_EINVAL, "recent buffer full (pos >= rcap)");
@@ -190,6 +205,7 @@ int sikv_decode_smem_bytes(int64_t tokens, int k, int sinks, int gq, int cap) {
 
 int sikv_pack16(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
                 const double* mu64, const float* alpha32, uint8_t* recs16, int* status_dev, void* stream) {
+  rt_bind();
   REQUIRE(keys && values && mu64 && alpha32 && recs16, SIKV_EINVAL, "null pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   REQUIRE(units >= 0 && tokens >= 0, SIKV_EINVAL, "bad shape");
@@ -206,6 +222,7 @@ int sikv_pack_forced(const float* sink_k, const float* sink_v, int sinks, const 
                      const float* recent_v, int64_t rcap, const int32_t* recent_n, int recent, const float* alpha32,
                      int64_t units, uint32_t* forced_frag, int frag_blocks, int row_begin, int row_end,
                      int* status_dev, void* stream) {
+  rt_bind();
   REQUIRE(alpha32 && forced_frag, SIKV_EINVAL, "null pointer");
   REQUIRE(sinks == 0 || (sink_k && sink_v), SIKV_EINVAL, "sink rows missing");
   REQUIRE(rcap == 0 || (recent_k && recent_v), SIKV_EINVAL, "recent rows missing");
@@ -222,6 +239,7 @@ int sikv_append_forced(const void* k, const void* v, int in_dtype, int64_t n, co
                        const double* mu64, const float* alpha32, const float* sink_k, const float* sink_v, int sinks,
                        float* recent_k, float* recent_v, int64_t rcap, int32_t* recent_n, uint32_t* forced_frag,
                        int frag_blocks, int* status_dev, void* stream) {
+  rt_bind();
   REQUIRE(k && v && mu64 && alpha32 && recent_k && recent_v && recent_n && forced_frag, SIKV_EINVAL, "null pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   REQUIRE(n >= 0 && rcap >= 1, SIKV_EINVAL, "bad row count or capacity");
@@ -250,6 +268,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
                      int32_t* diag, void* workspace, size_t workspace_bytes, const int32_t* unit_map,
                      int lut_mode, int kernel, void* stream) {
+  rt_bind();
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
@@ -344,11 +363,13 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
 }
 
 int sikv_debug_set_attend_skip(int v) {
+  rt_bind();
   cudaError_t e = set_k1_skip(v);
   return cuda_ret(e, "sikv_debug_set_attend_skip");
 }
 
 int sikv_debug_set_decode_profile(void* clocks) {
+  rt_bind();
   cudaError_t e = set_decode_profile((long long*)clocks);
   if (e == cudaSuccess) e = set_decode_two_profile((long long*)clocks);
   if (e == cudaSuccess) e = set_decode_split_profile((long long*)clocks);
@@ -357,6 +378,7 @@ int sikv_debug_set_decode_profile(void* clocks) {
 
 int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float* q, int gq, int64_t units,
                     int64_t tokens, int lut_mode, float* out, void* stream) {
+  rt_bind();
   REQUIRE(signs_fast && cent32 && q && out, SIKV_EINVAL, "null pointer");
   REQUIRE(gq >= 1 && units >= 1 && tokens >= 1, SIKV_EINVAL, "bad shape");
   return cuda_ret(launch_score_fast(signs_fast, cent32, q, gq, units, tokens, lut_mode, out, (cudaStream_t)stream),
@@ -365,6 +387,7 @@ int sikv_score_fast(const uint8_t* signs_fast, const float* cent32, const float*
 
 int sikv_build_lut_f64(const double* q, const double* cent64, int64_t units, int groups, int sign_only,
                        double* out, void* stream) {
+  rt_bind();
   REQUIRE(q && out && (sign_only || cent64), SIKV_EINVAL, "null pointer");
   REQUIRE(groups >= 1 && units >= 1, SIKV_EINVAL, "bad shape");
   return cuda_ret(launch_lut_f64(q, cent64, units, groups, sign_only, out, (cudaStream_t)stream),
@@ -373,6 +396,7 @@ int sikv_build_lut_f64(const double* q, const double* cent64, int64_t units, int
 
 int sikv_score_f64(const double* lut, const uint8_t* codes_ref, int64_t units, int groups, int64_t tokens,
                    double* out, void* stream) {
+  rt_bind();
   REQUIRE(lut && codes_ref && out, SIKV_EINVAL, "null pointer");
   REQUIRE(groups >= 1 && groups <= 128, SIKV_EUNSUPPORTED, "groups must be 1..128");
   return cuda_ret(launch_score_f64(lut, codes_ref, units, groups, tokens, out, (cudaStream_t)stream),
@@ -391,6 +415,7 @@ size_t sikv_window_sinks_workspace_bytes(int64_t units, int64_t tokens, int wind
 int sikv_window_sinks(const void* keys, int in_dtype, int64_t units, int64_t tokens, int64_t dim, const double* mu64,
                       const double* window, int window_n, int count, int pool_width, int32_t* sink_idx,
                       void* workspace, size_t workspace_bytes, void* stream) {
+  rt_bind();
   REQUIRE(keys && mu64 && window && sink_idx && workspace, SIKV_EINVAL, "null pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "in_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   REQUIRE(units >= 0 && tokens >= 1, SIKV_EINVAL, "keys must have at least one row");
@@ -415,6 +440,7 @@ int sikv_window_sinks(const void* keys, int in_dtype, int64_t units, int64_t tok
 
 int sikv_topk(const void* scores, int scores_f32, int64_t units, int64_t tokens, const int32_t* forced,
               int nforced, int k, void* workspace, int32_t* out, int out_stride, int32_t* counts, void* stream) {
+  rt_bind();
   REQUIRE(scores && workspace && out && counts, SIKV_EINVAL, "null pointer");
   REQUIRE(k >= 0, SIKV_EINVAL, "k must be non-negative");
   REQUIRE(nforced >= 0 && (nforced == 0 || forced), SIKV_EINVAL, "bad forced list");
@@ -461,6 +487,7 @@ int sikv_dequant_rows(const uint8_t* codes_ref, const uint8_t* kq_ref, const uin
                       const uint16_t* vq_zeros, const double* kfull, const double* vfull, const double* alpha64,
                       int bits, int group_size, int sign_in_quant, int64_t units, int64_t tokens, int64_t dim,
                       const int64_t* rows, int64_t n, int which, double* out, void* stream) {
+  rt_bind();
   RefPlanes p = make_planes(codes_ref, kq_ref, kq_scales, kq_zeros, vq_ref, vq_scales, vq_zeros, kfull, vfull,
                             alpha64, bits, group_size, sign_in_quant, tokens, dim);
   if (which == 0 && bits != 16) {
@@ -486,6 +513,7 @@ int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint1
                     const int32_t* sink_idx, int sinks, const double* sink_k, const double* sink_v,
                     const double* recent_k, const double* recent_v, int64_t rcap, double* ws, double* out,
                     double* chk, void* stream) {
+  rt_bind();
   RefPlanes p = make_planes(codes_ref, kq_ref, kq_scales, kq_zeros, vq_ref, vq_scales, vq_zeros, kfull, vfull,
                             alpha64, bits, group_size, sign_in_quant, tokens, dim);
   int rc = check_planes(p);
@@ -504,6 +532,7 @@ int sikv_attend_f64(const uint8_t* codes_ref, const uint8_t* kq_ref, const uint1
 
 int sikv_center(const void* x, int in_dtype, int64_t units, int64_t tokens, int64_t dim, const double* mu64,
                 double* out, void* stream) {
+  rt_bind();
   REQUIRE(x && mu64 && out, SIKV_EINVAL, "null pointer");
   REQUIRE(good_dtype(in_dtype), SIKV_EINVAL, "bad in_dtype");
   return cuda_ret(launch_center(x, in_dtype, units, tokens, (int)dim, mu64, out, (cudaStream_t)stream),

@@ -321,6 +321,28 @@ class TestRetrieval:   # test_retrieval.py
                 got = sk.top_k_select(s, k, sink=sink)
                 assert N(got.indices).tolist() == O.top_k(s, k, sink=sink)[0].tolist()
 
+    def test_top_k_radix_paths_vs_oracle(self):
+        """The 11-bit radix passes: continuous scores (one-warp finish after the first digits),
+        heavy ties and -inf tails (every pass), forced sets given as host sets and as device
+        tensors (both the host union and the device union)."""
+        import torch
+        rng = np.random.default_rng(11)
+        for L in (2048, 40000, 131072):
+            cont = rng.standard_normal(L)
+            tied = np.round(rng.standard_normal(L) * 2) / 2
+            tail = np.where(rng.random(L) < 0.3, -np.inf, rng.standard_normal(L))
+            for s in (cont, tied, tail):
+                for k in (1, 31, 33, L // 16, L - 5):
+                    sink = set(rng.integers(0, L, size=64).tolist())
+                    recent = set(range(L - 16, L))
+                    ref = O.top_k(s, k, sink=sink, recent=recent)[0].tolist()
+                    got = sk.top_k_select(s, k, sink=sink, recent=recent)
+                    assert N(got.indices).tolist() == ref, (L, k)
+                    dsink = torch.tensor(sorted(sink), device="cuda")
+                    got = sk.top_k_select(torch.tensor(s, device="cuda"), k, sink=dsink, recent=recent)
+                    assert N(got.indices).tolist() == ref, (L, k, "device sink")
+                    assert got.sink_count == len(sink) and got.recent_count == len(recent - sink)
+
     def test_dense_scores(self):
         """retrieval.py:80-89: the exact q . K'^T oracle (float64) and its validation / tallies."""
         rng = np.random.default_rng(7)
