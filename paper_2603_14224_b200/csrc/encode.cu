@@ -612,10 +612,33 @@ __device__ __forceinline__ void f2unpack(unsigned long long v, float& lo, float&
 // bound (0 = the estimates are exact), [mmin, mmax]: range of m, exact(n): float64 value.
 // emit(n, code) ORs a code into the caller's packed words (n is always a compile-time constant);
 // reset() clears them; fix[32] is this thread's shared-memory scratch for the exact codes.
-template <int BITS, typename Exact, typename Emit, typename Reset>
-__device__ __forceinline__ void quant_group32(const float (&m)[32], float E, float mmin, float mmax, Exact&& exact,
+// Per-element code decision of the slow path (the fast path's float32 estimate, exact float64
+// near rounding boundaries); shared by quant_group32 and the warp-cooperative fix-up below.
+struct QgRound {
+  float iqs, c0, B;
+  double zpd, qsd;
+};
+template <int BITS>
+__device__ __forceinline__ uint32_t qg_code(float m, double exact, const QgRound& r) {
+  constexpr int levels = (1 << BITS) - 1;
+  constexpr float kRnd = 12582912.f;
+  const float x = fmaf(m, r.iqs, r.c0);
+  const float y = __fadd_rd(x, kRnd);
+  const float fr = x - (y - kRnd);
+  if (fr < r.B || fr > 1.f - r.B) {
+    const double ce = floor((exact - r.zpd) / r.qsd + 0.5);
+    return (uint32_t)fmin(fmax(ce, 0.0), (double)levels);
+  }
+  return (uint32_t)min(max((int)(__float_as_uint(y) - 0x4B400000u), 0), levels);
+}
+
+// Defer: when the whole-group test fails, return true with the rounding parameters in *rp
+// (the caller recomputes the group's codes cooperatively) instead of running the per-element
+// path on this thread.
+template <int BITS, bool Defer = false, typename Exact, typename Emit, typename Reset>
+__device__ __forceinline__ bool quant_group32(const float (&m)[32], float E, float mmin, float mmax, Exact&& exact,
                                               Emit&& emit, Reset&& reset, uint8_t* fix, __half& qs16, __half& zp16,
-                                              double& mxo) {
+                                              double& mxo, QgRound* rp = nullptr) {
   constexpr int levels = (1 << BITS) - 1;
   double mn, mx;
   if (E == 0.f) {
@@ -645,7 +668,7 @@ __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, flo
   double qsd = (double)__half2float(qs16);
   const double zpd = (double)__half2float(zp16);
   if (qs > 0.0 && qsd == 0.0) { qs16 = __float2half(5.9604644775390625e-08f); qsd = 5.9604644775390625e-08; }
-  if (!(qsd > 0.0)) return;                        // all codes 0
+  if (!(qsd > 0.0)) return false;                  // all codes 0
   // x = m * iqs + (0.5 - zp * iqs) estimates T = (exact - zp) / qs + 0.5 with
   // |x - T| <= E iqs (1+2^-23) + |m| iqs 2^-23 + |zp iqs| 2^-22.5 + |x| 2^-24 + 2^-25 < B;
   // codes whose x lies within B of an integer are recomputed exactly afterwards.
@@ -679,7 +702,11 @@ __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, flo
       emit(n, (uint32_t)c0i);
       emit(n + 1, (uint32_t)c1i);
     }
-    if (!(amax > 0.5f - B - 1e-7f)) return;
+    if (!(amax > 0.5f - B - 1e-7f)) return false;
+    if constexpr (Defer) {
+      *rp = QgRound{iqs, c0, B, zpd, qsd};
+      return true;
+    }
     reset();                                       // rare: redo with per-element decisions
   }
   uint32_t amb = 0;
@@ -704,6 +731,7 @@ __device__ __forceinline__ void quant_group32(const float (&m)[32], float E, flo
     for (int n = 0; n < 32; ++n)
       if ((amb >> n) & 1u) emit(n, (uint32_t)fix[n]);
   }
+  return false;
 }
 
 struct QgSmem {
@@ -830,8 +858,34 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
           for (int q = 0; q < 8; ++q) vp8[q] = 0;
         };
         double vmx;
-        quant_group32<BITS>(vf, 0.f, vmin, vmax, [&](int n) -> double { return (double)load1<DTY>(a.values, row + n); },
-                            vemit, vreset, s_fix[tid], vqs, vzp, vmx);
+        QgRound vr2;
+        const bool vfail = quant_group32<BITS, true>(vf, 0.f, vmin, vmax, [&](int) -> double { return 0.0; }, vemit,
+                                                     vreset, s_fix[tid], vqs, vzp, vmx, &vr2);
+        // Groups whose estimates come near a rounding boundary (mostly exact ties of the bf16
+        // grid, ~2% of groups) are recomputed by the whole warp, one element per lane, instead
+        // of serially by their own thread while the other 31 lanes wait.
+        for (uint32_t fm = __ballot_sync(0xffffffffu, vfail); fm; fm &= fm - 1) {
+          const int src = __ffs((int)fm) - 1;
+          const int64_t srow = __shfl_sync(0xffffffffu, row, src);
+          QgRound rr;
+          rr.iqs = __shfl_sync(0xffffffffu, vr2.iqs, src);
+          rr.c0 = __shfl_sync(0xffffffffu, vr2.c0, src);
+          rr.B = __shfl_sync(0xffffffffu, vr2.B, src);
+          rr.zpd = __shfl_sync(0xffffffffu, vr2.zpd, src);
+          rr.qsd = __shfl_sync(0xffffffffu, vr2.qsd, src);
+          const float mv = load1<DTY>(a.values, srow + lane);
+          uint8_t* sf = s_fix[(tid & ~31) + src];
+          sf[lane] = (uint8_t)qg_code<BITS>(mv, (double)mv, rr);
+          __syncwarp();
+          if (lane == src) {
+            vreset();
+            const uint4 c0 = *reinterpret_cast<const uint4*>(sf), c1 = *reinterpret_cast<const uint4*>(sf + 16);
+            const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+            for (int n = 0; n < 32; ++n) vemit(n, (cw[n >> 2] >> (8 * (n & 3))) & 0xFFu);
+          }
+          __syncwarp();
+        }
       }
       if (valid) {
         const bool kbad = !isfinite(__half2float(kqs)) || !isfinite(__half2float(kzp));
