@@ -734,17 +734,27 @@ __device__ __forceinline__ bool quant_group32(const float (&m)[32], float E, flo
   return false;
 }
 
+// Staged K of the 64-token blocks (skewed columns) and their reference code words.  bf16 inputs
+// are staged as their own 16-bit words, double-buffered so that the codebook walk over block b
+// and the quantisation of block b + 1 need no barrier between them; float32 inputs are staged
+// as floats, single-buffered.
+template <int DTY>
 struct QgSmem {
-  float x[QG_TOK][130];                           // staged K of one 64-token block (skewed columns)
-  uint32_t cw[QG_TOK][4];                         // reference code words of the block
+  static constexpr int NBUF = DTY == IN_BF16 ? 2 : 1;
+  using XT = typename std::conditional<DTY == IN_BF16, uint16_t, float>::type;
+  XT x[NBUF][QG_TOK][130];
+  uint32_t cw[NBUF][QG_TOK][4];
   double acc[4][16][FD];                          // codebook sums per token quarter
   int cnt[16][32];
 };
+__device__ __forceinline__ float qg_xval(uint16_t v) { return __uint_as_float((uint32_t)v << 16); }
+__device__ __forceinline__ float qg_xval(float v) { return v; }
 
 template <int DTY, int BITS>
 __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
   extern __shared__ __align__(16) unsigned char qg_smem[];
-  QgSmem& S = *reinterpret_cast<QgSmem*>(qg_smem);
+  using Smem = QgSmem<DTY>;
+  Smem& S = *reinterpret_cast<Smem*>(qg_smem);
   auto& s_x = S.x;
   auto& s_cw = S.cw;
   __shared__ float4 s_c[4][33];                   // (sign threshold, mu32, 1/alpha or 1, -) per channel
@@ -777,7 +787,7 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
   const double wmu0 = a.mu64[u * FD + 2 * wp], wmu1 = a.mu64[u * FD + 2 * wp + 1];
   const int64_t tile0 = (int64_t)blockIdx.x * a.tile, tile1 = min(a.L, tile0 + a.tile);
   __syncthreads();
-  for (int64_t b0 = tile0; b0 < tile1; b0 += QG_TOK) {
+  auto quant_block = [&](const int64_t b0, const int buf) {
     const int64_t t = b0 + tl;
     const bool valid = t < tile1;
     const int64_t row = (u * a.L + (valid ? t : 0)) * FD + 32 * j;
@@ -803,9 +813,16 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
     uint32_t cw = __byte_perm(__brev(geb), 0, 0x0123);
     cw = ((cw >> 4) & 0x0F0F0F0Fu) | ((cw & 0x0F0F0F0Fu) << 4);
     // stage K and the codes for the codebook walk (channel 32j + n at 32j + ((n + 8j) & 31))
-    s_cw[tl][j] = cw;
+    s_cw[buf][tl][j] = cw;
+    if constexpr (DTY == IN_BF16) {
+      // element pairs (2 n2, 2 n2 + 1) stay adjacent under the skew: one word per pair
+      uint32_t* xw = reinterpret_cast<uint32_t*>(&s_x[buf][tl][32 * j]);
 #pragma unroll
-    for (int n = 0; n < 32; ++n) s_x[tl][32 * j + ((n + 8 * j) & 31)] = kr[n];   // 2-way bank conflict at most
+      for (int n2 = 0; n2 < 16; ++n2) xw[(n2 + 4 * j) & 15] = kr.w[n2];
+    } else {
+#pragma unroll
+      for (int n = 0; n < 32; ++n) s_x[buf][tl][32 * j + ((n + 8 * j) & 31)] = kr[n];   // 2-way bank conflict at most
+    }
     // packed codes: reference words (element n at bit BITS*n of the group's byte string) and,
     // for BITS == 2, this group's share of the fast record words
     constexpr int PER = BITS > 0 ? 32 / BITS : 32;
@@ -819,7 +836,7 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         const float E = __fmaf_ru(fmaxf(fabsf(kmin), fabsf(kmax)), 7.5e-7f, s_e0max[j]);
         auto kexact = [&](int n) -> double {
           // the K value staged for the codebook walk (the same float; no global reload)
-          const double kd = (double)s_x[tl][32 * j + ((n + 8 * j) & 31)] - s_mu[j][n];
+          const double kd = (double)qg_xval(s_x[buf][tl][32 * j + ((n + 8 * j) & 31)]) - s_mu[j][n];
           if (!siq) return kd;
           const double al = s_al[j][n];
           return al == 0.0 ? 0.0 : fabs(kd) / al;
@@ -956,10 +973,10 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
         }
       }
     }
-    // codebook walk: thread (channel pair wp, quarter wq) adds K' = fl64(K - mu) of its 16
-    // tokens, in token order, to the accumulators of each token's code (codebook.py:128-160)
-    __syncthreads();
-    {
+  };
+  // codebook walk: thread (channel pair wp, quarter wq) adds K' = fl64(K - mu) of its 16
+  // tokens, in token order, to the accumulators of each token's code (codebook.py:128-160)
+  auto walk_block = [&](const int64_t b0, const int buf) {
       const int nt = (int)min((int64_t)QG_TOK, tile1 - b0);
       const int jw = wp >> 4, nw = 2 * (wp & 15);
       const int pos = 32 * jw + ((nw + 8 * jw) & 31), sh = 4 * (nw >> 2);
@@ -967,8 +984,14 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
       int* cntw = &S.cnt[0][wp >> 1];
       const bool counter = (wp & 1) == 0;
       auto step = [&](int i) {
-        const uint32_t code = (s_cw[i][jw] >> sh) & 15u;
-        const float2 x = *reinterpret_cast<const float2*>(&s_x[i][pos]);
+        const uint32_t code = (s_cw[buf][i][jw] >> sh) & 15u;
+        float2 x;
+        if constexpr (DTY == IN_BF16) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(&s_x[buf][i][pos]);
+          x = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+        } else {
+          x = *reinterpret_cast<const float2*>(&s_x[buf][i][pos]);
+        }
         double2 v = accw[code * (FD / 2)];
         v.x += (double)x.x - wmu0;
         v.y += (double)x.y - wmu1;
@@ -981,8 +1004,18 @@ __global__ void __launch_bounds__(256, 2) quant_group_kernel(PackArgs a) {
       } else {
         for (int i = 16 * wq; i < 16 * wq + 16 && i < nt; ++i) step(i);
       }
-    }
+      };
+  constexpr int NB = Smem::NBUF;
+  if (tile0 < tile1) quant_block(tile0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t b0 = tile0; b0 < tile1; b0 += QG_TOK) {
+    walk_block(b0, buf);
+    const int nbuf = NB == 2 ? buf ^ 1 : 0;
+    if constexpr (NB == 1) __syncthreads();        // the next block overwrites the staging
+    if (b0 + QG_TOK < tile1) quant_block(b0 + QG_TOK, nbuf);
     __syncthreads();
+    buf = nbuf;
   }
   // this tile's partial sums, layout [g][code][i], quarters combined in fixed order
   double* outp = a.cb_part + (u * a.ntiles + blockIdx.x) * (int64_t)(32 * 64);
@@ -1129,8 +1162,8 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
     qa.tile = CB_TILE;
     qa.ntiles = cnt_tiles;
     const dim3 qg((unsigned)cnt_tiles, (unsigned)U);
-    const int qsm = (int)sizeof(QgSmem);
     cudaError_t e = cudaSuccess;
+    int qsm = 0;
     auto go = [&](auto kern) {
       if (e != cudaSuccess) return;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, qsm);
@@ -1138,6 +1171,7 @@ cudaError_t launch_encode(const void* keys, const void* values, int dt, int64_t 
     };
     auto run = [&](auto dty) {
       constexpr int DTY = decltype(dty)::value;
+      qsm = (int)sizeof(QgSmem<DTY>);
       switch (bits) {
         case 1: go(quant_group_kernel<DTY, 1>); break;
         case 2: go(quant_group_kernel<DTY, 2>); break;
