@@ -210,7 +210,7 @@ def run_ours(args, rank, world, cfg):
     import torch.distributed as dist
 
     from paper_2603_14224_b200 import batch as B
-    from paper_2603_14224_b200.shard import ShardPlan, gather_outputs
+    from paper_2603_14224_b200.shard import OutputExchange, ShardPlan, gather_outputs
 
     layers, batch, kvh, gq, L, k, label = cfg
     units = layers * batch * kvh
@@ -228,12 +228,20 @@ def run_ours(args, rank, world, cfg):
 
     per_head = args.policy == "per-head"
     decode = B.decode_step_per_head if per_head else B.decode_step
+    # the output all-gather (north_star: "NCCL over NVLink only for the final output
+    # all-gather"): fused into the decode's attention epilogue over NVLink peer memory
+    # (OutputExchange, CUDA IPC) by default, or NCCL all_gather_into_tensor + reassembly
+    xch = OutputExchange(plan, gq, rank, dev) if world > 1 and args.gather == "fused" else None
 
     def step(qq, o=out):
-        decode(cb, qq, k, out=o)
-        if world > 1:   # sharded outputs -> [layers, batch, H_q, D] on every rank (NCCL all-gather)
-            out16.copy_(o)
-            gather_outputs(out16, layers, batch, kvh, world, out=model_out, flat=flat)
+        if xch is not None:
+            decode(cb, qq, k, out=o, exchange=xch)
+            xch.wait()
+        else:
+            decode(cb, qq, k, out=o)
+            if world > 1:   # sharded outputs -> [layers, batch, H_q, D] on every rank (NCCL all-gather)
+                out16.copy_(o)
+                gather_outputs(out16, layers, batch, kvh, world, out=model_out, flat=flat)
 
     # correctness spot check on this rank (selection of unit 0 vs float32 restatement is in tests)
     for _ in range(args.warmup):
@@ -324,7 +332,9 @@ def run_ours(args, rank, world, cfg):
     fallbacks = int(((res.diag & 4) != 0).sum().item())
     from paper_2603_14224_b200 import _lib as L_
     path = int(L_.lib().sikv_decode_last_kernel())
-    launches_per_step = 2 if path == 4 else 1
+    launches_per_step = (2 if path == 4 else 1) + (0 if xch is None else (1 if path == 4 else 2))
+    if world > 1:
+        dist.barrier()         # no rank frees its exchange buffers while a peer still writes them
 
     if rank != 0:
         return None
@@ -349,7 +359,10 @@ def run_ours(args, rank, world, cfg):
         "dtype": "u2 K/V payload, f32 scores, f16 mma operands / f32 accumulate",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU), random-init caches",
         "config": dict(decode_config(args.config, world), policy=args.policy, bits=args.bits,
-                       keys="direct" if args.direct_keys else "sign-in-quant"),
+                       keys="direct" if args.direct_keys else "sign-in-quant",
+                       **({"output_gather": "fused into the attention epilogue (NVLink peer stores, CUDA IPC)"
+                           if xch is not None else "NCCL all_gather_into_tensor + reassembly"}
+                          if world > 1 else {})),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                      "traffic": traffic["bytes"] if traffic else None,
@@ -537,6 +550,8 @@ def main():
     ap.add_argument("--policy", default="group-sum", choices=["group-sum", "per-head"],
                     help="GQA selection policy: one selection per KV head from the summed queries "
                          "(default), or one per query head (SURVEY.md 8d)")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: output all-gather fused into the decode (peer stores) or NCCL")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="units in the CPU-baseline sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -45,7 +45,7 @@ extern "C" {
 #define SIKV_EUNSUPPORTED 3
 
 const char* sikv_last_error(void);
-int sikv_abi_version(void);   /* 7 */
+int sikv_abi_version(void);   /* 8 */
 
 /* ---------------------------------------------------------------- encoder (prefill)
  * replaces: compute_channel_stats   normalize.py:56-61
@@ -135,6 +135,44 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
                      size_t workspace_bytes, const int32_t* unit_map, int lut_mode, int kernel,
                      void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU output exchange
+ * The head x batch sharded decode ("NCCL over NVLink only for the final
+ * output all-gather") with the all-gather fused into the decode instead: every rank's
+ * attention epilogue stores its units' outputs as bf16 straight into every rank's model-layout
+ * buffer over NVLink (peer pointers from CUDA IPC), then releases a per-rank arrival counter.
+ * out[r] is rank r's bf16 buffer [units_total][gq][128] (row = global unit id, i.e. the
+ * [layers][batch][kv_heads * gq][128] model layout); flag[r] its u64 counter; npeers <= 8
+ * (this rank included); unit_gid [units] (device) the global id of each local unit.  After
+ * step e (1, 2, ...) of every rank, rank r's counter reaches e * units_total * gq (rows; the
+ * per-q-head policy pushes units_total * gq one-row query units): sikv_exchange_wait enqueues
+ * that wait on a stream. */
+#define SIKV_MAX_PEERS 8
+typedef struct {
+  int npeers;
+  void* out[SIKV_MAX_PEERS];
+  unsigned long long* flag[SIKV_MAX_PEERS];
+  const int32_t* unit_gid;
+} sikv_exchange;
+
+/* sikv_decode_step plus the fused output exchange (xchg NULL or npeers 0: none).  The two-
+ * kernel path stores from its attention epilogue; the other paths from one push kernel
+ * launched after the decode kernel on the same stream. */
+int sikv_decode_step_x(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
+                       const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
+                       int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
+                       int64_t tokens, int gq, int k, int cap, float* out, float* lse, int32_t* sel,
+                       int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
+                       size_t workspace_bytes, const int32_t* unit_map, int lut_mode, int kernel,
+                       const sikv_exchange* xchg, void* stream);
+/* enqueue on `stream` a wait until *flag >= target (system-scope acquire) */
+int sikv_exchange_wait(const unsigned long long* flag, unsigned long long target, void* stream);
+/* CUDA IPC for the peer buffers: the 64-byte handle of the allocation holding dev_ptr and
+ * dev_ptr's offset in it; the mapping of another process's handle into this one (the
+ * allocation's base; add the offset; peer access enabled lazily) / its release */
+int sikv_ipc_handle(const void* dev_ptr, void* handle64, size_t* offset);
+int sikv_ipc_open(const void* handle64, void** dev_ptr);
+int sikv_ipc_close(void* dev_ptr);
 
 /* the decode path (1, 3 or 4, as the kernel argument) the last sikv_decode_step of this host
  * thread launched; the two-kernel path (4) starts two kernels per step, the others one */

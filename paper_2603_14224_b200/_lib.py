@@ -37,6 +37,12 @@ _SIGS = {
     "sikv_decode_smem_bytes": (I, [I64, I, I, I, I]),
     "sikv_decode_default_cap": (I, [I64, I, I]),
     "sikv_decode_step": (I, [P, P, P, P, P, I, P, I, P, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, P, I, I, P]),
+    "sikv_decode_step_x": (I, [P, P, P, P, P, I, P, I, P, I, P, I64, I64, I, I, I, P, P, P, I, P, P, P, SZ, P, I, I,
+                               P, P]),
+    "sikv_exchange_wait": (I, [P, C.c_uint64, P]),
+    "sikv_ipc_handle": (I, [P, P, P]),
+    "sikv_ipc_open": (I, [P, P]),
+    "sikv_ipc_close": (I, [P]),
     "sikv_decode_workspace_bytes": (SZ, [I64, I64]),
     "sikv_decode_workspace_bytes_k": (SZ, [I64, I64, I, I]),
     "sikv_decode_last_kernel": (I, []),
@@ -58,6 +64,14 @@ _SIGS = {
     "sikv_center": (I, [P, I, I64, I64, I64, P, P, P]),
 }
 
+MAX_PEERS = 8
+
+
+class Exchange(C.Structure):
+    """sikv_exchange (include/sikv_b200.h): the fused multi-GPU output exchange."""
+    _fields_ = [("npeers", C.c_int), ("out", P * MAX_PEERS), ("flag", P * MAX_PEERS), ("unit_gid", P)]
+
+
 _lib = None
 
 
@@ -68,6 +82,8 @@ def lib() -> C.CDLL:
             raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2603_14224_b200.build`")
         h = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if "SIKV_LIB" in os.environ and not hasattr(h, name):
+                continue              # an older A/B build without this entry point
             f = getattr(h, name)
             f.restype = res
             f.argtypes = args

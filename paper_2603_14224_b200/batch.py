@@ -16,6 +16,8 @@ for every query head of the GQA group (cache.py:290-309, attention.py:52-62), fu
 
 from __future__ import annotations
 
+import ctypes as C
+
 from dataclasses import dataclass, field
 
 import torch
@@ -299,7 +301,7 @@ def _workspace(units: int, tokens: int, k: int, sinks: int, device) -> torch.Ten
 def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_selection: bool = False,
                 with_lse: bool = False, with_diag: bool = False, out: torch.Tensor | None = None,
                 sel_buf: torch.Tensor | None = None, kernel: int = 0, append=None,
-                sign_only: bool = False, unit_map=None) -> DecodeOutput:
+                sign_only: bool = False, unit_map=None, exchange=None) -> DecodeOutput:
     """One fused decode step over all units; q is [U, Gq, 128] (float32 or bf16).
 
     unit_map ([Uq] ints, each < cb.units): query unit i reads cache unit unit_map[i] (q, out and
@@ -308,7 +310,10 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
     retrieval.py:54-62).  append=(k, v) first appends one token per unit ([U, 128] rows, append_batch without the
     status sync), so a generation step is one call.  kernel: 0 auto, 1 one CTA per unit,
     3 each unit split across a CTA cluster (long contexts, few units), 4 two kernels
-    (selection with two unit groups per SM, then attention)."""
+    (selection with two unit groups per SM, then attention).
+    exchange (shard.OutputExchange): the multi-GPU output all-gather fused into the step; every
+    rank's outputs land as bf16 in every rank's exchange buffer (exchange.wait() orders a
+    stream after the step of every rank)."""
     if append is not None:
         append_batch(cb, append[0], append[1], check=False)
     umap = None
@@ -350,12 +355,15 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
         cnt = torch.empty(U, device=dev, dtype=torch.int32)
     diag = torch.empty(U, device=dev, dtype=torch.int32) if with_diag else None
     ws = _workspace(U, cb.tokens, k, cb.sinks, dev)
-    L_.call("sikv_decode_step", L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
+    args = (L_.ptr(cb.signs), L_.ptr(cb.recs), L_.ptr(cb.cent32), L_.ptr(cb.alpha32),
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], L_.ptr(cb.recent_n), R,
             L_.ptr(qf), U, cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), stride, L_.ptr(cnt),
-            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only) | (2 if cb.bits == 16 else 0), kernel,
-            L_.stream())
+            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only) | (2 if cb.bits == 16 else 0), kernel)
+    if exchange is None:
+        L_.call("sikv_decode_step", *args, L_.stream())
+    else:
+        L_.call("sikv_decode_step_x", *args, C.byref(exchange.cstruct(U, Gq)), L_.stream())
     return DecodeOutput(out, lse, sel, cnt, diag)
 
 

@@ -1,8 +1,10 @@
 // extern "C" boundary of libsikv_b200.so: argument validation, error reporting, launches.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <stdio.h>
 #include <string>
+#include <cstring>
 #include <algorithm>
 
 #include "../../include/sikv_b200.h"
@@ -48,7 +50,10 @@ int two_attend_smem_bytes(int64_t L, int k, int S, int Gq, bool rec16);
 size_t two_workspace_bytes(int64_t U, int64_t L, int k, int S);
 cudaError_t launch_decode_two(const uint8_t*, const uint8_t*, const float*, const float*, const int32_t*, int,
                               const uint32_t*, int, const int32_t*, int, const float*, int64_t, int64_t, int, int, int, float*, float*,
-                              int32_t*, int, int32_t*, int32_t*, void*, int, const int32_t*, int, cudaStream_t);
+                              int32_t*, int, int32_t*, int32_t*, void*, int, const int32_t*, int, const sikv_exchange*,
+                              cudaStream_t);
+cudaError_t launch_push_outputs(const sikv_exchange& x, const float* out, int64_t U, int Gq, cudaStream_t st);
+cudaError_t launch_exchange_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t st);
 // snapkv.cu
 size_t snap_workspace_bytes(int64_t U, int64_t L, int w);
 cudaError_t launch_snap_pooled(const void*, int, int64_t, int64_t, int, const double*, const double*, int, int, void*,
@@ -110,7 +115,7 @@ static int max_smem() {
 extern "C" {
 
 const char* sikv_last_error(void) { return g_err.c_str(); }
-int sikv_abi_version(void) { return 7; }
+int sikv_abi_version(void) { return 8; }
 
 size_t sikv_encode_workspace_bytes(int64_t units, int64_t tokens, int64_t dim) {
   return encode_workspace_bytes(units, tokens, (int)dim);
@@ -268,7 +273,86 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
                      int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
                      int32_t* diag, void* workspace, size_t workspace_bytes, const int32_t* unit_map,
                      int lut_mode, int kernel, void* stream) {
+  return sikv_decode_step_x(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
+                            recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count,
+                            diag, workspace, workspace_bytes, unit_map, lut_mode, kernel, nullptr, stream);
+}
+
+static int check_exchange(const sikv_exchange* x) {
+  REQUIRE(x->npeers >= 0 && x->npeers <= SIKV_MAX_PEERS, SIKV_EINVAL, "npeers must be 0..8");
+  if (x->npeers == 0) return SIKV_OK;
+  REQUIRE(x->unit_gid, SIKV_EINVAL, "the exchange needs unit_gid");
+  for (int p = 0; p < x->npeers; ++p)
+    REQUIRE(x->out[p] && x->flag[p], SIKV_EINVAL, "null peer buffer or counter");
+  return SIKV_OK;
+}
+
+int sikv_exchange_wait(const unsigned long long* flag, unsigned long long target, void* stream) {
   rt_bind();
+  REQUIRE(flag, SIKV_EINVAL, "null counter");
+  return cuda_ret(launch_exchange_wait(flag, target, (cudaStream_t)stream), "sikv_exchange_wait");
+}
+
+int sikv_ipc_handle(const void* dev_ptr, void* handle64, size_t* offset) {
+  rt_bind();
+  REQUIRE(dev_ptr && handle64 && offset, SIKV_EINVAL, "null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  // the handle names the whole allocation (a caching allocator hands out interior pointers):
+  // its base from the driver (entry point looked up at run time, no libcuda link)
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(SIKV_ECUDA, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  REQUIRE(get_range(&base, &size, (CUdeviceptr)dev_ptr) == CUDA_SUCCESS, SIKV_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e == cudaSuccess) {
+    memcpy(handle64, &h, sizeof(h));
+    *offset = (size_t)((CUdeviceptr)dev_ptr - base);
+  }
+  return cuda_ret(e, "sikv_ipc_handle");
+}
+
+int sikv_ipc_open(const void* handle64, void** dev_ptr) {
+  rt_bind();
+  REQUIRE(handle64 && dev_ptr, SIKV_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return cuda_ret(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "sikv_ipc_open");
+}
+
+int sikv_ipc_close(void* dev_ptr) {
+  rt_bind();
+  REQUIRE(dev_ptr, SIKV_EINVAL, "null pointer");
+  return cuda_ret(cudaIpcCloseMemHandle(dev_ptr), "sikv_ipc_close");
+}
+
+int sikv_decode_step_x(const uint8_t* signs_fast, const uint8_t* recs_fast, const float* cent32,
+                       const float* alpha32, const int32_t* sink_idx, int sinks, const uint32_t* forced_frag,
+                       int frag_blocks, const int32_t* recent_n, int recent, const float* q, int64_t units,
+                       int64_t tokens, int gq, int k,
+                       int cap, float* out, float* lse, int32_t* sel, int sel_stride, int32_t* sel_count,
+                       int32_t* diag, void* workspace, size_t workspace_bytes, const int32_t* unit_map,
+                       int lut_mode, int kernel, const sikv_exchange* xchg, void* stream) {
+  rt_bind();
+  if (xchg) {
+    const int rc = check_exchange(xchg);
+    if (rc != SIKV_OK) return rc;
+    if (xchg->npeers == 0) xchg = nullptr;
+  }
+  // paths without the fused epilogue push after their kernel, on the same stream
+  auto push = [&](cudaError_t e) -> cudaError_t {
+    if (e != cudaSuccess || !xchg) return e;
+    return launch_push_outputs(*xchg, out, units, gq, (cudaStream_t)stream);
+  };
   REQUIRE(signs_fast && recs_fast && cent32 && alpha32 && q && out, SIKV_EINVAL, "null required pointer");
   REQUIRE(units >= 1 && tokens >= 1, SIKV_EINVAL, "units and tokens must be positive");
   REQUIRE(tokens < (1ll << 31) - 65536, SIKV_EUNSUPPORTED, "tokens must fit in int32");
@@ -318,7 +402,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
       return cuda_ret(launch_decode_two(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
                                         frag_blocks, recent_n, recent, q, units, tokens, gq, k, tcap, out, lse, sel,
                                         sel_stride, sel_count, diag, workspace, num_sms(), unit_map, lut_mode,
-                                        (cudaStream_t)stream),
+                                        xchg, (cudaStream_t)stream),
                       "sikv_decode_step");
     }
     REQUIRE(kernel != 4 && !rec16, SIKV_EUNSUPPORTED,
@@ -344,9 +428,10 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
     REQUIRE(pick || kernel != 3, SIKV_EUNSUPPORTED, "the split kernel does not fit this configuration");
     if (pick) {
       g_last_decode_kernel = 3;
-      return cuda_ret(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
-                                          frag_blocks, recent_n, recent, q, units, tokens, gq, k, pick_cap, pick, out, lse,
-                                          sel, sel_stride, sel_count, diag, unit_map, lut_mode, (cudaStream_t)stream),
+      return cuda_ret(push(launch_decode_split(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag,
+                                               frag_blocks, recent_n, recent, q, units, tokens, gq, k, pick_cap, pick, out,
+                                               lse, sel, sel_stride, sel_count, diag, unit_map, lut_mode,
+                                               (cudaStream_t)stream)),
                       "sikv_decode_step");
     }
   }
@@ -359,7 +444,7 @@ int sikv_decode_step(const uint8_t* signs_fast, const uint8_t* recs_fast, const 
   cudaError_t e = launch_decode(signs_fast, recs_fast, cent32, alpha32, sink_idx, sinks, forced_frag, frag_blocks,
                                 recent_n, recent, q, units, tokens, gq, k, cap, out, lse, sel, sel_stride, sel_count, diag, unit_map,
                                 lut_mode, (cudaStream_t)stream, &smem);
-  return cuda_ret(e, "sikv_decode_step");
+  return cuda_ret(push(e), "sikv_decode_step");
 }
 
 int sikv_debug_set_attend_skip(int v) {

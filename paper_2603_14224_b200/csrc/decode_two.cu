@@ -22,6 +22,7 @@
 #include "select.cuh"
 #include "api_types.cuh"
 #include "decode_common.cuh"
+#include "../../include/sikv_b200.h"
 #include <algorithm>
 #include <type_traits>
 
@@ -62,7 +63,60 @@ struct TwoArgs {
   int lut_mode;         // 0: centroid LUT, 1: sign-only LUT
   // select-kernel shared-memory layout (per group: misc | hist | forced | cand)
   int g_bytes, g_hist, g_forced, g_cand, g_pre;   // g_forced < 0: forced bitmap in gforced
+  sikv_exchange x;      // fused multi-GPU output exchange (x.npeers 0: off)
 };
+
+// The fused output exchange: unit u's float32 rows (just written by this CTA) go as bf16 to
+// row gid[u] of every rank's model-layout buffer over NVLink; after a system-scope fence the
+// CTA adds its Gq rows to every rank's arrival counter (sikv_exchange_wait acquires them).
+__device__ __forceinline__ void push_unit(const sikv_exchange& x, const float* out, int64_t u, int Gq, int tid,
+                                          int nt) {
+  __syncthreads();                                   // the unit's rows are in global memory
+  const int n2 = Gq * FD / 2;
+  const float2* o = reinterpret_cast<const float2*>(out + u * Gq * FD);
+  const int64_t base = (int64_t)__ldg(x.unit_gid + u) * n2;
+  for (int i = tid; i < n2; i += nt) {
+    const float2 v = o[i];
+    const __nv_bfloat162 b = __floats2bfloat162_rn(v.x, v.y);
+    for (int p = 0; p < x.npeers; ++p) reinterpret_cast<__nv_bfloat162*>(x.out[p])[base + i] = b;
+  }
+  // the CTA barrier orders every thread's stores before the releasing reductions, whose
+  // system-scope release makes them visible to the peer before its counter moves
+  __syncthreads();
+  if (tid < x.npeers)
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(x.flag[tid]), "l"((unsigned long long)Gq)
+                 : "memory");
+}
+
+// the exchange for the paths whose kernels have no epilogue hook: one CTA per unit, after them
+__global__ void __launch_bounds__(128) push_outputs_kernel(const sikv_exchange x, const float* __restrict__ out,
+                                                           int Gq) {
+  push_unit(x, out, blockIdx.x, Gq, threadIdx.x, 128);
+}
+
+cudaError_t launch_push_outputs(const sikv_exchange& x, const float* out, int64_t U, int Gq, cudaStream_t st) {
+  push_outputs_kernel<<<(unsigned)U, 128, 0, st>>>(x, out, Gq);
+  return cudaGetLastError();
+}
+
+// spins until every rank's rows of this step have arrived; a peer that never delivers (a rank
+// died) traps after 20 s instead of hanging the stream
+__global__ void exchange_wait_kernel(const unsigned long long* flag, unsigned long long target) {
+  unsigned long long v, t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) break;
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+}
+
+cudaError_t launch_exchange_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t st) {
+  exchange_wait_kernel<<<1, 1, 0, st>>>(flag, target);
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------- selection
 constexpr int SINK_STAGE = 256;   // sink indices staged with the next unit's inputs (more: read from L2)
@@ -224,7 +278,7 @@ constexpr int ATT_STAGES = 3;   // cp.async staging buffers per warp (2: C2 0.84
 // units (C3) one CTA per unit would leave most warp slots idle.  Each CTA merges its warps;
 // the last CTA of the unit to finish (counter) merges the CTA partials in split order, so
 // the result does not depend on which CTA finishes last.
-template <int NW, bool R16, bool SPLIT>
+template <int NW, bool R16, bool SPLIT, bool XCH>
 __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64_t u, int sp) {
   constexpr int NT = 32 * NW;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -273,16 +327,22 @@ __device__ __forceinline__ void attend_unit(const TwoArgs& a, char* stage, int64
     if (!last) return;
     __threadfence();
     attn_merge_splits(sp_u, a.nsplit, Gq, tid, NT, a.out + u * Gq * FD, a.lse ? a.lse + u * Gq : nullptr);
+    if constexpr (XCH) push_unit(a.x, a.out, u, Gq, tid, NT);
   }
 }
 
 // R16: 16-bit records (512 B per token, stored fp16 fragments; 64 KB of staging per CTA);
 // SPLIT: nsplit CTAs per unit; NW warps per CTA
-template <bool R16, bool SPLIT, int NW>
+// XCH: the fused output exchange epilogue (separate instances: its code perturbs the register
+// allocation of the gather loop, +32 instructions per block, so the plain path never carries it)
+template <bool R16, bool SPLIT, int NW, bool XCH = false>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) decode_attend_kernel(const __grid_constant__ TwoArgs a) {
   extern __shared__ __align__(128) char sm[];
-  if constexpr (SPLIT) attend_unit<NW, R16, true>(a, sm, blockIdx.x / a.nsplit, (int)(blockIdx.x % a.nsplit));
-  else attend_unit<NW, R16, false>(a, sm, blockIdx.x, 0);
+  if constexpr (SPLIT) attend_unit<NW, R16, true, XCH>(a, sm, blockIdx.x / a.nsplit, (int)(blockIdx.x % a.nsplit));
+  else {
+    attend_unit<NW, R16, false, XCH>(a, sm, blockIdx.x, 0);
+    if constexpr (XCH) push_unit(a.x, a.out, blockIdx.x, a.Gq, threadIdx.x, 32 * NW);
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -354,7 +414,7 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
                               const int32_t* rn, int R,
                               const float* q, int64_t U, int64_t L, int Gq, int k, int cap, float* out, float* lse,
                               int32_t* sel, int sel_stride, int32_t* sel_count, int32_t* diag, void* workspace,
-                              int nsm, const int32_t* umap, int mode, cudaStream_t st) {
+                              int nsm, const int32_t* umap, int mode, const sikv_exchange* xchg, cudaStream_t st) {
   const int lut_mode = mode & 1;
   const bool rec16 = (mode & 2) != 0;
   TwoArgs a = two_layout(L, k, S, cap, Gq, two_forced_smem(L, k, S, cap, Gq));
@@ -377,6 +437,9 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   }
   a.L = L; a.U = U; a.fblocks = fblocks; a.S = S; a.R = R; a.Gq = Gq; a.k = k; a.sel_stride = sel_stride;
   a.lut_mode = lut_mode;
+  // the exchange rides on the attention epilogue (measured against a push kernel launched
+  // after the attention with PDL: C2 / 8 ranks +8.4 vs +8.8 us, C4 +7.8 vs +7.2 us)
+  a.x = xchg ? *xchg : sikv_exchange{};
   const int smem_s = TBL_BYTES + 2 * a.g_bytes;
   auto select = (L + 255) / 256 >= 256 ? decode_select_kernel<true> : decode_select_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(select, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s);
@@ -388,6 +451,9 @@ cudaError_t launch_decode_two(const uint8_t* signs, const uint8_t* recs, const f
   const int smem_a = attend_smem(nw, Gq, rec16);
   auto pick = [&](auto w) {
     constexpr int W = decltype(w)::value;
+    if (a.x.npeers)
+      return a.nsplit > 1 ? (rec16 ? decode_attend_kernel<true, true, W, true> : decode_attend_kernel<false, true, W, true>)
+                          : (rec16 ? decode_attend_kernel<true, false, W, true> : decode_attend_kernel<false, false, W, true>);
     return a.nsplit > 1 ? (rec16 ? decode_attend_kernel<true, true, W> : decode_attend_kernel<false, true, W>)
                         : (rec16 ? decode_attend_kernel<true, false, W> : decode_attend_kernel<false, false, W>);
   };

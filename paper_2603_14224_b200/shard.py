@@ -119,3 +119,118 @@ def gather_outputs(local_out: torch.Tensor, layers: int, batch: int, kv_heads: i
         out.copy_(x)
         return out
     return x
+
+
+class OutputExchange:
+    """The output all-gather fused into the decode step over NVLink peer memory.
+
+    Replaces ``gather_outputs``' NCCL all-gather + reassembly. Every rank owns a bf16 buffer
+    [units_total, Gq, 128], which is the model layout [layers, batch, kv_heads * Gq, 128], since
+    the row of a unit is its global id. It also owns a u64 arrival counter. CUDA IPC hands
+    every rank the other ranks' buffers and counters. ``batch.decode_step(...,
+    exchange=self)`` makes the attention epilogue store each finished unit's rows into every
+    rank's buffer and release one arrival on every counter (``sikv_decode_step_x``).
+    ``wait()`` then orders a stream after the current step of all ranks.
+
+    ``ranks`` simulates a world inside one process, one exchange per rank, sharing
+    buffers without IPC. Tests use it to run every rank's shard on a single GPU.
+    """
+
+    def __init__(self, plan: ShardPlan, gq: int, rank: int, device, group=None, ranks: list | None = None):
+        import ctypes as C
+
+        from . import _lib as L_
+        self.plan, self.gq, self.rank = plan, gq, rank
+        self.total = plan.layers * plan.batch * plan.kv_heads
+        if plan.world > L_.MAX_PEERS:
+            raise ValueError(f"the fused exchange supports at most {L_.MAX_PEERS} ranks, got {plan.world}")
+        dev = torch.device(device)
+        self.buffer = torch.zeros(self.total, gq, 128, dtype=torch.bfloat16, device=dev)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=dev)      # u64 arrivals
+        gid = plan.local_units(rank).to(torch.int32)
+        self.gid = gid.to(dev)
+        self.gid_heads = (gid[:, None] * gq + torch.arange(gq, dtype=torch.int32)[None, :]).reshape(-1).to(dev)
+        self.epoch = 0
+        self._opened = []
+        if ranks is not None:                       # in-process world (tests)
+            peers = [(r.buffer.data_ptr(), r.counter.data_ptr()) for r in ranks] + \
+                    [(self.buffer.data_ptr(), self.counter.data_ptr())]
+            if rank != len(ranks) or rank >= plan.world:
+                raise ValueError("ranks must hold the exchanges of ranks 0 .. rank-1, in order")
+            for i, r in enumerate(ranks):           # earlier ranks learn about this one
+                r._peers[rank] = peers[rank]
+                r._build()
+            self._peers = dict(enumerate(peers))
+        elif plan.world == 1:
+            self._peers = {0: (self.buffer.data_ptr(), self.counter.data_ptr())}
+        else:
+            import torch.distributed as dist
+            mine = (self._handle(self.buffer), self._handle(self.counter))
+            allh = [None] * plan.world
+            dist.all_gather_object(allh, mine, group=group)
+            self._peers = {}
+            for r, (hb, hc) in enumerate(allh):
+                if r == rank:
+                    self._peers[r] = (self.buffer.data_ptr(), self.counter.data_ptr())
+                else:
+                    self._peers[r] = (self._open(*hb), self._open(*hc))
+        self._C, self._L = C, L_
+        self._build()
+
+    # ---- CUDA IPC (the offset: the caching allocator hands out interior pointers)
+    def _handle(self, t: torch.Tensor):
+        import ctypes as C
+
+        from . import _lib as L_
+        h = (C.c_char * 64)()
+        off = C.c_size_t(0)
+        L_.call("sikv_ipc_handle", L_.ptr(t), h, C.byref(off))
+        return bytes(h), int(off.value)
+
+    def _open(self, handle: bytes, offset: int) -> int:
+        import ctypes as C
+
+        from . import _lib as L_
+        h = (C.c_char * 64).from_buffer_copy(handle)
+        p = C.c_void_p(0)
+        L_.call("sikv_ipc_open", h, C.byref(p))
+        self._opened.append(p.value)
+        return p.value + offset
+
+    def _build(self) -> None:
+        from . import _lib as L_
+        self._structs = {}
+        n = len(self._peers)
+        for per_head, gid in ((False, self.gid), (True, self.gid_heads)):
+            x = L_.Exchange()
+            x.npeers = n
+            for r in range(n):
+                x.out[r], x.flag[r] = self._peers[r]
+            x.unit_gid = gid.data_ptr()
+            self._structs[per_head] = x
+
+    def cstruct(self, units: int, gq: int):
+        """The C struct for a decode over `units` query units of `gq` heads (the group-sum
+        policy: the local units; the per-q-head policy: one query unit per head)."""
+        if units == self.gid.numel() and gq == self.gq:
+            return self._structs[False]
+        if units == self.gid_heads.numel() and gq == 1:
+            return self._structs[True]
+        raise ValueError(f"exchange built for {self.gid.numel()} units x {self.gq} heads, "
+                         f"got {units} x {gq}")
+
+    def wait(self, stream=None) -> torch.Tensor:
+        """Enqueue (on `stream`, default the current one) the wait for this step of every rank;
+        returns the model-layout view [layers, batch, kv_heads * Gq, 128] of the buffer."""
+        from . import _lib as L_
+        self.epoch += 1
+        st = L_.P((stream or torch.cuda.current_stream()).cuda_stream)
+        L_.call("sikv_exchange_wait", L_.ptr(self.counter), self.epoch * self.total * self.gq, st)
+        p = self.plan
+        return self.buffer.view(p.layers, p.batch, p.kv_heads * self.gq, 128)
+
+    def close(self) -> None:
+        from . import _lib as L_
+        for ptr in self._opened:
+            L_.call("sikv_ipc_close", ptr)
+        self._opened = []

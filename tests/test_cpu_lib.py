@@ -28,7 +28,7 @@ def test_header_symbols_exported():
 
 def test_host_queries():
     lib = _lib.lib()
-    assert lib.sikv_abi_version() == 7
+    assert lib.sikv_abi_version() == 8
     assert lib.sikv_encode_workspace_bytes(4, 4096, 128) > 0
     assert lib.sikv_topk_workspace_bytes(1, 1000) == 3 * 32 * 4
     cap = lib.sikv_decode_default_cap(32768, 2048, 64)

@@ -539,3 +539,37 @@ def test_long_units_extra_sample_passes_and_retries():
     attempts = clk[:, 9].cpu().numpy()
     fallback = (res.diag.cpu().numpy() & 4) != 0
     assert ((attempts >= 1) | fallback).all(), (attempts, fallback)
+
+
+_FIRST_CALL_IN_CAPTURE = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch
+from paper_2603_14224_b200 import _lib as L_
+L = 1000
+sc = torch.randn(L, dtype=torch.float64, device="cuda")
+ws = torch.empty(L_.lib().sikv_topk_workspace_bytes(1, L), dtype=torch.uint8, device="cuda")
+out = torch.empty(8, dtype=torch.int32, device="cuda")
+cnt = torch.zeros(2, dtype=torch.int32, device="cuda")
+s, g = torch.cuda.Stream(), torch.cuda.CUDAGraph()
+with torch.cuda.stream(s):
+    with torch.cuda.graph(g, stream=s):      # the library's first runtime call is captured
+        L_.call("sikv_topk", L_.ptr(sc), 0, 1, L, None, 0, 8, L_.ptr(ws), L_.ptr(out), 8, L_.ptr(cnt),
+                L_.stream())
+g.replay()
+torch.cuda.synchronize()
+assert torch.equal(out.sort().values, torch.topk(sc, 8).indices.int().sort().values)
+print("ok")
+"""
+
+
+def test_first_library_call_inside_graph_capture():
+    """The C ABI binds the thread's context before its first launch (capi.cu rt_bind) in a
+    capture-safe way: a fresh process whose first library call is captured into a CUDA graph."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FIRST_CALL_IN_CAPTURE, root], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

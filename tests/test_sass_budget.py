@@ -78,3 +78,16 @@ def test_attention_kernels_do_not_spill(funcs):
     for name in _one(funcs, r"decode_attend_kernel"):
         ops = collections.Counter(op.split(".")[0] for _, op, _ in funcs[name])
         assert ops["LDL"] == 0 and ops["STL"] == 0, (name, ops["LDL"], ops["STL"])
+
+
+def test_attention_gather_loop_budget(funcs):
+    """The plain two-kernel attention's 16-row gather/dequant loop (2-bit records, one CTA
+    per unit): 407 instructions for 4 warps, 411 for 2.  Code added elsewhere in the kernel
+    has moved it to 439 (+8% per gathered block, +2% on the C2 step); the exchange epilogue
+    lives in separate instances for that reason."""
+    for pat, budget in ((r"decode_attend_kernelILb0ELb0ELi4ELb0E", 412), (r"decode_attend_kernelILb0ELb0ELi2ELb0E", 416)):
+        for name in _one(funcs, pat):
+            loops = [c for c in _loops(funcs[name]) if c["HMMA"] >= 16]
+            assert loops, name
+            n = max(sum(c.values()) - c["moves"] for c in loops)
+            assert n <= budget, f"{name}: gather loop grew to {n} instructions per 16-row block"
