@@ -609,8 +609,15 @@ def main():
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH,NVLS")
         os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(os.environ.get("SIKV_NCCL_LOG_DIR", "/tmp"),
                                                               "sikv_nccl.%h.%p.log"))
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        if os.environ.get("SIKV_BENCH_SHARE_GPU"):
+            # code-path check on a one-GPU box: every rank on cuda:0, gloo for the host-side
+            # collectives (NCCL refuses two ranks on one device); timings are not meaningful
+            os.environ["LOCAL_RANK"] = "0"
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     line = run_prefill(args, rank, world, cfg) if args.config == "c5" else run_ours(args, rank, world, cfg)
     if rank == 0 and line is not None:
         if world == 1 and not args.no_cpu_baseline and args.config != "c5":   # rank 0 at N = 1 only

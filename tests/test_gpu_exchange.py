@@ -167,3 +167,22 @@ def test_two_processes_ipc():
         assert cnt == 2 * LAYERS * BATCH * KVH * GQ
     err = ((expect.float() - ref.float()).norm(dim=-1) / ref.float().norm(dim=-1)).max().item()
     assert err <= 1e-2          # bf16 of the shards' outputs vs bf16 of the full run's
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py --gpus 2 end to end (its own torchrun launch, the IPC exchange, the e2e
+    loop, the JSON line), both ranks on cuda:0 (SIKV_BENCH_SHARE_GPU: gloo for the host-side
+    collectives; the timings are not meaningful)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SIKV_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c1",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, env=env, timeout=600,
+                       cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["output_gather"].startswith("fused")
+    assert line["gpu_launches"] == 3 * 3      # per step: the decode kernel(s) + push (path 1) or not (path 4) + wait
