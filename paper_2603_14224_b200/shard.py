@@ -134,6 +134,10 @@ class OutputExchange:
 
     ``ranks`` simulates a world inside one process, one exchange per rank, sharing
     buffers without IPC. Tests use it to run every rank's shard on a single GPU.
+
+    The buffer holds the latest step. The next step's stores overwrite it, so whatever reads
+    it must be ordered before any rank enqueues its next exchange step. In a model forward the
+    layers' other collectives give that order; a standalone loop needs a barrier.
     """
 
     def __init__(self, plan: ShardPlan, gq: int, rank: int, device, group=None, ranks: list | None = None):
