@@ -47,7 +47,7 @@ SINKS = 64
 
 # bytes of one selected token's K/V: 2-bit (payloads 2 x 32 B + fp16 params 2 x 16 B), 1-bit
 # (2 x 16 B + 2 x 16 B), 16-bit (2 x 256 B)
-SEL_BYTES = {2: 96, 1: 64, 16: 512}
+SEL_BYTES = {2: 96, 1: 64, 16: 512, 4: 512, 8: 512}   # bits 4 / 8: stored as the 16-bit records
 
 
 def algo_bytes_per_unit(L: int, k: int, gq: int, S: int = SINKS, bits: int = 2) -> int:
@@ -545,7 +545,7 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--bits", type=int, default=2, choices=[1, 2, 16], help="payload bits of the fast path")
+    ap.add_argument("--bits", type=int, default=2, choices=[1, 2, 4, 8, 16], help="payload bits of the fast path")
     ap.add_argument("--direct-keys", action="store_true", help="keys quantised directly (no sign-in-quant)")
     ap.add_argument("--policy", default="group-sum", choices=["group-sum", "per-head"],
                     help="GQA selection policy: one selection per KV head from the summed queries "

@@ -48,8 +48,9 @@ class CacheBatch:
     ffrag: torch.Tensor                       # [U, blocks, FBLK] int32 forced-row fragments + row scales
     recent_host: torch.Tensor = None          # [U] int64 host mirror of recent_n (appends are host-issued)
     ref: dict = field(default_factory=dict)   # optional reference-layout planes
-    bits: int = 2                             # payload bits: 2, 1 (same record, codes in 2-bit fields) or
-                                              # 16 (fp16 K^ / V records of 512 B, the "16 bits" variant)
+    bits: int = 2                             # payload bits: 2, 1 (same record, codes in 2-bit fields),
+                                              # 16 (fp16 K^ / V records of 512 B, the "16 bits" variant) or
+                                              # 4 / 8 (codes dequantised at prefill into those 512-B records)
     sign_in_quant: bool = True                # False: keys quantised directly (cache.py:241-244)
 
     @property
@@ -82,9 +83,11 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
     """An empty batch of `units` caches of `tokens` prefill tokens.  Fast-path variants
     (cache.py:52-75): bits 2 or 1 (the 1-bit codes use the same record, in its 2-bit fields),
     sign_in_quant True (|K'| / alpha codes + sign plane) or False (direct signed K' codes), or
-    bits 16 (K' / alpha-hat and V stored in fp16: 512-B records, the two-kernel path)."""
-    if bits not in (1, 2, 16):
-        raise NotImplementedError("the fast path supports bits 1, 2 and 16 (the per-head API covers 4 and 8)")
+    bits 16 (K' / alpha-hat and V stored in fp16: 512-B records, the two-kernel path), or bits
+    4 / 8 (the reference's 4- / 8-bit codes, dequantised once at prefill into the same fp16
+    records: the decode reads 512 B per selected token as at bits 16)."""
+    if bits not in (1, 2, 4, 8, 16):
+        raise NotImplementedError("the fast path supports bits 1, 2, 4, 8 and 16")
     dev = device or L_.require_cuda()
     S = min(sink_count, tokens)
     f32 = dict(device=dev, dtype=torch.float32)
@@ -96,7 +99,7 @@ def empty_batch(units: int, tokens: int, *, sink_count: int = 64, recent_capacit
         mu32=torch.empty(units, FD, **f32), alpha32=torch.empty(units, FD, **f32),
         cent64=torch.empty(units, 32, 16, 4, **f64), cent32=torch.empty(units, 32, 16, 4, **f32),
         signs=torch.empty(units, tokens, 16, **u8),
-        recs=torch.empty(units, tokens, 512 if bits == 16 else 128, **u8),
+        recs=torch.empty(units, tokens, 512 if bits >= 4 else 128, **u8),
         sink_idx=torch.arange(S, device=dev, dtype=torch.int32).repeat(units, 1),
         sink_k=torch.empty(units, S, FD, **f32), sink_v=torch.empty(units, S, FD, **f32),
         recent_k=torch.zeros(units, recent_capacity, FD, **f32),
@@ -160,25 +163,10 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=keys.device)
     status = torch.zeros(1, dtype=torch.int32, device=keys.device)
-    r = cb.ref
-    r16 = cb.bits == 16
-    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, 0 if r16 else cb.bits, 32,
-            int(cb.sign_in_quant), 3, None,
-            L_.ptr(_sl(cb.mu64, u0, n)), L_.ptr(_sl(cb.alpha64, u0, n)), L_.ptr(_sl(cb.mu32, u0, n)),
-            L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.cent64, u0, n)), L_.ptr(_sl(cb.cent32, u0, n)),
-            L_.ptr(_sl(r.get("codes"), u0, n)), L_.ptr(_sl(r.get("kq"), u0, n)),
-            L_.ptr(_sl(r.get("ks"), u0, n)), L_.ptr(_sl(r.get("kz"), u0, n)),
-            L_.ptr(_sl(r.get("vq"), u0, n)), L_.ptr(_sl(r.get("vs"), u0, n)),
-            L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)),
-            None if r16 else L_.ptr(_sl(cb.recs, u0, n)),
-            L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
-    if r16:
-        # codes + codebook came from the encoder; the sign plane and the fp16 records here
-        L_.call("sikv_pack16", L_.ptr(keys), L_.ptr(values), dt, n, L, L_.ptr(_sl(cb.mu64, u0, n)),
-                L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.recs, u0, n)), L_.ptr(status), L_.stream())
-    if not cb.sign_in_quant:
-        # direct keys: the record dequantises to K' itself, so the attention's alpha-hat is 1
-        cb.alpha32[u0:u0 + n] = 1.0
+    if cb.bits in (4, 8):
+        _prefill_wide(cb, u0, keys, values, dt, workspace, status)
+    else:
+        _prefill_fast(cb, u0, keys, values, dt, workspace, status)
     S = cb.sinks
     if window is not None and 0 < S < L:
         if window.dim() != 3 or window.shape[0] != n or window.shape[2] != D:
@@ -198,6 +186,84 @@ def prefill_into(cb: CacheBatch, u0: int, keys: torch.Tensor, values: torch.Tens
     _pack_forced(cb, u0, n, 0, cb.ffrag.shape[1] * 16, status)
     if check:
         L_.raise_status(status, "keys")
+
+
+def _prefill_fast(cb: CacheBatch, u0: int, keys, values, dt: int, workspace, status) -> None:
+    """bits 1 / 2 (fused encoder: sign plane + 128-B records) and 16 (sign plane + pack16)."""
+    n, L, D = keys.shape
+    r = cb.ref
+    r16 = cb.bits == 16
+    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, 0 if r16 else cb.bits, 32,
+            int(cb.sign_in_quant), 3, None,
+            L_.ptr(_sl(cb.mu64, u0, n)), L_.ptr(_sl(cb.alpha64, u0, n)), L_.ptr(_sl(cb.mu32, u0, n)),
+            L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.cent64, u0, n)), L_.ptr(_sl(cb.cent32, u0, n)),
+            L_.ptr(_sl(r.get("codes"), u0, n)), L_.ptr(_sl(r.get("kq"), u0, n)),
+            L_.ptr(_sl(r.get("ks"), u0, n)), L_.ptr(_sl(r.get("kz"), u0, n)),
+            L_.ptr(_sl(r.get("vq"), u0, n)), L_.ptr(_sl(r.get("vs"), u0, n)),
+            L_.ptr(_sl(r.get("vz"), u0, n)), L_.ptr(_sl(cb.signs, u0, n)),
+            None if r16 else L_.ptr(_sl(cb.recs, u0, n)),
+            L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
+    if r16:
+        # codes + codebook came from the encoder; the sign plane and the fp16 records here
+        L_.call("sikv_pack16", L_.ptr(keys), L_.ptr(values), dt, n, L, L_.ptr(_sl(cb.mu64, u0, n)),
+                L_.ptr(_sl(cb.alpha32, u0, n)), L_.ptr(_sl(cb.recs, u0, n)), L_.ptr(status), L_.stream())
+    if not cb.sign_in_quant and not r16:
+        # direct keys: the record dequantises to K' itself, so the attention's alpha-hat is 1
+        # (16-bit records hold K' / alpha-hat whatever the key mode: alpha-hat stays)
+        cb.alpha32[u0:u0 + n] = 1.0
+
+
+def _prefill_wide(cb: CacheBatch, u0: int, keys, values, dt: int, workspace, status) -> None:
+    """bits 4 / 8 (cache.py:52-75 with QuantConfig(bits=4|8)): the encoder writes the
+    reference-layout planes (codes, key magnitudes or direct keys, values, fp16 scales / zeros:
+    quantizer.py:106-184, bit-exact), a second pass writes the rotated sign plane the scoring
+    kernels read; then every row is dequantised on the device exactly as cache.gather does
+    (K' = sign * alpha * (qs c + zp), V = qs c + zp, cache.py:118-158, float64) and stored once
+    as the 16-bit path's fp16 records (K' / alpha-hat, V): the decode is the bits-16 decode."""
+    n, L, D = keys.shape
+    dev = keys.device
+    u8 = dict(device=dev, dtype=torch.uint8)
+    f16 = dict(device=dev, dtype=torch.float16)
+    b = cb.bits
+    if cb.ref:
+        pl = {k: v[u0:u0 + n] for k, v in cb.ref.items()}
+    else:
+        pl = dict(codes=torch.empty(n, L, 16, **u8), kq=torch.empty(n, L, 16 * b, **u8),
+                  ks=torch.empty(n, L, 4, **f16), kz=torch.empty(n, L, 4, **f16),
+                  vq=torch.empty(n, L, 16 * b, **u8), vs=torch.empty(n, L, 4, **f16),
+                  vz=torch.empty(n, L, 4, **f16))
+    mu64, al64 = _sl(cb.mu64, u0, n), _sl(cb.alpha64, u0, n)
+    # pass 1: statistics, codebook and the reference-layout b-bit planes
+    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, b, 32, int(cb.sign_in_quant), 3, None,
+            L_.ptr(mu64), L_.ptr(al64), L_.ptr(_sl(cb.mu32, u0, n)), L_.ptr(_sl(cb.alpha32, u0, n)),
+            L_.ptr(_sl(cb.cent64, u0, n)), L_.ptr(_sl(cb.cent32, u0, n)),
+            L_.ptr(pl["codes"]), L_.ptr(pl["kq"]), L_.ptr(pl["ks"]), L_.ptr(pl["kz"]),
+            L_.ptr(pl["vq"]), L_.ptr(pl["vs"]), L_.ptr(pl["vz"]), None, None,
+            L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
+    # pass 2: the rotated sign plane (bits 0 = sign plane only; its codebook copy is discarded)
+    c64 = torch.empty(n, 32, 16, 4, device=dev, dtype=torch.float64)
+    c32 = torch.empty(n, 32, 16, 4, device=dev, dtype=torch.float32)
+    L_.call("sikv_encode", L_.ptr(keys), L_.ptr(values), dt, n, L, D, 0, 32, int(cb.sign_in_quant), 2, None,
+            L_.ptr(mu64), L_.ptr(al64), None, None, L_.ptr(c64), L_.ptr(c32),
+            None, None, None, None, None, None, None, L_.ptr(_sl(cb.signs, u0, n)), None,
+            L_.ptr(workspace), workspace.numel(), L_.ptr(status), L_.stream())
+    if not cb.sign_in_quant:
+        cb.alpha32[u0:u0 + n] = 1.0          # direct keys: the records hold K' itself
+    # dequantise in unit chunks (float64 K', V temporaries bounded at ~512 MiB) and pack
+    rows = torch.arange(L, device=dev, dtype=torch.int64)
+    zero_mu = torch.zeros(n, D, device=dev, dtype=torch.float64)
+    chunk = max(1, (1 << 29) // (2 * L * D * 8))
+    for c0 in range(0, n, chunk):
+        m = min(chunk, n - c0)
+        kd = torch.empty(m, L, D, device=dev, dtype=torch.float64)
+        vd = torch.empty(m, L, D, device=dev, dtype=torch.float64)
+        pa = [L_.ptr(pl[x][c0:c0 + m]) for x in ("codes", "kq", "ks", "kz", "vq", "vs", "vz")]
+        for which, out in ((1, kd), (0, vd)):
+            L_.call("sikv_dequant_rows", *pa, None, None, L_.ptr(al64[c0:c0 + m]), b, 32, int(cb.sign_in_quant),
+                    m, L, D, L_.ptr(rows), L, which, L_.ptr(out), L_.stream())
+        L_.call("sikv_pack16", L_.ptr(kd), L_.ptr(vd), 1, m, L, L_.ptr(zero_mu[c0:c0 + m]),
+                L_.ptr(cb.alpha32[u0 + c0:u0 + c0 + m]), L_.ptr(cb.recs[u0 + c0:u0 + c0 + m]), L_.ptr(status),
+                L_.stream())
 
 
 def _pack_forced(cb: CacheBatch, u0: int, n: int, row_begin: int, row_end: int, status=None) -> None:
@@ -359,7 +425,7 @@ def decode_step(cb: CacheBatch, q: torch.Tensor, k: int, *, cap: int = 0, with_s
             L_.ptr(cb.sink_idx), cb.sinks, L_.ptr(cb.ffrag), cb.ffrag.shape[1], L_.ptr(cb.recent_n), R,
             L_.ptr(qf), U, cb.tokens, Gq, k, cap,
             L_.ptr(out), L_.ptr(lse), L_.ptr(sel), stride, L_.ptr(cnt),
-            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only) | (2 if cb.bits == 16 else 0), kernel)
+            L_.ptr(diag), L_.ptr(ws), ws.numel(), L_.ptr(umap), int(sign_only) | (2 if cb.bits >= 4 else 0), kernel)
     if exchange is None:
         L_.call("sikv_decode_step", *args, L_.stream())
     else:

@@ -470,6 +470,44 @@ def test_sixteen_bit_records():
             B.decode_step(cb, q, 256, kernel=kern)
 
 
+@pytest.mark.parametrize("bits,siq", [(4, True), (8, True), (4, False), (8, False)])
+def test_wide_bit_records(bits, siq):
+    """bits 4 / 8 on the fast path (cache.py:52-75, QuantConfig(bits=4|8)): the reference-layout
+    planes bit-exact vs the oracle, the sign plane equal to its codes, the fp16 records equal
+    to the oracle's dequantised rows (cache.gather, cache.py:118-158) divided by alpha-hat and
+    rounded once, selections exact vs restate32, attention vs the float64 oracle on the same
+    b-bit cache; the two-kernel path runs it (1 / 3 refuse, as at bits 16)."""
+    from .fastlayout import records16_to_arrays
+    units, cb, oc, q = make_variant(4096, [820, 821], bits, siq)
+    torch.cuda.synchronize()
+    for i, c in enumerate(oc):
+        plane = c.kmag if siq else c.kdirect
+        np.testing.assert_array_equal(cb.mu64[i].cpu().numpy(), c.mu)
+        np.testing.assert_array_equal(cb.alpha64[i].cpu().numpy(), c.alpha)
+        np.testing.assert_array_equal(cb.ref["codes"][i].cpu().numpy(), c.packed_codes)
+        np.testing.assert_array_equal(cb.ref["kq"][i].cpu().numpy(), plane.packed)
+        np.testing.assert_array_equal(cb.ref["ks"][i].cpu().numpy(), plane.scales)
+        np.testing.assert_array_equal(cb.ref["kz"][i].cpu().numpy(), plane.zeros)
+        np.testing.assert_array_equal(cb.ref["vq"][i].cpu().numpy(), c.vq.packed)
+        np.testing.assert_array_equal(cb.ref["vs"][i].cpu().numpy(), c.vq.scales)
+        np.testing.assert_array_equal(cb.ref["vz"][i].cpu().numpy(), c.vq.zeros)
+        np.testing.assert_array_equal(unrotate_signs(cb.signs[i].cpu().numpy()), c.packed_codes)
+        kh, vh = records16_to_arrays(cb.recs[i].cpu().numpy())
+        kd = O.dequantize_keys(c.kmag, c.alpha, c.codes) if siq else O.dequantize(c.kdirect)
+        ahat = cb.alpha32[i].cpu().numpy().astype(np.float64)
+        if siq:
+            ahat[ahat == 0] = 1.0
+        else:
+            assert np.all(ahat == 1.0)
+        np.testing.assert_array_equal(kh, (kd / ahat).astype(np.float16))
+        np.testing.assert_array_equal(vh, O.dequantize(c.vq).astype(np.float16))
+    for kern in (0, 4):
+        _check_decode(units, cb, oc, q, 256, kernel=kern)
+    for kern in (1, 3):
+        with pytest.raises(NotImplementedError):
+            B.decode_step(cb, q, 256, kernel=kern)
+
+
 @pytest.mark.parametrize("name,bits,siq", [("direct_d128", 2, False), ("b1_sinks_d128", 1, True),
                                            ("lossless_d128", 16, True), ("c1_u0", 2, True)])
 def test_fast_variants_match_reference_golden(golden, name, bits, siq):
