@@ -68,7 +68,9 @@ int sikv_encode(const void* keys, const void* values, int in_dtype, int64_t unit
 
 /* 16-bit fast-path records (bits = 16, "Ours (16 bits)"; cache.py:236-238 at model precision):
  * recs16 [U][L][512] u8 = K^ = (K - mu) / alpha32 and V in fp16, in the mma fragment orders of
- * DESIGN.md §3; decode with sikv_decode_step(mode bit 1).  status bit 4: V outside fp16. */
+ * DESIGN.md §3; decode with sikv_decode_step(mode bit 1).  status bit 4: V outside fp16.
+ * bits 4 / 8 use the same records: the 4- / 8-bit planes from sikv_encode are dequantised by
+ * sikv_dequant_rows (float64, cache.gather order) and passed here with mu64 = 0. */
 int sikv_pack16(const void* keys, const void* values, int in_dtype, int64_t units, int64_t tokens,
                 const double* mu64, const float* alpha32, uint8_t* recs16, int* status_dev, void* stream);
 

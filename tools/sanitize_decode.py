@@ -47,6 +47,12 @@ cb16 = B.prefill_batch(K, V, sink_count=64, bits=16)
 B.decode_step(cb16, qw, 200, with_selection=True, kernel=4)
 torch.cuda.synchronize()
 print("16-bit records ok", flush=True)
+# 4- / 8-bit codes: reference-layout planes + sign-plane pass + dequantise / pack16
+for b, siq in ((4, True), (8, False)):
+    cbw4 = B.prefill_batch(K, V, sink_count=64, bits=b, sign_in_quant=siq, keep_reference=(b == 4))
+    B.decode_step(cbw4, qw, 200, with_selection=True, kernel=4)
+torch.cuda.synchronize()
+print("4 / 8-bit codes ok", flush=True)
 # a long unit: extra sample passes (>= 64K tokens) on the two-kernel path, split attention
 cbl, ql = bench.build_cache(range(8), 65536, 4, 78, dev)
 B.decode_step(cbl, ql, 2048, with_selection=True, kernel=4)
