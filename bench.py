@@ -162,16 +162,31 @@ def ncu_traffic(config: str):
     return best
 
 
-def decode_config(name: str, world: int) -> dict:
+def scaled_config(name: str, n: int, scaling: str):
+    """The workload at N GPUs.  Weak scaling (default; the decode units are independent, so
+    the path partitions): the model's batch grows with N, every GPU keeps the N = 1 config's
+    unit count (KV-head x batch shard), and `value` counts N = 1-sized steps (units processed
+    / units per N = 1 step / time).  Strong: the N = 1 model split over N GPUs."""
+    layers, batch, kvh, gq, L, k, label = CONFIGS[name]
+    if scaling == "weak" and n > 1:
+        return (layers, batch * n, kvh, gq, L, k, f"{label}; batch x{n} over {n} GPUs (weak scaling)"), n
+    return CONFIGS[name], 1
+
+
+def decode_config(name: str, world: int, cfg=None, rep: int = 1) -> dict:
     """The workload description both arms print (identical for the same config and N)."""
     from paper_2603_14224_b200.shard import ShardPlan
-    layers, batch, kvh, gq, L, k, label = CONFIGS[name]
+    layers, batch, kvh, gq, L, k, label = cfg or CONFIGS[name]
     plan = ShardPlan(layers, batch, kvh, world)
     planes = (16 + 128) * L * plan.units_per_rank / 1e9
     return {"workload": name, "label": label, "layers": layers, "batch": batch, "kv_heads": kvh,
             "q_heads_per_kv": gq, "context": L, "top_k": k, "sinks": SINKS, "units": layers * batch * kvh,
             "units_per_gpu": plan.units_per_rank,
             "parallelism": f"kv-head x batch shard {plan.head_parts}x{plan.batch_parts}",
+            "global_batch": batch,
+            "value_counts": (f"steps of the N = 1 model ({layers * batch * kvh // rep} units) per second, "
+                             f"all GPUs: {rep} per step of this {rep}x-batch model" if rep > 1
+                             else "decode steps of this model per second"),
             "l2": (f"inputs > L2: {planes:.1f} GB of compressed planes per GPU, every step reads them afresh"
                    if planes > 0.5 else f"inputs {planes * 1e3:.0f} MB, smaller than L2 (CPU-reference config)")}
 
@@ -347,18 +362,18 @@ def run_ours(args, rank, world, cfg):
     traffic = ncu_traffic(args.config) if world == 1 else None
     line = {
         "metric": "decode steps/sec + HBM roofline fraction, Llama-3-8B geometry, 32K ctx",
-        "value": round(1000.0 / ms, 3),
+        "value": round(args.rep * 1000.0 / ms, 3),
         "unit": "decode steps/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms, 5),
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "u2 K/V payload, f32 scores, f16 mma operands / f32 accumulate",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU), random-init caches",
-        "config": dict(decode_config(args.config, world), policy=args.policy, bits=args.bits,
+        "config": dict(decode_config(args.config, world, cfg, args.rep), policy=args.policy, bits=args.bits,
                        keys="direct" if args.direct_keys else "sign-in-quant",
                        **({"output_gather": "fused into the attention epilogue (NVLink peer stores, CUDA IPC)"
                            if xch is not None else "NCCL all_gather_into_tensor + reassembly"}
@@ -369,7 +384,7 @@ def run_ours(args, rank, world, cfg):
                      "traffic_source": traffic["source"] if traffic else None,
                      "algo_bytes_per_launch": bytes_step,
                      "kernel_ms": round(kern_ms, 5)},
-        "e2e": {"value": round(1000.0 / e2e_ms, 3), "unit": "decode steps/s",
+        "e2e": {"value": round(args.rep * 1000.0 / e2e_ms, 3), "unit": "decode steps/s",
                 "h2d_bytes_per_step": int(qh.numel() * qh.element_size()),
                 "d2h_bytes_per_step": int(oh[0].numel() * oh[0].element_size()),
                 "overlap": "H2D and D2H on two side streams, double-buffered device q / out"},
@@ -430,7 +445,7 @@ def run_prefill(args, rank, world, cfg):
     return {
         "metric": "prefill key/value compression throughput, Llama-3-8B geometry, 128K tokens x 32 layers",
         "value": round(th, 1), "unit": "token-heads/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64 math on bf16 inputs -> u2 payloads, f16 params",
         "data": "synthetic (gen_synthetic distribution, Philox on GPU)",
         "config": {"workload": "c5", "label": label, "units": units, "tokens": L,
@@ -555,8 +570,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="units in the CPU-baseline sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = batch x N, fixed units per GPU (default); strong = the N = 1 model split")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
         # not launched by torchrun: become the launcher of N ranks (one process per GPU)
         import socket
@@ -569,6 +585,7 @@ def main():
         os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    cfg, args.rep = scaled_config(args.config, world if world > 1 else args.gpus, args.scaling)
 
     if args.impl == "reference":
         if rank != 0:
@@ -585,6 +602,7 @@ def main():
                 arm.step()
             secs = (time.perf_counter() - t0) / args.steps
             v = arm.line(secs)
+            v["value"] = v["value"] * args.rep      # weak scaling: in steps of the N = 1 model
         finally:
             arm.close()
         layers, batch, kvh, gq, L, k, label = cfg
@@ -592,9 +610,10 @@ def main():
             "metric": "decode steps/sec + HBM roofline fraction, Llama-3-8B geometry, 32K ctx",
             "value": v["value"], "unit": "decode steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1000.0 / v["value"], 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_synthetic distribution)", "impl": "reference",
-            "config": dict(decode_config(args.config, world if world > 1 else args.gpus), policy=args.policy,
+            "config": dict(decode_config(args.config, world if world > 1 else args.gpus, cfg, args.rep),
+                           policy=args.policy,
                            bits=args.bits, keys="direct" if args.direct_keys else "sign-in-quant"),
             "cpu_baseline": v,
             "e2e": {"value": v["value"], "unit": "decode steps/s", "h2d_bytes_per_step": 0,
