@@ -80,6 +80,27 @@ def test_plan_partition():
         ShardPlan(32, 1, 8, 16)    # batch 1 cannot be split
 
 
+def test_weak_scaling_keeps_units_per_gpu():
+    """bench.py's default weak scaling: at N GPUs the batch is N x the config's and every rank
+    keeps the N = 1 unit count (KV-head x batch shard); strong scaling splits the N = 1 model."""
+    import bench
+    for name in ("c2", "c3", "c4"):
+        base = bench.CONFIGS[name]
+        n1 = base[0] * base[1] * base[2]
+        for n in (1, 2, 4, 8):
+            cfg, rep = bench.scaled_config(name, n, "weak")
+            layers, batch, kvh = cfg[:3]
+            assert rep == n and batch == base[1] * n
+            plan = ShardPlan(layers, batch, kvh, n)
+            assert plan.units_per_rank == n1
+            allu = torch.cat([plan.local_units(r) for r in range(n)])
+            assert sorted(allu.tolist()) == list(range(n * n1))
+            d = bench.decode_config(name, n, cfg, rep)
+            assert d["units_per_gpu"] == n1 and d["global_batch"] == base[1] * n
+            cfg_s, rep_s = bench.scaled_config(name, n, "strong")
+            assert rep_s == 1 and cfg_s == base
+
+
 def test_assemble_is_the_model_layout():
     for (layers, batch, kvh, world) in [(3, 2, 4, 1), (3, 2, 4, 2), (3, 4, 2, 4), (2, 6, 1, 3)]:
         plan = ShardPlan(layers, batch, kvh, world)
