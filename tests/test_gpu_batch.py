@@ -508,6 +508,35 @@ def test_wide_bit_records(bits, siq):
             B.decode_step(cb, q, 256, kernel=kern)
 
 
+def test_wide_bits_with_window_sinks_and_appends():
+    """bits 4 with SnapKV window sinks and decode-time appends (the recent ring) through the
+    16-bit-record decode: the same sinks as the oracle, selections exact vs restate32 and the
+    attention vs the float64 4-bit oracle cache with its appended rows."""
+    L, seeds, gq, appends = 4096, [830, 831], 4, 3
+    units = [gen_unit(L, 128, gq + appends, s, window=32) for s in seeds]
+    K = torch.tensor(np.stack([u.keys for u in units]), dtype=torch.bfloat16, device="cuda")
+    V = torch.tensor(np.stack([u.values for u in units]), dtype=torch.bfloat16, device="cuda")
+    W = torch.tensor(np.stack([u.window for u in units]), device="cuda")
+    cb = B.prefill_batch(K, V, sink_count=64, window=W, bits=4, recent_capacity=1)
+    oc = []
+    for u in units:
+        c = O.prefill(u.keys, u.values, bits=4, sink_count=64)
+        c.sinks = O.window_sinks(u.keys - c.mu, u.window, 64, 7)
+        c.sink_k = (u.keys - c.mu)[c.sinks].copy()
+        c.sink_v = u.values[c.sinks].copy()
+        oc.append(c)
+    for i, c in enumerate(oc):
+        np.testing.assert_array_equal(cb.sink_idx[i].cpu().numpy(), c.sinks)
+    for a in range(appends):
+        kk = np.stack([u.queries[gq + a] * 0.5 for u in units])
+        vv = np.stack([u.queries[gq + a][::-1].copy() for u in units])
+        B.append_batch(cb, torch.tensor(kk, device="cuda"), torch.tensor(vv, device="cuda"))
+        for i, c in enumerate(oc):
+            O.append(c, kk[i], vv[i])
+    q = torch.tensor(np.stack([u.queries[:gq] for u in units]), dtype=torch.float32, device="cuda")
+    _check_decode(units, cb, oc, q, 300, kernel=0)
+
+
 @pytest.mark.parametrize("name,bits,siq", [("direct_d128", 2, False), ("b1_sinks_d128", 1, True),
                                            ("lossless_d128", 16, True), ("c1_u0", 2, True)])
 def test_fast_variants_match_reference_golden(golden, name, bits, siq):
